@@ -1,0 +1,142 @@
+/* mumode_gpu.h -- C-ABI of the B200 (sm_100a) mu-mode product / Tucker engine.
+ *
+ * This is the drop-in boundary for the hot path of the reference library
+ * (arXiv 2112.11238's mu-mode BLAS, /root/reference/proj). The reference is
+ * header-only C++ whose only compiled seam is la::gemm_raw
+ * (proj/include/mumode/gemm.hpp:15-18, proj/src/gemm.cpp:53-66); replacing
+ * that seam alone would keep the host permutes, so this ABI sits one level up,
+ * at the operators themselves. Each entry point names the reference interface
+ * it replaces.
+ *
+ * Conventions (identical to the reference, proj/include/mumode/shape.hpp:68-77,
+ * matrix.hpp:14):
+ *   - tensors are column-major, first index fastest; extents are int64
+ *     (the reference's int32 GEMM casts, src/gemm.cpp:55-57, do not apply);
+ *   - modes are 1-based (shape.hpp:91-95);
+ *   - a factor matrix L_mu is column-major with ld = rows. Forward products
+ *     use L_mu as n_mu x m_mu; adjoint (cttucker) products use L_mu^H, so the
+ *     stored L_mu is m_mu x n_mu (tucker.hpp:73);
+ *   - complex128 data is interleaved (re, im) doubles (std::complex<double>).
+ *
+ * Device entry points take caller-owned DEVICE pointers, run stream-ordered on
+ * the handle's stream and do not allocate after the first call with a given
+ * shape (the handle owns workspace and TMA descriptors). Host entry points
+ * (mumode_host_*) take HOST pointers and include the host<->device copies; they
+ * are what the reference-shaped C++ API (include/mumode_b200/mumode.hpp) calls.
+ *
+ * Errors: every call returns a status; the message is mumode_last_error()
+ * (thread-local). MUMODE_ERR_SIZE carries the reference's SizeError text,
+ * naming the offending mode ("... mode 2 ..."), MUMODE_ERR_ARGUMENT the
+ * ArgumentError text (errors.hpp:8-26).
+ */
+#ifndef MUMODE_GPU_H
+#define MUMODE_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum mumode_status {
+  MUMODE_OK = 0,
+  MUMODE_ERR_SIZE = 1,      /* reference SizeError      (errors.hpp:8-11)  */
+  MUMODE_ERR_ARGUMENT = 2,  /* reference ArgumentError  (errors.hpp:13-16) */
+  MUMODE_ERR_CUDA = 3,
+  MUMODE_ERR_NCCL = 4,
+  MUMODE_ERR_OOM = 5,
+  MUMODE_ERR_CONTRACT = 6,  /* reference ContractError  (errors.hpp:23-26) */
+  MUMODE_ERR_NUMERICAL = 7  /* reference NumericalError (errors.hpp:18-21) */
+};
+
+typedef struct mumode_handle_s* mumode_handle_t;
+
+/* ---- handle ---------------------------------------------------------- */
+int mumode_handle_create(mumode_handle_t* h, int device);
+int mumode_handle_destroy(mumode_handle_t h);
+/* cudaStream_t passed as void*, used as given (NULL = the legacy default
+ * stream). A new handle starts on its own non-blocking stream. */
+int mumode_set_stream(mumode_handle_t h, void* stream);
+void* mumode_get_stream(mumode_handle_t h);
+const char* mumode_last_error(void);
+const char* mumode_version(void);
+/* Number of mumode kernels launched on this handle since creation (the bench
+ * reports it as gpu_launches). */
+int64_t mumode_launch_count(mumode_handle_t h);
+/* Kernel path selection for tests/benchmarks: 0 = auto (default),
+ * 1 = force the generic SIMT kernel, 2 = force the TMA/DMMA kernel where the
+ * shape allows it. Not a fallback switch: both are CUDA kernels. */
+int mumode_set_kernel_policy(mumode_handle_t h, int policy);
+
+/* ---- device-resident operators --------------------------------------- */
+
+/* Replaces core::mode_product (proj/include/mumode/mode_product.hpp:64-77):
+ * S = T x_mu L, T with d extents m[0..d-1], L n_mu x m[mu-1]; S has m with
+ * m[mu-1] replaced by n_mu. No permutation is materialised. */
+int mumode_mode_product_f64(mumode_handle_t h, int d, const int64_t* m, int mu, int64_t n_mu,
+                            const double* T, const double* L, double* S);
+int mumode_mode_product_c128(mumode_handle_t h, int d, const int64_t* m, int mu, int64_t n_mu,
+                             const double* T, const double* L, double* S);
+
+/* Replaces ops::tucker (adjoint = 0, tucker.hpp:129-132) and ops::cttucker
+ * (adjoint = 1, tucker.hpp:149-151): S = T x_1 op(L_1) ... x_d op(L_d),
+ * modes applied in order 1..d. n[mu] = output extent of mode mu, i.e. rows of
+ * L_mu (forward) or columns of L_mu (adjoint). */
+int mumode_tucker_f64(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                      const double* T, const double* const* L, double* S, int adjoint);
+int mumode_tucker_c128(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                       const double* T, const double* const* L, double* S, int adjoint);
+/* Real tensor against a complex stack (tucker.hpp:142-144, :153-155):
+ * T real, L and S complex. */
+int mumode_tucker_promote(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                          const double* T, const double* const* L, double* S, int adjoint);
+
+/* Replaces ops::kronsumv (tucker.hpp:209-232): W = sum_mu V x_mu A_mu with
+ * square A_mu of size m[mu]. */
+int mumode_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double* V,
+                        const double* const* A, double* W);
+
+/* Exponential-integrator march (apps::linear_evolution_exact applied
+ * repeatedly, src/evolution.cpp:70-82): u <- tucker(u; E_1..E_d) `steps`
+ * times with square E_mu; u0 and u_out may alias. Captured in a CUDA graph
+ * after the first call with a given shape. */
+int mumode_expint_f64(mumode_handle_t h, int d, const int64_t* m, const double* const* E,
+                      const double* u0, double* u_out, int steps);
+
+/* ---- host-buffer drop-in (copies included) ---------------------------- */
+int mumode_host_mode_product_f64(mumode_handle_t h, int d, const int64_t* m, int mu,
+                                 int64_t n_mu, const double* T, const double* L, double* S);
+int mumode_host_mode_product_c128(mumode_handle_t h, int d, const int64_t* m, int mu,
+                                  int64_t n_mu, const double* T, const double* L, double* S);
+int mumode_host_tucker_f64(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                           const double* T, const double* const* L, double* S, int adjoint);
+int mumode_host_tucker_c128(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                            const double* T, const double* const* L, double* S, int adjoint);
+int mumode_host_tucker_promote(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                               const double* T, const double* const* L, double* S, int adjoint);
+int mumode_host_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double* V,
+                             const double* const* A, double* W);
+int mumode_host_expint_f64(mumode_handle_t h, int d, const int64_t* m, const double* const* E,
+                           const double* u0, double* u_out, int steps);
+
+/* ---- host preprocessing ---------------------------------------------- */
+/* Matrix exponential, scaling-and-squaring with the degree-13 Pade
+ * approximant (Higham 2005), host fp64. Role of la::expm
+ * (proj/src/expm.cpp:97-151) for the exponential integrator's E_mu. */
+int mumode_expm_f64(int64_t n, const double* A, double* E);
+
+/* Seeded input generator reproducing the reference's draws bit-for-bit:
+ * std::mt19937_64(seed) and a FRESH std::normal_distribution<double> per
+ * filled object (tools/mumode_cli.cpp:94-121). Complex draws re then im. */
+typedef struct mumode_rng_s* mumode_rng_t;
+int mumode_rng_create(mumode_rng_t* r, uint64_t seed);
+int mumode_rng_destroy(mumode_rng_t r);
+/* Fill n doubles (or n complex = 2n doubles if complex_ != 0). */
+int mumode_rng_normal(mumode_rng_t r, double* out, int64_t n, int complex_);
+/* Raw 64-bit draws (the reference's `g() % k` shape draws). */
+int mumode_rng_u64(mumode_rng_t r, uint64_t* out, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MUMODE_GPU_H */

@@ -1,0 +1,29 @@
+"""B200-native mu-mode product / Tucker engine (arXiv 2112.11238 hot path).
+
+Public API mirrors the reference's ``mumode::core`` / ``mumode::ops`` hot-path
+operators; see ``api.py``. Compute lives in ``libmumode_b200.so`` (sm_100a).
+"""
+from .api import (  # noqa: F401
+    ArgumentError,
+    ContractError,
+    CudaError,
+    Handle,
+    MumodeError,
+    NumericalError,
+    Rng,
+    SizeError,
+    colmajor_empty,
+    cttucker,
+    expint,
+    expm,
+    get_handle,
+    is_colmajor,
+    kronsumv,
+    launch_count,
+    mode_product,
+    to_colmajor,
+    tucker,
+    tucker_sequential,
+)
+
+__version__ = "0.1.0"

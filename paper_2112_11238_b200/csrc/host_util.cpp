@@ -1,0 +1,218 @@
+// Host preprocessing for the mu-mode engine: the seeded input generator and
+// the matrix exponential used to build exponential-integrator factors.
+// Neither is on the timed hot path.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/mumode_gpu.h"
+
+namespace mumode_gpu {
+void set_error(const std::string& msg);
+}
+
+// ------------------------------------------------------------------ rng
+// The reference draws every benchmark/test input from std::mt19937_64 with a
+// FRESH std::normal_distribution<double> per tensor or matrix
+// (tools/mumode_cli.cpp:94-121, tests/acceptance.cpp:41-66); libstdc++'s
+// polar method caches its second sample inside the distribution object, so
+// the call structure matters. These entry points reproduce it exactly by
+// using the same libstdc++ engine and distribution.
+struct mumode_rng_s {
+  std::mt19937_64 eng;
+};
+
+extern "C" int mumode_rng_create(mumode_rng_t* r, uint64_t seed) {
+  if (!r) return MUMODE_ERR_ARGUMENT;
+  *r = new (std::nothrow) mumode_rng_s{std::mt19937_64(seed)};
+  return *r ? MUMODE_OK : MUMODE_ERR_OOM;
+}
+
+extern "C" int mumode_rng_destroy(mumode_rng_t r) {
+  delete r;
+  return MUMODE_OK;
+}
+
+extern "C" int mumode_rng_normal(mumode_rng_t r, double* out, int64_t n, int complex_) {
+  if (!r || (n > 0 && !out)) return MUMODE_ERR_ARGUMENT;
+  std::normal_distribution<double> dist;
+  const int64_t count = complex_ ? 2 * n : n;
+  for (int64_t k = 0; k < count; ++k) out[k] = dist(r->eng);
+  return MUMODE_OK;
+}
+
+extern "C" int mumode_rng_u64(mumode_rng_t r, uint64_t* out, int64_t n) {
+  if (!r || (n > 0 && !out)) return MUMODE_ERR_ARGUMENT;
+  for (int64_t k = 0; k < n; ++k) out[k] = r->eng();
+  return MUMODE_OK;
+}
+
+// ------------------------------------------------------------------ expm
+// Scaling and squaring with diagonal Pade approximants of degree 3,5,7,9,13
+// (N. J. Higham, "The scaling and squaring method for the matrix exponential
+// revisited", SIAM J. Matrix Anal. Appl. 26(4), 2005, Algorithm 2.3): pick the
+// lowest degree whose theta bound covers ||A||_1, otherwise scale by 2^-s to
+// reach theta_13, evaluate r_13 = (V-U)^{-1}(V+U) and square s times.
+namespace {
+
+using Mat = std::vector<double>;  // column-major n x n
+
+void matmul(const Mat& A, const Mat& B, Mat& C, int64_t n) {
+  std::fill(C.begin(), C.end(), 0.0);
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t k = 0; k < n; ++k) {
+      const double b = B[k + j * n];
+      if (b == 0.0) continue;
+      const double* a = &A[k * n];
+      double* c = &C[j * n];
+      for (int64_t i = 0; i < n; ++i) c[i] += a[i] * b;
+    }
+}
+
+double norm1(const Mat& A, int64_t n) {
+  double best = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s += std::fabs(A[i + j * n]);
+    best = std::max(best, s);
+  }
+  return best;
+}
+
+// Solve Q X = P in place (P overwritten by X); Gaussian elimination with
+// partial pivoting. Returns false on an exactly singular pivot.
+bool solve(Mat Q, Mat& P, int64_t n) {
+  std::vector<int64_t> piv(static_cast<size_t>(n));
+  for (int64_t k = 0; k < n; ++k) {
+    int64_t p = k;
+    double best = std::fabs(Q[k + k * n]);
+    for (int64_t i = k + 1; i < n; ++i)
+      if (std::fabs(Q[i + k * n]) > best) best = std::fabs(Q[i + k * n]), p = i;
+    if (best == 0.0) return false;
+    piv[static_cast<size_t>(k)] = p;
+    if (p != k)
+      for (int64_t j = 0; j < n; ++j) std::swap(Q[k + j * n], Q[p + j * n]);
+    for (int64_t i = k + 1; i < n; ++i) {
+      const double f = Q[i + k * n] / Q[k + k * n];
+      Q[i + k * n] = f;
+      if (f == 0.0) continue;
+      for (int64_t j = k + 1; j < n; ++j) Q[i + j * n] -= f * Q[k + j * n];
+    }
+  }
+  for (int64_t c = 0; c < n; ++c) {
+    double* x = &P[c * n];
+    for (int64_t k = 0; k < n; ++k) {
+      const int64_t p = piv[static_cast<size_t>(k)];
+      if (p != k) std::swap(x[k], x[p]);
+    }
+    for (int64_t k = 0; k < n; ++k)
+      for (int64_t i = k + 1; i < n; ++i) x[i] -= Q[i + k * n] * x[k];
+    for (int64_t k = n - 1; k >= 0; --k) {
+      x[k] /= Q[k + k * n];
+      for (int64_t i = 0; i < k; ++i) x[i] -= Q[i + k * n] * x[k];
+    }
+  }
+  return true;
+}
+
+}  // namespace
+
+extern "C" int mumode_expm_f64(int64_t n, const double* Ain, double* E) {
+  if (n < 1 || !Ain || !E) {
+    mumode_gpu::set_error("expm: matrix must be non-empty");
+    return MUMODE_ERR_ARGUMENT;
+  }
+  const size_t nn = static_cast<size_t>(n * n);
+  for (size_t k = 0; k < nn; ++k)
+    if (!std::isfinite(Ain[k])) {
+      mumode_gpu::set_error("expm: input has non-finite entries");
+      return MUMODE_ERR_ARGUMENT;
+    }
+  // Pade coefficients b_0..b_m (Higham 2005, Table 2.3 / eq. (2.11)).
+  static const double b3[] = {120, 60, 12, 1};
+  static const double b5[] = {30240, 15120, 3360, 420, 30, 1};
+  static const double b7[] = {17297280, 8648640, 1995840, 277200, 25200, 1512, 56, 1};
+  static const double b9[] = {17643225600.0, 8821612800.0, 2075673600.0, 302702400.0,
+                              30270240.0,    2162160.0,    110880.0,     3960.0,
+                              90.0,          1.0};
+  static const double b13[] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
+                               1187353796428800.0,  129060195264000.0,   10559470521600.0,
+                               670442572800.0,      33522128640.0,       1323241920.0,
+                               40840800.0,          960960.0,            16380.0,
+                               182.0,               1.0};
+  static const double theta[] = {1.495585217958292e-2, 2.539398330063230e-1,
+                                 9.504178996162932e-1, 2.097847961257068e0,
+                                 5.371920351148152e0};
+  Mat A(Ain, Ain + nn), I(nn, 0.0), U(nn), V(nn), tmp(nn);
+  for (int64_t i = 0; i < n; ++i) I[i + i * n] = 1.0;
+  const double nrm = norm1(A, n);
+  auto axpy = [&](Mat& Y, double a, const Mat& X) {
+    for (size_t k = 0; k < nn; ++k) Y[k] += a * X[k];
+  };
+  int s = 0;
+  const double* b = nullptr;
+  int deg = 13;
+  if (nrm <= theta[0]) b = b3, deg = 3;
+  else if (nrm <= theta[1]) b = b5, deg = 5;
+  else if (nrm <= theta[2]) b = b7, deg = 7;
+  else if (nrm <= theta[3]) b = b9, deg = 9;
+  if (deg < 13) {
+    std::vector<Mat> even{I};  // I, A^2, A^4, ...
+    Mat A2(nn);
+    matmul(A, A, A2, n);
+    even.push_back(A2);
+    for (int k = 2; 2 * k < deg + 1; ++k) {
+      Mat next(nn);
+      matmul(even.back(), A2, next, n);
+      even.push_back(next);
+    }
+    Mat Us(nn, 0.0);
+    std::fill(V.begin(), V.end(), 0.0);
+    for (int k = 0; 2 * k + 1 <= deg; ++k) axpy(Us, b[2 * k + 1], even[static_cast<size_t>(k)]);
+    for (int k = 0; 2 * k <= deg - 1; ++k) axpy(V, b[2 * k], even[static_cast<size_t>(k)]);
+    matmul(A, Us, U, n);
+  } else {
+    if (nrm > theta[4]) s = static_cast<int>(std::ceil(std::log2(nrm / theta[4])));
+    const double sc = std::ldexp(1.0, -s);
+    for (auto& v : A) v *= sc;
+    Mat A2(nn), A4(nn), A6(nn), W(nn, 0.0), Us(nn);
+    matmul(A, A, A2, n);
+    matmul(A2, A2, A4, n);
+    matmul(A2, A4, A6, n);
+    axpy(W, b13[13], A6);
+    axpy(W, b13[11], A4);
+    axpy(W, b13[9], A2);
+    matmul(A6, W, Us, n);
+    axpy(Us, b13[7], A6);
+    axpy(Us, b13[5], A4);
+    axpy(Us, b13[3], A2);
+    axpy(Us, b13[1], I);
+    matmul(A, Us, U, n);
+    Mat W2(nn, 0.0);
+    axpy(W2, b13[12], A6);
+    axpy(W2, b13[10], A4);
+    axpy(W2, b13[8], A2);
+    matmul(A6, W2, V, n);
+    axpy(V, b13[6], A6);
+    axpy(V, b13[4], A4);
+    axpy(V, b13[2], A2);
+    axpy(V, b13[0], I);
+  }
+  Mat P(nn), Q(nn);
+  for (size_t k = 0; k < nn; ++k) P[k] = V[k] + U[k], Q[k] = V[k] - U[k];
+  if (!solve(Q, P, n)) {
+    mumode_gpu::set_error("expm: singular Pade denominator");
+    return MUMODE_ERR_NUMERICAL;
+  }
+  for (int k = 0; k < s; ++k) {
+    matmul(P, P, tmp, n);
+    std::swap(P, tmp);
+  }
+  std::memcpy(E, P.data(), sizeof(double) * nn);
+  return MUMODE_OK;
+}

@@ -1,0 +1,748 @@
+// C-ABI implementation of the B200 mu-mode product / Tucker engine
+// (include/mumode_gpu.h). Host orchestration only: argument checks with the
+// reference's error contract, workspace + TMA-descriptor ownership, kernel
+// selection, the Tucker chain, the exponential-integrator graph, and the
+// host-buffer drop-in entry points. All arithmetic runs in the CUDA kernels of
+// generic.cuh / tma_dmma.cuh / elementwise kernels below; there is no CPU
+// compute path.
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/mumode_gpu.h"
+#include "common.cuh"
+#include "generic.cuh"
+#include "tma_dmma.cuh"
+
+namespace mumode_gpu {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+struct Status {
+  int code;
+  std::string msg;
+};
+
+#define MM_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      set_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #call); \
+      return MUMODE_ERR_CUDA;                                                          \
+    }                                                                                  \
+  } while (0)
+
+#define MM_TRY(expr)          \
+  do {                        \
+    int rc_ = (expr);         \
+    if (rc_ != MUMODE_OK) return rc_; \
+  } while (0)
+
+static int fail(int code, const std::string& msg) {
+  set_error(msg);
+  return code;
+}
+
+// ------------------------------------------------------------------ handle
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t want) {
+    if (want <= bytes) return MUMODE_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    if (cudaMalloc(&p, want) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(MUMODE_ERR_OOM, "device allocation of " + std::to_string(want) + " bytes failed");
+    }
+    bytes = want;
+    return MUMODE_OK;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+using MapKey = std::tuple<const void*, int, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, int, int, int>;
+
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  int64_t nodes = 0;
+};
+
+}  // namespace mumode_gpu
+
+struct mumode_handle_s {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int policy = 0;
+  int64_t launches = 0;
+  mumode_gpu::DevBuf ws[3];     // Tucker ping-pong intermediates + expint buffer
+  mumode_gpu::DevBuf lbuf;      // materialised op(L) for adjoint / promotion
+  mumode_gpu::DevBuf host_in, host_out, host_mats;  // host drop-in staging
+  std::map<mumode_gpu::MapKey, CUtensorMap> maps;
+  std::map<std::vector<uint64_t>, mumode_gpu::GraphEntry> graphs;
+};
+
+namespace mumode_gpu {
+
+// ------------------------------------------------------------------ TMA maps
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// fp64 tiled map with 128B swizzle. dims/strides in elements (dim0 contiguous).
+static int get_map(mumode_handle_s* h, const void* base, int rank, const uint64_t* dims,
+                   const uint64_t* strides_el, const uint32_t* box, const CUtensorMap** out) {
+  MapKey key{base,
+             rank,
+             dims[0],
+             rank > 1 ? dims[1] : 0,
+             rank > 2 ? dims[2] : 0,
+             rank > 1 ? strides_el[0] : 0,
+             rank > 2 ? strides_el[1] : 0,
+             static_cast<int>(box[0]),
+             rank > 1 ? static_cast<int>(box[1]) : 0,
+             rank > 2 ? static_cast<int>(box[2]) : 0};
+  auto it = h->maps.find(key);
+  if (it != h->maps.end()) {
+    *out = &it->second;
+    return MUMODE_OK;
+  }
+  auto fn = encode_fn();
+  if (!fn) return fail(MUMODE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  CUtensorMap map;
+  cuuint64_t gdim[5];
+  cuuint64_t gstride[4];
+  cuuint32_t bdim[5], estride[5];
+  for (int r = 0; r < rank; ++r) {
+    gdim[r] = dims[r];
+    bdim[r] = box[r];
+    estride[r] = 1;
+  }
+  for (int r = 0; r + 1 < rank; ++r) gstride[r] = strides_el[r] * sizeof(double);
+  CUresult res = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), gdim,
+                    gstride, bdim, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (res != CUDA_SUCCESS)
+    return fail(MUMODE_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(res) + ")");
+  auto ins = h->maps.emplace(key, map);
+  *out = &ins.first->second;
+  return MUMODE_OK;
+}
+
+// ------------------------------------------------------------------ small kernels
+__global__ void transpose_conj_kernel(const double* __restrict__ L, double* __restrict__ out,
+                                      int64_t rows, int64_t cols, int cplx, int conj) {
+  // out (cols x rows) = L^T (or L^H), column-major.
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % cols, j = e / cols;  // out(i, j) = L(j, i)
+    const int64_t src = j + i * rows;
+    if (cplx) {
+      out[2 * e] = L[2 * src];
+      out[2 * e + 1] = conj ? -L[2 * src + 1] : L[2 * src + 1];
+    } else {
+      out[e] = L[src];
+    }
+  }
+}
+
+__global__ void real_to_complex_kernel(const double* __restrict__ x, double* __restrict__ z,
+                                       int64_t n) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    z[2 * e] = x[e];
+    z[2 * e + 1] = 0.0;
+  }
+}
+
+__global__ void accumulate_kernel(double* __restrict__ acc, const double* __restrict__ x,
+                                  int64_t n) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x)
+    acc[e] += x[e];
+}
+
+static int grid_for(int64_t n, int sms) {
+  int64_t b = (n + 255) / 256;
+  int64_t cap = int64_t(sms) * 8;
+  return static_cast<int>(b < cap ? (b > 0 ? b : 1) : cap);
+}
+
+// ------------------------------------------------------------------ checks
+static int check_shape(int d, const int64_t* m, const char* who) {
+  if (d < 1) return fail(MUMODE_ERR_ARGUMENT, "tensor order must be >= 1");
+  if (d > 32) return fail(MUMODE_ERR_ARGUMENT, std::string(who) + ": tensor order above 32");
+  for (int k = 0; k < d; ++k)
+    if (m[k] < 1) return fail(MUMODE_ERR_ARGUMENT, "tensor extents must be positive");
+  return MUMODE_OK;
+}
+
+static int64_t prod(const int64_t* m, int lo, int hi) {
+  int64_t p = 1;
+  for (int k = lo; k < hi; ++k) p *= m[k];
+  return p;
+}
+
+// ------------------------------------------------------------------ one product
+// S(a, i, c) = sum_k op(L)(i, k) T(a, k, c); op(L)(i,k) = L[i*sLi + k*sLk].
+struct ModeJob {
+  const double* T;
+  const double* L;
+  double* S;
+  int64_t A, K, N, C;
+  int64_t sLi, sLk;
+  bool cplx;
+  bool conj;
+};
+
+using CfgBig = TmaCfg<128, 128, 16, 4, 2, 4>;
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Can the TMA/DMMA kernel describe this job? (16-byte strides and bases,
+// forward layout of L, real, M even, sizes within int32 coordinates.)
+static bool tma_ok(const ModeJob& j) {
+  if (j.cplx || j.conj) return false;
+  if (j.sLi != 1) return false;  // L must be used forward: op(L) = L, ld = N
+  if (!aligned16(j.T) || !aligned16(j.L) || !aligned16(j.S)) return false;
+  if (j.sLk % 2) return false;
+  const int64_t lim = int64_t(1) << 31;
+  if (j.N >= lim || j.K >= lim || j.C >= lim || j.A >= lim) return false;
+  if (j.A == 1) {  // mode 1: M = N_out, Q = T (K x C)
+    if (j.N % 2 || j.K % 2) return false;
+  } else {
+    if (j.A % 2) return false;
+  }
+  return true;
+}
+
+static bool tma_worthwhile(const ModeJob& j) {
+  const int64_t M = (j.A == 1) ? j.N : j.A;
+  return M >= 32 && j.K >= 16 && ((j.A == 1) ? j.C : j.N) >= 32;
+}
+
+template <class Cfg>
+static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
+  const CUtensorMap* mp = nullptr;
+  const CUtensorMap* mq = nullptr;
+  TmaParams p{};
+  p.D = j.S;
+  const bool mode1 = (j.A == 1);
+  if (mode1) {
+    // P = L: dims {N_out (contig), K}, ld = sLk; Q = T: dims {K (contig), C}
+    uint64_t dP[2] = {uint64_t(j.N), uint64_t(j.K)}, sP[1] = {uint64_t(j.sLk)};
+    uint32_t bP[2] = {16, Cfg::BK};
+    MM_TRY(get_map(h, j.L, 2, dP, sP, bP, &mp));
+    uint64_t dQ[2] = {uint64_t(j.K), uint64_t(j.C)}, sQ[1] = {uint64_t(j.K)};
+    uint32_t bQ[2] = {16, Cfg::BN};
+    MM_TRY(get_map(h, j.T, 2, dQ, sQ, bQ, &mq));
+    p.M = int(j.N);
+    p.N = int(j.C);
+    p.ldD = j.N;
+    p.bstride = 0;
+    p.mt = (p.M + Cfg::BM - 1) / Cfg::BM;
+    p.nt = (p.N + Cfg::BN - 1) / Cfg::BN;
+    p.tiles = int64_t(p.mt) * p.nt;
+  } else {
+    // P = T: dims {A (contig), K, C}; Q = L: dims {N_out (contig), K}
+    uint64_t dP[3] = {uint64_t(j.A), uint64_t(j.K), uint64_t(j.C)};
+    uint64_t sP[2] = {uint64_t(j.A), uint64_t(j.A * j.K)};
+    uint32_t bP[3] = {16, Cfg::BK, 1};
+    MM_TRY(get_map(h, j.T, 3, dP, sP, bP, &mp));
+    uint64_t dQ[2] = {uint64_t(j.N), uint64_t(j.K)}, sQ[1] = {uint64_t(j.sLk)};
+    uint32_t bQ[2] = {16, Cfg::BK};
+    MM_TRY(get_map(h, j.L, 2, dQ, sQ, bQ, &mq));
+    p.M = int(j.A);
+    p.N = int(j.N);
+    p.ldD = j.A;
+    p.bstride = j.A * j.N;
+    p.mt = (p.M + Cfg::BM - 1) / Cfg::BM;
+    p.nt = (p.N + Cfg::BN - 1) / Cfg::BN;
+    p.tiles = int64_t(p.mt) * p.nt * j.C;
+  }
+  p.K = int(j.K);
+  const int grid = static_cast<int>(p.tiles < h->num_sms ? p.tiles : h->num_sms);
+  if (mode1) {
+    auto k = modeprod_tma_kernel<Cfg, true>;
+    MM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mp, *mq, p);
+  } else {
+    auto k = modeprod_tma_kernel<Cfg, false>;
+    MM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mp, *mq, p);
+  }
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return MUMODE_OK;
+}
+
+static int launch_generic(mumode_handle_s* h, const ModeJob& j) {
+  GenericArgs g{j.T, j.L, j.S, j.A, j.K, j.N, j.C, j.sLi, j.sLk, j.conj ? 1 : 0};
+  const int64_t nfib = j.A * j.C;
+  dim3 grid(static_cast<unsigned>((nfib + kGenFibers - 1) / kGenFibers),
+            static_cast<unsigned>((j.N + kGenRows - 1) / kGenRows));
+  if (grid.y > 65535) return fail(MUMODE_ERR_SIZE, "mode product output extent too large");
+  if (j.cplx)
+    modeprod_generic_kernel<true><<<grid, kGenThreads, 0, h->stream>>>(g);
+  else
+    modeprod_generic_kernel<false><<<grid, kGenThreads, 0, h->stream>>>(g);
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return MUMODE_OK;
+}
+
+static int run_job(mumode_handle_s* h, const ModeJob& j) {
+  const bool can_tma = tma_ok(j);
+  if (h->policy == 1 || !can_tma) return launch_generic(h, j);
+  if (h->policy == 2 || tma_worthwhile(j)) return launch_tma<CfgBig>(h, j);
+  return launch_generic(h, j);
+}
+
+// One mode product on device buffers: T with extents m (d modes), op(L)
+// n_mu x m_mu given by (L, sLi, sLk, conj).
+static int mode_product_dev(mumode_handle_s* h, int d, const int64_t* m, int mu, int64_t n_mu,
+                            const double* T, const double* L, int64_t sLi, int64_t sLk,
+                            bool cplx, bool conj, double* S) {
+  ModeJob j;
+  j.T = T;
+  j.L = L;
+  j.S = S;
+  j.A = prod(m, 0, mu - 1);
+  j.K = m[mu - 1];
+  j.C = prod(m, mu, d);
+  j.N = n_mu;
+  j.sLi = sLi;
+  j.sLk = sLk;
+  j.cplx = cplx;
+  j.conj = conj;
+  return run_job(h, j);
+}
+
+// ------------------------------------------------------------------ tucker chain
+// Modes 1..d in order (tucker.hpp:84-110). Lmat[mu] points at the stored
+// matrix; forward: op(L) = L (n x m, ld n); adjoint: op(L) = L^H (L is m x n).
+// Real adjoint and complex adjoint use the generic kernel's strided/conj
+// access, or a materialised op(L) when the TMA path applies.
+static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t* n,
+                      const double* T, const double* const* L, double* S, bool adjoint,
+                      bool cplx) {
+  const int el = cplx ? 2 : 1;
+  // workspace: largest intermediate
+  std::vector<int64_t> ext(m, m + d);
+  size_t maxel = 0;
+  for (int mu = 0; mu < d - 1; ++mu) {
+    ext[mu] = n[mu];
+    maxel = std::max(maxel, size_t(prod(ext.data(), 0, d)));
+  }
+  if (d > 1) {
+    MM_TRY(h->ws[0].ensure(maxel * el * sizeof(double)));
+    if (d > 2) MM_TRY(h->ws[1].ensure(maxel * el * sizeof(double)));
+  }
+  // materialise op(L) = L^T / L^H when adjoint (tiny: n x m per mode)
+  std::vector<const double*> Lop(d);
+  if (adjoint) {
+    size_t tot = 0;
+    for (int mu = 0; mu < d; ++mu) tot += size_t(m[mu] * n[mu]) * el;
+    MM_TRY(h->lbuf.ensure(tot * sizeof(double) + 256));
+    double* dst = static_cast<double*>(h->lbuf.p);
+    for (int mu = 0; mu < d; ++mu) {
+      const int64_t rows = m[mu], cols = n[mu];  // stored L is m x n
+      transpose_conj_kernel<<<grid_for(rows * cols, h->num_sms), 256, 0, h->stream>>>(
+          L[mu], dst, rows, cols, cplx ? 1 : 0, 1);
+      MM_CUDA(cudaGetLastError());
+      h->launches++;
+      Lop[mu] = dst;
+      dst += ((rows * cols * el + 1) / 2) * 2;  // keep 16-B alignment
+    }
+  } else {
+    for (int mu = 0; mu < d; ++mu) Lop[mu] = L[mu];
+  }
+  ext.assign(m, m + d);
+  const double* src = T;
+  for (int mu = 1; mu <= d; ++mu) {
+    double* dst = (mu == d) ? S : static_cast<double*>(h->ws[(mu - 1) % 2].p);
+    MM_TRY(mode_product_dev(h, d, ext.data(), mu, n[mu - 1], src, Lop[mu - 1], 1, n[mu - 1],
+                            cplx, false, dst));
+    ext[mu - 1] = n[mu - 1];
+    src = dst;
+  }
+  return MUMODE_OK;
+}
+
+static int check_stack(int d, const int64_t* m, const int64_t* n, const double* T,
+                       const double* const* L, const void* S, const char* who) {
+  MM_TRY(check_shape(d, m, who));
+  if (!T || !L || !S || !n) return fail(MUMODE_ERR_ARGUMENT, std::string(who) + ": null pointer");
+  for (int k = 0; k < d; ++k) {
+    if (n[k] < 1) return fail(MUMODE_ERR_ARGUMENT, "matrix dimensions must be positive");
+    if (!L[k])
+      return fail(MUMODE_ERR_ARGUMENT,
+                  std::string(who) + ": null matrix for mode " + std::to_string(k + 1));
+  }
+  return MUMODE_OK;
+}
+
+}  // namespace mumode_gpu
+
+using namespace mumode_gpu;
+
+// ====================================================================== C-ABI
+extern "C" {
+
+const char* mumode_last_error(void) { return g_err.c_str(); }
+const char* mumode_version(void) { return "mumode-b200 0.1 (sm_100a)"; }
+
+int mumode_handle_create(mumode_handle_t* out, int device) {
+  if (!out) return fail(MUMODE_ERR_ARGUMENT, "null handle pointer");
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(MUMODE_ERR_CUDA, "no CUDA device available: the mu-mode engine has no CPU path");
+  }
+  if (device < 0 || device >= ndev) return fail(MUMODE_ERR_ARGUMENT, "bad device index");
+  MM_CUDA(cudaSetDevice(device));
+  int major = 0;
+  MM_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major != 10)
+    return fail(MUMODE_ERR_CUDA, "this build targets sm_100a (B200); device has compute major " +
+                                     std::to_string(major));
+  auto* h = new mumode_handle_s();
+  h->device = device;
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete h;
+    return fail(MUMODE_ERR_CUDA, "stream creation failed");
+  }
+  h->stream = h->own_stream;
+  *out = h;
+  return MUMODE_OK;
+}
+
+int mumode_handle_destroy(mumode_handle_t h) {
+  if (!h) return MUMODE_OK;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  for (auto& kv : h->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  delete h;
+  return MUMODE_OK;
+}
+
+int mumode_set_stream(mumode_handle_t h, void* stream) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  // The caller's stream exactly (NULL = the legacy default stream, which is
+  // what torch's default stream reports), so work is ordered with theirs.
+  h->stream = static_cast<cudaStream_t>(stream);
+  return MUMODE_OK;
+}
+
+void* mumode_get_stream(mumode_handle_t h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+int64_t mumode_launch_count(mumode_handle_t h) { return h ? h->launches : -1; }
+
+int mumode_set_kernel_policy(mumode_handle_t h, int policy) {
+  if (!h || policy < 0 || policy > 2) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
+  h->policy = policy;
+  return MUMODE_OK;
+}
+
+static int mode_product_entry(mumode_handle_t h, int d, const int64_t* m, int mu, int64_t n_mu,
+                              const double* T, const double* L, double* S, bool cplx) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  MM_TRY(check_shape(d, m, "mode_product"));
+  if (mu < 1 || mu > d)
+    return fail(MUMODE_ERR_ARGUMENT, "mode index " + std::to_string(mu) + " out of range 1.." +
+                                         std::to_string(d));
+  if (n_mu < 1) return fail(MUMODE_ERR_ARGUMENT, "matrix dimensions must be positive");
+  if (!T || !L || !S) return fail(MUMODE_ERR_ARGUMENT, "mode_product: null pointer");
+  MM_CUDA(cudaSetDevice(h->device));
+  return mode_product_dev(h, d, m, mu, n_mu, T, L, 1, n_mu, cplx, false, S);
+}
+
+int mumode_mode_product_f64(mumode_handle_t h, int d, const int64_t* m, int mu, int64_t n_mu,
+                            const double* T, const double* L, double* S) {
+  return mode_product_entry(h, d, m, mu, n_mu, T, L, S, false);
+}
+int mumode_mode_product_c128(mumode_handle_t h, int d, const int64_t* m, int mu, int64_t n_mu,
+                             const double* T, const double* L, double* S) {
+  return mode_product_entry(h, d, m, mu, n_mu, T, L, S, true);
+}
+
+static int tucker_entry(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                        const double* T, const double* const* L, double* S, int adjoint,
+                        bool cplx) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  MM_TRY(check_stack(d, m, n, T, L, S, adjoint ? "cttucker" : "tucker"));
+  MM_CUDA(cudaSetDevice(h->device));
+  return tucker_dev(h, d, m, n, T, L, S, adjoint != 0, cplx);
+}
+
+int mumode_tucker_f64(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                      const double* T, const double* const* L, double* S, int adjoint) {
+  return tucker_entry(h, d, m, n, T, L, S, adjoint, false);
+}
+int mumode_tucker_c128(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                       const double* T, const double* const* L, double* S, int adjoint) {
+  return tucker_entry(h, d, m, n, T, L, S, adjoint, true);
+}
+
+int mumode_tucker_promote(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                          const double* T, const double* const* L, double* S, int adjoint) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  MM_TRY(check_stack(d, m, n, T, L, S, adjoint ? "cttucker" : "tucker"));
+  MM_CUDA(cudaSetDevice(h->device));
+  const int64_t numel = prod(m, 0, d);
+  MM_TRY(h->ws[2].ensure(size_t(numel) * 2 * sizeof(double)));
+  double* z = static_cast<double*>(h->ws[2].p);
+  real_to_complex_kernel<<<grid_for(numel, h->num_sms), 256, 0, h->stream>>>(T, z, numel);
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return tucker_dev(h, d, m, n, z, L, S, adjoint != 0, true);
+}
+
+int mumode_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double* V,
+                        const double* const* A, double* W) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  MM_TRY(check_stack(d, m, m, V, A, W, "kronsumv"));
+  MM_CUDA(cudaSetDevice(h->device));
+  const int64_t numel = prod(m, 0, d);
+  MM_TRY(mode_product_dev(h, d, m, 1, m[0], V, A[0], 1, m[0], false, false, W));
+  if (d > 1) MM_TRY(h->ws[0].ensure(size_t(numel) * sizeof(double)));
+  double* term = static_cast<double*>(h->ws[0].p);
+  for (int mu = 2; mu <= d; ++mu) {
+    MM_TRY(mode_product_dev(h, d, m, mu, m[mu - 1], V, A[mu - 1], 1, m[mu - 1], false, false,
+                            term));
+    accumulate_kernel<<<grid_for(numel, h->num_sms), 256, 0, h->stream>>>(W, term, numel);
+    MM_CUDA(cudaGetLastError());
+    h->launches++;
+  }
+  return MUMODE_OK;
+}
+
+int mumode_expint_f64(mumode_handle_t h, int d, const int64_t* m, const double* const* E,
+                      const double* u0, double* u_out, int steps) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  MM_TRY(check_stack(d, m, m, u0, E, u_out, "expint"));
+  if (steps < 0) return fail(MUMODE_ERR_ARGUMENT, "expint: steps must be non-negative");
+  MM_CUDA(cudaSetDevice(h->device));
+  const int64_t numel = prod(m, 0, d);
+  const size_t bytes = size_t(numel) * sizeof(double);
+  if (steps == 0) {
+    if (u_out != u0) MM_CUDA(cudaMemcpyAsync(u_out, u0, bytes, cudaMemcpyDeviceToDevice, h->stream));
+    return MUMODE_OK;
+  }
+  MM_TRY(h->ws[2].ensure(bytes));
+  double* spare = static_cast<double*>(h->ws[2].p);
+  // Graph key: shape, pointers, steps.
+  std::vector<uint64_t> key{uint64_t(d), uint64_t(steps), reinterpret_cast<uint64_t>(u0),
+                            reinterpret_cast<uint64_t>(u_out)};
+  for (int k = 0; k < d; ++k) {
+    key.push_back(uint64_t(m[k]));
+    key.push_back(reinterpret_cast<uint64_t>(E[k]));
+  }
+  auto body = [&]() -> int {
+    const double* cur = u0;
+    for (int s = 0; s < steps; ++s) {
+      // end in u_out; never read and write the same buffer within one step
+      double* dst = ((steps - 1 - s) % 2 == 0) ? u_out : spare;
+      if (dst == cur) dst = (dst == u_out) ? spare : u_out;
+      MM_TRY(tucker_dev(h, d, m, m, cur, E, dst, false, false));
+      cur = dst;
+    }
+    if (cur != u_out)
+      MM_CUDA(cudaMemcpyAsync(u_out, cur, bytes, cudaMemcpyDeviceToDevice, h->stream));
+    return MUMODE_OK;
+  };
+  auto it = h->graphs.find(key);
+  if (it == h->graphs.end()) {
+    // First call: run eagerly (allocates workspace, encodes TMA maps), then
+    // capture the identical launch sequence for later calls.
+    const int64_t before = h->launches;
+    MM_TRY(body());
+    GraphEntry ge;
+    cudaGraph_t graph = nullptr;
+    // Capture on the handle's own stream (the legacy stream cannot be
+    // captured); nothing executes during capture. Replays go to h->stream.
+    cudaStream_t user = h->stream;
+    h->stream = h->own_stream;
+    MM_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    const int64_t l0 = h->launches;
+    int rc = body();
+    cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
+    h->stream = user;
+    if (rc != MUMODE_OK) return rc;
+    if (ce != cudaSuccess) return fail(MUMODE_ERR_CUDA, "graph capture failed");
+    ge.nodes = h->launches - l0;
+    h->launches = l0;  // captured, not executed
+    MM_CUDA(cudaGraphInstantiate(&ge.exec, graph, 0));
+    cudaGraphDestroy(graph);
+    h->graphs.emplace(key, ge);
+    (void)before;
+    return MUMODE_OK;
+  }
+  MM_CUDA(cudaGraphLaunch(it->second.exec, h->stream));
+  h->launches += it->second.nodes;
+  return MUMODE_OK;
+}
+
+// ---------------------------------------------------------------- host drop-in
+static int stage_in(mumode_handle_t h, const double* src, size_t bytes, mumode_gpu::DevBuf& buf,
+                    size_t offset) {
+  MM_CUDA(cudaMemcpyAsync(static_cast<char*>(buf.p) + offset, src, bytes, cudaMemcpyHostToDevice,
+                          h->stream));
+  return MUMODE_OK;
+}
+
+// Upload T and the d matrices (sizes el*Lsz[k] doubles) into staging; returns
+// device pointers.
+static int upload(mumode_handle_t h, const double* T, size_t t_el, int d, const double* const* L,
+                  const int64_t* Lsz, const double** dT, std::vector<const double*>& dL) {
+  size_t mat_bytes = 0;
+  for (int k = 0; k < d; ++k) mat_bytes += ((size_t(Lsz[k]) * sizeof(double) + 255) / 256) * 256;
+  MM_TRY(h->host_in.ensure(t_el * sizeof(double)));
+  MM_TRY(h->host_mats.ensure(mat_bytes + 256));
+  MM_TRY(stage_in(h, T, t_el * sizeof(double), h->host_in, 0));
+  *dT = static_cast<const double*>(h->host_in.p);
+  size_t off = 0;
+  dL.resize(d);
+  for (int k = 0; k < d; ++k) {
+    MM_TRY(stage_in(h, L[k], size_t(Lsz[k]) * sizeof(double), h->host_mats, off));
+    dL[k] = reinterpret_cast<const double*>(static_cast<char*>(h->host_mats.p) + off);
+    off += ((size_t(Lsz[k]) * sizeof(double) + 255) / 256) * 256;
+  }
+  return MUMODE_OK;
+}
+
+static int download(mumode_handle_t h, double* S, size_t el) {
+  MM_CUDA(cudaMemcpyAsync(S, h->host_out.p, el * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  MM_CUDA(cudaStreamSynchronize(h->stream));
+  return MUMODE_OK;
+}
+
+static int host_tucker_impl(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                            const double* T, const double* const* L, double* S, int adjoint,
+                            int t_el, int l_el) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  MM_TRY(check_stack(d, m, n, T, L, S, adjoint ? "cttucker" : "tucker"));
+  MM_CUDA(cudaSetDevice(h->device));
+  std::vector<int64_t> lsz(d);
+  for (int k = 0; k < d; ++k) lsz[k] = m[k] * n[k] * l_el;
+  const double* dT;
+  std::vector<const double*> dL;
+  MM_TRY(upload(h, T, size_t(prod(m, 0, d)) * t_el, d, L, lsz.data(), &dT, dL));
+  const size_t out_el = size_t(prod(n, 0, d)) * l_el;
+  MM_TRY(h->host_out.ensure(out_el * sizeof(double)));
+  double* dS = static_cast<double*>(h->host_out.p);
+  if (t_el == 1 && l_el == 2)
+    MM_TRY(mumode_tucker_promote(h, d, m, n, dT, dL.data(), dS, adjoint));
+  else
+    MM_TRY(tucker_dev(h, d, m, n, dT, dL.data(), dS, adjoint != 0, l_el == 2));
+  return download(h, S, out_el);
+}
+
+int mumode_host_tucker_f64(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                           const double* T, const double* const* L, double* S, int adjoint) {
+  return host_tucker_impl(h, d, m, n, T, L, S, adjoint, 1, 1);
+}
+int mumode_host_tucker_c128(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                            const double* T, const double* const* L, double* S, int adjoint) {
+  return host_tucker_impl(h, d, m, n, T, L, S, adjoint, 2, 2);
+}
+int mumode_host_tucker_promote(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                               const double* T, const double* const* L, double* S, int adjoint) {
+  return host_tucker_impl(h, d, m, n, T, L, S, adjoint, 1, 2);
+}
+
+static int host_mode_product_impl(mumode_handle_t h, int d, const int64_t* m, int mu,
+                                  int64_t n_mu, const double* T, const double* L, double* S,
+                                  int el) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  MM_TRY(check_shape(d, m, "mode_product"));
+  if (mu < 1 || mu > d)
+    return fail(MUMODE_ERR_ARGUMENT, "mode index " + std::to_string(mu) + " out of range 1.." +
+                                         std::to_string(d));
+  if (!T || !L || !S) return fail(MUMODE_ERR_ARGUMENT, "mode_product: null pointer");
+  MM_CUDA(cudaSetDevice(h->device));
+  int64_t lsz = n_mu * m[mu - 1] * el;
+  const double* dT;
+  std::vector<const double*> dL;
+  MM_TRY(upload(h, T, size_t(prod(m, 0, d)) * el, 1, &L, &lsz, &dT, dL));
+  std::vector<int64_t> out(m, m + d);
+  out[mu - 1] = n_mu;
+  const size_t out_el = size_t(prod(out.data(), 0, d)) * el;
+  MM_TRY(h->host_out.ensure(out_el * sizeof(double)));
+  MM_TRY(mode_product_dev(h, d, m, mu, n_mu, dT, dL[0], 1, n_mu, el == 2, false,
+                          static_cast<double*>(h->host_out.p)));
+  return download(h, S, out_el);
+}
+
+int mumode_host_mode_product_f64(mumode_handle_t h, int d, const int64_t* m, int mu,
+                                 int64_t n_mu, const double* T, const double* L, double* S) {
+  return host_mode_product_impl(h, d, m, mu, n_mu, T, L, S, 1);
+}
+int mumode_host_mode_product_c128(mumode_handle_t h, int d, const int64_t* m, int mu,
+                                  int64_t n_mu, const double* T, const double* L, double* S) {
+  return host_mode_product_impl(h, d, m, mu, n_mu, T, L, S, 2);
+}
+
+int mumode_host_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double* V,
+                             const double* const* A, double* W) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  MM_TRY(check_stack(d, m, m, V, A, W, "kronsumv"));
+  MM_CUDA(cudaSetDevice(h->device));
+  std::vector<int64_t> lsz(d);
+  for (int k = 0; k < d; ++k) lsz[k] = m[k] * m[k];
+  const double* dV;
+  std::vector<const double*> dA;
+  const size_t el = size_t(prod(m, 0, d));
+  MM_TRY(upload(h, V, el, d, A, lsz.data(), &dV, dA));
+  MM_TRY(h->host_out.ensure(el * sizeof(double)));
+  MM_TRY(mumode_kronsumv_f64(h, d, m, dV, dA.data(), static_cast<double*>(h->host_out.p)));
+  return download(h, W, el);
+}
+
+int mumode_host_expint_f64(mumode_handle_t h, int d, const int64_t* m, const double* const* E,
+                           const double* u0, double* u_out, int steps) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  MM_TRY(check_stack(d, m, m, u0, E, u_out, "expint"));
+  MM_CUDA(cudaSetDevice(h->device));
+  std::vector<int64_t> lsz(d);
+  for (int k = 0; k < d; ++k) lsz[k] = m[k] * m[k];
+  const double* du;
+  std::vector<const double*> dE;
+  const size_t el = size_t(prod(m, 0, d));
+  MM_TRY(upload(h, u0, el, d, E, lsz.data(), &du, dE));
+  MM_TRY(h->host_out.ensure(el * sizeof(double)));
+  MM_TRY(mumode_expint_f64(h, d, m, dE.data(), du, static_cast<double*>(h->host_out.p), steps));
+  return download(h, u_out, el);
+}
+
+}  // extern "C"

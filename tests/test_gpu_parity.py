@@ -1,0 +1,302 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracles.
+
+Restates the reference's hot-path test suite (test_tucker_ops.cpp,
+test_tensor_core.cpp, acceptance C1) on the device path (torch CUDA tensors)
+and the host drop-in path (numpy in, numpy out), against the golden vectors
+made by the reference library and against the oracles on fresh seeded inputs.
+Tolerances are the reference's own (1e-13 small cases, bitwise where the
+reference is bitwise) and the north-star gate (relative Frobenius <= 1e-12).
+"""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+import paper_2112_11238_b200 as mm  # noqa: E402
+
+GOLD = np.load(Path(__file__).resolve().parents[0] / "golden" / "golden.npz")
+
+
+def dev(x):
+    return torch.from_numpy(np.asfortranarray(x)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def stack(prefix, tag, d):
+    return [GOLD[f"{prefix}_{tag}{k}"] for k in range(d)]
+
+
+@pytest.fixture(autouse=True)
+def _require_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test run without a GPU")
+
+
+@pytest.fixture(params=[0, 1, 2], ids=["auto", "generic", "tma"])
+def policy(request):
+    h = mm.get_handle(0)
+    h.set_kernel_policy(request.param)
+    yield request.param
+    h.set_kernel_policy(0)
+
+
+# ----------------------------------------------------------- golden vectors
+def test_golden_tucker_cases_device_and_host(policy):
+    worst = 0.0
+    for c in range(24):
+        T = GOLD[f"tk{c}_T"]
+        Ls = stack(f"tk{c}", "L", T.ndim)
+        Sd = host(mm.tucker(dev(T), [dev(L) for L in Ls]))
+        Sh = mm.tucker(T, Ls)
+        worst = max(worst, O.rel_max(Sd, GOLD[f"tk{c}_S"]), O.rel_max(Sh, GOLD[f"tk{c}_K"]))
+        np.testing.assert_array_equal(Sd, Sh)
+    assert worst < 1e-13
+
+
+def test_golden_cttucker(policy):
+    for c in range(6):
+        T = GOLD[f"ct{c}_T"]
+        Ps = stack(f"ct{c}", "P", T.ndim)
+        assert O.rel_max(host(mm.cttucker(dev(T), [dev(P) for P in Ps])), GOLD[f"ct{c}_S"]) < 1e-14
+
+
+def test_golden_mode_products(policy):
+    T = GOLD["mp_T"]
+    for mu in range(1, 5):
+        S = host(mm.mode_product(dev(T), dev(GOLD[f"mp_L{mu}"]), mu))
+        assert O.rel_max(S, GOLD[f"mp_S{mu}"]) < 1e-13
+    Tc = GOLD["mpc_T"]
+    for mu in range(1, 4):
+        S = mm.mode_product(Tc, GOLD[f"mpc_L{mu}"], mu)
+        assert O.rel_max(S, GOLD[f"mpc_S{mu}"]) < 1e-13
+
+
+def test_golden_kronsumv_promotion_configs(policy):
+    assert O.rel_max(mm.kronsumv(GOLD["ks_V"], stack("ks", "A", 3)), GOLD["ks_W"]) < 1e-13
+    assert O.rel_max(mm.tucker(GOLD["pr_T"], stack("pr", "L", 3)), GOLD["pr_S"]) < 1e-15
+    assert O.rel_fro(host(mm.tucker(dev(GOLD["c2_T"]), [dev(L) for L in stack("c2", "L", 3)])), GOLD["c2_S"]) < 1e-13
+    E = GOLD["c3_E"]
+    u10 = host(mm.expint(dev(GOLD["c3_u0"]), [dev(E)] * 3, 10))
+    assert O.rel_fro(u10, GOLD["c3_u10"]) < 1e-12
+    assert O.rel_fro(mm.tucker(GOLD["c4_T"], stack("c4", "L", 3)), GOLD["c4_S"]) < 1e-13
+    assert O.rel_fro(mm.tucker(GOLD["c5_T"], stack("c5", "L", 6)), GOLD["c5_S"]) < 1e-13
+
+
+# ------------------------------------------------ restated reference tests
+def rnd(rng, shape, cplx=False):
+    x = rng.uniform(-1, 1, shape)
+    if cplx:
+        x = x + 1j * rng.uniform(-1, 1, shape)
+    return np.asfortranarray(x)
+
+
+def test_identity_stack_is_exact(policy):
+    # test_tucker_ops.cpp:41-52 (max_abs_diff == 0)
+    rng = np.random.default_rng(100)
+    for _ in range(10):
+        d = int(rng.integers(1, 6))
+        m = [int(x) for x in rng.integers(1, 5, d)]
+        T = rnd(rng, m)
+        S = host(mm.tucker(dev(T), [dev(np.eye(e)) for e in m]))
+        assert np.max(np.abs(S - T)) == 0.0
+
+
+def test_identity_mode_product_is_exact_large(policy):
+    # test_tensor_core.cpp:180-190 at TMA-sized shapes
+    rng = np.random.default_rng(17)
+    T = rnd(rng, (64, 48, 32))
+    for mu in (1, 2, 3):
+        S = host(mm.mode_product(dev(T), dev(np.eye(T.shape[mu - 1])), mu))
+        np.testing.assert_array_equal(S, T)
+
+
+def test_d2_two_sided_product(policy):
+    # test_tucker_ops.cpp:54-69
+    rng = np.random.default_rng(101)
+    for _ in range(10):
+        T = rnd(rng, (4, 3))
+        L1, L2 = rnd(rng, (2, 4)), rnd(rng, (5, 3))
+        S = host(mm.tucker(dev(T), [dev(L1), dev(L2)]))
+        assert O.rel_max(S, L1 @ T @ L2.T) < 1e-13
+
+
+def test_kron_oracle_orders_1_to_5_real_and_complex(policy):
+    # test_tucker_ops.cpp:71-88, acceptance C1 (seed 20260825, 200 cases)
+    rng = np.random.default_rng(20260825)
+    worst = 0.0
+    for rep in range(200):
+        d = int(rng.integers(1, 6))
+        m = [int(x) for x in rng.integers(1, 5, d)]
+        n = [int(x) for x in rng.integers(1, 5, d)]
+        cplx = rep % 2 == 1
+        T = rnd(rng, m, cplx)
+        Ls = [rnd(rng, (n[k], m[k]), cplx) for k in range(d)]
+        worst = max(worst, O.rel_max(host(mm.tucker(dev(T), [dev(L) for L in Ls])), O.port_tucker(T, Ls)))
+    assert worst < 1e-13
+
+
+def test_mode_order_invariance(policy):
+    # test_tucker_ops.cpp:90-108
+    rng = np.random.default_rng(103)
+    for _ in range(15):
+        d = int(rng.integers(2, 5))
+        m = [int(x) for x in rng.integers(1, 5, d)]
+        n = [int(x) for x in rng.integers(1, 5, d)]
+        T = rnd(rng, m)
+        Ls = [rnd(rng, (n[k], m[k])) for k in range(d)]
+        fused = host(mm.tucker(dev(T), [dev(L) for L in Ls]))
+        cur = dev(T)
+        for mu in rng.permutation(d) + 1:
+            cur = mm.mode_product(cur, dev(Ls[mu - 1]), int(mu))
+        assert O.rel_max(fused, host(cur)) < 1e-13
+
+
+def test_fused_equals_sequential_complex(policy):
+    # test_tucker_ops.cpp:110-120
+    rng = np.random.default_rng(104)
+    for _ in range(20):
+        d = int(rng.integers(1, 6))
+        m = [int(x) for x in rng.integers(1, 5, d)]
+        n = [int(x) for x in rng.integers(1, 5, d)]
+        T = rnd(rng, m, True)
+        Ls = [rnd(rng, (n[k], m[k]), True) for k in range(d)]
+        a = host(mm.tucker(dev(T), [dev(L) for L in Ls]))
+        b = host(mm.tucker_sequential(dev(T), [dev(L) for L in Ls]))
+        assert O.rel_max(a, b) < 1e-13
+
+
+def test_promotion_real_tensor_complex_stack(policy):
+    # test_tucker_ops.cpp:145-153 and test_tensor_core.cpp:262-269
+    rng = np.random.default_rng(107)
+    T = rnd(rng, (3, 2, 3))
+    Ls = [rnd(rng, (n, m), True) for n, m in ((2, 3), (3, 2), (2, 3))]
+    S = host(mm.tucker(dev(T), [dev(L) for L in Ls]))
+    Sref = host(mm.tucker(dev(T.astype(complex)), [dev(L) for L in Ls]))
+    assert O.rel_max(S, Sref) < 1e-15
+    L = rnd(rng, (5, 2), True)
+    r = host(mm.mode_product(dev(T), dev(L), 2))
+    assert O.rel_max(r, O.port_mode_product(T.astype(complex), L, 2)) < 1e-14
+
+
+def test_cttucker_against_explicit_conjugate_transpose(policy):
+    # test_tucker_ops.cpp:189-206 and :208-215
+    rng = np.random.default_rng(111)
+    for _ in range(10):
+        d = int(rng.integers(1, 5))
+        m = [int(x) for x in rng.integers(1, 5, d)]
+        n = [int(x) for x in rng.integers(1, 5, d)]
+        T = rnd(rng, m, True)
+        Ps = [rnd(rng, (m[k], n[k]), True) for k in range(d)]
+        a = host(mm.cttucker(dev(T), [dev(P) for P in Ps]))
+        b = host(mm.tucker(dev(T), [dev(np.conj(P.T)) for P in Ps]))
+        assert O.rel_max(a, b) < 1e-14
+    T = np.array([2.0 + 1.0j])
+    S = host(mm.cttucker(dev(T), [dev(np.array([[1.0j]]))]))
+    assert abs(S[0] - (-1.0j) * T[0]) < 1e-15
+
+
+def test_cttucker_of_tucker_with_rotations_is_identity(policy):
+    # test_tucker_ops.cpp:217-234
+    rng = np.random.default_rng(112)
+    for _ in range(10):
+        T = rnd(rng, (2, 2, 2))
+        Qs = []
+        for _ in range(3):
+            a = float(rng.integers(0, 1000)) / 500.0
+            Qs.append(np.array([[np.cos(a), -np.sin(a)], [np.sin(a), np.cos(a)]]))
+        r = host(mm.cttucker(mm.tucker(dev(T), [dev(Q) for Q in Qs]), [dev(Q) for Q in Qs]))
+        assert O.rel_max(r, T) < 1e-12
+
+
+def test_kronsumv_exactness_and_oracle(policy):
+    # test_tucker_ops.cpp:290-355
+    rng = np.random.default_rng(117)
+    V = rnd(rng, (2, 3, 2))
+    W = host(mm.kronsumv(dev(V), [dev(np.eye(2)), dev(np.eye(3)), dev(np.eye(2))]))
+    assert np.max(np.abs(W - 3 * V)) == 0.0
+    V1 = rnd(rng, (4,))
+    A = rnd(rng, (4, 4))
+    np.testing.assert_array_equal(host(mm.kronsumv(dev(V1), [dev(A)])), host(mm.mode_product(dev(V1), dev(A), 1)))
+    for _ in range(10):
+        V = rnd(rng, (2, 3, 2))
+        As = [rnd(rng, (e, e)) for e in V.shape]
+        assert O.rel_max(host(mm.kronsumv(dev(V), [dev(A) for A in As])), O.port_kronsumv(V, As)) < 1e-13
+    # linearity
+    V, Wt = rnd(rng, (3, 2, 3)), rnd(rng, (3, 2, 3))
+    As = [rnd(rng, (e, e)) for e in V.shape]
+    lhs = host(mm.kronsumv(dev(0.37 * V + Wt), [dev(A) for A in As]))
+    rhs = 0.37 * host(mm.kronsumv(dev(V), [dev(A) for A in As])) + host(mm.kronsumv(dev(Wt), [dev(A) for A in As]))
+    assert O.rel_max(lhs, rhs) < 1e-13
+
+
+def test_mode_product_matches_nested_loop_oracle(policy):
+    # test_tensor_core.cpp:207-223, :225-242
+    rng = np.random.default_rng(19)
+    done = 0
+    while done < 60:
+        d = int(rng.integers(1, 6))
+        m = [int(x) for x in rng.integers(1, 6, d)]
+        if int(np.prod(m)) > 200:
+            continue
+        done += 1
+        mu = int(rng.integers(1, d + 1))
+        L = rnd(rng, (int(rng.integers(1, 6)), m[mu - 1]))
+        T = rnd(rng, m)
+        assert O.rel_max(host(mm.mode_product(dev(T), dev(L), mu)), O.port_mode_product(T, L, mu)) < 1e-13
+    # commutation across modes, composition within a mode
+    for _ in range(30):
+        m = [int(x) for x in rng.integers(1, 5, int(rng.integers(2, 5)))]
+        T = rnd(rng, m)
+        A, B, C = rnd(rng, (3, m[0])), rnd(rng, (2, m[1])), rnd(rng, (4, 3))
+        ab = mm.mode_product(mm.mode_product(dev(T), dev(A), 1), dev(B), 2)
+        ba = mm.mode_product(mm.mode_product(dev(T), dev(B), 2), dev(A), 1)
+        assert O.rel_max(host(ab), host(ba)) < 1e-13
+        ch = mm.mode_product(mm.mode_product(dev(T), dev(A), 1), dev(C), 1)
+        fu = mm.mode_product(dev(T), dev(C @ A), 1)
+        assert O.rel_max(host(ch), host(fu)) < 1e-13
+
+
+def test_ragged_and_unaligned_shapes_against_oracle(policy):
+    # odd extents, extents that are not multiples of the tile sizes, 1-extents
+    rng = np.random.default_rng(5)
+    for m, n in [((33, 17, 9), (31, 18, 7)), ((130, 3, 66), (2, 129, 64)), ((1, 200, 1), (1, 7, 3)),
+                 ((18, 34, 50), (48, 34, 18)), ((256, 2, 40), (256, 2, 40))]:
+        T = rnd(rng, m)
+        Ls = [rnd(rng, (n[k], m[k])) for k in range(len(m))]
+        S = host(mm.tucker(dev(T), [dev(L) for L in Ls]))
+        assert O.rel_max(S, O.port_tucker(T, Ls)) < 1e-13, (m, n)
+
+
+def test_aligned_medium_shapes_all_modes(policy):
+    # shapes that take the TMA/DMMA path: every mode, rectangular factors
+    rng = np.random.default_rng(6)
+    T = rnd(rng, (96, 64, 80))
+    for mu, n in ((1, 112), (2, 48), (3, 130)):
+        L = rnd(rng, (n, T.shape[mu - 1]))
+        S = host(mm.mode_product(dev(T), dev(L), mu))
+        assert O.rel_max(S, O.port_mode_product(T, L, mu)) < 1e-13
+    Ls = [rnd(rng, (n, e)) for n, e in zip((128, 64, 32), T.shape)]
+    assert O.rel_fro(host(mm.tucker(dev(T), [dev(L) for L in Ls])), O.port_tucker(T, Ls)) < 1e-14
+
+
+def test_host_and_device_paths_agree_bitwise():
+    rng = np.random.default_rng(7)
+    T = rnd(rng, (64, 64, 64))
+    Ls = [rnd(rng, (64, 64)) for _ in range(3)]
+    np.testing.assert_array_equal(mm.tucker(T, Ls), host(mm.tucker(dev(T), [dev(L) for L in Ls])))
+
+
+def test_launch_counter_moves():
+    h = mm.get_handle(0)
+    before = h.launches
+    mm.tucker(dev(np.ones((4, 4, 4))), [dev(np.eye(4))] * 3)
+    torch.cuda.synchronize()
+    assert h.launches - before == 3
