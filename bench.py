@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 mu-mode engine (driver contract).
+
+Metric (BASELINE.json): Tucker operator fp64 GFLOP/s and % of roofline.
+Workload at N=1: BASELINE configs[1] (C2) -- 3-D Tucker operator
+S = T x_1 L_1 x_2 L_2 x_3 L_3, real fp64, T in R^{256^3}, L_mu 256 x 256, all
+standard normal from the reference's generator (mt19937_64 seed 1234, tensor
+then matrices). One step = one Tucker application (3 mode products,
+2.577e10 flop). FLOP = sum_mu 2 n_mu (elements entering mode mu).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+* ``value``     device-resident throughput through the C-ABI
+                (mumode_tucker_f64), CUDA events per step, L2 flushed between
+                steps (256 MiB write, outside the events), max over ranks.
+* ``e2e``       the same metric through the host drop-in entry point
+                (mumode_host_tucker_f64) with pinned host buffers: H2D of T and
+                the factors and D2H of S inside every timed step.
+* ``roofline``  the dominant kernel (the TMA/DMMA mode-product kernel): its
+                algorithmic flops per launch / its mean CUDA-event duration,
+                against the fp64 tensor-pipe peak measured live (DMMA probe;
+                MEASURED_PEAKS.json has no fp64 entry).
+* ``cpu_baseline`` the reference library itself (oracle/_ref, compiled from the
+                reference sources) on the host cores, same workload and bytes.
+
+Multi-GPU (torchrun, N>1): the C2 tensor is slab-partitioned over the last
+mode; see paper_2112_11238_b200/dist.py.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Tucker operator fp64 GFLOP/s and % of roofline at 1/2/4/8 B200 vs host CPU"
+UNIT = "GFLOP/s"
+SEED = 1234
+C2 = (256, 256, 256)
+PAPER_C2_GFLOPS = 115.0  # paper Fig. 1, tucker d=3 n=256, MATLAB on i7-8750H
+WORKLOAD = "C2: 3-D Tucker operator fp64, T 256^3 (128 MiB), three 256x256 factors (BASELINE configs[1])"
+
+
+def tucker_flops(m, n):
+    ext, f = list(m), 0.0
+    for mu in range(len(m)):
+        f += 2.0 * n[mu] * float(np.prod(ext))
+        ext[mu] = n[mu]
+    return f
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks line via NVML, sampled every 50 ms during the run."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device: int):
+        self.samples = []
+        self.reasons = 0
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                util = nv.nvmlDeviceGetUtilizationRates(self.h).gpu
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((mhz, util, r))
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self._t:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        loaded = [s for s in self.samples if s[1] > 0] or self.samples
+        bits = 0
+        for s in loaded:
+            bits |= s[2]
+        reasons = [name for bit, name in self.REASONS.items() if bits & bit and bit != 0x1]
+        return {"sm_mhz": statistics.median(s[0] for s in loaded), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(loaded)}
+
+
+# ----------------------------------------------------------------- reference arm
+def run_reference(args, rank: int) -> None:
+    if rank != 0:
+        return
+    import oracle as O
+    from paper_2112_11238_b200 import Rng
+    cores = os.cpu_count() or 1
+    O.ref_lib(threads=cores)
+    g = Rng(SEED)
+    T = g.normal(C2)
+    Ls = [g.normal((256, 256)) for _ in range(3)]
+    flops = tucker_flops(C2, [256, 256, 256])
+    for _ in range(args.warmup):
+        O.ref_tucker(T, Ls)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.ref_tucker(T, Ls)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = flops * args.steps / total / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": round(value / PAPER_C2_GFLOPS, 4), "dtype": "f64",
+        "data": "synthetic (mt19937_64 seed 1234, standard normal, reference draw order)",
+        "config": {"workload": WORKLOAD, "seed": SEED, "parallelism": "host CPU (OpenMP + OpenBLAS)"},
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"ops::tucker 256^3 x {args.steps} steps (full C2 workload per step), "
+                                   f"reference library compiled from /root/reference/proj/src "
+                                   f"(oracle/_ref), OpenBLAS {O.ref_blas_kernel_name()}"},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the C1/C3/C4/C5 side measurements")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2112_11238_b200 as mm
+    from paper_2112_11238_b200 import _lib
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    h = mm.get_handle(local)
+    lib = _lib.lib()
+    stream = torch.cuda.current_stream(dev)
+    h.bind_stream(stream.cuda_stream)
+
+    # ---- inputs (reference draw order), resident in HBM
+    g = mm.Rng(SEED)
+    T_host = g.normal(C2)
+    L_host = [g.normal((256, 256)) for _ in range(3)]
+    T = torch.from_numpy(T_host).to(dev)
+    Ls = [torch.from_numpy(L).to(dev) for L in L_host]
+    m = mm.api._lib.i64_array(C2)
+    n = mm.api._lib.i64_array((256, 256, 256))
+    S = mm.colmajor_empty(C2, torch.float64, dev)
+    Lptr = _lib.ptr_array([L.data_ptr() for L in Ls])
+    flops = tucker_flops(C2, [256, 256, 256])
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        rc = lib.mumode_tucker_f64(h.h, 3, m, n, T.data_ptr(), Lptr, S.data_ptr(), 0)
+        if rc:
+            raise RuntimeError(lib.mumode_last_error().decode())
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: exactly K steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = h.launches
+    for a, b in ev:
+        flush.fill_(1.0)  # evict L2 between steps (outside the events)
+        a.record(stream)
+        step()
+        b.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = h.launches - l0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * flops * args.steps / (total_ms * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel: per-launch events on the same stream
+    mode_ms = []
+    ext = list(C2)
+    bufs = [T, mm.colmajor_empty(C2, torch.float64, dev), mm.colmajor_empty(C2, torch.float64, dev)]
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        src = T
+        for mu in (1, 2, 3):
+            dst = bufs[1 + (mu % 2)]
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            rc = lib.mumode_mode_product_f64(h.h, 3, m, mu, 256, src.data_ptr(), Ls[mu - 1].data_ptr(), dst.data_ptr())
+            b.record(stream)
+            if rc:
+                raise RuntimeError(lib.mumode_last_error().decode())
+            mode_ms.append((a, b))
+            src = dst
+    torch.cuda.synchronize()
+    launch_ms = statistics.mean(a.elapsed_time(b) for a, b in mode_ms)
+    flops_per_launch = 2.0 * 256 * float(np.prod(ext))
+    peak = ctypes_peak(lib, h)
+    achieved_tf = flops_per_launch / (launch_ms * 1e-3) / 1e12
+    clocks.stop()
+
+    # ---- e2e through the host drop-in entry point, pinned buffers
+    Tpin = torch.from_numpy(T_host).pin_memory()
+    Lpin = [torch.from_numpy(L).pin_memory() for L in L_host]
+    Spin = torch.empty(int(np.prod(C2)), dtype=torch.float64).pin_memory()
+    Lhptr = _lib.ptr_array([L.data_ptr() for L in Lpin])
+
+    def e2e_step():
+        rc = lib.mumode_host_tucker_f64(h.h, 3, m, n, Tpin.data_ptr(), Lhptr, Spin.data_ptr(), 0)
+        if rc:
+            raise RuntimeError(lib.mumode_last_error().decode())
+
+    for _ in range(2):
+        e2e_step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * flops * args.steps / e2e_s / 1e9
+    h2d = Tpin.numel() * 8 + sum(L.numel() * 8 for L in Lpin)
+    d2h = Spin.numel() * 8
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    traffic = None
+    prof = ROOT / "profiles" / "roofline_traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": round(value / PAPER_C2_GFLOPS, 3), "dtype": "f64",
+        "data": "synthetic (mt19937_64 seed 1234, standard normal, reference draw order)",
+        "config": {"workload": WORKLOAD, "seed": SEED,
+                   "l2": "flushed between steps (256 MiB write outside the step events)",
+                   "parallelism": "single GPU" if world == 1 else f"replicas x{world}",
+                   "pct_fp64_roofline": round(100.0 * (flops / (peak * 1e12)) / (total_ms * 1e-3 / args.steps), 2),
+                   "vs_baseline_source": "BASELINE.md: paper Fig.1 tucker d=3 n=256, 0.224 s = 115.0 GFLOP/s (MATLAB, i7-8750H)"},
+        "roofline": {"bound": "tensor", "achieved": round(achieved_tf, 3), "peak": round(peak, 3),
+                     "unit": "TFLOP/s", "frac": round(achieved_tf / peak, 4), "traffic": traffic,
+                     "kernel": "modeprod_tma_kernel (TMA 128B-swizzle ring + DMMA.8x8x4)",
+                     "flops_per_launch": flops_per_launch, "mean_launch_ms": round(launch_ms, 5),
+                     "peak_source": "fp64 DMMA probe measured live in this run (mumode_probe_fp64_peak); "
+                                    "MEASURED_PEAKS.json has no fp64 entry"},
+        "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h),
+                "path": "mumode_host_tucker_f64 (host drop-in C-ABI), pinned host buffers"},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(T_host, L_host, flops)
+    if world == 1 and not args.no_extras:
+        line["extras"] = extras(mm, lib, h, dev, stream, peak, flush)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ctypes_peak(lib, h) -> float:
+    import ctypes
+    v = ctypes.c_double()
+    rc = lib.mumode_probe_fp64_peak(h.h, ctypes.byref(v))
+    if rc:
+        raise RuntimeError(lib.mumode_last_error().decode())
+    return float(v.value)
+
+
+def cpu_baseline(T_host, L_host, flops):
+    """The reference library (oracle/_ref) on this box's host cores, same bytes."""
+    try:
+        import oracle as O
+        cores = os.cpu_count() or 1
+        O.ref_lib(threads=cores)
+        reps = 5
+        med, _ = O.ref_time_tucker(T_host, L_host, steps=1, reps=reps)
+        return {"value": round(flops / med / 1e9, 3), "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"ops::tucker on the full C2 workload (256^3), 1 warm-up + median of {reps}; "
+                          f"OMP/OpenBLAS threads = {cores}; OpenBLAS core {O.ref_blas_kernel_name()}",
+                "seconds_per_step": round(med, 4)}
+    except Exception as e:  # reported, never silently replaced
+        return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                "sample": f"unavailable: {e}"}
+
+
+def extras(mm, lib, h, dev, stream, peak, flush):
+    """Side measurements on the other BASELINE configs (device-resident,
+    events, L2 flushed): GFLOP/s and fraction of the fp64 roofline."""
+    import torch
+    out = {}
+
+    def timeit(fn, reps=10):
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1.0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            ts.append((a, b))
+        torch.cuda.synchronize()
+        return statistics.median(a.elapsed_time(b) for a, b in ts)
+
+    def rec(name, flops, ms, bytes_alg):
+        t_roof = max(flops / (peak * 1e12), bytes_alg / 6545.6e9)
+        out[name] = {"ms": round(ms, 4), "gflops": round(flops / ms / 1e6, 2),
+                     "roofline_frac": round(t_roof / (ms * 1e-3), 4)}
+
+    def normal(shape, cplx=False):
+        t = mm.colmajor_empty(shape, torch.complex128 if cplx else torch.float64, dev)
+        return t.normal_()
+
+    # C2 single modes
+    T = normal((256, 256, 256))
+    L = mm.to_colmajor(torch.randn(256, 256, dtype=torch.float64, device=dev))
+    for mu in (1, 2, 3):
+        ms = timeit(lambda: mm.mode_product(T, L, mu))
+        rec(f"C2_mode{mu}", 2.0 * 256 * 256 ** 3, ms, 2 * 8 * 256 ** 3)
+    # C1 2-D
+    T1 = normal((100, 100))
+    L1 = [mm.to_colmajor(torch.randn(100, 100, dtype=torch.float64, device=dev)) for _ in range(2)]
+    ms = timeit(lambda: mm.tucker(T1, L1))
+    rec("C1_2d_n100", tucker_flops((100, 100), (100, 100)), ms, 3 * 8 * 100 * 100 + 8 * 100 * 100)
+    # C3: 100 exponential-integrator steps (one CUDA graph)
+    A = torch.zeros(200, 200, dtype=torch.float64)
+    hh = 1.0 / 201
+    for i in range(200):
+        A[i, i] = -2 / hh ** 2
+        if i > 0:
+            A[i, i - 1] = 1 / hh ** 2 - 0.5 / (2 * hh)
+        if i < 199:
+            A[i, i + 1] = 1 / hh ** 2 + 0.5 / (2 * hh)
+    E = torch.from_numpy(mm.expm((1e-3 * A).numpy())).to(dev)
+    u0 = normal((200, 200, 200))
+    u1 = mm.colmajor_empty((200, 200, 200), torch.float64, dev)
+    ms = timeit(lambda: mm.expint(u0, [E, E, E], 100, out=u1), reps=3)
+    rec("C3_expint_200cube_100steps", 100 * tucker_flops((200,) * 3, (200,) * 3), ms, 100 * 2 * 8 * 200 ** 3)
+    # C4 complex 128^3 -> 192^3
+    Tc = normal((128, 128, 128), True)
+    Lc = [mm.to_colmajor(torch.randn(192, 128, dtype=torch.complex128, device=dev)) for _ in range(3)]
+    ms = timeit(lambda: mm.tucker(Tc, Lc))
+    rec("C4_complex_128_to_192", 4 * tucker_flops((128,) * 3, (192,) * 3), ms, 16 * (128 ** 3 + 192 ** 3))
+    # C5 6-D 24^6
+    del T
+    T5 = normal((24,) * 6)
+    L5 = [mm.to_colmajor(torch.randn(24, 24, dtype=torch.float64, device=dev)) for _ in range(6)]
+    ms = timeit(lambda: mm.tucker(T5, L5), reps=3)
+    rec("C5_6d_24", tucker_flops((24,) * 6, (24,) * 6), ms, 2 * 8 * 24 ** 6)
+    return out
+
+
+if __name__ == "__main__":
+    main()

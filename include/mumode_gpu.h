@@ -119,6 +119,11 @@ int mumode_host_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const d
 int mumode_host_expint_f64(mumode_handle_t h, int d, const int64_t* m, const double* const* E,
                            const double* u0, double* u_out, int steps);
 
+/* ---- diagnostics ------------------------------------------------------ */
+/* FP64 tensor-pipe (DMMA) peak of this GPU at its current clocks, TFLOP/s:
+ * the roofline denominator bench.py reports against. */
+int mumode_probe_fp64_peak(mumode_handle_t h, double* tflops);
+
 /* ---- host preprocessing ---------------------------------------------- */
 /* Matrix exponential, scaling-and-squaring with the degree-13 Pade
  * approximant (Higham 2005), host fp64. Role of la::expm

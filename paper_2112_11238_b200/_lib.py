@@ -43,6 +43,7 @@ SIGNATURES = {
     "mumode_host_tucker_promote": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
     "mumode_host_kronsumv_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, VP, ctypes.POINTER(VP), VP]),
     "mumode_host_expint_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, ctypes.POINTER(VP), VP, VP, ctypes.c_int]),
+    "mumode_probe_fp64_peak": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_double)]),
     "mumode_expm_f64": (ctypes.c_int, [I64, VP, VP]),
     "mumode_rng_create": (ctypes.c_int, [ctypes.POINTER(VP), ctypes.c_uint64]),
     "mumode_rng_destroy": (ctypes.c_int, [VP]),

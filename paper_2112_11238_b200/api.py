@@ -407,9 +407,12 @@ class Rng:
         self.r = r
 
     def __del__(self):
-        if getattr(self, "r", None):
-            _lib.lib().mumode_rng_destroy(self.r)
-            self.r = None
+        try:
+            if getattr(self, "r", None):
+                _lib.lib().mumode_rng_destroy(self.r)
+                self.r = None
+        except Exception:  # interpreter shutdown
+            pass
 
     def normal(self, shape, complex_: bool = False, out: np.ndarray | None = None) -> np.ndarray:
         shape = [int(e) for e in shape]

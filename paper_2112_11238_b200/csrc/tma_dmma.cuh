@@ -16,9 +16,8 @@
 //
 // Shared-memory layout: operands arrive as 16-double (128 B) wide boxes with
 // the TMA 128B swizzle (16-B chunk j of 128-B row r stored at chunk j ^ (r&7)).
-// A k-step's four k rows are taken in the order {0,4,1,5} / {2,6,3,7} of each
-// 8-row group, which makes every fragment load hit each bank exactly twice
-// (two wavefronts for 256 B: conflict-free) in all three operand layouts.
+// Fragment-to-element maps (below) keep every 64-bit fragment load
+// conflict-free (two wavefronts per warp) in all three operand layouts.
 #pragma once
 #include "common.cuh"
 
@@ -51,10 +50,17 @@ struct TmaCfg {
   static_assert(BN <= 256 && BK <= 256, "TMA box extent limit");
 };
 
-// Physical k row (within a stage) of k-step s for lane quad index t.
-__device__ __forceinline__ int krow_of(int s, int t) {
-  return 8 * (s >> 1) + 2 * (s & 1) + (t >> 1) + 4 * (t & 1);
-}
+// Fragment -> element maps (lane = 4*g + t). 64-bit shared loads are served
+// per half-warp, so each half-warp's 16 addresses must land on 16 distinct
+// 8-byte bank slots. With k-step s reading k rows 4s + t:
+//   x-contiguous operands ([k][x] 128B-swizzled rows: P, and Q when QK=false)
+//     fragment pair half h, column g  ->  x = 16*blk + 4h + xmap(g)
+//     xmap(g) = (g&1) + 8((g>>1)&1) + 2(g>>2)     {0,1,8,9,2,3,10,11}
+//   k-contiguous Q ([n][k] rows, QK=true)
+//     fragment pair half h, row g     ->  n = 16*blk + 2g + h
+// Both are bijections onto the 16-wide box and conflict-free for every s, h;
+// xmap(2t), xmap(2t)+1 stay adjacent so the epilogue keeps 16-byte stores.
+__device__ __forceinline__ int xmap(int g) { return (g & 1) + 8 * ((g >> 1) & 1) + 2 * (g >> 2); }
 
 template <class Cfg, bool QK>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
@@ -62,9 +68,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
                         const __grid_constant__ CUtensorMap mapQ, const TmaParams p) {
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
   constexpr int FM = Cfg::FM, FN = Cfg::FN;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  static_assert(FM % 2 == 0 && FN % 2 == 0, "fragments come in 16-wide pairs");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B alignment for the 128B-swizzle atoms, by pointer arithmetic so the
+  // compiler keeps the shared address space (LDS, not generic LD).
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty_bar = full_bar + STAGES;
 
@@ -80,6 +88,23 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   }
   __syncthreads();
 
+  // tile -> (mtile, ntile, batch); the operand tile shared by consecutive
+  // CTAs is the big tensor (Q = T for mode 1: m fastest; P = T_c otherwise:
+  // n fastest), so T streams from HBM once and repeats hit L2.
+  auto decode = [&](int64_t tile, int& mt, int& nt, int64_t& b) {
+    if constexpr (QK) {
+      mt = static_cast<int>(tile % p.mt);
+      const int64_t r = tile / p.mt;
+      nt = static_cast<int>(r % p.nt);
+      b = r / p.nt;
+    } else {
+      nt = static_cast<int>(tile % p.nt);
+      const int64_t r = tile / p.nt;
+      mt = static_cast<int>(r % p.mt);
+      b = r / p.mt;
+    }
+  };
+
   if (warp >= Cfg::MMA_WARPS) {
     // ------------------------------------------------------------ producer
     // 12 warps at launch cap every thread at 168 registers; the producer
@@ -91,10 +116,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-        const int mtile = static_cast<int>(tile % p.mt);
-        const int64_t rest = tile / p.mt;
-        const int ntile = static_cast<int>(rest % p.nt);
-        const int batch = static_cast<int>(rest / p.nt);
+        int mtile, ntile;
+        int64_t batch;
+        decode(tile, mtile, ntile, batch);
         const int m0 = mtile * BM, n0 = ntile * BN;
         for (int kb = 0; kb < KT; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -107,7 +131,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             if constexpr (QK)
               tma_load_2d(sP + b * BK * 128, &mapP, &full_bar[stage], m0 + 16 * b, k0);
             else
-              tma_load_3d(sP + b * BK * 128, &mapP, &full_bar[stage], m0 + 16 * b, k0, batch);
+              tma_load_3d(sP + b * BK * 128, &mapP, &full_bar[stage], m0 + 16 * b, k0,
+                          static_cast<int32_t>(batch));
           }
           if constexpr (QK) {
 #pragma unroll
@@ -134,37 +159,23 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   const int wm = warp % Cfg::WM, wn = warp / Cfg::WM;
   const int mw = wm * Cfg::WTM, nw = wn * Cfg::WTN;
 
-  // Per-fragment byte offsets that do not depend on the k-step.
-  // P sub-tile (16 m) b: rows k (128 B each); chunk index = (m%16)>>1.
-  uint32_t p_off[FM];
-  int p_ch[FM];
-#pragma unroll
-  for (int fm = 0; fm < FM; ++fm) {
-    const int m = mw + fm * 8 + g;
-    p_off[fm] = (m >> 4) * (BK * 128) + ((m & 1) << 3);
-    p_ch[fm] = (m & 15) >> 1;
-  }
-  uint32_t q_off[FN];
-  int q_ch[FN];
-#pragma unroll
-  for (int fn = 0; fn < FN; ++fn) {
-    const int n = nw + fn * 8 + g;
-    if constexpr (QK) {
-      q_off[fn] = n * 128;  // row n of each 16-k sub-tile
-      q_ch[fn] = n & 7;     // swizzle key of row n
-    } else {
-      q_off[fn] = (n >> 4) * (BK * 128) + ((n & 1) << 3);
-      q_ch[fn] = (n & 15) >> 1;
-    }
-  }
+  // Per-thread byte offsets inside a stage. x-contiguous operand, element
+  // (x = 16*blk + 4h + xmap(g), k = 4s + t): blk*BK*128 + k*128 + chunk*16 + (g&1)*8
+  // with chunk = (j ^ (k&7)), j = 4((g>>1)&1) + (g>>2) + 2h, so
+  // chunk*16 = ((j0 ^ t) << 4) ^ (2h << 4) ^ ((4(s&1)) << 4).
+  const uint32_t jx = static_cast<uint32_t>((4 * ((g >> 1) & 1) + (g >> 2)) ^ t) << 4;
+  const uint32_t xoff = static_cast<uint32_t>(t * 128 + (g & 1) * 8);
+  // k-contiguous Q, element (n = 16*blk + 2g + h, k = 4s + t):
+  // n*128 + (((2s + (t>>1)) ^ (n&7)) << 4) + (t&1)*8.
+  const uint32_t jq = static_cast<uint32_t>(((t >> 1) ^ ((2 * g) & 7))) << 4;
+  const uint32_t qoff = static_cast<uint32_t>(2 * g * 128 + (t & 1) * 8);
 
   int stage = 0;
   uint32_t phase = 0;
   for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-    const int mtile = static_cast<int>(tile % p.mt);
-    const int64_t rest = tile / p.mt;
-    const int ntile = static_cast<int>(rest % p.nt);
-    const int64_t batch = rest / p.nt;
+    int mtile, ntile;
+    int64_t batch;
+    decode(tile, mtile, ntile, batch);
 
     double acc[FM][FN][2];
 #pragma unroll
@@ -178,23 +189,26 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       const uint8_t* sQ = sP + Cfg::P_BYTES;
 #pragma unroll
       for (int s = 0; s < BK / 4; ++s) {
-        const int kr = krow_of(s, t);  // 0..BK-1
-        const int kx = kr & 7;
         double pf[FM], qf[FN];
 #pragma unroll
-        for (int fm = 0; fm < FM; ++fm)
-          pf[fm] = *reinterpret_cast<const double*>(sP + p_off[fm] + kr * 128 +
-                                                    ((p_ch[fm] ^ kx) << 4));
+        for (int fm = 0; fm < FM; ++fm) {
+          const int blk = (mw >> 4) + (fm >> 1), h = fm & 1;
+          const uint32_t ch = jx ^ (static_cast<uint32_t>(2 * h) << 4) ^
+                              (static_cast<uint32_t>(4 * (s & 1)) << 4);
+          pf[fm] = *reinterpret_cast<const double*>(sP + blk * (BK * 128) + (4 * s) * 128 + xoff + ch);
+        }
 #pragma unroll
         for (int fn = 0; fn < FN; ++fn) {
+          const int blk = (nw >> 4) + (fn >> 1), h = fn & 1;
           if constexpr (QK) {
-            const int kk = kr & 15;
-            qf[fn] = *reinterpret_cast<const double*>(
-                sQ + (kr >> 4) * (BN * 128) + q_off[fn] + ((((kk >> 1) ^ q_ch[fn])) << 4) +
-                ((kk & 1) << 3));
+            const int kb16 = (4 * s) >> 4, s4 = s & 3;
+            const uint32_t ch = jq ^ (static_cast<uint32_t>((2 * s4) ^ h) << 4);
+            qf[fn] = *reinterpret_cast<const double*>(sQ + kb16 * (BN * 128) + (16 * blk + h) * 128 +
+                                                      qoff + ch);
           } else {
-            qf[fn] = *reinterpret_cast<const double*>(sQ + q_off[fn] + kr * 128 +
-                                                      ((q_ch[fn] ^ kx) << 4));
+            const uint32_t ch = jx ^ (static_cast<uint32_t>(2 * h) << 4) ^
+                                (static_cast<uint32_t>(4 * (s & 1)) << 4);
+            qf[fn] = *reinterpret_cast<const double*>(sQ + blk * (BK * 128) + (4 * s) * 128 + xoff + ch);
           }
         }
 #pragma unroll
@@ -210,18 +224,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       }
     }
 
-    // epilogue: D(m, m+1 ; n) from registers, 16-B stores along M
+    // epilogue: D(m, m+1 ; n) straight from registers, 16-byte stores along M
     double* Db = p.D + batch * p.bstride;
-    const int mbase = mtile * BM + mw + 2 * t;
-    const int nbase = ntile * BN + nw + g;
+    const int mrow = mtile * BM + mw + 8 * (t & 1) + 2 * (t >> 1);
 #pragma unroll
     for (int fn = 0; fn < FN; ++fn) {
-      const int n = nbase + fn * 8;
+      const int blk = (nw >> 4) + (fn >> 1), h = fn & 1;
+      const int n = ntile * BN + 16 * blk + (QK ? (2 * g + h) : (4 * h + xmap(g)));
       if (n >= p.N) continue;
       double* col = Db + static_cast<int64_t>(n) * p.ldD;
 #pragma unroll
       for (int fm = 0; fm < FM; ++fm) {
-        const int m = mbase + fm * 8;
+        const int m = mrow + 16 * (fm >> 1) + 4 * (fm & 1);
         if (m < p.M) stg_f64x2(col + m, acc[fm][fn][0], acc[fm][fn][1]);
       }
     }
