@@ -65,7 +65,8 @@ const char* mumode_version(void);
 int64_t mumode_launch_count(mumode_handle_t h);
 /* Kernel path selection for tests/benchmarks: 0 = auto (default),
  * 1 = force the generic SIMT kernel, 2 = force the TMA/DMMA kernel where the
- * shape allows it. Not a fallback switch: both are CUDA kernels. */
+ * shape allows it (tile shape by cost model), 3..6 = TMA/DMMA kernel with tile
+ * configuration 0..3 forced. Not a fallback switch: all are CUDA kernels. */
 int mumode_set_kernel_policy(mumode_handle_t h, int policy);
 
 /* ---- device-resident operators --------------------------------------- */

@@ -73,7 +73,7 @@ struct DevBuf {
   }
 };
 
-using MapKey = std::tuple<const void*, int, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, int, int, int>;
+using MapKey = std::vector<uint64_t>;  // base, rank, dims, strides, box
 
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
@@ -113,19 +113,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// fp64 tiled map with 128B swizzle. dims/strides in elements (dim0 contiguous).
+// fp64 tiled map with 64B swizzle (8-double boxes). dims/strides in elements (dim0 contiguous).
 static int get_map(mumode_handle_s* h, const void* base, int rank, const uint64_t* dims,
                    const uint64_t* strides_el, const uint32_t* box, const CUtensorMap** out) {
-  MapKey key{base,
-             rank,
-             dims[0],
-             rank > 1 ? dims[1] : 0,
-             rank > 2 ? dims[2] : 0,
-             rank > 1 ? strides_el[0] : 0,
-             rank > 2 ? strides_el[1] : 0,
-             static_cast<int>(box[0]),
-             rank > 1 ? static_cast<int>(box[1]) : 0,
-             rank > 2 ? static_cast<int>(box[2]) : 0};
+  MapKey key{reinterpret_cast<uint64_t>(base), uint64_t(rank)};
+  for (int r = 0; r < rank; ++r) key.push_back(dims[r]);
+  for (int r = 0; r + 1 < rank; ++r) key.push_back(strides_el[r]);
+  for (int r = 0; r < rank; ++r) key.push_back(box[r]);
   auto it = h->maps.find(key);
   if (it != h->maps.end()) {
     *out = &it->second;
@@ -145,7 +139,7 @@ static int get_map(mumode_handle_s* h, const void* base, int rank, const uint64_
   for (int r = 0; r + 1 < rank; ++r) gstride[r] = strides_el[r] * sizeof(double);
   CUresult res = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), gdim,
                     gstride, bdim, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (res != CUDA_SUCCESS)
     return fail(MUMODE_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(res) + ")");
@@ -221,12 +215,16 @@ struct ModeJob {
   bool conj;
 };
 
-using CfgBig = TmaCfg<128, 128, 16, 4, 2, 4>;
+// Compiled tile configurations (BM, BN, BK, stages, warps along M, along N).
+using CfgBig = TmaCfg<128, 128, 16, 4, 2, 4>;  // 64x32 warp tiles (C2-class shapes)
+using CfgTM = TmaCfg<128, 40, 40, 3, 8, 1>;    // T-side M, small L-side N (n = 40k)
+using CfgLM = TmaCfg<40, 128, 40, 3, 1, 8>;    // small L-side M, T-side N (mode 1, n = 40k)
+using CfgMid = TmaCfg<64, 128, 32, 4, 2, 4>;   // 32x32 warp tiles
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // Can the TMA/DMMA kernel describe this job? (16-byte strides and bases,
-// forward layout of L, real, M even, sizes within int32 coordinates.)
+// forward layout of L, real, even M, sizes within int32 coordinates.)
 static bool tma_ok(const ModeJob& j) {
   if (j.cplx || j.conj) return false;
   if (j.sLi != 1) return false;  // L must be used forward: op(L) = L, ld = N
@@ -238,13 +236,46 @@ static bool tma_ok(const ModeJob& j) {
     if (j.N % 2 || j.K % 2) return false;
   } else {
     if (j.A % 2) return false;
+    if ((j.A + 7) / 8 * j.C >= lim) return false;
   }
   return true;
 }
 
 static bool tma_worthwhile(const ModeJob& j) {
   const int64_t M = (j.A == 1) ? j.N : j.A;
-  return M >= 32 && j.K >= 16 && ((j.A == 1) ? j.C : j.N) >= 32;
+  return M >= 16 && j.K >= 16 && ((j.A == 1) ? j.C : j.N) >= 16;
+}
+
+struct TileChoice {
+  int cfg;  // 0 Big, 1 TM, 2 LM, 3 Mid
+  double cost;
+};
+
+// Wave-quantised padded work: waves * (BM * BN * K_padded) / efficiency.
+template <class Cfg>
+static double tile_cost(int64_t mfrags, int64_t N, int64_t K, int sms, double eff) {
+  const int64_t mt = (mfrags + Cfg::BM / 8 - 1) / (Cfg::BM / 8);
+  const int64_t nt = (N + Cfg::BN - 1) / Cfg::BN;
+  const int64_t tiles = mt * nt;
+  const int64_t waves = (tiles + sms - 1) / sms;
+  const int64_t kp = (K + Cfg::BK - 1) / Cfg::BK * Cfg::BK;
+  return double(waves) * double(Cfg::BM) * double(Cfg::BN) * double(kp) / eff;
+}
+
+static int choose_cfg(const ModeJob& j, int sms) {
+  const bool mode1 = (j.A == 1);
+  const int64_t mfrags = mode1 ? (j.N + 7) / 8 : (j.A + 7) / 8 * j.C;
+  const int64_t N = mode1 ? j.C : j.N;
+  const double c0 = tile_cost<CfgBig>(mfrags, N, j.K, sms, 1.00);
+  const double c1 = tile_cost<CfgTM>(mfrags, N, j.K, sms, 0.96);
+  const double c2 = tile_cost<CfgLM>(mfrags, N, j.K, sms, 0.96);
+  const double c3 = tile_cost<CfgMid>(mfrags, N, j.K, sms, 0.97);
+  int best = 0;
+  double bc = c0;
+  if (c1 < bc) best = 1, bc = c1;
+  if (c2 < bc) best = 2, bc = c2;
+  if (c3 < bc) best = 3, bc = c3;
+  return best;
 }
 
 template <class Cfg>
@@ -254,39 +285,71 @@ static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
   TmaParams p{};
   p.D = j.S;
   const bool mode1 = (j.A == 1);
+  constexpr uint32_t BM8 = Cfg::BM / 8, BN8 = Cfg::BN / 8, BK8 = Cfg::BK / 8;
   if (mode1) {
-    // P = L: dims {N_out (contig), K}, ld = sLk; Q = T: dims {K (contig), C}
-    uint64_t dP[2] = {uint64_t(j.N), uint64_t(j.K)}, sP[1] = {uint64_t(j.sLk)};
-    uint32_t bP[2] = {16, Cfg::BK};
-    MM_TRY(get_map(h, j.L, 2, dP, sP, bP, &mp));
-    uint64_t dQ[2] = {uint64_t(j.K), uint64_t(j.C)}, sQ[1] = {uint64_t(j.K)};
-    uint32_t bQ[2] = {16, Cfg::BN};
-    MM_TRY(get_map(h, j.T, 2, dQ, sQ, bQ, &mq));
-    p.M = int(j.N);
+    // P = L (n_out x K, ld = sLk), Q = T (K x C, K contiguous)
+    p.p_blocked = (j.N % 8 == 0);
+    if (p.p_blocked) {
+      uint64_t d[3] = {8, uint64_t(j.K), uint64_t(j.N / 8)}, st[2] = {uint64_t(j.sLk), 8};
+      uint32_t b[3] = {8, Cfg::BK, BM8};
+      MM_TRY(get_map(h, j.L, 3, d, st, b, &mp));
+    } else {
+      uint64_t d[2] = {uint64_t(j.N), uint64_t(j.K)}, st[1] = {uint64_t(j.sLk)};
+      uint32_t b[2] = {8, Cfg::BK};
+      MM_TRY(get_map(h, j.L, 2, d, st, b, &mp));
+    }
+    p.q_blocked = (j.K % 8 == 0);
+    if (p.q_blocked) {
+      uint64_t d[3] = {8, uint64_t(j.C), uint64_t(j.K / 8)}, st[2] = {uint64_t(j.K), 8};
+      uint32_t b[3] = {8, Cfg::BN, BK8};
+      MM_TRY(get_map(h, j.T, 3, d, st, b, &mq));
+    } else {
+      uint64_t d[2] = {uint64_t(j.K), uint64_t(j.C)}, st[1] = {uint64_t(j.K)};
+      uint32_t b[2] = {8, Cfg::BN};
+      MM_TRY(get_map(h, j.T, 2, d, st, b, &mq));
+    }
+    p.Mlim = int(j.N);
     p.N = int(j.C);
     p.ldD = j.N;
     p.bstride = 0;
-    p.mt = (p.M + Cfg::BM - 1) / Cfg::BM;
-    p.nt = (p.N + Cfg::BN - 1) / Cfg::BN;
-    p.tiles = int64_t(p.mt) * p.nt;
+    p.AB = int((j.N + 7) / 8);
+    p.mfrags = p.AB;
   } else {
-    // P = T: dims {A (contig), K, C}; Q = L: dims {N_out (contig), K}
-    uint64_t dP[3] = {uint64_t(j.A), uint64_t(j.K), uint64_t(j.C)};
-    uint64_t sP[2] = {uint64_t(j.A), uint64_t(j.A * j.K)};
-    uint32_t bP[3] = {16, Cfg::BK, 1};
-    MM_TRY(get_map(h, j.T, 3, dP, sP, bP, &mp));
-    uint64_t dQ[2] = {uint64_t(j.N), uint64_t(j.K)}, sQ[1] = {uint64_t(j.sLk)};
-    uint32_t bQ[2] = {16, Cfg::BK};
-    MM_TRY(get_map(h, j.L, 2, dQ, sQ, bQ, &mq));
-    p.M = int(j.A);
+    // P = T (A x K x C, A contiguous), Q = L (n_out x K, ld = sLk)
+    const int64_t AB = (j.A + 7) / 8;
+    p.p_blocked = (j.A % 8 == 0) && (AB % BM8 == 0);
+    if (p.p_blocked) {
+      uint64_t d[4] = {8, uint64_t(j.K), uint64_t(AB), uint64_t(j.C)};
+      uint64_t st[3] = {uint64_t(j.A), 8, uint64_t(j.A * j.K)};
+      uint32_t b[4] = {8, Cfg::BK, BM8, 1};
+      MM_TRY(get_map(h, j.T, 4, d, st, b, &mp));
+    } else {
+      uint64_t d[3] = {uint64_t(j.A), uint64_t(j.K), uint64_t(j.C)};
+      uint64_t st[2] = {uint64_t(j.A), uint64_t(j.A * j.K)};
+      uint32_t b[3] = {8, Cfg::BK, 1};
+      MM_TRY(get_map(h, j.T, 3, d, st, b, &mp));
+    }
+    p.q_blocked = (j.N % 8 == 0);
+    if (p.q_blocked) {
+      uint64_t d[3] = {8, uint64_t(j.K), uint64_t(j.N / 8)}, st[2] = {uint64_t(j.sLk), 8};
+      uint32_t b[3] = {8, Cfg::BK, BN8};
+      MM_TRY(get_map(h, j.L, 3, d, st, b, &mq));
+    } else {
+      uint64_t d[2] = {uint64_t(j.N), uint64_t(j.K)}, st[1] = {uint64_t(j.sLk)};
+      uint32_t b[2] = {8, Cfg::BK};
+      MM_TRY(get_map(h, j.L, 2, d, st, b, &mq));
+    }
+    p.Mlim = int(j.A);
     p.N = int(j.N);
     p.ldD = j.A;
     p.bstride = j.A * j.N;
-    p.mt = (p.M + Cfg::BM - 1) / Cfg::BM;
-    p.nt = (p.N + Cfg::BN - 1) / Cfg::BN;
-    p.tiles = int64_t(p.mt) * p.nt * j.C;
+    p.AB = int(AB);
+    p.mfrags = AB * j.C;
   }
   p.K = int(j.K);
+  p.mt = int((p.mfrags + Cfg::BM / 8 - 1) / (Cfg::BM / 8));
+  p.nt = (p.N + Cfg::BN - 1) / Cfg::BN;
+  p.tiles = int64_t(p.mt) * p.nt;
   const int grid = static_cast<int>(p.tiles < h->num_sms ? p.tiles : h->num_sms);
   if (mode1) {
     auto k = modeprod_tma_kernel<Cfg, true>;
@@ -300,6 +363,16 @@ static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
   MM_CUDA(cudaGetLastError());
   h->launches++;
   return MUMODE_OK;
+}
+
+static int launch_tma_auto(mumode_handle_s* h, const ModeJob& j) {
+  const int forced = h->policy >= 3 ? h->policy - 3 : -1;
+  switch (forced >= 0 ? forced : choose_cfg(j, h->num_sms)) {
+    case 1: return launch_tma<CfgTM>(h, j);
+    case 2: return launch_tma<CfgLM>(h, j);
+    case 3: return launch_tma<CfgMid>(h, j);
+    default: return launch_tma<CfgBig>(h, j);
+  }
 }
 
 static int launch_generic(mumode_handle_s* h, const ModeJob& j) {
@@ -320,7 +393,7 @@ static int launch_generic(mumode_handle_s* h, const ModeJob& j) {
 static int run_job(mumode_handle_s* h, const ModeJob& j) {
   const bool can_tma = tma_ok(j);
   if (h->policy == 1 || !can_tma) return launch_generic(h, j);
-  if (h->policy == 2 || tma_worthwhile(j)) return launch_tma<CfgBig>(h, j);
+  if (h->policy >= 2 || tma_worthwhile(j)) return launch_tma_auto(h, j);
   return launch_generic(h, j);
 }
 
@@ -469,7 +542,7 @@ void* mumode_get_stream(mumode_handle_t h) { return h ? static_cast<void*>(h->st
 int64_t mumode_launch_count(mumode_handle_t h) { return h ? h->launches : -1; }
 
 int mumode_set_kernel_policy(mumode_handle_t h, int policy) {
-  if (!h || policy < 0 || policy > 2) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
+  if (!h || policy < 0 || policy > 6) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
   h->policy = policy;
   return MUMODE_OK;
 }

@@ -40,7 +40,7 @@ def _require_gpu():
         pytest.fail("GPU test run without a GPU")
 
 
-@pytest.fixture(params=[0, 1, 2], ids=["auto", "generic", "tma"])
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6], ids=["auto", "generic", "tma", "tma_big", "tma_tm", "tma_lm", "tma_mid"])
 def policy(request):
     h = mm.get_handle(0)
     h.set_kernel_policy(request.param)
