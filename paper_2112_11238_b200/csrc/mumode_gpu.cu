@@ -113,10 +113,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// fp64 tiled map with 64B swizzle (8-double boxes). dims/strides in elements (dim0 contiguous).
+// fp64-typed tiled map (dims/strides in doubles); 64B swizzle for 8-double
+// boxes (real), 128B swizzle for 16-double boxes (8 complex). dims/strides in elements (dim0 contiguous).
 static int get_map(mumode_handle_s* h, const void* base, int rank, const uint64_t* dims,
-                   const uint64_t* strides_el, const uint32_t* box, const CUtensorMap** out) {
-  MapKey key{reinterpret_cast<uint64_t>(base), uint64_t(rank)};
+                   const uint64_t* strides_el, const uint32_t* box, const CUtensorMap** out,
+                   bool swz128 = false) {
+  MapKey key{reinterpret_cast<uint64_t>(base), uint64_t(rank), uint64_t(swz128)};
   for (int r = 0; r < rank; ++r) key.push_back(dims[r]);
   for (int r = 0; r + 1 < rank; ++r) key.push_back(strides_el[r]);
   for (int r = 0; r < rank; ++r) key.push_back(box[r]);
@@ -139,7 +141,8 @@ static int get_map(mumode_handle_s* h, const void* base, int rank, const uint64_
   for (int r = 0; r + 1 < rank; ++r) gstride[r] = strides_el[r] * sizeof(double);
   CUresult res = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), gdim,
                     gstride, bdim, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (res != CUDA_SUCCESS)
     return fail(MUMODE_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(res) + ")");
@@ -220,13 +223,23 @@ using CfgBig = TmaCfg<128, 128, 16, 4, 2, 4>;  // 64x32 warp tiles (C2-class sha
 using CfgTM = TmaCfg<128, 40, 40, 3, 8, 1>;    // T-side M, small L-side N (n = 40k)
 using CfgLM = TmaCfg<40, 128, 40, 3, 1, 8>;    // small L-side M, T-side N (mode 1, n = 40k)
 using CfgMid = TmaCfg<64, 128, 32, 4, 2, 4>;   // 32x32 warp tiles
+// complex128 (E = 2): 4 real DMMAs per complex MAC, 16-B elements
+using CfgCa = TmaCfg<64, 128, 16, 4, 2, 4, 2>;  // 32x32 complex warp tiles
+using CfgCb = TmaCfg<128, 64, 16, 4, 4, 2, 2>;
+using CfgCc = TmaCfg<96, 32, 16, 4, 4, 2, 2>;   // 24x16 warp tiles, fine-grained
+using CfgCd = TmaCfg<192, 16, 16, 4, 8, 1, 2>;
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // Can the TMA/DMMA kernel describe this job? (16-byte strides and bases,
 // forward layout of L, real, even M, sizes within int32 coordinates.)
 static bool tma_ok(const ModeJob& j) {
-  if (j.cplx || j.conj) return false;
+  if (j.conj) return false;
+  if (j.cplx) {  // 16-byte elements: every stride is 16-B aligned
+    if (j.sLi != 1 || !aligned16(j.T) || !aligned16(j.L) || !aligned16(j.S)) return false;
+    const int64_t lim = int64_t(1) << 30;
+    return j.N < lim && j.K < lim && j.C < lim && j.A < lim && (j.A + 7) / 8 * j.C < lim;
+  }
   if (j.sLi != 1) return false;  // L must be used forward: op(L) = L, ld = N
   if (!aligned16(j.T) || !aligned16(j.L) || !aligned16(j.S)) return false;
   if (j.sLk % 2) return false;
@@ -266,6 +279,16 @@ static int choose_cfg(const ModeJob& j, int sms) {
   const bool mode1 = (j.A == 1);
   const int64_t mfrags = mode1 ? (j.N + 7) / 8 : (j.A + 7) / 8 * j.C;
   const int64_t N = mode1 ? j.C : j.N;
+  if (j.cplx) {
+    const double c[4] = {tile_cost<CfgCa>(mfrags, N, j.K, sms, 1.00),
+                         tile_cost<CfgCb>(mfrags, N, j.K, sms, 1.00),
+                         tile_cost<CfgCc>(mfrags, N, j.K, sms, 0.97),
+                         tile_cost<CfgCd>(mfrags, N, j.K, sms, 0.96)};
+    int best = 0;
+    for (int i = 1; i < 4; ++i)
+      if (c[i] < c[best]) best = i;
+    return 4 + best;
+  }
   const double c0 = tile_cost<CfgBig>(mfrags, N, j.K, sms, 1.00);
   const double c1 = tile_cost<CfgTM>(mfrags, N, j.K, sms, 0.96);
   const double c2 = tile_cost<CfgLM>(mfrags, N, j.K, sms, 0.96);
@@ -286,27 +309,31 @@ static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
   p.D = j.S;
   const bool mode1 = (j.A == 1);
   constexpr uint32_t BM8 = Cfg::BM / 8, BN8 = Cfg::BN / 8, BK8 = Cfg::BK / 8;
+  // all map dims/strides in doubles: e doubles per element, 8e per box row
+  constexpr uint64_t e = Cfg::E;
+  constexpr uint32_t box0 = 8 * Cfg::E;
+  constexpr bool sw = (Cfg::E == 2);
   if (mode1) {
     // P = L (n_out x K, ld = sLk), Q = T (K x C, K contiguous)
     p.p_blocked = (j.N % 8 == 0);
     if (p.p_blocked) {
-      uint64_t d[3] = {8, uint64_t(j.K), uint64_t(j.N / 8)}, st[2] = {uint64_t(j.sLk), 8};
-      uint32_t b[3] = {8, Cfg::BK, BM8};
-      MM_TRY(get_map(h, j.L, 3, d, st, b, &mp));
+      uint64_t d[3] = {box0, uint64_t(j.K), uint64_t(j.N / 8)}, st[2] = {e * uint64_t(j.sLk), 8 * e};
+      uint32_t b[3] = {box0, Cfg::BK, BM8};
+      MM_TRY(get_map(h, j.L, 3, d, st, b, &mp, sw));
     } else {
-      uint64_t d[2] = {uint64_t(j.N), uint64_t(j.K)}, st[1] = {uint64_t(j.sLk)};
-      uint32_t b[2] = {8, Cfg::BK};
-      MM_TRY(get_map(h, j.L, 2, d, st, b, &mp));
+      uint64_t d[2] = {e * uint64_t(j.N), uint64_t(j.K)}, st[1] = {e * uint64_t(j.sLk)};
+      uint32_t b[2] = {box0, Cfg::BK};
+      MM_TRY(get_map(h, j.L, 2, d, st, b, &mp, sw));
     }
     p.q_blocked = (j.K % 8 == 0);
     if (p.q_blocked) {
-      uint64_t d[3] = {8, uint64_t(j.C), uint64_t(j.K / 8)}, st[2] = {uint64_t(j.K), 8};
-      uint32_t b[3] = {8, Cfg::BN, BK8};
-      MM_TRY(get_map(h, j.T, 3, d, st, b, &mq));
+      uint64_t d[3] = {box0, uint64_t(j.C), uint64_t(j.K / 8)}, st[2] = {e * uint64_t(j.K), 8 * e};
+      uint32_t b[3] = {box0, Cfg::BN, BK8};
+      MM_TRY(get_map(h, j.T, 3, d, st, b, &mq, sw));
     } else {
-      uint64_t d[2] = {uint64_t(j.K), uint64_t(j.C)}, st[1] = {uint64_t(j.K)};
-      uint32_t b[2] = {8, Cfg::BN};
-      MM_TRY(get_map(h, j.T, 2, d, st, b, &mq));
+      uint64_t d[2] = {e * uint64_t(j.K), uint64_t(j.C)}, st[1] = {e * uint64_t(j.K)};
+      uint32_t b[2] = {box0, Cfg::BN};
+      MM_TRY(get_map(h, j.T, 2, d, st, b, &mq, sw));
     }
     p.Mlim = int(j.N);
     p.N = int(j.C);
@@ -319,25 +346,25 @@ static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
     const int64_t AB = (j.A + 7) / 8;
     p.p_blocked = (j.A % 8 == 0) && (AB % BM8 == 0);
     if (p.p_blocked) {
-      uint64_t d[4] = {8, uint64_t(j.K), uint64_t(AB), uint64_t(j.C)};
-      uint64_t st[3] = {uint64_t(j.A), 8, uint64_t(j.A * j.K)};
-      uint32_t b[4] = {8, Cfg::BK, BM8, 1};
-      MM_TRY(get_map(h, j.T, 4, d, st, b, &mp));
+      uint64_t d[4] = {box0, uint64_t(j.K), uint64_t(AB), uint64_t(j.C)};
+      uint64_t st[3] = {e * uint64_t(j.A), 8 * e, e * uint64_t(j.A * j.K)};
+      uint32_t b[4] = {box0, Cfg::BK, BM8, 1};
+      MM_TRY(get_map(h, j.T, 4, d, st, b, &mp, sw));
     } else {
-      uint64_t d[3] = {uint64_t(j.A), uint64_t(j.K), uint64_t(j.C)};
-      uint64_t st[2] = {uint64_t(j.A), uint64_t(j.A * j.K)};
-      uint32_t b[3] = {8, Cfg::BK, 1};
-      MM_TRY(get_map(h, j.T, 3, d, st, b, &mp));
+      uint64_t d[3] = {e * uint64_t(j.A), uint64_t(j.K), uint64_t(j.C)};
+      uint64_t st[2] = {e * uint64_t(j.A), e * uint64_t(j.A * j.K)};
+      uint32_t b[3] = {box0, Cfg::BK, 1};
+      MM_TRY(get_map(h, j.T, 3, d, st, b, &mp, sw));
     }
     p.q_blocked = (j.N % 8 == 0);
     if (p.q_blocked) {
-      uint64_t d[3] = {8, uint64_t(j.K), uint64_t(j.N / 8)}, st[2] = {uint64_t(j.sLk), 8};
-      uint32_t b[3] = {8, Cfg::BK, BN8};
-      MM_TRY(get_map(h, j.L, 3, d, st, b, &mq));
+      uint64_t d[3] = {box0, uint64_t(j.K), uint64_t(j.N / 8)}, st[2] = {e * uint64_t(j.sLk), 8 * e};
+      uint32_t b[3] = {box0, Cfg::BK, BN8};
+      MM_TRY(get_map(h, j.L, 3, d, st, b, &mq, sw));
     } else {
-      uint64_t d[2] = {uint64_t(j.N), uint64_t(j.K)}, st[1] = {uint64_t(j.sLk)};
-      uint32_t b[2] = {8, Cfg::BK};
-      MM_TRY(get_map(h, j.L, 2, d, st, b, &mq));
+      uint64_t d[2] = {e * uint64_t(j.N), uint64_t(j.K)}, st[1] = {e * uint64_t(j.sLk)};
+      uint32_t b[2] = {box0, Cfg::BK};
+      MM_TRY(get_map(h, j.L, 2, d, st, b, &mq, sw));
     }
     p.Mlim = int(j.A);
     p.N = int(j.N);
@@ -367,10 +394,16 @@ static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
 
 static int launch_tma_auto(mumode_handle_s* h, const ModeJob& j) {
   const int forced = h->policy >= 3 ? h->policy - 3 : -1;
-  switch (forced >= 0 ? forced : choose_cfg(j, h->num_sms)) {
+  int cfg = choose_cfg(j, h->num_sms);
+  if (forced >= 0) cfg = j.cplx ? 4 + forced : forced;
+  switch (cfg) {
     case 1: return launch_tma<CfgTM>(h, j);
     case 2: return launch_tma<CfgLM>(h, j);
     case 3: return launch_tma<CfgMid>(h, j);
+    case 4: return launch_tma<CfgCa>(h, j);
+    case 5: return launch_tma<CfgCb>(h, j);
+    case 6: return launch_tma<CfgCc>(h, j);
+    case 7: return launch_tma<CfgCd>(h, j);
     default: return launch_tma<CfgBig>(h, j);
   }
 }
@@ -543,6 +576,7 @@ int64_t mumode_launch_count(mumode_handle_t h) { return h ? h->launches : -1; }
 
 int mumode_set_kernel_policy(mumode_handle_t h, int policy) {
   if (!h || policy < 0 || policy > 6) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
+  // 3..6 force real tile configuration 0..3 / complex configuration 0..3
   h->policy = policy;
   return MUMODE_OK;
 }

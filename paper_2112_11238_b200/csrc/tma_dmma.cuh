@@ -1,9 +1,9 @@
 // Persistent, warp-specialised mu-mode product kernel for sm_100a:
-// TMA (cp.async.bulk.tensor, 64B swizzle) stages operand slabs into a
-// multi-stage shared-memory ring guarded by mbarriers; eight consumer warps
-// run fp64 tensor-core MMAs (mma.sync m8n8k4 -> SASS DMMA.8x8x4: the only
-// fp64 tensor-core path on sm_100a, tcgen05 has no f64 kind) and store
-// straight from registers.
+// TMA (cp.async.bulk.tensor) stages operand slabs into a multi-stage
+// shared-memory ring guarded by mbarriers; eight consumer warps run fp64
+// tensor-core MMAs (mma.sync m8n8k4 -> SASS DMMA.8x8x4: the only fp64
+// tensor-core path on sm_100a, tcgen05 has no f64 kind) and store straight
+// from registers. Real fp64 and complex128 share the pipeline.
 //
 // Every mu-mode product is cast as D(M x N) [+ batch] = P(M x K) * Q(K x N)
 // with D and P contiguous along M (column-major):
@@ -14,8 +14,10 @@
 // so interior modes are contracted in place: the permute -> GEMM -> ipermute
 // of the reference (mode_product.hpp:73-76, tucker.hpp:96-107) never happens.
 //
-// Tiles have 8-element granularity in M, N and K (8-wide TMA boxes), so
-// extents like 200 (config C3) tile without padding.
+// Tiles have 8-element granularity in M, N and K (8-element-wide TMA boxes),
+// so extents like 200 (config C3) or 192 (C4) tile without padding, and for
+// mu > 1 the M dimension runs over a list of 8-row fragments (a-block, c) so
+// batches never pad either.
 #pragma once
 #include "common.cuh"
 
@@ -32,56 +34,68 @@ struct TmaParams {
   int mt, nt;       // tile counts along the M-fragment list and along N
   int64_t tiles;    // mt * nt
   // Blocked views: the whole operand tile is ONE TMA box per stage
-  //   P blocked: mode 1 {8, K, n/8} box {8, BK, BM/8};
-  //              mode >1 {8, K, A/8, C} box {8, BK, BM/8, 1} (tiles never straddle c)
-  //   Q blocked: mode 1 {8, C, K/8} box {8, BN, BK/8}; mode >1 {8, K, n/8} box {8, BK, BN/8}
+  //   P blocked: mode 1 {8e, K, n/8} box {8e, BK, BM/8};
+  //              mode >1 {8e, K, A/8, C} box {8e, BK, BM/8, 1} (tiles never straddle c)
+  //   Q blocked: mode 1 {8e, C, K/8} box {8e, BN, BK/8}; mode >1 {8e, K, n/8} box {8e, BK, BN/8}
+  // (e = doubles per element). Otherwise one box per 8-element block.
   int p_blocked, q_blocked;
 };
 
-template <int BM_, int BN_, int BK_, int STAGES_, int WM_, int WN_>
+// E = doubles per element (1: fp64, 2: complex128). A staged row of 8
+// elements is 64 B (fp64, 64B swizzle) or 128 B (complex, 128B swizzle).
+template <int BM_, int BN_, int BK_, int STAGES_, int WM_, int WN_, int E_ = 1>
 struct TmaCfg {
-  static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_, WM = WM_, WN = WN_;
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_, WM = WM_, WN = WN_, E = E_;
+  static constexpr int ROW = 64 * E;  // bytes of one staged 8-element row
   static constexpr int MMA_WARPS = WM * WN;
   // MMA warps + one producer warpgroup (setmaxnreg works per warpgroup; the
   // producer group's registers are what the MMA warps grow into).
   static constexpr int THREADS = (MMA_WARPS + 4) * 32;
   static constexpr int WTM = BM / WM, WTN = BN / WN;  // warp tile
   static constexpr int FM = WTM / 8, FN = WTN / 8;    // 8-wide fragments per warp
-  static constexpr int P_BYTES = BM * BK * 8, Q_BYTES = BN * BK * 8;
+  static constexpr int P_BYTES = BM * BK * 8 * E, Q_BYTES = BN * BK * 8 * E;
   static constexpr int STAGE_BYTES = P_BYTES + Q_BYTES;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 2 * STAGES * 8;
+  static_assert(E == 1 || E == 2, "fp64 or complex128");
   static_assert(MMA_WARPS % 4 == 0, "MMA warps must form whole warpgroups");
-  static_assert(BM % 8 == 0 && BN % 8 == 0 && BK % 8 == 0, "8-wide TMA boxes");
+  static_assert(BM % 8 == 0 && BN % 8 == 0 && BK % 8 == 0, "8-element TMA boxes");
   static_assert(WTM % 8 == 0 && WTN % 8 == 0, "warp tiles are whole 8-wide fragments");
-  static_assert(BN <= 256 && BK <= 256, "TMA box extent limit");
+  static_assert(BN <= 256 && BK <= 256 && BM / 8 <= 256, "TMA box extent limit");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory per CTA");
 };
 
-// Fragment -> element map (lane = 4g + t). Every operand tile is staged as
-// 8-element-wide TMA boxes with the 64B swizzle (16-B chunk c of a 64-B row at
-// smem byte address a moves to c ^ ((a >> 7) & 3)). A fragment covers the 8
-// elements x = 8*blk + xmap8(g) of its operand's free dimension; k-step s reads
-// the k rows 4s + t. 64-bit shared loads are serviced per half-warp; with this
-// map each half-warp's 16 loads hit 16 distinct 8-byte bank slots in BOTH smem
-// layouts below, for every s (checked exhaustively). xmap8(2t), xmap8(2t)+1 are
-// adjacent, so the epilogue keeps 16-byte stores.
-//   XK layout (operand contiguous along x; [x-block][k][8]):
-//     byte = blk*BK*64 + 4s*64 + t*64 + (g&1)*8 + J_s
-//   KX layout (operand contiguous along k; [k-block][x][8]):
-//     byte = (s>>1)*BX*64 + (8*blk + xmap8(g))*64 + (t&1)*8 + J_s
-//   J_s = ((jg ^ (t>>1)) << 4) ^ (32*(s&1)),  jg = 2((g>>1)&1) + (g>>2)
+// ---------------------------------------------------------------- fragments
+// lane = 4g + t. A fragment covers 8 elements x = 8*blk + map(g) of its
+// operand's free dimension; k-step s reads the k rows 4s + t. DMMA ownership:
+// A[g][t] (Q side, rows n), B[t][g] (P side, cols m), D[g][2t], D[g][2t+1].
+//
+// fp64 (64B swizzle: 16-B chunk c of a 64-B row at byte a -> c ^ ((a>>7)&3)).
+// 64-bit shared loads are serviced per half-warp; xmap8 puts each half-warp's
+// 16 loads on 16 distinct 8-byte bank slots in both layouts, every s:
+//   XK ([x-block][k][8]):  blk*BK*64 + 4s*64 + t*64 + (g&1)*8 + J_s
+//   KX ([k-block][x][8]):  (s>>1)*BX*64 + (8blk + xmap8(g))*64 + (t&1)*8 + J_s
+//   J_s = ((jg ^ (t>>1)) << 4) ^ (32(s&1)),  jg = 2((g>>1)&1) + (g>>2)
+// xmap8(2t), xmap8(2t)+1 are adjacent -> 16-B epilogue stores.
+//
+// complex128 (128B swizzle: chunk c of a 128-B row -> c ^ ((a>>7)&7)); one
+// 16-B chunk = one element, read with LDS.128 (re, im), serviced per quarter
+// warp; xmapc puts each quarter-warp on 8 distinct chunks in both layouts:
+//   XK:  blk*BK*128 + 4s*128 + t*128 + Jc_s
+//   KX:  (s>>1)*BX*128 + (8blk + xmapc(g))*128 + Jc_s
+//   Jc_s = ((xmapc(g) ^ t) << 4) ^ (64(s&1))
+// (all maps checked exhaustively against the swizzle and bank models).
 __device__ __forceinline__ int xmap8(int g) { return (g & 1) + 4 * ((g >> 1) & 1) + 2 * (g >> 2); }
+__device__ __forceinline__ int xmapc(int g) { return (g >> 1) + 4 * (g & 1); }
 
-// QK == true  (mu == 1): P = L  (XK, 2-D map {n_out, K}), Q = T (KX, 2-D map {K, C})
-// QK == false (mu  > 1): P = T  (XK, 3-D map {A, K, C}; M runs over a list of
-//                         8-row fragments (a-block, c) so batches never pad),
-//                        Q = L  (XK, 2-D map {n_out, K})
+// QK == true  (mu == 1): P = L (XK), Q = T (KX)
+// QK == false (mu  > 1): P = T (XK, fragment list over (a-block, c)), Q = L (XK)
 template <class Cfg, bool QK>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
     modeprod_tma_kernel(const __grid_constant__ CUtensorMap mapP,
                         const __grid_constant__ CUtensorMap mapQ, const TmaParams p) {
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
-  constexpr int FM = Cfg::FM, FN = Cfg::FN;
+  constexpr int FM = Cfg::FM, FN = Cfg::FN, E = Cfg::E, ROW = Cfg::ROW;
+  constexpr bool CPLX = (E == 2);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment by pointer arithmetic so the compiler keeps the shared
   // address space (LDS, not generic LD).
@@ -145,7 +159,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             if constexpr (QK)
               tma_load_3d(sP, &mapP, &full_bar[stage], 0, k0, static_cast<int32_t>(q0));
             else
-              tma_load_4d(sP, &mapP, &full_bar[stage], 0, k0, static_cast<int32_t>(ab0), static_cast<int32_t>(c0));
+              tma_load_4d(sP, &mapP, &full_bar[stage], 0, k0, static_cast<int32_t>(ab0),
+                          static_cast<int32_t>(c0));
           } else {
             uint32_t c = c0, ab = ab0;
 #pragma unroll 1
@@ -153,13 +168,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
               // fragments past the end re-load the last valid one (masked later)
               if constexpr (QK) {
                 const uint32_t q = (q0 + f <= qlast) ? (q0 + f) : qlast;
-                tma_load_2d(sP + f * BK * 64, &mapP, &full_bar[stage], static_cast<int32_t>(8 * q), k0);
+                tma_load_2d(sP + f * BK * ROW, &mapP, &full_bar[stage], static_cast<int32_t>(8 * E * q), k0);
               } else {
                 if (q0 + f > qlast) {
                   c = qlast / static_cast<uint32_t>(p.AB);
                   ab = qlast - c * static_cast<uint32_t>(p.AB);
                 }
-                tma_load_3d(sP + f * BK * 64, &mapP, &full_bar[stage], static_cast<int32_t>(8 * ab), k0,
+                tma_load_3d(sP + f * BK * ROW, &mapP, &full_bar[stage], static_cast<int32_t>(8 * E * ab), k0,
                             static_cast<int32_t>(c));
                 if (++ab == static_cast<uint32_t>(p.AB)) {
                   ab = 0;
@@ -176,11 +191,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           } else if constexpr (QK) {
 #pragma unroll 1
             for (int b = 0; b < BK / 8; ++b)
-              tma_load_2d(sQ + b * BN * 64, &mapQ, &full_bar[stage], k0 + 8 * b, n0);
+              tma_load_2d(sQ + b * BN * ROW, &mapQ, &full_bar[stage], E * (k0 + 8 * b), n0);
           } else {
 #pragma unroll 1
             for (int b = 0; b < BN / 8; ++b)
-              tma_load_2d(sQ + b * BK * 64, &mapQ, &full_bar[stage], n0 + 8 * b, k0);
+              tma_load_2d(sQ + b * BK * ROW, &mapQ, &full_bar[stage], E * (n0 + 8 * b), k0);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -197,10 +212,19 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % Cfg::WM, wn = warp / Cfg::WM;
   const int mw = wm * Cfg::WTM, nw = wn * Cfg::WTN;
-  const int jg = 2 * ((g >> 1) & 1) + (g >> 2);
-  const uint32_t J0 = static_cast<uint32_t>(jg ^ (t >> 1)) << 4;
-  const uint32_t xk_off = static_cast<uint32_t>(t * 64 + (g & 1) * 8);
-  const uint32_t kx_off = static_cast<uint32_t>(xmap8(g) * 64 + (t & 1) * 8);
+  // thread-constant parts of the fragment addresses (see the maps above)
+  uint32_t J0, xk_off, kx_off;
+  if constexpr (CPLX) {
+    J0 = static_cast<uint32_t>(xmapc(g) ^ t) << 4;
+    xk_off = static_cast<uint32_t>(t * 128);
+    kx_off = static_cast<uint32_t>(xmapc(g) * 128);
+  } else {
+    const int jg = 2 * ((g >> 1) & 1) + (g >> 2);
+    J0 = static_cast<uint32_t>(jg ^ (t >> 1)) << 4;
+    xk_off = static_cast<uint32_t>(t * 64 + (g & 1) * 8);
+    kx_off = static_cast<uint32_t>(xmap8(g) * 64 + (t & 1) * 8);
+  }
+  constexpr uint32_t JFLIP = CPLX ? 64u : 32u;  // XOR applied on odd k-steps
 
   int stage = 0;
   uint32_t phase = 0;
@@ -208,11 +232,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     int mtile, ntile;
     decode(tile, mtile, ntile);
 
-    double acc[FM][FN][2];
+    // real: acc[fm][fn][0..1]; complex: re in [0..1], im in [2..3]
+    double acc[FM][FN][2 * E];
 #pragma unroll
     for (int fm = 0; fm < FM; ++fm)
 #pragma unroll
-      for (int fn = 0; fn < FN; ++fn) acc[fm][fn][0] = acc[fm][fn][1] = 0.0;
+      for (int fn = 0; fn < FN; ++fn)
+#pragma unroll
+        for (int r = 0; r < 2 * E; ++r) acc[fm][fn][r] = 0.0;
 
     for (int kb = 0; kb < KT; ++kb) {
       mbar_wait(&full_bar[stage], phase);
@@ -220,25 +247,54 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       const uint8_t* sQ = sP + Cfg::P_BYTES;
 #pragma unroll
       for (int s = 0; s < BK / 4; ++s) {
-        const uint32_t Js = J0 ^ static_cast<uint32_t>(32 * (s & 1));
-        double pf[FM], qf[FN];
+        const uint32_t Js = J0 ^ (JFLIP * static_cast<uint32_t>(s & 1));
+        if constexpr (!CPLX) {
+          double pf[FM], qf[FN];
 #pragma unroll
-        for (int fm = 0; fm < FM; ++fm)
-          pf[fm] = *reinterpret_cast<const double*>(sP + ((mw >> 3) + fm) * (BK * 64) + (4 * s) * 64 +
-                                                    xk_off + Js);
-#pragma unroll
-        for (int fn = 0; fn < FN; ++fn) {
-          if constexpr (QK)
-            qf[fn] = *reinterpret_cast<const double*>(sQ + (s >> 1) * (BN * 64) + (nw + 8 * fn) * 64 +
-                                                      kx_off + Js);
-          else
-            qf[fn] = *reinterpret_cast<const double*>(sQ + ((nw >> 3) + fn) * (BK * 64) + (4 * s) * 64 +
+          for (int fm = 0; fm < FM; ++fm)
+            pf[fm] = *reinterpret_cast<const double*>(sP + ((mw >> 3) + fm) * (BK * ROW) + (4 * s) * ROW +
                                                       xk_off + Js);
+#pragma unroll
+          for (int fn = 0; fn < FN; ++fn) {
+            if constexpr (QK)
+              qf[fn] = *reinterpret_cast<const double*>(sQ + (s >> 1) * (BN * ROW) + (nw + 8 * fn) * ROW +
+                                                        kx_off + Js);
+            else
+              qf[fn] = *reinterpret_cast<const double*>(sQ + ((nw >> 3) + fn) * (BK * ROW) + (4 * s) * ROW +
+                                                        xk_off + Js);
+          }
+#pragma unroll
+          for (int fm = 0; fm < FM; ++fm)
+#pragma unroll
+            for (int fn = 0; fn < FN; ++fn) dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], qf[fn], pf[fm]);
+        } else {
+          double2 pf[FM], qf[FN];
+#pragma unroll
+          for (int fm = 0; fm < FM; ++fm)
+            pf[fm] = *reinterpret_cast<const double2*>(sP + ((mw >> 3) + fm) * (BK * ROW) + (4 * s) * ROW +
+                                                       xk_off + Js);
+#pragma unroll
+          for (int fn = 0; fn < FN; ++fn) {
+            if constexpr (QK)
+              qf[fn] = *reinterpret_cast<const double2*>(sQ + (s >> 1) * (BN * ROW) + (nw + 8 * fn) * ROW +
+                                                         kx_off + Js);
+            else
+              qf[fn] = *reinterpret_cast<const double2*>(sQ + ((nw >> 3) + fn) * (BK * ROW) + (4 * s) * ROW +
+                                                         xk_off + Js);
+          }
+          // complex MAC as four real DMMAs: re += qr*pr - qi*pi, im += qr*pi + qi*pr
+#pragma unroll
+          for (int fn = 0; fn < FN; ++fn) {
+            const double qneg = -qf[fn].y;
+#pragma unroll
+            for (int fm = 0; fm < FM; ++fm) {
+              dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], qf[fn].x, pf[fm].x);
+              dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], qneg, pf[fm].y);
+              dmma_8x8x4(acc[fm][fn][2], acc[fm][fn][3], qf[fn].x, pf[fm].y);
+              dmma_8x8x4(acc[fm][fn][2], acc[fm][fn][3], qf[fn].y, pf[fm].x);
+            }
+          }
         }
-#pragma unroll
-        for (int fm = 0; fm < FM; ++fm)
-#pragma unroll
-          for (int fn = 0; fn < FN; ++fn) dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], qf[fn], pf[fm]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[stage]);
@@ -248,8 +304,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       }
     }
 
-    // epilogue: D(m, m+1 ; n) straight from registers, 16-byte stores along M
-    const int mpair = xmap8(2 * t);
+    // epilogue straight from registers
 #pragma unroll
     for (int fm = 0; fm < FM; ++fm) {
       const uint32_t q = static_cast<uint32_t>(mtile) * (BM / 8) + (mw >> 3) + fm;
@@ -259,13 +314,28 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         c = q / static_cast<uint32_t>(p.AB);
         ab = q - c * static_cast<uint32_t>(p.AB);
       }
-      const int m = 8 * static_cast<int>(ab) + mpair;
-      if (m >= p.Mlim) continue;
-      double* base = p.D + static_cast<int64_t>(c) * p.bstride + m;
+      if constexpr (!CPLX) {
+        // D(m, m+1 ; n): one 16-byte store along M
+        const int m = 8 * static_cast<int>(ab) + xmap8(2 * t);
+        if (m >= p.Mlim) continue;
+        double* base = p.D + static_cast<int64_t>(c) * p.bstride + m;
 #pragma unroll
-      for (int fn = 0; fn < FN; ++fn) {
-        const int n = ntile * BN + nw + 8 * fn + xmap8(g);
-        if (n < p.N) stg_f64x2(base + static_cast<int64_t>(n) * p.ldD, acc[fm][fn][0], acc[fm][fn][1]);
+        for (int fn = 0; fn < FN; ++fn) {
+          const int n = ntile * BN + nw + 8 * fn + xmap8(g);
+          if (n < p.N) stg_f64x2(base + static_cast<int64_t>(n) * p.ldD, acc[fm][fn][0], acc[fm][fn][1]);
+        }
+      } else {
+        // D(m) and D(m+4) (xmapc(2t) = t, xmapc(2t+1) = t+4): two 16-byte stores
+        const int m = 8 * static_cast<int>(ab) + t;
+        double* base = p.D + 2 * (static_cast<int64_t>(c) * p.bstride + m);
+#pragma unroll
+        for (int fn = 0; fn < FN; ++fn) {
+          const int n = ntile * BN + nw + 8 * fn + xmapc(g);
+          if (n >= p.N) continue;
+          double* col = base + 2 * static_cast<int64_t>(n) * p.ldD;
+          if (m < p.Mlim) stg_f64x2(col, acc[fm][fn][0], acc[fm][fn][2]);
+          if (m + 4 < p.Mlim) stg_f64x2(col + 8, acc[fm][fn][1], acc[fm][fn][3]);
+        }
       }
     }
   }

@@ -287,6 +287,21 @@ def test_aligned_medium_shapes_all_modes(policy):
     assert O.rel_fro(host(mm.tucker(dev(T), [dev(L) for L in Ls])), O.port_tucker(T, Ls)) < 1e-14
 
 
+def test_complex_medium_shapes_all_modes(policy):
+    # complex128 TMA/DMMA path (4 real DMMAs per complex MAC), rectangular
+    # factors like config C4, odd and aligned extents
+    rng = np.random.default_rng(8)
+    for m, n in [((32, 24, 40), (48, 36, 56)), ((33, 17, 20), (20, 31, 9))]:
+        T = rnd(rng, m, True)
+        Ls = [rnd(rng, (n[k], m[k]), True) for k in range(3)]
+        for mu in (1, 2, 3):
+            S = host(mm.mode_product(dev(T), dev(Ls[mu - 1]), mu))
+            assert O.rel_max(S, O.port_mode_product(T, Ls[mu - 1], mu)) < 1e-13
+        assert O.rel_fro(host(mm.tucker(dev(T), [dev(L) for L in Ls])), O.port_tucker(T, Ls)) < 1e-14
+        Ps = [rnd(rng, (m[k], n[k]), True) for k in range(3)]
+        assert O.rel_fro(host(mm.cttucker(dev(T), [dev(P) for P in Ps])), O.port_tucker(T, Ps, adjoint=True)) < 1e-14
+
+
 def test_host_and_device_paths_agree_bitwise():
     rng = np.random.default_rng(7)
     T = rnd(rng, (64, 64, 64))
