@@ -92,6 +92,20 @@ int mumode_tucker_c128(mumode_handle_t h, int d, const int64_t* m, const int64_t
 int mumode_tucker_promote(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
                           const double* T, const double* const* L, double* S, int adjoint);
 
+/* Modes mu_lo..mu_hi (1-based, inclusive) of the Tucker chain only; extents
+ * of the other modes pass through. The local step of the slab-partitioned
+ * Tucker (modes 1..d-1 on each rank's slab). */
+int mumode_tucker_range_f64(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                            const double* T, const double* const* L, double* S, int mu_lo,
+                            int mu_hi);
+
+/* Slab-transpose pack for the all-to-all: Y is A x C column-major; for each
+ * destination rank q the row block Y[a_off[q]:a_off[q+1], :] is written as a
+ * contiguous column-major block, blocks in rank order (a_off has P+1
+ * entries, a_off[0] = 0, a_off[P] = A, P <= 64). */
+int mumode_slab_pack_f64(mumode_handle_t h, int64_t A, int64_t C, int P, const int64_t* a_off,
+                         const double* Y, double* send);
+
 /* Replaces ops::kronsumv (tucker.hpp:209-232): W = sum_mu V x_mu A_mu with
  * square A_mu of size m[mu]. */
 int mumode_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double* V,

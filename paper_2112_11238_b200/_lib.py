@@ -34,6 +34,8 @@ SIGNATURES = {
     "mumode_tucker_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
     "mumode_tucker_c128": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
     "mumode_tucker_promote": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
+    "mumode_tucker_range_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int, ctypes.c_int]),
+    "mumode_slab_pack_f64": (ctypes.c_int, [H, I64, I64, ctypes.c_int, I64P, VP, VP]),
     "mumode_kronsumv_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, VP, ctypes.POINTER(VP), VP]),
     "mumode_expint_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, ctypes.POINTER(VP), VP, VP, ctypes.c_int]),
     "mumode_host_mode_product_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, ctypes.c_int, I64, VP, VP, VP]),

@@ -185,6 +185,26 @@ __global__ void accumulate_kernel(double* __restrict__ acc, const double* __rest
     acc[e] += x[e];
 }
 
+// Slab-transpose pack: Y (A x C, column-major) -> send buffer holding, for
+// each destination q, the row block Y[a_off[q] : a_off[q+1], 0:C] as a
+// contiguous column-major (|A_q| x C) matrix, blocks in q order.
+constexpr int kMaxRanks = 64;
+struct PackOffsets {
+  int64_t a[kMaxRanks + 1];
+};
+__global__ void slab_pack_kernel(const double* __restrict__ Y, double* __restrict__ send, int64_t A,
+                                 int64_t C, int P, PackOffsets off) {
+  const int64_t total = A * C;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t a = e % A, c = e / A;
+    int q = 0;
+    while (q + 1 < P && a >= off.a[q + 1]) ++q;
+    const int64_t rows = off.a[q + 1] - off.a[q];
+    send[off.a[q] * C + (a - off.a[q]) + c * rows] = Y[e];
+  }
+}
+
 static int grid_for(int64_t n, int sms) {
   int64_t b = (n + 255) / 256;
   int64_t cap = int64_t(sms) * 8;
@@ -457,27 +477,29 @@ static int mode_product_dev(mumode_handle_s* h, int d, const int64_t* m, int mu,
 // access, or a materialised op(L) when the TMA path applies.
 static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t* n,
                       const double* T, const double* const* L, double* S, bool adjoint,
-                      bool cplx) {
+                      bool cplx, int mu_lo = 1, int mu_hi = 0) {
+  if (mu_hi == 0) mu_hi = d;
   const int el = cplx ? 2 : 1;
+  const int nmodes = mu_hi - mu_lo + 1;
   // workspace: largest intermediate
   std::vector<int64_t> ext(m, m + d);
   size_t maxel = 0;
-  for (int mu = 0; mu < d - 1; ++mu) {
+  for (int mu = mu_lo - 1; mu < mu_hi - 1; ++mu) {
     ext[mu] = n[mu];
     maxel = std::max(maxel, size_t(prod(ext.data(), 0, d)));
   }
-  if (d > 1) {
+  if (nmodes > 1) {
     MM_TRY(h->ws[0].ensure(maxel * el * sizeof(double)));
-    if (d > 2) MM_TRY(h->ws[1].ensure(maxel * el * sizeof(double)));
+    if (nmodes > 2) MM_TRY(h->ws[1].ensure(maxel * el * sizeof(double)));
   }
   // materialise op(L) = L^T / L^H when adjoint (tiny: n x m per mode)
   std::vector<const double*> Lop(d);
   if (adjoint) {
     size_t tot = 0;
-    for (int mu = 0; mu < d; ++mu) tot += size_t(m[mu] * n[mu]) * el;
+    for (int mu = mu_lo - 1; mu < mu_hi; ++mu) tot += size_t(m[mu] * n[mu]) * el + 2;
     MM_TRY(h->lbuf.ensure(tot * sizeof(double) + 256));
     double* dst = static_cast<double*>(h->lbuf.p);
-    for (int mu = 0; mu < d; ++mu) {
+    for (int mu = mu_lo - 1; mu < mu_hi; ++mu) {
       const int64_t rows = m[mu], cols = n[mu];  // stored L is m x n
       transpose_conj_kernel<<<grid_for(rows * cols, h->num_sms), 256, 0, h->stream>>>(
           L[mu], dst, rows, cols, cplx ? 1 : 0, 1);
@@ -491,8 +513,8 @@ static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t
   }
   ext.assign(m, m + d);
   const double* src = T;
-  for (int mu = 1; mu <= d; ++mu) {
-    double* dst = (mu == d) ? S : static_cast<double*>(h->ws[(mu - 1) % 2].p);
+  for (int mu = mu_lo; mu <= mu_hi; ++mu) {
+    double* dst = (mu == mu_hi) ? S : static_cast<double*>(h->ws[(mu - mu_lo) % 2].p);
     MM_TRY(mode_product_dev(h, d, ext.data(), mu, n[mu - 1], src, Lop[mu - 1], 1, n[mu - 1],
                             cplx, false, dst));
     ext[mu - 1] = n[mu - 1];
@@ -619,6 +641,34 @@ int mumode_tucker_f64(mumode_handle_t h, int d, const int64_t* m, const int64_t*
 int mumode_tucker_c128(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
                        const double* T, const double* const* L, double* S, int adjoint) {
   return tucker_entry(h, d, m, n, T, L, S, adjoint, true);
+}
+
+int mumode_tucker_range_f64(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                            const double* T, const double* const* L, double* S, int mu_lo,
+                            int mu_hi) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  MM_TRY(check_shape(d, m, "tucker_range"));
+  if (mu_lo < 1 || mu_hi > d || mu_lo > mu_hi)
+    return fail(MUMODE_ERR_ARGUMENT, "tucker_range: bad mode range");
+  if (!T || !L || !S || !n) return fail(MUMODE_ERR_ARGUMENT, "tucker_range: null pointer");
+  for (int k = mu_lo - 1; k < mu_hi; ++k)
+    if (!L[k] || n[k] < 1) return fail(MUMODE_ERR_ARGUMENT, "tucker_range: bad matrix for mode " + std::to_string(k + 1));
+  MM_CUDA(cudaSetDevice(h->device));
+  return tucker_dev(h, d, m, n, T, L, S, false, false, mu_lo, mu_hi);
+}
+
+int mumode_slab_pack_f64(mumode_handle_t h, int64_t A, int64_t C, int P, const int64_t* a_off,
+                         const double* Y, double* send) {
+  if (!h || !a_off || !Y || !send) return fail(MUMODE_ERR_ARGUMENT, "slab_pack: null pointer");
+  if (P < 1 || P > kMaxRanks) return fail(MUMODE_ERR_ARGUMENT, "slab_pack: 1..64 ranks");
+  if (a_off[0] != 0 || a_off[P] != A) return fail(MUMODE_ERR_SIZE, "slab_pack: row offsets must cover 0..A");
+  PackOffsets off{};
+  for (int q = 0; q <= P; ++q) off.a[q] = a_off[q];
+  MM_CUDA(cudaSetDevice(h->device));
+  slab_pack_kernel<<<grid_for(A * C, h->num_sms), 256, 0, h->stream>>>(Y, send, A, C, P, off);
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return MUMODE_OK;
 }
 
 int mumode_tucker_promote(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,

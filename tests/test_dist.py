@@ -1,0 +1,176 @@
+"""Slab-partitioned Tucker (paper_2112_11238_b200/dist.py).
+
+CPU (no GPU): the partition / pack / all-to-all / assembly logic with
+world_size 2 and 3 over gloo, local contractions by the CPU oracle (a test
+backend that lives here -- the product has only the CUDA backend).
+GPU: the CUDA backend's kernels (mumode_tucker_range_f64, mumode_slab_pack_f64,
+the last-mode product) for P simulated ranks on one device with the exchange
+emulated by slicing, and a real 1-rank NCCL group.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from paper_2112_11238_b200.dist import SlabPlan, gather_rows, scatter_slabs, slab_tucker
+
+
+class OracleGlooBackend:
+    """Test backend: oracle (plain C restatement) for the local modes, numpy for
+    the pack, gloo for the exchange."""
+
+    def local_modes(self, T, m, n_all, Ls, lo, hi):
+        cur = np.asfortranarray(np.asarray(T).reshape(m, order="F"))
+        for mu in range(lo, hi + 1):
+            cur = O.port_mode_product(cur, Ls[mu - 1], mu)
+        return cur.reshape(-1, order="F")
+
+    def pack(self, Y, A, C, a_off):
+        Y2 = np.asarray(Y).reshape((A, C), order="F")
+        return np.concatenate([Y2[a_off[q]:a_off[q + 1], :].reshape(-1, order="F") for q in range(len(a_off) - 1)])
+
+    def alltoall(self, send, send_counts, recv_counts):
+        out = torch.empty(sum(recv_counts), dtype=torch.float64)
+        dist.all_to_all_single(out, torch.from_numpy(np.ascontiguousarray(send)), recv_counts, send_counts)
+        return out.numpy()
+
+    def last_mode(self, Z, rows, m_d, L_d):
+        Z2 = np.asarray(Z).reshape((rows, m_d), order="F")
+        return O.port_mode_product(Z2, L_d, 2).reshape(-1, order="F")
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cases, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        for m, n, seed in cases:
+            rng = np.random.default_rng(seed)
+            T = np.asfortranarray(rng.standard_normal(m))
+            Ls = [np.asfortranarray(rng.standard_normal((n[k], m[k]))) for k in range(len(m))]
+            plan = SlabPlan(m, n, world)
+            T_r = scatter_slabs(plan, T)[rank]
+            S_r = slab_tucker(plan, rank, T_r, Ls, OracleGlooBackend())
+            blocks = [None] * world
+            dist.all_gather_object(blocks, S_r)
+            if rank == 0:
+                S = gather_rows(plan, blocks)
+                q.put((m, n, O.rel_fro(S, O.port_tucker(T, Ls))))
+    finally:
+        dist.destroy_process_group()
+
+
+CASES = [((6, 5, 4), (3, 7, 5), 1), ((4, 4, 4, 6), (4, 4, 4, 6), 2), ((7, 3, 9), (5, 4, 2), 3),
+         ((5, 6), (8, 3), 4), ((2, 3, 2, 3, 4), (3, 2, 3, 2, 5), 5)]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_tucker_gloo_matches_oracle(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    results = [q.get(timeout=10) for _ in CASES]
+    for m, n, err in results:
+        assert err < 1e-13, (m, n, err)
+
+
+def test_plan_bookkeeping():
+    plan = SlabPlan((256, 256, 256), (256, 256, 256), 8)
+    assert plan.c_sizes == [32] * 8 and plan.A == 65536 and plan.a_sizes == [8192] * 8
+    assert sum(plan.send_counts(3)) == 65536 * 32 == sum(plan.recv_counts(3))
+    assert plan.exchange_bytes(0) == 7 * 8192 * 32 * 8  # 14.7 MB per rank on 8 GPUs
+    uneven = SlabPlan((5, 7), (4, 3), 3)
+    assert uneven.c_sizes == [3, 2, 2] and uneven.a_sizes == [2, 1, 1]
+    with pytest.raises(ValueError):
+        SlabPlan((4, 2), (4, 2), 3)
+
+
+# ------------------------------------------------------------------ GPU
+class SimulatedExchange:
+    """Wraps the CUDA backend for P ranks simulated on one GPU: the exchange
+    is emulated by slicing the other ranks' send buffers (no kernels wait on
+    one another)."""
+
+    def __init__(self, inner, plan):
+        self.inner, self.plan = inner, plan
+        self.sends = {}
+
+    def run(self, T_slabs, Ls):
+        plan, P = self.plan, self.plan.P
+        d = len(plan.m)
+        sends = []
+        for r in range(P):
+            Y = self.inner.local_modes(T_slabs[r], plan.local_in_extents(r), plan.n, Ls, 1, d - 1)
+            sends.append(self.inner.pack(Y, plan.A, plan.c_sizes[r], plan.a_off))
+        outs = []
+        for r in range(P):
+            parts = []
+            for s in range(P):
+                off = offsets_of(plan.send_counts(s))
+                parts.append(sends[s][off[r]:off[r + 1]])
+            recv = torch.cat(parts)
+            outs.append(self.inner.last_mode(recv, plan.a_sizes[r], plan.m[-1], Ls[-1]))
+        return outs
+
+
+def offsets_of(counts):
+    o = [0]
+    for c in counts:
+        o.append(o[-1] + c)
+    return o
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_slab_tucker_cuda_kernels_simulated_ranks(P):
+    from paper_2112_11238_b200.dist import CudaSlabBackend
+    assert torch.cuda.is_available()
+    for m, n in [((64, 48, 40), (56, 48, 72)), ((24, 24, 24, 24), (24, 24, 24, 24))]:
+        rng = np.random.default_rng(P)
+        T = np.asfortranarray(rng.standard_normal(m))
+        Ls = [np.asfortranarray(rng.standard_normal((n[k], m[k]))) for k in range(len(m))]
+        plan = SlabPlan(m, n, P)
+        slabs = [torch.from_numpy(s).cuda() for s in scatter_slabs(plan, T)]
+        Lds = [torch.from_numpy(L).cuda() for L in Ls]
+        outs = SimulatedExchange(CudaSlabBackend(0), plan).run(slabs, Lds)
+        S = gather_rows(plan, [o.cpu().numpy() for o in outs])
+        assert O.rel_fro(S, O.port_tucker(T, Ls)) < 1e-13
+
+
+@pytest.mark.gpu
+def test_slab_tucker_nccl_single_rank():
+    from paper_2112_11238_b200.dist import CudaSlabBackend
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(9)
+        m = n = (48, 40, 32)
+        T = np.asfortranarray(rng.standard_normal(m))
+        Ls = [np.asfortranarray(rng.standard_normal((n[k], m[k]))) for k in range(3)]
+        plan = SlabPlan(m, n, 1)
+        S_r = slab_tucker(plan, 0, torch.from_numpy(T).cuda(), [torch.from_numpy(L).cuda() for L in Ls],
+                          CudaSlabBackend(0))
+        S = gather_rows(plan, [S_r.cpu().numpy()])
+        assert O.rel_fro(S, O.port_tucker(T, Ls)) < 1e-13
+    finally:
+        dist.destroy_process_group()
