@@ -103,6 +103,16 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                : "d"(a), "d"(b));
 }
 
+// Fragment column maps (see tma_dmma.cuh): fp64 64B-swizzle and complex
+// 128B-swizzle layouts; both keep fragment loads bank-conflict-free.
+__device__ __forceinline__ int xmap8(int g) { return (g & 1) + 4 * ((g >> 1) & 1) + 2 * (g >> 2); }
+__device__ __forceinline__ int xmapc(int g) { return (g >> 1) + 4 * (g & 1); }
+
+// Named barrier among `count` threads (warps that do not take part skip it).
+__device__ __forceinline__ void named_barrier_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
 __device__ __forceinline__ void stg_f64x2(double* p, double a, double b) {
   asm volatile("st.global.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(a), "d"(b) : "memory");
 }

@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "generic.cuh"
 #include "tma_dmma.cuh"
+#include "fused.cuh"
 
 namespace mumode_gpu {
 
@@ -220,6 +221,8 @@ static int check_shape(int d, const int64_t* m, const char* who) {
   return MUMODE_OK;
 }
 
+static bool aligned16_ptr(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 static int64_t prod(const int64_t* m, int lo, int hi) {
   int64_t p = 1;
   for (int k = lo; k < hi; ++k) p *= m[k];
@@ -249,7 +252,7 @@ using CfgCb = TmaCfg<128, 64, 16, 4, 4, 2, 2>;
 using CfgCc = TmaCfg<96, 32, 16, 4, 4, 2, 2>;   // 24x16 warp tiles, fine-grained
 using CfgCd = TmaCfg<192, 16, 16, 4, 8, 1, 2>;
 
-static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+static bool aligned16(const void* p) { return aligned16_ptr(p); }
 
 // Can the TMA/DMMA kernel describe this job? (16-byte strides and bases,
 // forward layout of L, real, even M, sizes within int32 coordinates.)
@@ -413,7 +416,7 @@ static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
 }
 
 static int launch_tma_auto(mumode_handle_s* h, const ModeJob& j) {
-  const int forced = h->policy >= 3 ? h->policy - 3 : -1;
+  const int forced = (h->policy >= 3 && h->policy <= 6) ? h->policy - 3 : -1;
   int cfg = choose_cfg(j, h->num_sms);
   if (forced >= 0) cfg = j.cplx ? 4 + forced : forced;
   switch (cfg) {
@@ -446,8 +449,63 @@ static int launch_generic(mumode_handle_s* h, const ModeJob& j) {
 static int run_job(mumode_handle_s* h, const ModeJob& j) {
   const bool can_tma = tma_ok(j);
   if (h->policy == 1 || !can_tma) return launch_generic(h, j);
-  if (h->policy >= 2 || tma_worthwhile(j)) return launch_tma_auto(h, j);
+  if ((h->policy >= 2 && h->policy <= 6) || tma_worthwhile(j)) return launch_tma_auto(h, j);
   return launch_generic(h, j);
+}
+
+// ------------------------------------------------------------------ fused pairs
+template <int MU, bool FIRST>
+static int launch_fused(mumode_handle_s* h, const double* T, double* S, const double* L1,
+                        const double* L2, int64_t A, int64_t C) {
+  using Cfg = FusedCfg<MU, FIRST>;
+  const CUtensorMap* mp = nullptr;
+  FusedParams p{S, L1, L2, A, C, 0};
+  if (FIRST) {
+    uint64_t d[3] = {8, uint64_t(MU) * uint64_t(C), uint64_t(MU / 8)}, st[2] = {uint64_t(MU), 8};
+    uint32_t b[3] = {8, 8 * MU, MU / 8};
+    MM_TRY(get_map(h, T, 3, d, st, b, &mp));
+    p.tiles = (C + 7) / 8;
+  } else {
+    uint64_t d[4] = {uint64_t(A), uint64_t(MU), uint64_t(MU), uint64_t(C)};
+    uint64_t st[3] = {uint64_t(A), uint64_t(A) * MU, uint64_t(A) * MU * MU};
+    uint32_t b[4] = {8, MU, MU, 1};
+    MM_TRY(get_map(h, T, 4, d, st, b, &mp));
+    p.tiles = (A / 8) * C;
+  }
+  const int grid = static_cast<int>(p.tiles < h->num_sms ? p.tiles : h->num_sms);
+  auto k = fused_pair_kernel<MU, FIRST>;
+  MM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mp, p);
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return MUMODE_OK;
+}
+
+template <int MU>
+static int launch_fused_mu(mumode_handle_s* h, bool first, const double* T, double* S,
+                           const double* L1, const double* L2, int64_t A, int64_t C) {
+  return first ? launch_fused<MU, true>(h, T, S, L1, L2, A, C)
+               : launch_fused<MU, false>(h, T, S, L1, L2, A, C);
+}
+
+// Fused two-mode passes apply to real, forward chains whose modes are all
+// square with one small extent MU in {8, 16, 24, 32} (e.g. config C5, 24^6):
+// there each single product is HBM-bound and pairing halves the HBM passes.
+static int fused_extent(int d, const int64_t* m, const int64_t* n, bool cplx, bool adjoint,
+                        int policy, int mu_lo, int mu_hi, const double* T, const double* S,
+                        const double* const* L) {
+  if (cplx || adjoint || !(policy == 0 || policy == 7) || mu_hi - mu_lo < 1) return 0;
+  const int64_t MU = m[0];
+  if (MU != 8 && MU != 16 && MU != 24 && MU != 32) return 0;
+  for (int k = 0; k < d; ++k)
+    if (m[k] != MU || n[k] != MU) return 0;
+  if (!aligned16_ptr(T) || !aligned16_ptr(S)) return 0;
+  for (int k = mu_lo - 1; k < mu_hi; ++k)
+    if (!aligned16_ptr(L[k])) return 0;
+  int64_t total = 1;
+  for (int k = 0; k < d; ++k) total *= MU;
+  if (total / MU >= (int64_t(1) << 31)) return 0;
+  return static_cast<int>(MU);
 }
 
 // One mode product on device buffers: T with extents m (d modes), op(L)
@@ -513,6 +571,27 @@ static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t
   }
   ext.assign(m, m + d);
   const double* src = T;
+  const int MU = fused_extent(d, m, n, cplx, adjoint, h->policy, mu_lo, mu_hi, T, S, L);
+  if (MU) {
+    // pairs (mu, mu+1) as fused passes; an odd last mode runs alone below
+    int pass = 0, mu = mu_lo;
+    for (; mu + 1 <= mu_hi; mu += 2, ++pass) {
+      double* dst = (mu + 1 == mu_hi) ? S : static_cast<double*>(h->ws[pass % 2].p);
+      const int64_t A = prod(ext.data(), 0, mu - 1), C = prod(ext.data(), mu + 1, d);
+      int rc;
+      switch (MU) {
+        case 8: rc = launch_fused_mu<8>(h, mu == 1, src, dst, L[mu - 1], L[mu], A, C); break;
+        case 16: rc = launch_fused_mu<16>(h, mu == 1, src, dst, L[mu - 1], L[mu], A, C); break;
+        case 24: rc = launch_fused_mu<24>(h, mu == 1, src, dst, L[mu - 1], L[mu], A, C); break;
+        default: rc = launch_fused_mu<32>(h, mu == 1, src, dst, L[mu - 1], L[mu], A, C); break;
+      }
+      MM_TRY(rc);
+      src = dst;
+    }
+    if (mu == mu_hi)
+      MM_TRY(mode_product_dev(h, d, ext.data(), mu, n[mu - 1], src, L[mu - 1], 1, n[mu - 1], false, false, S));
+    return MUMODE_OK;
+  }
   for (int mu = mu_lo; mu <= mu_hi; ++mu) {
     double* dst = (mu == mu_hi) ? S : static_cast<double*>(h->ws[(mu - mu_lo) % 2].p);
     MM_TRY(mode_product_dev(h, d, ext.data(), mu, n[mu - 1], src, Lop[mu - 1], 1, n[mu - 1],
@@ -597,7 +676,7 @@ void* mumode_get_stream(mumode_handle_t h) { return h ? static_cast<void*>(h->st
 int64_t mumode_launch_count(mumode_handle_t h) { return h ? h->launches : -1; }
 
 int mumode_set_kernel_policy(mumode_handle_t h, int policy) {
-  if (!h || policy < 0 || policy > 6) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
+  if (!h || policy < 0 || policy > 7) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
   // 3..6 force real tile configuration 0..3 / complex configuration 0..3
   h->policy = policy;
   return MUMODE_OK;

@@ -84,8 +84,7 @@ struct TmaCfg {
 //   KX:  (s>>1)*BX*128 + (8blk + xmapc(g))*128 + Jc_s
 //   Jc_s = ((xmapc(g) ^ t) << 4) ^ (64(s&1))
 // (all maps checked exhaustively against the swizzle and bank models).
-__device__ __forceinline__ int xmap8(int g) { return (g & 1) + 4 * ((g >> 1) & 1) + 2 * (g >> 2); }
-__device__ __forceinline__ int xmapc(int g) { return (g >> 1) + 4 * (g & 1); }
+// (xmap8 / xmapc live in common.cuh)
 
 // QK == true  (mu == 1): P = L (XK), Q = T (KX)
 // QK == false (mu  > 1): P = T (XK, fragment list over (a-block, c)), Q = L (XK)

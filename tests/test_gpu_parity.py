@@ -40,7 +40,8 @@ def _require_gpu():
         pytest.fail("GPU test run without a GPU")
 
 
-@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6], ids=["auto", "generic", "tma", "tma_big", "tma_tm", "tma_lm", "tma_mid"])
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7],
+                ids=["auto", "generic", "tma", "tma_big", "tma_tm", "tma_lm", "tma_mid", "fused"])
 def policy(request):
     h = mm.get_handle(0)
     h.set_kernel_policy(request.param)
@@ -300,6 +301,18 @@ def test_complex_medium_shapes_all_modes(policy):
         assert O.rel_fro(host(mm.tucker(dev(T), [dev(L) for L in Ls])), O.port_tucker(T, Ls)) < 1e-14
         Ps = [rnd(rng, (m[k], n[k]), True) for k in range(3)]
         assert O.rel_fro(host(mm.cttucker(dev(T), [dev(P) for P in Ps])), O.port_tucker(T, Ps, adjoint=True)) < 1e-14
+
+
+@pytest.mark.parametrize("shape", [(8,) * 6, (16,) * 4, (24,) * 4, (24,) * 5, (24,) * 3, (32,) * 3, (16, 16)])
+def test_fused_small_square_modes(policy, shape):
+    # the fused two-mode passes (config C5-class shapes): even and odd orders
+    rng = np.random.default_rng(len(shape) * 100 + shape[0])
+    T = rnd(rng, shape)
+    Ls = [rnd(rng, (e, e)) for e in shape]
+    S = host(mm.tucker(dev(T), [dev(L) for L in Ls]))
+    assert O.rel_fro(S, O.port_tucker(T, Ls)) < 1e-14
+    I = [dev(np.eye(e)) for e in shape]
+    np.testing.assert_array_equal(host(mm.tucker(dev(T), I)), T)
 
 
 def test_host_and_device_paths_agree_bitwise():
