@@ -321,7 +321,7 @@ def main():
                    "vs_baseline_source": "BASELINE.md: paper Fig.1 tucker d=3 n=256, 0.224 s = 115.0 GFLOP/s (MATLAB, i7-8750H)"},
         "roofline": {"bound": "tensor", "achieved": round(achieved_tf, 3), "peak": round(peak, 3),
                      "unit": "TFLOP/s", "frac": round(achieved_tf / peak, 4), "traffic": traffic,
-                     "kernel": "modeprod_tma_kernel (TMA 128B-swizzle ring + DMMA.8x8x4)",
+                     "kernel": "modeprod_tma_kernel (TMA 64B-swizzle ring + DMMA.8x8x4)",
                      "flops_per_launch": flops_per_launch, "mean_launch_ms": round(launch_ms, 5),
                      "peak_source": "fp64 DMMA probe measured live in this run (mumode_probe_fp64_peak); "
                                     "MEASURED_PEAKS.json has no fp64 entry"},
