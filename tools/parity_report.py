@@ -1,0 +1,82 @@
+"""Parity report: the CUDA path vs the compiled reference library (oracle/_ref)
+on the BASELINE configs, identical seeded bytes. Prints one JSON object with
+relative Frobenius and relative max-norm errors per config (gate 1e-12).
+Test infrastructure: imports the oracle as the checker."""
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import oracle as O  # noqa: E402
+import paper_2112_11238_b200 as mm  # noqa: E402
+
+
+def dev(x):
+    return torch.from_numpy(np.asfortranarray(x)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def rec(out, name, got, want, t_ref):
+    out[name] = {"rel_fro": O.rel_fro(got, want), "rel_max": O.rel_max(got, want),
+                 "ref_seconds": round(t_ref, 3)}
+
+
+def main():
+    out = {"reference": f"oracle/_ref (reference library), OpenBLAS {O.ref_blas_kernel_name()}"}
+    g = mm.Rng(1234 + 100)
+    L1, L2 = g.normal((100, 100)), g.normal((100, 100))
+    T = g.normal((100, 100))
+    t0 = time.time(); ref = O.ref_tucker(T, [L1, L2]); t = time.time() - t0
+    rec(out, "C1_2d_n100", host(mm.tucker(dev(T), [dev(L1), dev(L2)])), ref, t)
+
+    g = mm.Rng(1234)
+    T = g.normal((256,) * 3)
+    Ls = [g.normal((256, 256)) for _ in range(3)]
+    t0 = time.time(); ref = O.ref_tucker(T, Ls); t = time.time() - t0
+    rec(out, "C2_tucker_256", host(mm.tucker(dev(T), [dev(L) for L in Ls])), ref, t)
+    for mu in (1, 2, 3):
+        t0 = time.time(); ref = O.ref_mode_product(T, Ls[mu - 1], mu); t = time.time() - t0
+        rec(out, f"C2_mode{mu}", host(mm.mode_product(dev(T), dev(Ls[mu - 1]), mu)), ref, t)
+
+    n = 200
+    A = O.port_advection_diffusion(n, 0.5)
+    E = O.ref_expm(1e-3 * A)
+    g = mm.Rng(1234)
+    u0 = g.normal((n,) * 3)
+    t0 = time.time()
+    u = u0
+    steps = []
+    for s in range(100):
+        u = O.ref_tucker(u, [E, E, E])
+        if s in (0, 9, 99):
+            steps.append((s + 1, u))
+    t = time.time() - t0
+    for k, uref in steps:
+        rec(out, f"C3_expint_step{k}_sameE", host(mm.expint(dev(u0), [dev(E)] * 3, k)), uref, t)
+    E2 = mm.expm(1e-3 * A)
+    out["C3_expm_engine_vs_reference"] = O.rel_fro(E2, E)
+    rec(out, "C3_expint_step100_engineE", host(mm.expint(dev(u0), [dev(E2)] * 3, 100)), steps[-1][1], t)
+
+    g = mm.Rng(1234)
+    T = g.normal((128,) * 3, True)
+    Ls = [g.normal((192, 128), True) for _ in range(3)]
+    t0 = time.time(); ref = O.ref_tucker(T, Ls); t = time.time() - t0
+    rec(out, "C4_complex_128_to_192", host(mm.tucker(dev(T), [dev(L) for L in Ls])), ref, t)
+
+    g = mm.Rng(1234)
+    T = g.normal((24,) * 6)
+    Ls = [g.normal((24, 24)) for _ in range(6)]
+    t0 = time.time(); ref = O.ref_tucker(T, Ls); t = time.time() - t0
+    rec(out, "C5_6d_24", host(mm.tucker(dev(T), [dev(L) for L in Ls])), ref, t)
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
