@@ -403,5 +403,35 @@ inline Tensor<double> kronsumv(const Tensor<double>& v, const MatrixStack<double
   return W;
 }
 
+/// Per-mode factorizations for the inverse Tucker operator
+/// (ops::FactorizedStack, tucker.hpp:34-51), real. Factorizes (LU with partial
+/// pivoting) at construction and throws NumericalError on a singular pivot
+/// (lu.hpp:33); keeps P_mu^-1 for the GPU.
+class FactorizedStack {
+ public:
+  explicit FactorizedStack(const MatrixStack<double>& Ps) {
+    for (const auto& P : Ps) {
+      if (P.rows() != P.cols()) throw core::SizeError("lu_factor: matrix must be square");
+      Matrix<double> inv(P.rows(), P.cols());
+      engine::check(mumode_inverse_f64(P.rows(), P.data(), inv.data()));
+      inv_.push_back(std::move(inv));
+    }
+  }
+  index_t size() const { return static_cast<index_t>(inv_.size()); }
+  const MatrixStack<double>& inverses() const { return inv_; }
+
+ private:
+  MatrixStack<double> inv_;
+};
+
+/// Inverse Tucker S = T x_1 P_1^-1 ... x_d P_d^-1 (ops::itucker, tucker.hpp:187-204).
+inline Tensor<double> itucker(const Tensor<double>& t, const FactorizedStack& F) {
+  if (F.size() != t.order()) throw core::SizeError("itucker: stack length does not match tensor order");
+  for (index_t mu = 1; mu <= t.order(); ++mu)
+    if (F.inverses()[static_cast<std::size_t>(mu - 1)].rows() != t.extent(mu))
+      throw core::SizeError("itucker: factor size does not match extent of mode " + std::to_string(mu));
+  return tucker(t, F.inverses());
+}
+
 }  // namespace ops
 }  // namespace mumode

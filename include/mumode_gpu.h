@@ -145,6 +145,12 @@ int mumode_probe_fp64_peak(mumode_handle_t h, double* tflops);
  * (proj/src/expm.cpp:97-151) for the exponential integrator's E_mu. */
 int mumode_expm_f64(int64_t n, const double* A, double* E);
 
+/* Inverse of a square matrix (LU with partial pivoting, host fp64); the
+ * per-mode factor of the inverse Tucker operator ops::itucker
+ * (tucker.hpp:187-204): itucker(T, P) = tucker(T, {P_mu^-1}). Returns
+ * MUMODE_ERR_NUMERICAL on a zero pivot, like FactorizedStack (lu.hpp:33). */
+int mumode_inverse_f64(int64_t n, const double* P, double* Pinv);
+
 /* Seeded input generator reproducing the reference's draws bit-for-bit:
  * std::mt19937_64(seed) and a FRESH std::normal_distribution<double> per
  * filled object (tools/mumode_cli.cpp:94-121). Complex draws re then im. */

@@ -7,6 +7,7 @@ from .api import (  # noqa: F401
     ArgumentError,
     ContractError,
     CudaError,
+    FactorizedStack,
     Handle,
     MumodeError,
     NumericalError,
@@ -18,6 +19,7 @@ from .api import (  # noqa: F401
     expm,
     get_handle,
     is_colmajor,
+    itucker,
     kronsumv,
     launch_count,
     mode_product,

@@ -47,6 +47,7 @@ SIGNATURES = {
     "mumode_host_expint_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, ctypes.POINTER(VP), VP, VP, ctypes.c_int]),
     "mumode_probe_fp64_peak": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_double)]),
     "mumode_expm_f64": (ctypes.c_int, [I64, VP, VP]),
+    "mumode_inverse_f64": (ctypes.c_int, [I64, VP, VP]),
     "mumode_rng_create": (ctypes.c_int, [ctypes.POINTER(VP), ctypes.c_uint64]),
     "mumode_rng_destroy": (ctypes.c_int, [VP]),
     "mumode_rng_normal": (ctypes.c_int, [VP, VP, I64, ctypes.c_int]),

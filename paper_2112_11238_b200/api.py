@@ -385,6 +385,39 @@ def expint(u0, Es, steps: int, out=None):
     return res
 
 
+class FactorizedStack:
+    """Per-mode factorizations of square P_1..P_d for the inverse Tucker
+    operator (ops::FactorizedStack, tucker.hpp:34-51). Factorizes at
+    construction, raising NumericalError on a singular pivot (lu.hpp:33); what
+    is kept is each P_mu^-1, applied on the GPU as a Tucker operator."""
+
+    def __init__(self, Ps):
+        self.inverses = []
+        for mu, P in enumerate(Ps, 1):
+            Pn = _np_f(np.asarray(P.cpu() if _is_torch(P) else P), False)
+            if Pn.ndim != 2 or Pn.shape[0] != Pn.shape[1]:
+                raise SizeError("lu_factor: matrix must be square")
+            inv = np.empty(Pn.shape, order="F")
+            _check(_lib.lib().mumode_inverse_f64(int(Pn.shape[0]), Pn.ctypes.data, inv.ctypes.data))
+            self.inverses.append(inv)
+
+    def size(self) -> int:
+        return len(self.inverses)
+
+
+def itucker(T, F: FactorizedStack):
+    """S = T x_1 P_1^-1 ... x_d P_d^-1 (ops::itucker, tucker.hpp:187-204)."""
+    _validate_tensor(T)
+    if F.size() != T.ndim:
+        raise SizeError("itucker: stack length does not match tensor order")
+    for mu, inv in enumerate(F.inverses, 1):
+        if inv.shape[0] != int(T.shape[mu - 1]):
+            raise SizeError(f"itucker: factor size does not match extent of mode {mu}")
+    if _is_torch(T):
+        return tucker(T, [torch.from_numpy(inv).to(T.device) for inv in F.inverses])
+    return tucker(T, F.inverses)
+
+
 def expm(A) -> np.ndarray:
     """Matrix exponential on the host (scaling and squaring, Pade 13)."""
     An = _np_f(np.asarray(A), False)

@@ -18,6 +18,7 @@ struct GenericArgs {
   int64_t A, K, N, C;
   int64_t sLi, sLk;
   int conj;  // complex only: conjugate L entries (cttucker)
+  int accumulate;  // S += result (kronsumv)
 };
 
 constexpr int kGenFibers = 64;  // fibers (a, c) per CTA
@@ -105,7 +106,15 @@ __global__ void __launch_bounds__(kGenThreads)
 #pragma unroll
     for (int j = 0; j < kGenRows / 4; ++j) {
       const int64_t i = i0 + ig + 4 * j;
-      if (i < g.N) S[a + i * g.A + c * g.A * g.N] = acc[j];
+      if (i < g.N) {
+        V* dst = &S[a + i * g.A + c * g.A * g.N];
+        if (g.accumulate) {
+          if constexpr (CPLX) *dst = make_double2(dst->x + acc[j].x, dst->y + acc[j].y);
+          else *dst = *dst + acc[j];
+        } else {
+          *dst = acc[j];
+        }
+      }
     }
   }
 }

@@ -216,3 +216,24 @@ extern "C" int mumode_expm_f64(int64_t n, const double* Ain, double* E) {
   std::memcpy(E, P.data(), sizeof(double) * nn);
   return MUMODE_OK;
 }
+
+// ------------------------------------------------------------------ inverse
+// Per-mode inverse for the inverse Tucker operator (ops::itucker,
+// tucker.hpp:187-204): LU with partial pivoting (the FactorizedStack role,
+// lu.hpp:23-47), then n solves against the identity. A zero pivot reports the
+// reference's NumericalError text.
+extern "C" int mumode_inverse_f64(int64_t n, const double* P, double* Pinv) {
+  if (n < 1 || !P || !Pinv) {
+    mumode_gpu::set_error("inverse: matrix must be non-empty");
+    return MUMODE_ERR_ARGUMENT;
+  }
+  const size_t nn = static_cast<size_t>(n * n);
+  Mat Q(P, P + nn), X(nn, 0.0);
+  for (int64_t i = 0; i < n; ++i) X[static_cast<size_t>(i + i * n)] = 1.0;
+  if (!solve(Q, X, n)) {
+    mumode_gpu::set_error("lu_factor: singular pivot");
+    return MUMODE_ERR_NUMERICAL;
+  }
+  std::memcpy(Pinv, X.data(), sizeof(double) * nn);
+  return MUMODE_OK;
+}

@@ -179,12 +179,6 @@ __global__ void real_to_complex_kernel(const double* __restrict__ x, double* __r
   }
 }
 
-__global__ void accumulate_kernel(double* __restrict__ acc, const double* __restrict__ x,
-                                  int64_t n) {
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
-       e += int64_t(gridDim.x) * blockDim.x)
-    acc[e] += x[e];
-}
 
 // Slab-transpose pack: Y (A x C, column-major) -> send buffer holding, for
 // each destination q, the row block Y[a_off[q] : a_off[q+1], 0:C] as a
@@ -239,6 +233,7 @@ struct ModeJob {
   int64_t sLi, sLk;
   bool cplx;
   bool conj;
+  bool accumulate = false;  // S += T x_mu op(L)
 };
 
 // Compiled tile configurations (BM, BN, BK, stages, warps along M, along N).
@@ -396,6 +391,7 @@ static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
     p.AB = int(AB);
     p.mfrags = AB * j.C;
   }
+  p.accumulate = j.accumulate ? 1 : 0;
   p.K = int(j.K);
   p.mt = int((p.mfrags + Cfg::BM / 8 - 1) / (Cfg::BM / 8));
   p.nt = (p.N + Cfg::BN - 1) / Cfg::BN;
@@ -432,7 +428,7 @@ static int launch_tma_auto(mumode_handle_s* h, const ModeJob& j) {
 }
 
 static int launch_generic(mumode_handle_s* h, const ModeJob& j) {
-  GenericArgs g{j.T, j.L, j.S, j.A, j.K, j.N, j.C, j.sLi, j.sLk, j.conj ? 1 : 0};
+  GenericArgs g{j.T, j.L, j.S, j.A, j.K, j.N, j.C, j.sLi, j.sLk, j.conj ? 1 : 0, j.accumulate ? 1 : 0};
   const int64_t nfib = j.A * j.C;
   dim3 grid(static_cast<unsigned>((nfib + kGenFibers - 1) / kGenFibers),
             static_cast<unsigned>((j.N + kGenRows - 1) / kGenRows));
@@ -512,8 +508,9 @@ static int fused_extent(int d, const int64_t* m, const int64_t* n, bool cplx, bo
 // n_mu x m_mu given by (L, sLi, sLk, conj).
 static int mode_product_dev(mumode_handle_s* h, int d, const int64_t* m, int mu, int64_t n_mu,
                             const double* T, const double* L, int64_t sLi, int64_t sLk,
-                            bool cplx, bool conj, double* S) {
+                            bool cplx, bool conj, double* S, bool accumulate = false) {
   ModeJob j;
+  j.accumulate = accumulate;
   j.T = T;
   j.L = L;
   j.S = S;
@@ -769,17 +766,12 @@ int mumode_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double
   if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
   MM_TRY(check_stack(d, m, m, V, A, W, "kronsumv"));
   MM_CUDA(cudaSetDevice(h->device));
-  const int64_t numel = prod(m, 0, d);
+  // W = V x_1 A_1, then W += V x_mu A_mu for mu = 2..d in the products'
+  // epilogues (the reference's acc += term order, tucker.hpp:222-231): no
+  // term buffer and no separate accumulation pass over W.
   MM_TRY(mode_product_dev(h, d, m, 1, m[0], V, A[0], 1, m[0], false, false, W));
-  if (d > 1) MM_TRY(h->ws[0].ensure(size_t(numel) * sizeof(double)));
-  double* term = static_cast<double*>(h->ws[0].p);
-  for (int mu = 2; mu <= d; ++mu) {
-    MM_TRY(mode_product_dev(h, d, m, mu, m[mu - 1], V, A[mu - 1], 1, m[mu - 1], false, false,
-                            term));
-    accumulate_kernel<<<grid_for(numel, h->num_sms), 256, 0, h->stream>>>(W, term, numel);
-    MM_CUDA(cudaGetLastError());
-    h->launches++;
-  }
+  for (int mu = 2; mu <= d; ++mu)
+    MM_TRY(mode_product_dev(h, d, m, mu, m[mu - 1], V, A[mu - 1], 1, m[mu - 1], false, false, W, true));
   return MUMODE_OK;
 }
 

@@ -39,6 +39,7 @@ struct TmaParams {
   //   Q blocked: mode 1 {8e, C, K/8} box {8e, BN, BK/8}; mode >1 {8e, K, n/8} box {8e, BK, BN/8}
   // (e = doubles per element). Otherwise one box per 8-element block.
   int p_blocked, q_blocked;
+  int accumulate;  // D += result (kronsumv term accumulation, tucker.hpp:222-231)
 };
 
 // E = doubles per element (1: fp64, 2: complex128). A staged row of 8
@@ -321,7 +322,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
 #pragma unroll
         for (int fn = 0; fn < FN; ++fn) {
           const int n = ntile * BN + nw + 8 * fn + xmap8(g);
-          if (n < p.N) stg_f64x2(base + static_cast<int64_t>(n) * p.ldD, acc[fm][fn][0], acc[fm][fn][1]);
+          if (n >= p.N) continue;
+          double* dst = base + static_cast<int64_t>(n) * p.ldD;
+          if (p.accumulate) {
+            const double2 o = *reinterpret_cast<const double2*>(dst);
+            stg_f64x2(dst, o.x + acc[fm][fn][0], o.y + acc[fm][fn][1]);
+          } else {
+            stg_f64x2(dst, acc[fm][fn][0], acc[fm][fn][1]);
+          }
         }
       } else {
         // D(m) and D(m+4) (xmapc(2t) = t, xmapc(2t+1) = t+4): two 16-byte stores
@@ -332,8 +340,19 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           const int n = ntile * BN + nw + 8 * fn + xmapc(g);
           if (n >= p.N) continue;
           double* col = base + 2 * static_cast<int64_t>(n) * p.ldD;
-          if (m < p.Mlim) stg_f64x2(col, acc[fm][fn][0], acc[fm][fn][2]);
-          if (m + 4 < p.Mlim) stg_f64x2(col + 8, acc[fm][fn][1], acc[fm][fn][3]);
+          double r0 = acc[fm][fn][0], i0 = acc[fm][fn][2], r1 = acc[fm][fn][1], i1 = acc[fm][fn][3];
+          if (p.accumulate) {
+            if (m < p.Mlim) {
+              const double2 o = *reinterpret_cast<const double2*>(col);
+              r0 += o.x, i0 += o.y;
+            }
+            if (m + 4 < p.Mlim) {
+              const double2 o = *reinterpret_cast<const double2*>(col + 8);
+              r1 += o.x, i1 += o.y;
+            }
+          }
+          if (m < p.Mlim) stg_f64x2(col, r0, i0);
+          if (m + 4 < p.Mlim) stg_f64x2(col + 8, r1, i1);
         }
       }
     }

@@ -174,6 +174,27 @@ int main() {
                                 rand_matrix<double>(g, 40, 40)};
     CHECK(rel(ops::tucker(T, Ls), ops::tucker_sequential(T, Ls)) < 1e-13);
   }
+  // itucker: identity factors, 2I divides by 2^d, singular factor refused
+  {
+    auto T = rand_tensor<double>(g, Shape({2, 3, 2}));
+    ops::MatrixStack<double> twoI;
+    for (index_t e : {2, 3, 2}) {
+      Matrix<double> P = Matrix<double>::identity(e);
+      for (index_t i = 0; i < e; ++i) P(i, i) = 2.0;
+      twoI.push_back(P);
+    }
+    auto S = ops::itucker(T, ops::FactorizedStack(twoI));
+    double diff = 0;
+    for (index_t k = 0; k < T.numel(); ++k) diff = std::max(diff, std::abs(S[k] - T[k] / 8.0));
+    CHECK(diff < 1e-15);
+    bool num = false;
+    try {
+      ops::FactorizedStack({Matrix<double>(2, 2)});
+    } catch (const NumericalError&) {
+      num = true;
+    }
+    CHECK(num);
+  }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "PASSED", failures);
   return failures ? 1 : 0;
 }

@@ -147,3 +147,11 @@ def test_expm_matches_reference_expm():
         if ref is not None:
             assert O.rel_fro(got, ref) < 1e-14
     np.testing.assert_array_equal(mm.expm(np.zeros((3, 3))), np.eye(3))
+
+
+def test_factorized_stack_refuses_singular_matrices():
+    # test_tucker_ops.cpp:285-288 (host factorization, no GPU needed)
+    with pytest.raises(mm.NumericalError):
+        mm.FactorizedStack([np.zeros((2, 2))])
+    F = mm.FactorizedStack([np.array([[4.0, 1.0], [2.0, 3.0]])])
+    np.testing.assert_allclose(F.inverses[0] @ np.array([[4.0, 1.0], [2.0, 3.0]]), np.eye(2), atol=1e-15)

@@ -315,6 +315,45 @@ def test_fused_small_square_modes(policy, shape):
     np.testing.assert_array_equal(host(mm.tucker(dev(T), I)), T)
 
 
+def test_kronsumv_fused_epilogue_vs_reference(policy):
+    # W = sum_mu V x_mu A_mu with the terms accumulated in the epilogues, at
+    # TMA-sized shapes, against the reference library's ops::kronsumv
+    rng = np.random.default_rng(21)
+    for shape in [(64, 48, 40), (24, 24, 24, 24), (33, 17, 9)]:
+        V = rnd(rng, shape)
+        As = [rnd(rng, (e, e)) for e in shape]
+        W = host(mm.kronsumv(dev(V), [dev(A) for A in As]))
+        want = O.ref_tucker(V, As, "kronsumv") if O.ref_available() else O.port_kronsumv(V, As)
+        assert O.rel_max(W, want) < 1e-14, shape
+
+
+def test_itucker_restated_reference_cases(policy):
+    # test_tucker_ops.cpp:236-288
+    rng = np.random.default_rng(113)
+    T = rnd(rng, (3, 2, 4))
+    S = host(mm.itucker(dev(T), mm.FactorizedStack([np.eye(3), np.eye(2), np.eye(4)])))
+    assert O.rel_max(S, T) < 1e-15
+    T = rnd(rng, (2, 3, 2))
+    S = host(mm.itucker(dev(T), mm.FactorizedStack([2 * np.eye(e) for e in T.shape])))
+    assert np.max(np.abs(S - T / 8.0)) < 1e-15
+    for _ in range(15):
+        d = int(rng.integers(1, 5))
+        m = [int(x) for x in rng.integers(1, 5, d)]
+        T = rnd(rng, m)
+        Ps = [rnd(rng, (e, e)) + 4.0 * np.eye(e) for e in m]
+        back = host(mm.itucker(mm.tucker(dev(T), [dev(P) for P in Ps]), mm.FactorizedStack(Ps)))
+        assert O.rel_max(back, T) < 1e-10
+    T = rnd(rng, (3, 2))
+    with pytest.raises(mm.SizeError, match="mode 2"):
+        mm.itucker(dev(T), mm.FactorizedStack([np.eye(3), np.eye(3)]))
+    # against the reference's own triangular-solve path, medium size
+    if O.ref_available():
+        T = rnd(rng, (40, 32, 24))
+        Ps = [rnd(rng, (e, e)) + 4.0 * np.eye(e) for e in T.shape]
+        got = host(mm.itucker(dev(T), mm.FactorizedStack(Ps)))
+        assert O.rel_fro(got, O.ref_itucker(T, Ps)) < 1e-13
+
+
 def test_host_and_device_paths_agree_bitwise():
     rng = np.random.default_rng(7)
     T = rnd(rng, (64, 64, 64))
