@@ -92,7 +92,9 @@ struct mumode_handle_s {
   int64_t launches = 0;
   mumode_gpu::DevBuf ws[3];     // Tucker ping-pong intermediates + expint buffer
   mumode_gpu::DevBuf lbuf;      // materialised op(L) for adjoint / promotion
-  mumode_gpu::DevBuf host_in, host_out, host_mats;  // host drop-in staging
+  mumode_gpu::DevBuf host_in, host_out, host_mats, host_mid;  // host drop-in staging
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;         // host drop-in copy engines
+  std::vector<cudaEvent_t> events;                            // pipeline events (reused)
   std::map<mumode_gpu::MapKey, CUtensorMap> maps;
   std::map<std::vector<uint64_t>, mumode_gpu::GraphEntry> graphs;
 };
@@ -655,6 +657,9 @@ int mumode_handle_destroy(mumode_handle_t h) {
   cudaStreamSynchronize(h->stream);
   for (auto& kv : h->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  for (auto e : h->events) cudaEventDestroy(e);
+  if (h->copy_in) cudaStreamDestroy(h->copy_in);
+  if (h->copy_out) cudaStreamDestroy(h->copy_out);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
   return MUMODE_OK;
@@ -875,12 +880,98 @@ static int download(mumode_handle_t h, double* S, size_t el) {
   return MUMODE_OK;
 }
 
+// Pipelined host drop-in for real forward Tucker chains (d >= 2): the input
+// streams in as last-mode slabs on a copy stream while modes 1..d-1 run on
+// each arrived slab (the slabs of the intermediate are contiguous), then the
+// last mode runs in row blocks of L_d whose outputs (contiguous last-mode
+// slabs of S) stream back on a second copy stream. H2D and D2H stay serial
+// (every output needs all of the input) but the compute hides under them.
+static int ensure_pipeline(mumode_handle_t h, size_t nev) {
+  if (!h->copy_in) MM_CUDA(cudaStreamCreateWithFlags(&h->copy_in, cudaStreamNonBlocking));
+  if (!h->copy_out) MM_CUDA(cudaStreamCreateWithFlags(&h->copy_out, cudaStreamNonBlocking));
+  while (h->events.size() < nev) {
+    cudaEvent_t e;
+    MM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h->events.push_back(e);
+  }
+  return MUMODE_OK;
+}
+
+static int host_tucker_pipelined(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                                 const double* T, const double* const* L, double* S) {
+  constexpr int kChunks = 8;
+  MM_TRY(ensure_pipeline(h, 2 * kChunks + 2));
+  cudaEvent_t* ev = h->events.data();
+  const int64_t md = m[d - 1], nd = n[d - 1];
+  const int64_t in_slab = prod(m, 0, d - 1);   // elements per unit of the last input mode
+  const int64_t A = prod(n, 0, d - 1);         // rows of the (A x m_d) intermediate
+  // factors: one contiguous upload
+  size_t mat_bytes = 0;
+  for (int k = 0; k < d; ++k) mat_bytes += ((size_t(m[k] * n[k]) * sizeof(double) + 255) / 256) * 256;
+  MM_TRY(h->host_mats.ensure(mat_bytes + 256));
+  MM_TRY(h->host_in.ensure(size_t(in_slab * md) * sizeof(double)));
+  MM_TRY(h->host_mid.ensure(size_t(A * md) * sizeof(double)));
+  MM_TRY(h->host_out.ensure(size_t(A * nd) * sizeof(double)));
+  std::vector<const double*> dL(d);
+  size_t off = 0;
+  for (int k = 0; k < d; ++k) {
+    const size_t b = size_t(m[k] * n[k]) * sizeof(double);
+    MM_CUDA(cudaMemcpyAsync(static_cast<char*>(h->host_mats.p) + off, L[k], b, cudaMemcpyHostToDevice,
+                            h->copy_in));
+    dL[k] = reinterpret_cast<const double*>(static_cast<char*>(h->host_mats.p) + off);
+    off += ((b + 255) / 256) * 256;
+  }
+  double* dT = static_cast<double*>(h->host_in.p);
+  double* dY = static_cast<double*>(h->host_mid.p);
+  double* dS = static_cast<double*>(h->host_out.p);
+  // input slabs of the last mode (8-aligned boundaries keep TMA bases 16-B aligned)
+  auto bounds = [](int64_t total, int parts, int64_t q, int64_t align) {
+    int64_t step = (total + parts - 1) / parts;
+    step = (step + align - 1) / align * align;
+    return std::min(total, q * step);
+  };
+  const cudaStream_t cs = h->stream;
+  for (int q = 0; q < kChunks; ++q) {
+    const int64_t c0 = bounds(md, kChunks, q, 2), c1 = bounds(md, kChunks, q + 1, 2);
+    if (c1 <= c0) continue;
+    MM_CUDA(cudaMemcpyAsync(dT + c0 * in_slab, T + c0 * in_slab, size_t((c1 - c0) * in_slab) * sizeof(double),
+                            cudaMemcpyHostToDevice, h->copy_in));
+    MM_CUDA(cudaEventRecord(ev[q], h->copy_in));
+  }
+  for (int q = 0; q < kChunks; ++q) {
+    const int64_t c0 = bounds(md, kChunks, q, 2), c1 = bounds(md, kChunks, q + 1, 2);
+    if (c1 <= c0) continue;
+    MM_CUDA(cudaStreamWaitEvent(cs, ev[q], 0));
+    std::vector<int64_t> ms(m, m + d), ns(n, n + d);
+    ms[d - 1] = ns[d - 1] = c1 - c0;
+    MM_TRY(tucker_dev(h, d, ms.data(), ns.data(), dT + c0 * in_slab, dL.data(), dY + c0 * A, false, false, 1,
+                      d - 1));
+  }
+  // last mode in row blocks of L_d -> contiguous slabs of S, streamed back
+  const int64_t ym[2] = {A, md};
+  for (int q = 0; q < kChunks; ++q) {
+    const int64_t i0 = bounds(nd, kChunks, q, 8), i1 = bounds(nd, kChunks, q + 1, 8);
+    if (i1 <= i0) continue;
+    MM_TRY(mode_product_dev(h, 2, ym, 2, i1 - i0, dY, dL[d - 1] + i0, 1, nd, false, false, dS + i0 * A));
+    MM_CUDA(cudaEventRecord(ev[kChunks + q], cs));
+    MM_CUDA(cudaStreamWaitEvent(h->copy_out, ev[kChunks + q], 0));
+    MM_CUDA(cudaMemcpyAsync(S + i0 * A, dS + i0 * A, size_t((i1 - i0) * A) * sizeof(double), cudaMemcpyDeviceToHost,
+                            h->copy_out));
+  }
+  MM_CUDA(cudaStreamSynchronize(h->copy_out));
+  MM_CUDA(cudaStreamSynchronize(cs));
+  return MUMODE_OK;
+}
+
 static int host_tucker_impl(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
                             const double* T, const double* const* L, double* S, int adjoint,
                             int t_el, int l_el) {
   if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
   MM_TRY(check_stack(d, m, n, T, L, S, adjoint ? "cttucker" : "tucker"));
   MM_CUDA(cudaSetDevice(h->device));
+  if (d >= 2 && !adjoint && t_el == 1 && l_el == 1 && m[d - 1] >= 16 && n[d - 1] >= 16 &&
+      prod(m, 0, d) >= (int64_t(1) << 20))
+    return host_tucker_pipelined(h, d, m, n, T, L, S);
   std::vector<int64_t> lsz(d);
   for (int k = 0; k < d; ++k) lsz[k] = m[k] * n[k] * l_el;
   const double* dT;

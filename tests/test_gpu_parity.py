@@ -354,6 +354,21 @@ def test_itucker_restated_reference_cases(policy):
         assert O.rel_fro(got, O.ref_itucker(T, Ps)) < 1e-13
 
 
+@pytest.mark.parametrize("m,n", [((100, 90, 130), (96, 120, 72)), ((128, 128, 64), (128, 128, 64)),
+                                 ((24, 24, 24, 24, 24), (24, 24, 24, 24, 24)), ((1024, 1030), (512, 258))])
+def test_pipelined_host_path_bitwise_equals_device_path(m, n):
+    # the host drop-in streams slabs through copy engines; same math as the
+    # device path, element for element
+    rng = np.random.default_rng(31)
+    T = rnd(rng, m)
+    Ls = [rnd(rng, (n[k], m[k])) for k in range(len(m))]
+    Sh = mm.tucker(T, Ls)
+    Sd = host(mm.tucker(dev(T), [dev(L) for L in Ls]))
+    np.testing.assert_array_equal(Sh, Sd)
+    if len(m) == 3:
+        assert O.rel_fro(Sh, O.port_tucker(T, Ls)) < 1e-14
+
+
 def test_host_and_device_paths_agree_bitwise():
     rng = np.random.default_rng(7)
     T = rnd(rng, (64, 64, 64))
