@@ -134,3 +134,34 @@ def test_c2_properties_at_full_size():
     two = mm.tucker(mm.tucker(T1, Ls), Bs)
     one = mm.tucker(T1, [B @ L for B, L in zip(Bs, Ls)])
     assert (torch.linalg.vector_norm(two - one) / torch.linalg.vector_norm(one)).item() < 1e-12
+
+
+def test_more_than_2_31_elements():
+    # int64 extents end to end: the reference's GEMM seam casts every dimension
+    # to int (src/gemm.cpp:55-57). 64 x 32776 x 1024 = 2.148e9 > 2^31 elements
+    # (17.2 GB). Identity factors must reproduce T exactly on modes 1 and 3;
+    # for a rectangular factor on mode 2, summing S over i equals the product
+    # with the column-sum row of L2 (linearity, size independent).
+    if torch.cuda.get_device_properties(0).total_memory < 80e9:
+        pytest.skip("needs a large-HBM GPU")
+    shape = (64, 32776, 1024)
+    assert np.prod(shape) > 2 ** 31
+    T = mm.colmajor_empty(shape, torch.float64, "cuda")
+    T.uniform_(-1, 1)
+    I1 = torch.eye(64, dtype=torch.float64, device="cuda")
+    S = mm.mode_product(T, I1, 1)
+    assert torch.equal(S, T)
+    del S
+    I3 = torch.eye(1024, dtype=torch.float64, device="cuda")
+    S = mm.mode_product(T, I3, 3)
+    assert torch.equal(S, T)
+    del S
+    g = torch.Generator(device="cuda").manual_seed(5)
+    L2 = mm.to_colmajor(torch.rand(4, 32776, dtype=torch.float64, device="cuda", generator=g))
+    S = mm.mode_product(T, L2, 2)              # 64 x 4 x 1024
+    colsum = mm.to_colmajor(L2.sum(dim=0, keepdim=True))
+    R = mm.mode_product(T, colsum, 2)          # 64 x 1 x 1024
+    lhs = S.sum(dim=1)
+    rhs = R[:, 0, :]
+    err = (torch.linalg.vector_norm(lhs - rhs) / torch.linalg.vector_norm(rhs)).item()
+    assert err < 1e-13, err
