@@ -88,6 +88,18 @@ int main() {
     std::printf("{\"variant\": \"dmma_m8n8k4_acc8\", \"blocks_per_sm\": %d, \"ms\": %.3f, \"tflops\": %.3f}\n",
                 bps, ms, flops / ms / 1e9);
   }
+  // one warp per SMSP (128-thread CTA, 1 CTA/SM): can a single warp keep the
+  // DMMA pipe busy with enough independent accumulators?
+  for (int acc : {4, 8, 16}) {
+    const int blocks = sms, iters = 4096, thr = 128;
+    float ms;
+    if (acc == 4) ms = time_it([&] { dmma_kernel<4><<<blocks, thr>>>(out, iters, 0.999, 1e-3); }, 5);
+    else if (acc == 8) ms = time_it([&] { dmma_kernel<8><<<blocks, thr>>>(out, iters, 0.999, 1e-3); }, 5);
+    else ms = time_it([&] { dmma_kernel<16><<<blocks, thr>>>(out, iters, 0.999, 1e-3); }, 5);
+    double flops = 2.0 * 256 * (thr / 32) * double(blocks) * iters * 4 * acc;
+    std::printf("{\"variant\": \"dmma_1warp_per_smsp_acc%d\", \"ms\": %.3f, \"tflops\": %.3f}\n", acc, ms,
+                flops / ms / 1e9);
+  }
   CK(cudaGetLastError());
   return 0;
 }
