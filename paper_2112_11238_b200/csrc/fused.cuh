@@ -19,24 +19,35 @@
 // tensor. The mode-mu result goes to a padded shared buffer Y (one pad row
 // per 64-B-row slab, software 64B swizzle) whose 16-byte writes and fragment
 // reads are both bank-optimal; mode mu+1 reads Y and stores the final values
-// straight to HBM as 16-byte stores. The tensor tile is double buffered: the
-// producer warp's TMA for tile i+1 overlaps tile i's math and stores.
+// straight to HBM as 16-byte stores. The tensor tile ring is 2-4 deep (as deep
+// as shared memory allows): the producer warp keeps several TMA boxes in
+// flight so HBM latency (each box row of the last pass of 24^6 lies 2.65 MB
+// from the next) is covered while earlier tiles compute and store.
 #pragma once
 #include "common.cuh"
 
 namespace mumode_gpu {
 
-template <int MU, bool FIRST>
+// RA = a's per tile for FIRST == false (8 or 16: 16 halves the number of
+// scattered 64-B box rows per byte when the a-stride is large).
+template <int MU, bool FIRST, int RA = 8>
 struct FusedCfg {
   static constexpr int NF = MU / 8;   // 8-wide output fragments per mode
   static constexpr int KS = MU / 4;   // k-steps per contraction
-  static constexpr int WARPS = 8;     // consumer warps; MU units per mode, MU/8 per warp
+  static constexpr int WARPS = 8;     // consumer warps
+  static constexpr int AH = FIRST ? 1 : RA / 8;  // 8-a halves per tile
+  static constexpr int UNITS = MU * AH;          // units per mode (UNITS / 8 per warp)
   static constexpr int THREADS = (WARPS + 1) * 32;
-  static constexpr int X_BYTES = 8 * MU * MU * 8;
-  static constexpr int Y_ROWS = (FIRST ? 8 * NF : MU) * (MU + 1);
+  static constexpr int X_BYTES = 8 * AH * MU * MU * 8;
+  static constexpr int Y_ROWS = (FIRST ? 8 * NF : AH * MU) * (MU + 1);
   static constexpr int Y_BYTES = Y_ROWS * 64;
-  static constexpr int SMEM_BYTES = 2 * X_BYTES + Y_BYTES + 1024 + 64;
+  // tensor-tile ring depth: enough bytes in flight per SM to cover HBM latency
+  // (Little's law: ~90 KB at ~2 us), within the 227 KB shared-memory limit
+  static constexpr int NBUF = (4 * X_BYTES + Y_BYTES + 2048 <= 227 * 1024) ? 4
+                              : (3 * X_BYTES + Y_BYTES + 2048 <= 227 * 1024) ? 3 : 2;
+  static constexpr int SMEM_BYTES = NBUF * X_BYTES + Y_BYTES + 1024 + 128;
   static_assert(MU % 8 == 0 && MU >= 8 && MU <= 32, "square modes of 8..32");
+  static_assert(RA == 8 || RA == 16, "8 or 16 a's per tile");
 };
 
 struct FusedParams {
@@ -53,20 +64,22 @@ __device__ __forceinline__ uint32_t y_off(int r, int x) {
   return static_cast<uint32_t>(r * 64 + ((((x >> 1) ^ ((r >> 1) & 3))) << 4) + (x & 1) * 8);
 }
 
-template <int MU, bool FIRST>
-__global__ void __launch_bounds__(FusedCfg<MU, FIRST>::THREADS, 1)
+template <int MU, bool FIRST, int RA>
+__global__ void __launch_bounds__(FusedCfg<MU, FIRST, RA>::THREADS, 1)
     fused_pair_kernel(const __grid_constant__ CUtensorMap mapX, const FusedParams p) {
-  using Cfg = FusedCfg<MU, FIRST>;
+  using Cfg = FusedCfg<MU, FIRST, RA>;
+  constexpr int AH = Cfg::AH;
   constexpr int NF = Cfg::NF, KS = Cfg::KS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* Y = smem + 2 * Cfg::X_BYTES;
+  constexpr int NBUF = Cfg::NBUF;
+  uint8_t* Y = smem + NBUF * Cfg::X_BYTES;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(Y + Cfg::Y_BYTES);
-  uint64_t* empty_bar = full_bar + 2;
+  uint64_t* empty_bar = full_bar + NBUF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NBUF; ++b) {
       mbar_init(&full_bar[b], 1);
       mbar_init(&empty_bar[b], Cfg::WARPS);
     }
@@ -80,7 +93,7 @@ __global__ void __launch_bounds__(FusedCfg<MU, FIRST>::THREADS, 1)
       tma_prefetch_desc(&mapX);
       int buf = 0;
       uint32_t phase = 0;
-      const int64_t ablks = FIRST ? 1 : p.A / 8;
+      const int64_t ablks = FIRST ? 1 : p.A / RA;
       for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
         mbar_wait(&empty_bar[buf], phase ^ 1);
         mbar_arrive_expect_tx(&full_bar[buf], Cfg::X_BYTES);
@@ -89,9 +102,12 @@ __global__ void __launch_bounds__(FusedCfg<MU, FIRST>::THREADS, 1)
           tma_load_3d(dst, &mapX, &full_bar[buf], 0, static_cast<int32_t>(tile * 8 * MU), 0);
         } else {
           const int64_t c = tile / ablks, ab = tile - c * ablks;
-          tma_load_4d(dst, &mapX, &full_bar[buf], static_cast<int32_t>(8 * ab), 0, 0, static_cast<int32_t>(c));
+#pragma unroll
+          for (int hh = 0; hh < AH; ++hh)
+            tma_load_4d(dst + hh * (MU * MU * 64), &mapX, &full_bar[buf], static_cast<int32_t>(RA * ab + 8 * hh), 0,
+                        0, static_cast<int32_t>(c));
         }
-        if (++buf == 2) {
+        if (++buf == NBUF) {
           buf = 0;
           phase ^= 1;
         }
@@ -122,15 +138,15 @@ __global__ void __launch_bounds__(FusedCfg<MU, FIRST>::THREADS, 1)
 
   int buf = 0;
   uint32_t phase = 0;
-  const int64_t ablks = FIRST ? 1 : p.A / 8;
+  const int64_t ablks = FIRST ? 1 : p.A / RA;
   for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
     mbar_wait(&full_bar[buf], phase);
     const uint8_t* X = smem + buf * Cfg::X_BYTES;
 
     // ---- mode mu: X -> Y
 #pragma unroll
-    for (int uu = 0; uu < MU / 8; ++uu) {
-      const int u = warp + 8 * uu;
+    for (int uu = 0; uu < Cfg::UNITS / 8; ++uu) {
+      const int u = warp + 8 * uu;  // FIRST: fibre fragment; else (a-half, b2) = (u / MU, u % MU)
       double acc[NF][2];
 #pragma unroll
       for (int nf = 0; nf < NF; ++nf) acc[nf][0] = acc[nf][1] = 0.0;
@@ -144,7 +160,7 @@ __global__ void __launch_bounds__(FusedCfg<MU, FIRST>::THREADS, 1)
 #pragma unroll
           for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[nf][0], acc[nf][1], xf, l1[nf][s]);
         } else {
-          // B = X fragment (k = b1 = 4s + t, a = xmap8(g)) in slab b2 = u, XK layout
+          // B = X fragment (k = b1 = 4s + t, a = xmap8(g)) in slab (a-half, b2) = u, XK layout
           const double xf = *reinterpret_cast<const double*>(X + u * (MU * 64) + (4 * s) * 64 + xk_off + Js);
 #pragma unroll
           for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[nf][0], acc[nf][1], l1[nf][s], xf);
@@ -160,10 +176,11 @@ __global__ void __launch_bounds__(FusedCfg<MU, FIRST>::THREADS, 1)
           *reinterpret_cast<double2*>(Y + y_off(r, xmap8(2 * t))) = make_double2(acc[nf][0], acc[nf][1]);
         }
       } else {
-        // D[g <-> i = 8nf + g][a pair = xmap8(2t)] -> Y row (i, b2 = u)
+        // D[g <-> i = 8nf + g][a pair = xmap8(2t)] -> Y row (a-half, i, b2)
+        const int ah = u / MU, b2 = u % MU;
 #pragma unroll
         for (int nf = 0; nf < NF; ++nf) {
-          const int r = (8 * nf + g) * (MU + 1) + u;
+          const int r = (ah * MU + 8 * nf + g) * (MU + 1) + b2;
           *reinterpret_cast<double2*>(Y + y_off(r, xmap8(2 * t))) = make_double2(acc[nf][0], acc[nf][1]);
         }
       }
@@ -178,11 +195,11 @@ __global__ void __launch_bounds__(FusedCfg<MU, FIRST>::THREADS, 1)
       c_base = tile * 8;
     } else {
       c_base = tile / ablks;
-      a_base = 8 * (tile - c_base * ablks);
+      a_base = RA * (tile - c_base * ablks);
     }
 #pragma unroll
-    for (int uu = 0; uu < MU / 8; ++uu) {
-      const int u = warp + 8 * uu;  // FIRST: (cl, ib) = (u / NF, u % NF); else i = u
+    for (int uu = 0; uu < Cfg::UNITS / 8; ++uu) {
+      const int u = warp + 8 * uu;  // FIRST: (cl, ib) = (u / NF, u % NF); else (a-half, i)
       double acc[NF][2];
 #pragma unroll
       for (int nf = 0; nf < NF; ++nf) acc[nf][0] = acc[nf][1] = 0.0;
@@ -206,16 +223,18 @@ __global__ void __launch_bounds__(FusedCfg<MU, FIRST>::THREADS, 1)
           }
         }
       } else {
+        const int ah = u / MU, i = u % MU;
 #pragma unroll
         for (int nf = 0; nf < NF; ++nf) {
           const int j = 8 * nf + g;
-          stg_f64x2(p.S + a_base + x + p.A * (u + static_cast<int64_t>(MU) * (j + static_cast<int64_t>(MU) * c_base)),
+          stg_f64x2(p.S + a_base + 8 * ah + x +
+                        p.A * (i + static_cast<int64_t>(MU) * (j + static_cast<int64_t>(MU) * c_base)),
                     acc[nf][0], acc[nf][1]);
         }
       }
     }
     named_barrier_sync(1, Cfg::WARPS * 32);  // Y free for the next tile
-    if (++buf == 2) {
+    if (++buf == NBUF) {
       buf = 0;
       phase ^= 1;
     }

@@ -452,10 +452,10 @@ static int run_job(mumode_handle_s* h, const ModeJob& j) {
 }
 
 // ------------------------------------------------------------------ fused pairs
-template <int MU, bool FIRST>
+template <int MU, bool FIRST, int RA>
 static int launch_fused(mumode_handle_s* h, const double* T, double* S, const double* L1,
                         const double* L2, int64_t A, int64_t C) {
-  using Cfg = FusedCfg<MU, FIRST>;
+  using Cfg = FusedCfg<MU, FIRST, RA>;
   const CUtensorMap* mp = nullptr;
   FusedParams p{S, L1, L2, A, C, 0};
   if (FIRST) {
@@ -468,10 +468,10 @@ static int launch_fused(mumode_handle_s* h, const double* T, double* S, const do
     uint64_t st[3] = {uint64_t(A), uint64_t(A) * MU, uint64_t(A) * MU * MU};
     uint32_t b[4] = {8, MU, MU, 1};
     MM_TRY(get_map(h, T, 4, d, st, b, &mp));
-    p.tiles = (A / 8) * C;
+    p.tiles = (A / RA) * C;
   }
   const int grid = static_cast<int>(p.tiles < h->num_sms ? p.tiles : h->num_sms);
-  auto k = fused_pair_kernel<MU, FIRST>;
+  auto k = fused_pair_kernel<MU, FIRST, RA>;
   MM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
   k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mp, p);
   MM_CUDA(cudaGetLastError());
@@ -482,8 +482,12 @@ static int launch_fused(mumode_handle_s* h, const double* T, double* S, const do
 template <int MU>
 static int launch_fused_mu(mumode_handle_s* h, bool first, const double* T, double* S,
                            const double* L1, const double* L2, int64_t A, int64_t C) {
-  return first ? launch_fused<MU, true>(h, T, S, L1, L2, A, C)
-               : launch_fused<MU, false>(h, T, S, L1, L2, A, C);
+  if (first) return launch_fused<MU, true, 8>(h, T, S, L1, L2, A, C);
+  // 16 a's per tile when shared memory allows it and A tiles evenly
+  constexpr bool wide_fits = FusedCfg<MU, false, 16>::SMEM_BYTES <= 227 * 1024 &&
+                             FusedCfg<MU, false, 16>::NBUF >= 2;
+  if (wide_fits && A % 16 == 0 && A <= 4096) return launch_fused<MU, false, (wide_fits ? 16 : 8)>(h, T, S, L1, L2, A, C);
+  return launch_fused<MU, false, 8>(h, T, S, L1, L2, A, C);
 }
 
 // Fused two-mode passes apply to real, forward chains whose modes are all
