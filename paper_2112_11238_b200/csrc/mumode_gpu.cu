@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <unordered_map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -74,7 +75,14 @@ struct DevBuf {
   }
 };
 
-using MapKey = std::vector<uint64_t>;  // base, rank, dims, strides, box
+using MapKey = std::vector<uint64_t>;  // base, rank, swizzle, dims, strides, box
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const noexcept {
+    uint64_t h = 1469598103934665603ull;
+    for (uint64_t v : k) h = (h ^ v) * 1099511628211ull;
+    return static_cast<size_t>(h);
+  }
+};
 
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
@@ -95,11 +103,27 @@ struct mumode_handle_s {
   mumode_gpu::DevBuf host_in, host_out, host_mats, host_mid;  // host drop-in staging
   cudaStream_t copy_in = nullptr, copy_out = nullptr;         // host drop-in copy engines
   std::vector<cudaEvent_t> events;                            // pipeline events (reused)
-  std::map<mumode_gpu::MapKey, CUtensorMap> maps;
+  std::unordered_map<mumode_gpu::MapKey, CUtensorMap, mumode_gpu::MapKeyHash> maps;
   std::map<std::vector<uint64_t>, mumode_gpu::GraphEntry> graphs;
 };
 
 namespace mumode_gpu {
+
+// Opt a kernel instance into its dynamic shared memory once per process
+// (keyed by the kernel's address; attributes are per function, not per device
+// for the single-architecture build).
+template <class K>
+static int smem_opt_in(K kernel, int bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> done;
+  const void* key = reinterpret_cast<const void*>(kernel);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return MUMODE_OK;
+  MM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done[key] = bytes;
+  return MUMODE_OK;
+}
 
 // ------------------------------------------------------------------ TMA maps
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -393,7 +417,6 @@ static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
     p.AB = int(AB);
     p.mfrags = AB * j.C;
   }
-  p.accumulate = j.accumulate ? 1 : 0;
   p.K = int(j.K);
   p.mt = int((p.mfrags + Cfg::BM / 8 - 1) / (Cfg::BM / 8));
   p.nt = (p.N + Cfg::BN - 1) / Cfg::BN;
@@ -401,11 +424,19 @@ static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
   const int grid = static_cast<int>(p.tiles < h->num_sms ? p.tiles : h->num_sms);
   if (mode1) {
     auto k = modeprod_tma_kernel<Cfg, true>;
-    MM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
     k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mp, *mq, p);
+  } else if (j.accumulate) {
+    if constexpr (Cfg::E == 1) {
+      auto k = modeprod_tma_kernel<Cfg, false, true>;
+      MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
+      k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mp, *mq, p);
+    } else {
+      return fail(MUMODE_ERR_ARGUMENT, "accumulating complex mode product is not compiled");
+    }
   } else {
     auto k = modeprod_tma_kernel<Cfg, false>;
-    MM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
     k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mp, *mq, p);
   }
   MM_CUDA(cudaGetLastError());
@@ -445,7 +476,8 @@ static int launch_generic(mumode_handle_s* h, const ModeJob& j) {
 }
 
 static int run_job(mumode_handle_s* h, const ModeJob& j) {
-  const bool can_tma = tma_ok(j);
+  // accumulating products: real mu > 1 have a TMA instantiation; others generic
+  const bool can_tma = tma_ok(j) && !(j.accumulate && (j.A == 1 || j.cplx));
   if (h->policy == 1 || !can_tma) return launch_generic(h, j);
   if ((h->policy >= 2 && h->policy <= 6) || tma_worthwhile(j)) return launch_tma_auto(h, j);
   return launch_generic(h, j);
@@ -472,7 +504,7 @@ static int launch_fused(mumode_handle_s* h, const double* T, double* S, const do
   }
   const int grid = static_cast<int>(p.tiles < h->num_sms ? p.tiles : h->num_sms);
   auto k = fused_pair_kernel<MU, FIRST, RA>;
-  MM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+  MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
   k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mp, p);
   MM_CUDA(cudaGetLastError());
   h->launches++;

@@ -39,7 +39,6 @@ struct TmaParams {
   //   Q blocked: mode 1 {8e, C, K/8} box {8e, BN, BK/8}; mode >1 {8e, K, n/8} box {8e, BK, BN/8}
   // (e = doubles per element). Otherwise one box per 8-element block.
   int p_blocked, q_blocked;
-  int accumulate;  // D += result (kronsumv term accumulation, tucker.hpp:222-231)
 };
 
 // E = doubles per element (1: fp64, 2: complex128). A staged row of 8
@@ -89,7 +88,9 @@ struct TmaCfg {
 
 // QK == true  (mu == 1): P = L (XK), Q = T (KX)
 // QK == false (mu  > 1): P = T (XK, fragment list over (a-block, c)), Q = L (XK)
-template <class Cfg, bool QK>
+// ACC: D += result (kronsumv term accumulation, tucker.hpp:222-231); a
+// compile-time switch -- a runtime branch in the epilogue costs ~2 % on C2.
+template <class Cfg, bool QK, bool ACC = false>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
     modeprod_tma_kernel(const __grid_constant__ CUtensorMap mapP,
                         const __grid_constant__ CUtensorMap mapQ, const TmaParams p) {
@@ -324,7 +325,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           const int n = ntile * BN + nw + 8 * fn + xmap8(g);
           if (n >= p.N) continue;
           double* dst = base + static_cast<int64_t>(n) * p.ldD;
-          if (p.accumulate) {
+          if constexpr (ACC) {
             const double2 o = *reinterpret_cast<const double2*>(dst);
             stg_f64x2(dst, o.x + acc[fm][fn][0], o.y + acc[fm][fn][1]);
           } else {
@@ -341,7 +342,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           if (n >= p.N) continue;
           double* col = base + 2 * static_cast<int64_t>(n) * p.ldD;
           double r0 = acc[fm][fn][0], i0 = acc[fm][fn][2], r1 = acc[fm][fn][1], i1 = acc[fm][fn][3];
-          if (p.accumulate) {
+          if constexpr (ACC) {
             if (m < p.Mlim) {
               const double2 o = *reinterpret_cast<const double2*>(col);
               r0 += o.x, i0 += o.y;
