@@ -111,6 +111,16 @@ int mumode_slab_pack_f64(mumode_handle_t h, int64_t A, int64_t C, int P, const i
 int mumode_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double* V,
                         const double* const* A, double* W);
 
+/* Direct solve with the Kronecker sum of d symmetric factors
+ * M_mu = Q_mu diag(evals_mu) Q_mu^T: x = tucker(tucker(b, Q^T) ./ Lambda, Q),
+ * Lambda(j) = evals_1[j_1] + ... + evals_d[j_d] -- the IMEX direct backend's
+ * solve (apps DirectSolver::solve, src/imex.cpp:67-86). Q, Qt (= Q^T) are
+ * device m_mu x m_mu matrices; evals are HOST arrays (small). A zero
+ * denominator returns MUMODE_ERR_NUMERICAL like the reference. */
+int mumode_kronsum_solve_f64(mumode_handle_t h, int d, const int64_t* m, const double* const* Q,
+                             const double* const* Qt, const double* const* evals, const double* b,
+                             double* x);
+
 /* Exponential-integrator march (apps::linear_evolution_exact applied
  * repeatedly, src/evolution.cpp:70-82): u <- tucker(u; E_1..E_d) `steps`
  * times with square E_mu; u0 and u_out may alias. Captured in a CUDA graph

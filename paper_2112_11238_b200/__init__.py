@@ -9,6 +9,7 @@ from .api import (  # noqa: F401
     CudaError,
     FactorizedStack,
     Handle,
+    KronSumSolver,
     MumodeError,
     NumericalError,
     Rng,

@@ -38,6 +38,7 @@ SIGNATURES = {
     "mumode_slab_pack_f64": (ctypes.c_int, [H, I64, I64, ctypes.c_int, I64P, VP, VP]),
     "mumode_kronsumv_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, VP, ctypes.POINTER(VP), VP]),
     "mumode_expint_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, ctypes.POINTER(VP), VP, VP, ctypes.c_int]),
+    "mumode_kronsum_solve_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, ctypes.POINTER(VP), ctypes.POINTER(VP), ctypes.POINTER(VP), VP, VP]),
     "mumode_host_mode_product_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, ctypes.c_int, I64, VP, VP, VP]),
     "mumode_host_mode_product_c128": (ctypes.c_int, [H, ctypes.c_int, I64P, ctypes.c_int, I64, VP, VP, VP]),
     "mumode_host_tucker_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),

@@ -418,6 +418,56 @@ def itucker(T, F: FactorizedStack):
     return tucker(T, F.inverses)
 
 
+class KronSumSolver:
+    """Direct solver for (sum_mu I x ... x M_mu x ... x I) x = b with symmetric
+    M_mu = Q_mu diag(evals_mu) Q_mu^T -- the IMEX direct backend
+    (DirectSolver, src/imex.cpp:53-86): two Tucker applications around a
+    pointwise division by the eigenvalue Kronecker sum, on the GPU. The
+    eigendecompositions are host preprocessing (given, or numpy.linalg.eigh
+    here when built from the M_mu)."""
+
+    def __init__(self, Ms=None, Qs=None, evals=None, device=None):
+        if Ms is not None:
+            Qs, evals = [], []
+            for M in Ms:
+                Mn = np.asarray(M.cpu() if _is_torch(M) else M, dtype=np.float64)
+                w, V = np.linalg.eigh(0.5 * (Mn + Mn.T))
+                Qs.append(np.asfortranarray(V))
+                evals.append(np.ascontiguousarray(w))
+        self.evals = [np.ascontiguousarray(np.asarray(e, dtype=np.float64)) for e in evals]
+        self.Q = [np.asfortranarray(np.asarray(Q, dtype=np.float64)) for Q in Qs]
+        self.Qt = [np.asfortranarray(Q.T) for Q in self.Q]
+        self._dev = {}
+
+    def _device_mats(self, device):
+        key = str(device)
+        if key not in self._dev:
+            self._dev[key] = ([torch.from_numpy(Q).to(device) for Q in self.Q],
+                              [torch.from_numpy(Q).to(device) for Q in self.Qt])
+        return self._dev[key]
+
+    def solve(self, b):
+        _validate_tensor(b)
+        d = b.ndim
+        if len(self.Q) != d:
+            raise SizeError("kronsum_solve: stack length does not match tensor order")
+        for mu in range(1, d + 1):
+            if self.Q[mu - 1].shape != (int(b.shape[mu - 1]),) * 2:
+                raise SizeError(f"kronsum_solve: factor size does not match extent of mode {mu}")
+        m = _extents(b)
+        host_in = not _is_torch(b)
+        bd = torch.from_numpy(_np_f(b, False)).cuda() if host_in else to_colmajor(b)
+        h = get_handle(bd.device.index)
+        h.bind_torch_stream()
+        Qd, Qtd = self._device_mats(bd.device)
+        x = colmajor_empty(m, torch.float64, bd.device)
+        ev_ptrs = _lib.ptr_array([e.ctypes.data for e in self.evals])
+        _check(_lib.lib().mumode_kronsum_solve_f64(
+            h.h, d, _lib.i64_array(m), _lib.ptr_array([Q.data_ptr() for Q in Qd]),
+            _lib.ptr_array([Q.data_ptr() for Q in Qtd]), ev_ptrs, bd.data_ptr(), x.data_ptr()))
+        return x.cpu().numpy() if host_in else x
+
+
 def expm(A) -> np.ndarray:
     """Matrix exponential on the host (scaling and squaring, Pade 13)."""
     An = _np_f(np.asarray(A), False)

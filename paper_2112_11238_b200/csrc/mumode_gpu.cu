@@ -226,6 +226,18 @@ __global__ void slab_pack_kernel(const double* __restrict__ Y, double* __restric
   }
 }
 
+// w(a, n) /= (esum_front[a] + ev_last[n]) for the direct Kronecker-sum solve;
+// denominators summed in the reference's order (imex.cpp:70-77).
+__global__ void eigsum_divide_kernel(double* __restrict__ w, const double* __restrict__ esum_front,
+                                     const double* __restrict__ ev_last, int64_t A, int64_t N) {
+  const int64_t total = A * N;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t a = e % A, n = e / A;
+    w[e] /= (esum_front[a] + ev_last[n]);
+  }
+}
+
 static int grid_for(int64_t n, int sms) {
   int64_t b = (n + 255) / 256;
   int64_t cap = int64_t(sms) * 8;
@@ -785,6 +797,51 @@ int mumode_slab_pack_f64(mumode_handle_t h, int64_t A, int64_t C, int P, const i
   slab_pack_kernel<<<grid_for(A * C, h->num_sms), 256, 0, h->stream>>>(Y, send, A, C, P, off);
   MM_CUDA(cudaGetLastError());
   h->launches++;
+  return MUMODE_OK;
+}
+
+int mumode_kronsum_solve_f64(mumode_handle_t h, int d, const int64_t* m, const double* const* Q,
+                             const double* const* Qt, const double* const* evals, const double* b,
+                             double* x) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  MM_TRY(check_stack(d, m, m, b, Q, x, "kronsum_solve"));
+  if (!Qt || !evals) return fail(MUMODE_ERR_ARGUMENT, "kronsum_solve: null pointer");
+  for (int k = 0; k < d; ++k)
+    if (!Qt[k] || !evals[k])
+      return fail(MUMODE_ERR_ARGUMENT, "kronsum_solve: null data for mode " + std::to_string(k + 1));
+  MM_CUDA(cudaSetDevice(h->device));
+  const int64_t numel = prod(m, 0, d);
+  const int64_t A = prod(m, 0, d - 1), N = m[d - 1];
+  // eigenvalue sums over modes 1..d-1 (the reference adds mode by mode from 0)
+  std::vector<double> esum(static_cast<size_t>(A + N));
+  std::vector<int64_t> j(static_cast<size_t>(d), 0);
+  for (int64_t a = 0; a < A; ++a) {
+    double s = 0.0;
+    for (int k = 0; k < d - 1; ++k) s += evals[k][j[k]];
+    esum[static_cast<size_t>(a)] = s;
+    for (int k = 0; k < d - 1; ++k) {
+      if (++j[k] < m[k]) break;
+      j[k] = 0;
+    }
+  }
+  for (int64_t n = 0; n < N; ++n) {
+    esum[static_cast<size_t>(A + n)] = evals[d - 1][n];
+    for (int64_t a = 0; a < A; ++a)
+      if (esum[static_cast<size_t>(a)] + evals[d - 1][n] == 0.0)
+        return fail(MUMODE_ERR_NUMERICAL, "imex direct backend: singular implicit operator");
+  }
+  MM_TRY(h->ws[2].ensure(size_t(numel) * sizeof(double)));
+  MM_TRY(h->lbuf.ensure(esum.size() * sizeof(double)));
+  double* w = static_cast<double*>(h->ws[2].p);
+  double* dsum = static_cast<double*>(h->lbuf.p);
+  MM_CUDA(cudaMemcpyAsync(dsum, esum.data(), esum.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  MM_TRY(tucker_dev(h, d, m, m, b, Qt, w, false, false));
+  eigsum_divide_kernel<<<grid_for(numel, h->num_sms), 256, 0, h->stream>>>(w, dsum, dsum + A, A, N);
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  MM_TRY(tucker_dev(h, d, m, m, w, Q, x, false, false));
+  // the host staging of esum must outlive the async copy
+  MM_CUDA(cudaStreamSynchronize(h->stream));
   return MUMODE_OK;
 }
 
