@@ -29,11 +29,6 @@ namespace mumode_gpu {
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 
-struct Status {
-  int code;
-  std::string msg;
-};
-
 #define MM_CUDA(call)                                                                  \
   do {                                                                                 \
     cudaError_t e_ = (call);                                                           \
@@ -889,7 +884,7 @@ int mumode_expint_f64(mumode_handle_t h, int d, const int64_t* m, const double* 
   double* spare = static_cast<double*>(h->ws[2].p);
   // Graph key: shape, pointers, steps.
   std::vector<uint64_t> key{uint64_t(d), uint64_t(steps), reinterpret_cast<uint64_t>(u0),
-                            reinterpret_cast<uint64_t>(u_out)};
+                            reinterpret_cast<uint64_t>(u_out), uint64_t(h->policy)};
   for (int k = 0; k < d; ++k) {
     key.push_back(uint64_t(m[k]));
     key.push_back(reinterpret_cast<uint64_t>(E[k]));
@@ -911,7 +906,6 @@ int mumode_expint_f64(mumode_handle_t h, int d, const int64_t* m, const double* 
   if (it == h->graphs.end()) {
     // First call: run eagerly (allocates workspace, encodes TMA maps), then
     // capture the identical launch sequence for later calls.
-    const int64_t before = h->launches;
     MM_TRY(body());
     GraphEntry ge;
     cudaGraph_t graph = nullptr;
@@ -919,7 +913,11 @@ int mumode_expint_f64(mumode_handle_t h, int d, const int64_t* m, const double* 
     // captured); nothing executes during capture. Replays go to h->stream.
     cudaStream_t user = h->stream;
     h->stream = h->own_stream;
-    MM_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    if (cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      h->stream = user;
+      cudaGetLastError();
+      return fail(MUMODE_ERR_CUDA, "graph capture could not begin");
+    }
     const int64_t l0 = h->launches;
     int rc = body();
     cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
@@ -931,7 +929,6 @@ int mumode_expint_f64(mumode_handle_t h, int d, const int64_t* m, const double* 
     MM_CUDA(cudaGraphInstantiate(&ge.exec, graph, 0));
     cudaGraphDestroy(graph);
     h->graphs.emplace(key, ge);
-    (void)before;
     return MUMODE_OK;
   }
   MM_CUDA(cudaGraphLaunch(it->second.exec, h->stream));
