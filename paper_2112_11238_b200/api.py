@@ -110,15 +110,23 @@ class Handle:
             self.h = None
 
 
-_handles: dict[int, Handle] = {}
+import threading
+
+# One handle (workspaces, descriptor cache, graphs) per thread and device: the
+# reference's operators are pure functions safe for concurrent callers
+# (SPEC.md:134-135), so concurrent threads must never share a workspace.
+_tls = threading.local()
 
 
 def get_handle(device: int | None = None) -> Handle:
     if device is None:
         device = torch.cuda.current_device() if torch is not None and torch.cuda.is_available() else 0
-    if device not in _handles:
-        _handles[device] = Handle(device)
-    return _handles[device]
+    handles = getattr(_tls, "handles", None)
+    if handles is None:
+        handles = _tls.handles = {}
+    if device not in handles:
+        handles[device] = Handle(device)
+    return handles[device]
 
 
 # ------------------------------------------------------------------ layout helpers

@@ -414,3 +414,30 @@ def test_kronsum_direct_solve():
     with pytest.raises(mm.NumericalError):
         mm.KronSumSolver(Qs=[np.eye(2), np.eye(2)], evals=[np.array([1.0, 0.0]), np.array([-1.0, 2.0])]).solve(
             dev(np.ones((2, 2))))
+
+
+def test_concurrent_threads_get_independent_workspaces():
+    # the reference's operators are safe for concurrent callers; each thread
+    # gets its own handle (workspaces), results match the single-thread ones
+    import threading
+    rng = np.random.default_rng(77)
+    cases = []
+    for k in range(4):
+        T = rnd(rng, (64, 48, 40))
+        Ls = [rnd(rng, (56, 64)), rnd(rng, (48, 48)), rnd(rng, (72, 40))]
+        cases.append((T, Ls, O.port_tucker(T, Ls)))
+    errs = [None] * len(cases)
+
+    def work(i):
+        T, Ls, want = cases[i]
+        for _ in range(5):
+            with torch.cuda.stream(torch.cuda.Stream()):
+                got = host(mm.tucker(dev(T), [dev(L) for L in Ls]))
+            errs[i] = max(errs[i] or 0.0, O.rel_fro(got, want))
+
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(len(cases))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert all(e is not None and e < 1e-14 for e in errs), errs
