@@ -103,6 +103,53 @@ def slab_tucker(plan: SlabPlan, rank: int, T_local, Ls, backend):
     return backend.last_mode(recv, Z_rows, plan.m[-1], Ls[-1])
 
 
+def slab_tucker_overlapped(plan: SlabPlan, rank: int, T_local, Ls, backend, chunks: int = 4):
+    """Same result as ``slab_tucker`` with the exchange overlapped with the
+    local contraction: each rank splits its slab's last-mode columns into
+    ``chunks`` sub-slabs; sub-slab j is contracted (modes 1..d-1), packed by
+    destination row block and posted as grouped send/recv while sub-slab j+1
+    is contracted. Every received block (A_r x w columns) lands directly in
+    its final columns of the (A_r x m_d) matrix, which are contiguous in the
+    column-major layout -- no unpack. All ranks derive every other rank's
+    chunking from the plan, so the posted sends and receives always match."""
+    P, d = plan.P, len(plan.m)
+    subs = [even_splits(c, min(chunks, c)) for c in plan.c_sizes]
+    nchunks = max(len(sv) for sv in subs)
+    subs = [sv + [0] * (nchunks - len(sv)) for sv in subs]
+    suboffs = [offsets(sv) for sv in subs]
+    A_r = plan.a_sizes[rank]
+    Z = backend.empty(A_r * plan.m[-1])
+    slab_rows = int(np.prod(plan.m[:-1]))
+    pending = []
+    for j in range(nchunks):
+        w = subs[rank][j]
+        if w > 0:
+            Tj = backend.cols(T_local, slab_rows, suboffs[rank][j], w)
+            ext = plan.m[:-1] + (w,)
+            Yj = backend.local_modes(Tj, ext, plan.n, Ls, 1, d - 1)
+            send = backend.pack(Yj, plan.A, w, plan.a_off)
+        sends, recvs = [], []
+        for q in range(P):
+            if q == rank or w == 0:
+                continue
+            sends.append((q, backend.view(send, plan.a_off[q] * w, plan.a_off[q + 1] * w)))
+        for s_ in range(P):
+            ws = subs[s_][j]
+            if s_ == rank or ws == 0:
+                continue
+            col0 = plan.c_off[s_] + suboffs[s_][j]
+            recvs.append((s_, backend.view(Z, A_r * col0, A_r * (col0 + ws))))
+        if w > 0:  # own block: device copy into place
+            col0 = plan.c_off[rank] + suboffs[rank][j]
+            backend.copy(backend.view(Z, A_r * col0, A_r * (col0 + w)),
+                         backend.view(send, plan.a_off[rank] * w, plan.a_off[rank + 1] * w))
+        if sends or recvs:
+            pending.append(backend.post(sends, recvs))
+    for handle in pending:
+        backend.wait(handle)
+    return backend.last_mode(Z, A_r, plan.m[-1], Ls[-1])
+
+
 class CudaSlabBackend:
     """Product backend: CUDA kernels of libmumode_b200.so for the local steps,
     one NCCL all-to-all (torch.distributed) for the exchange."""
@@ -148,6 +195,35 @@ class CudaSlabBackend:
         recv = self.torch.empty(sum(recv_counts), dtype=self.torch.float64, device=self.dev)
         self.dist.all_to_all_single(recv, send, recv_counts, send_counts, group=self.group)
         return recv
+
+    # --- overlapped variant
+    def empty(self, n):
+        return self.torch.empty(n, dtype=self.torch.float64, device=self.dev)
+
+    def cols(self, T, rows_per_col, c0, w):
+        # raw column-major storage (T.reshape(-1) would flatten in logical,
+        # row-major order): the last-mode columns are contiguous runs
+        from .api import is_colmajor
+        if not is_colmajor(T):
+            raise ValueError("slab tensors must be column-major")
+        flat = T.as_strided((T.numel(),), (1,))
+        return flat[rows_per_col * c0: rows_per_col * (c0 + w)]
+
+    def view(self, x, lo, hi):
+        return x[lo:hi]
+
+    def copy(self, dst, src):
+        dst.copy_(src)
+
+    def post(self, sends, recvs):
+        dist = self.dist
+        ops = [dist.P2POp(dist.isend, t, peer, group=self.group) for peer, t in sends]
+        ops += [dist.P2POp(dist.irecv, t, peer, group=self.group) for peer, t in recvs]
+        return dist.batch_isend_irecv(ops)
+
+    def wait(self, works):
+        for w in works:
+            w.wait()
 
     def last_mode(self, Z, rows, m_d, L_d):
         n_d = int(L_d.shape[0])

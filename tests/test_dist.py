@@ -17,7 +17,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle as O
-from paper_2112_11238_b200.dist import SlabPlan, gather_rows, scatter_slabs, slab_tucker
+from paper_2112_11238_b200.dist import (SlabPlan, gather_rows, scatter_slabs, slab_tucker,
+                                        slab_tucker_overlapped)
 
 
 class OracleGlooBackend:
@@ -43,6 +44,28 @@ class OracleGlooBackend:
         Z2 = np.asarray(Z).reshape((rows, m_d), order="F")
         return O.port_mode_product(Z2, L_d, 2).reshape(-1, order="F")
 
+    # overlapped variant: torch CPU tensors as buffers, gloo point-to-point
+    def empty(self, n):
+        return torch.empty(n, dtype=torch.float64)
+
+    def cols(self, T, rows_per_col, c0, w):
+        return np.asarray(T).reshape(-1, order="F")[rows_per_col * c0: rows_per_col * (c0 + w)]
+
+    def view(self, x, lo, hi):
+        return x[lo:hi]
+
+    def copy(self, dst, src):
+        dst.copy_(torch.as_tensor(np.ascontiguousarray(src)))
+
+    def post(self, sends, recvs):
+        ops = [dist.P2POp(dist.isend, torch.as_tensor(np.ascontiguousarray(t)), p) for p, t in sends]
+        ops += [dist.P2POp(dist.irecv, t, p) for p, t in recvs]
+        return dist.batch_isend_irecv(ops)
+
+    def wait(self, works):
+        for w in works:
+            w.wait()
+
 
 def free_port():
     s = socket.socket()
@@ -64,11 +87,16 @@ def _worker(rank, world, port, cases, q):
             plan = SlabPlan(m, n, world)
             T_r = scatter_slabs(plan, T)[rank]
             S_r = slab_tucker(plan, rank, T_r, Ls, OracleGlooBackend())
+            S_o = slab_tucker_overlapped(plan, rank, T_r, Ls, OracleGlooBackend(), chunks=3)
             blocks = [None] * world
             dist.all_gather_object(blocks, S_r)
+            blocks_o = [None] * world
+            dist.all_gather_object(blocks_o, np.asarray(S_o))
             if rank == 0:
                 S = gather_rows(plan, blocks)
-                q.put((m, n, O.rel_fro(S, O.port_tucker(T, Ls))))
+                So = gather_rows(plan, blocks_o)
+                ref = O.port_tucker(T, Ls)
+                q.put((m, n, max(O.rel_fro(S, ref), O.rel_fro(So, ref))))
     finally:
         dist.destroy_process_group()
 
@@ -88,7 +116,7 @@ def test_slab_tucker_gloo_matches_oracle(world):
     for p in procs:
         p.join(timeout=240)
         assert p.exitcode == 0
-    results = [q.get(timeout=10) for _ in CASES]
+    results = [q.get(timeout=30) for _ in CASES]
     for m, n, err in results:
         assert err < 1e-13, (m, n, err)
 
@@ -154,6 +182,26 @@ def test_slab_tucker_cuda_kernels_simulated_ranks(P):
         outs = SimulatedExchange(CudaSlabBackend(0), plan).run(slabs, Lds)
         S = gather_rows(plan, [o.cpu().numpy() for o in outs])
         assert O.rel_fro(S, O.port_tucker(T, Ls)) < 1e-13
+
+
+@pytest.mark.gpu
+def test_slab_tucker_overlapped_nccl_single_rank():
+    from paper_2112_11238_b200.dist import CudaSlabBackend
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(10)
+        m, n = (48, 40, 32), (40, 56, 24)
+        T = np.asfortranarray(rng.standard_normal(m))
+        Ls = [np.asfortranarray(rng.standard_normal((n[k], m[k]))) for k in range(3)]
+        plan = SlabPlan(m, n, 1)
+        S_r = slab_tucker_overlapped(plan, 0, torch.from_numpy(T).cuda(),
+                                     [torch.from_numpy(L).cuda() for L in Ls], CudaSlabBackend(0), chunks=4)
+        S = gather_rows(plan, [S_r.cpu().numpy()])
+        assert O.rel_fro(S, O.port_tucker(T, Ls)) < 1e-13
+    finally:
+        dist.destroy_process_group()
 
 
 @pytest.mark.gpu
