@@ -60,7 +60,7 @@ def tucker_flops(m, n):
 
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks line via NVML, sampled every 50 ms during the run."""
+    """nvidia-smi clocks line via NVML, sampled every 10 ms during the run."""
 
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
                0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
@@ -93,7 +93,7 @@ class ClockSampler:
                 self.samples.append((mhz, util, r))
             except Exception:
                 pass
-            time.sleep(0.05)
+            time.sleep(0.01)
 
     def start(self):
         if self.ok:

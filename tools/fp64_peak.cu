@@ -48,6 +48,46 @@ __global__ void dmma_kernel(double* out, int iters, double a0, double b0) {
   if (s == 1.2345) out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// DMMA fed from shared memory at the mode-product kernel's ratio: per k-step
+// 12 conflict-free LDS.64 (8 B-frags + 4 A-frags) and 32 DMMAs (64x32 warp
+// tile), 8 warps per CTA, 1 CTA per SM. Tells whether ~92 % of the DMMA pipe
+// is a ceiling of the mma.sync + LDS instruction mix itself.
+__global__ void __launch_bounds__(256) dmma_lds_kernel(double* out, int iters) {
+  __shared__ double sm[8][512];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 8 * 512; i += blockDim.x) (&sm[0][0])[i] = 1e-3 * (i & 63);
+  __syncthreads();
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const double* base = &sm[warp][0];
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      double pf[8], qf[4];
+      const int off = (s * 96 + lane + (it & 1) * 64) & 511;
+#pragma unroll
+      for (int a = 0; a < 8; ++a) pf[a] = base[(off + 32 * a) & 511];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) qf[b] = base[(off + 32 * (8 + b)) & 511];
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+              : "+d"(acc[a][b][0]), "+d"(acc[a][b][1]) : "d"(qf[b]), "d"(pf[a]));
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) s += acc[a][b][0] + acc[a][b][1];
+  if (s == 1.2345) out[threadIdx.x] = s;
+}
+
 template <class F>
 float time_it(F f, int reps) {
   cudaEvent_t e0, e1;
@@ -98,6 +138,13 @@ int main() {
     else ms = time_it([&] { dmma_kernel<16><<<blocks, thr>>>(out, iters, 0.999, 1e-3); }, 5);
     double flops = 2.0 * 256 * (thr / 32) * double(blocks) * iters * 4 * acc;
     std::printf("{\"variant\": \"dmma_1warp_per_smsp_acc%d\", \"ms\": %.3f, \"tflops\": %.3f}\n", acc, ms,
+                flops / ms / 1e9);
+  }
+  {
+    const int blocks = sms, iters = 2048;
+    float ms = time_it([&] { dmma_lds_kernel<<<blocks, 256>>>(out, iters); }, 5);
+    double flops = 2.0 * 256 * 8 * double(blocks) * iters * 4 * 32;
+    std::printf("{\"variant\": \"dmma_with_lds_gemm_mix\", \"ms\": %.3f, \"tflops\": %.3f}\n", ms,
                 flops / ms / 1e9);
   }
   CK(cudaGetLastError());
