@@ -208,10 +208,6 @@ def _dev_matrix(L, cplx: bool, device):
     return to_colmajor(L)
 
 
-def _real_view_ptr(t) -> int:
-    return t.data_ptr()
-
-
 # ------------------------------------------------------------------ operators
 def mode_product(T, L, mu: int):
     """S = T x_mu L (core::mode_product, mode_product.hpp:64-83).

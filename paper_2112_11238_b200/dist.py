@@ -68,9 +68,6 @@ class SlabPlan:
     def local_in_extents(self, r: int) -> tuple[int, ...]:
         return self.m[:-1] + (self.c_sizes[r],)
 
-    def local_mid_extents(self, r: int) -> tuple[int, ...]:
-        return self.n[:-1] + (self.c_sizes[r],)
-
     def send_counts(self, r: int) -> list[int]:
         return [a * self.c_sizes[r] for a in self.a_sizes]
 
