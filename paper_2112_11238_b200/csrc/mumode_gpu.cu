@@ -644,6 +644,17 @@ static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t
   return MUMODE_OK;
 }
 
+// [a, a + na) and [b, b + nb) (doubles) overlap?
+static bool overlaps(const double* a, int64_t na, const double* b, int64_t nb) {
+  return a < b + nb && b < a + na;
+}
+
+static int check_no_alias(const double* T, int64_t nt, const double* S, int64_t ns, const char* who) {
+  if (overlaps(T, nt, S, ns))
+    return fail(MUMODE_ERR_ARGUMENT, std::string(who) + ": output overlaps the input (results are new tensors)");
+  return MUMODE_OK;
+}
+
 static int check_stack(int d, const int64_t* m, const int64_t* n, const double* T,
                        const double* const* L, const void* S, const char* who) {
   MM_TRY(check_shape(d, m, who));
@@ -736,6 +747,12 @@ static int mode_product_entry(mumode_handle_t h, int d, const int64_t* m, int mu
                                          std::to_string(d));
   if (n_mu < 1) return fail(MUMODE_ERR_ARGUMENT, "matrix dimensions must be positive");
   if (!T || !L || !S) return fail(MUMODE_ERR_ARGUMENT, "mode_product: null pointer");
+  {
+    const int el = cplx ? 2 : 1;
+    std::vector<int64_t> out(m, m + d);
+    out[mu - 1] = n_mu;
+    MM_TRY(check_no_alias(T, prod(m, 0, d) * el, S, prod(out.data(), 0, d) * el, "mode_product"));
+  }
   MM_CUDA(cudaSetDevice(h->device));
   return mode_product_dev(h, d, m, mu, n_mu, T, L, 1, n_mu, cplx, false, S);
 }
@@ -754,6 +771,10 @@ static int tucker_entry(mumode_handle_t h, int d, const int64_t* m, const int64_
                         bool cplx) {
   if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
   MM_TRY(check_stack(d, m, n, T, L, S, adjoint ? "cttucker" : "tucker"));
+  if (d == 1) {  // d >= 2 reads T only in mode 1 and writes S only in mode d
+    const int el = cplx ? 2 : 1;
+    MM_TRY(check_no_alias(T, prod(m, 0, d) * el, S, prod(n, 0, d) * el, "tucker"));
+  }
   MM_CUDA(cudaSetDevice(h->device));
   return tucker_dev(h, d, m, n, T, L, S, adjoint != 0, cplx);
 }

@@ -441,3 +441,15 @@ def test_concurrent_threads_get_independent_workspaces():
     for t in ths:
         t.join()
     assert all(e is not None and e < 1e-14 for e in errs), errs
+
+
+def test_aliasing_output_rejected_by_the_abi():
+    # a mode product written over its own input would race; the C-ABI refuses
+    import ctypes
+    from paper_2112_11238_b200 import _lib
+    h = mm.get_handle(0)
+    T = mm.colmajor_empty((32, 32, 32), torch.float64, "cuda").normal_()
+    L = torch.eye(32, dtype=torch.float64, device="cuda")
+    rc = _lib.lib().mumode_mode_product_f64(h.h, 3, _lib.i64_array((32, 32, 32)), 2, 32,
+                                            T.data_ptr(), L.data_ptr(), T.data_ptr())
+    assert rc == 2 and b"overlaps" in _lib.lib().mumode_last_error()
