@@ -879,6 +879,7 @@ int mumode_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double
                         const double* const* A, double* W) {
   if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
   MM_TRY(check_stack(d, m, m, V, A, W, "kronsumv"));
+  MM_TRY(check_no_alias(V, prod(m, 0, d), W, prod(m, 0, d), "kronsumv"));
   MM_CUDA(cudaSetDevice(h->device));
   // W = V x_1 A_1, then W += V x_mu A_mu for mu = 2..d in the products'
   // epilogues (the reference's acc += term order, tucker.hpp:222-231): no
