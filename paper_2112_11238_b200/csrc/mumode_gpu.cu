@@ -22,6 +22,7 @@
 #include "generic.cuh"
 #include "tma_dmma.cuh"
 #include "fused.cuh"
+#include "ldg_dmma.cuh"
 
 namespace mumode_gpu {
 
@@ -482,10 +483,63 @@ static int launch_generic(mumode_handle_s* h, const ModeJob& j) {
   return MUMODE_OK;
 }
 
+// LDG-staged DMMA kernel for real shapes the TMA path cannot describe.
+constexpr int kLdgBM = 64, kLdgBN = 64, kLdgBK = 16, kLdgWM = 2, kLdgWN = 2;
+
+static int launch_ldg(mumode_handle_s* h, const ModeJob& j) {
+  LdgArgs g{};
+  g.T = j.T;
+  g.L = j.L;
+  g.S = j.S;
+  g.A = j.A;
+  g.K = j.K;
+  g.N = j.N;
+  g.C = j.C;
+  g.sLi = j.sLi;
+  g.sLk = j.sLk;
+  g.accumulate = j.accumulate ? 1 : 0;
+  const bool mode1 = (j.A == 1);
+  if (mode1) {
+    g.Mlim = j.N;
+    g.ntot = j.C;
+    g.AB = int((j.N + 7) / 8);
+    g.mfrags = g.AB;
+  } else {
+    g.Mlim = j.A;
+    g.ntot = j.N;
+    g.AB = int((j.A + 7) / 8);
+    g.mfrags = int64_t(g.AB) * j.C;
+  }
+  g.mt = int((g.mfrags + kLdgBM / 8 - 1) / (kLdgBM / 8));
+  g.nt = int((g.ntot + kLdgBN - 1) / kLdgBN);
+  const int64_t tiles = int64_t(g.mt) * g.nt;
+  if (tiles >= (int64_t(1) << 31)) return fail(MUMODE_ERR_SIZE, "mode product too large for one launch");
+  constexpr int smem = 2 * (kLdgBM + kLdgBN) * kLdgBK * 8 + 1024;
+  if (mode1) {
+    auto k = modeprod_ldg_kernel<true, kLdgBM, kLdgBN, kLdgBK, kLdgWM, kLdgWN>;
+    MM_TRY(smem_opt_in(k, smem));
+    k<<<static_cast<unsigned>(tiles), kLdgWM * kLdgWN * 32, smem, h->stream>>>(g);
+  } else {
+    auto k = modeprod_ldg_kernel<false, kLdgBM, kLdgBN, kLdgBK, kLdgWM, kLdgWN>;
+    MM_TRY(smem_opt_in(k, smem));
+    k<<<static_cast<unsigned>(tiles), kLdgWM * kLdgWN * 32, smem, h->stream>>>(g);
+  }
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return MUMODE_OK;
+}
+
+static bool ldg_worthwhile(const ModeJob& j) {
+  const int64_t M = (j.A == 1) ? j.N : j.A;
+  return M >= 16 && j.K >= 8 && ((j.A == 1) ? j.C : j.N) >= 16;
+}
+
 static int run_job(mumode_handle_s* h, const ModeJob& j) {
   // accumulating products: real mu > 1 have a TMA instantiation; others generic
   const bool can_tma = tma_ok(j) && !(j.accumulate && (j.A == 1 || j.cplx));
-  if (h->policy == 1 || !can_tma) return launch_generic(h, j);
+  if (h->policy == 8 && !j.cplx) return launch_ldg(h, j);
+  if (h->policy == 1) return launch_generic(h, j);
+  if (!can_tma) return (!j.cplx && ldg_worthwhile(j)) ? launch_ldg(h, j) : launch_generic(h, j);
   if ((h->policy >= 2 && h->policy <= 6) || tma_worthwhile(j)) return launch_tma_auto(h, j);
   return launch_generic(h, j);
 }
@@ -732,7 +786,7 @@ void* mumode_get_stream(mumode_handle_t h) { return h ? static_cast<void*>(h->st
 int64_t mumode_launch_count(mumode_handle_t h) { return h ? h->launches : -1; }
 
 int mumode_set_kernel_policy(mumode_handle_t h, int policy) {
-  if (!h || policy < 0 || policy > 7) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
+  if (!h || policy < 0 || policy > 8) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
   // 3..6 force real tile configuration 0..3 / complex configuration 0..3
   h->policy = policy;
   return MUMODE_OK;

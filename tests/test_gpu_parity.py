@@ -40,8 +40,8 @@ def _require_gpu():
         pytest.fail("GPU test run without a GPU")
 
 
-@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7],
-                ids=["auto", "generic", "tma", "tma_big", "tma_tm", "tma_lm", "tma_mid", "fused"])
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8],
+                ids=["auto", "generic", "tma", "tma_big", "tma_tm", "tma_lm", "tma_mid", "fused", "ldg"])
 def policy(request):
     h = mm.get_handle(0)
     h.set_kernel_policy(request.param)
@@ -269,7 +269,8 @@ def test_ragged_and_unaligned_shapes_against_oracle(policy):
     # odd extents, extents that are not multiples of the tile sizes, 1-extents
     rng = np.random.default_rng(5)
     for m, n in [((33, 17, 9), (31, 18, 7)), ((130, 3, 66), (2, 129, 64)), ((1, 200, 1), (1, 7, 3)),
-                 ((18, 34, 50), (48, 34, 18)), ((256, 2, 40), (256, 2, 40))]:
+                 ((18, 34, 50), (48, 34, 18)), ((256, 2, 40), (256, 2, 40)), ((65, 71, 33), (63, 70, 35)),
+                 ((129, 67, 17), (127, 65, 19))]:
         T = rnd(rng, m)
         Ls = [rnd(rng, (n[k], m[k])) for k in range(len(m))]
         S = host(mm.tucker(dev(T), [dev(L) for L in Ls]))
@@ -319,7 +320,7 @@ def test_kronsumv_fused_epilogue_vs_reference(policy):
     # W = sum_mu V x_mu A_mu with the terms accumulated in the epilogues, at
     # TMA-sized shapes, against the reference library's ops::kronsumv
     rng = np.random.default_rng(21)
-    for shape in [(64, 48, 40), (24, 24, 24, 24), (33, 17, 9)]:
+    for shape in [(64, 48, 40), (24, 24, 24, 24), (33, 17, 9), (65, 33, 31)]:
         V = rnd(rng, shape)
         As = [rnd(rng, (e, e)) for e in shape]
         W = host(mm.kronsumv(dev(V), [dev(A) for A in As]))
