@@ -271,14 +271,14 @@ struct ModeJob {
 };
 
 // Compiled tile configurations (BM, BN, BK, stages, warps along M, along N).
-using CfgBig = TmaCfg<128, 128, 16, 4, 2, 4>;  // 64x32 warp tiles (C2-class shapes)
-using CfgTM = TmaCfg<128, 40, 40, 3, 8, 1>;    // T-side M, small L-side N (n = 40k)
-using CfgLM = TmaCfg<40, 128, 40, 3, 1, 8>;    // small L-side M, T-side N (mode 1, n = 40k)
+using CfgBig = TmaCfg<128, 128, 16, 4, 4, 4>;  // 16 MMA warps, 32x32 warp tiles (C2-class shapes)
+using CfgTM = TmaCfg<128, 40, 40, 3, 16, 1>;   // T-side M, small L-side N (n = 40k)
+using CfgLM = TmaCfg<40, 128, 40, 3, 1, 16>;   // small L-side M, T-side N (mode 1, n = 40k)
 using CfgMid = TmaCfg<64, 128, 32, 4, 2, 4>;   // 32x32 warp tiles
 // complex128 (E = 2): 4 real DMMAs per complex MAC, 16-B elements
-using CfgCa = TmaCfg<64, 128, 16, 4, 2, 4, 2>;  // 32x32 complex warp tiles
-using CfgCb = TmaCfg<128, 64, 16, 4, 4, 2, 2>;
-using CfgCc = TmaCfg<96, 32, 16, 4, 4, 2, 2>;   // 24x16 warp tiles, fine-grained
+using CfgCa = TmaCfg<64, 128, 16, 4, 4, 4, 2>;  // 16 MMA warps, 16x32 complex warp tiles
+using CfgCb = TmaCfg<128, 64, 16, 4, 4, 4, 2>;
+using CfgCc = TmaCfg<96, 32, 16, 4, 4, 4, 2>;   // 24x8 warp tiles, fine-grained
 using CfgCd = TmaCfg<192, 16, 16, 4, 8, 1, 2>;
 
 static bool aligned16(const void* p) { return aligned16_ptr(p); }

@@ -51,6 +51,17 @@ struct TmaCfg {
   // MMA warps + one producer warpgroup (setmaxnreg works per warpgroup; the
   // producer group's registers are what the MMA warps grow into).
   static constexpr int THREADS = (MMA_WARPS + 4) * 32;
+  // Register split after setmaxnreg. setmaxnreg.inc draws from the CTA's LAUNCH
+  // allocation (per-thread limit of the launch bounds x THREADS), not the whole
+  // register file -- asking for more blocks forever. The producer warpgroup
+  // keeps 24; the MMA warps share the rest (multiple of 8, <= 232).
+  static constexpr int LAUNCH_REGS = (65536 / THREADS) / 8 * 8 > 255 ? 248 : (65536 / THREADS) / 8 * 8;
+  static constexpr int POOL = LAUNCH_REGS * THREADS;
+  static constexpr int PRODUCER_REGS = 24;
+  static constexpr int CONSUMER_REGS_RAW = ((POOL - 4 * 32 * PRODUCER_REGS) / (MMA_WARPS * 32)) / 8 * 8;
+  static constexpr int CONSUMER_REGS = CONSUMER_REGS_RAW > 232 ? 232 : CONSUMER_REGS_RAW;
+  static_assert(4 * 32 * PRODUCER_REGS + MMA_WARPS * 32 * CONSUMER_REGS <= POOL, "setmaxnreg budget");
+  static_assert(CONSUMER_REGS >= LAUNCH_REGS, "setmaxnreg.inc must not shrink");
   static constexpr int WTM = BM / WM, WTN = BN / WN;  // warp tile
   static constexpr int FM = WTM / 8, FN = WTN / 8;    // 8-wide fragments per warp
   static constexpr int P_BYTES = BM * BK * 8 * E, Q_BYTES = BN * BK * 8 * E;
@@ -131,7 +142,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
 
   if (warp >= Cfg::MMA_WARPS) {
     // ------------------------------------------------------------ producer
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Cfg::PRODUCER_REGS) : "memory");
     if (warp == Cfg::MMA_WARPS && lane == 0) {
       tma_prefetch_desc(&mapP);
       tma_prefetch_desc(&mapQ);
@@ -209,7 +220,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   }
 
   // -------------------------------------------------------------- consumers
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Cfg::CONSUMER_REGS) : "memory");
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % Cfg::WM, wn = warp / Cfg::WM;
   const int mw = wm * Cfg::WTM, nw = wn * Cfg::WTN;
