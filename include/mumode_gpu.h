@@ -66,7 +66,11 @@ int64_t mumode_launch_count(mumode_handle_t h);
 /* Kernel path selection for tests/benchmarks: 0 = auto (default),
  * 1 = force the generic SIMT kernel, 2 = force the TMA/DMMA kernel where the
  * shape allows it (tile shape by cost model), 3..6 = TMA/DMMA kernel with tile
- * configuration 0..3 forced. Not a fallback switch: all are CUDA kernels. */
+ * configuration 0..3 forced, 7 = auto including the fused two-mode passes,
+ * 8 = force the LDG-staged DMMA kernel for real products, 9 = auto with the
+ * 32-wide strided-pair (tail) pass forced wherever the shape allows it,
+ * 10 = auto with the tail pass disabled. Not a fallback switch: all are CUDA
+ * kernels. */
 int mumode_set_kernel_policy(mumode_handle_t h, int policy);
 
 /* ---- device-resident operators --------------------------------------- */

@@ -22,6 +22,7 @@
 #include "generic.cuh"
 #include "tma_dmma.cuh"
 #include "fused.cuh"
+#include "tail.cuh"
 #include "ldg_dmma.cuh"
 
 namespace mumode_gpu {
@@ -572,10 +573,40 @@ static int launch_fused(mumode_handle_s* h, const double* T, double* S, const do
   return MUMODE_OK;
 }
 
+// Strided-pair pass with 32-wide a tiles (tail.cuh): 256-B rows for loads and
+// stores instead of 64-B ones.
+template <int MU>
+static int launch_tail(mumode_handle_s* h, const double* T, double* S, const double* L1,
+                       const double* L2, int64_t A, int64_t C) {
+  using Cfg = TailCfg<MU>;
+  const CUtensorMap *mx = nullptr, *ms = nullptr;
+  uint64_t d[5] = {16, uint64_t(A / 16), uint64_t(MU), uint64_t(MU), uint64_t(C)};
+  uint64_t st[4] = {16, uint64_t(A), uint64_t(A) * MU, uint64_t(A) * MU * MU};
+  uint32_t bx[5] = {16, 2, MU, Cfg::KB, 1}, bs[5] = {16, 2, 1, MU, 1};
+  MM_TRY(get_map(h, T, 5, d, st, bx, &mx, true));
+  MM_TRY(get_map(h, S, 5, d, st, bs, &ms, true));
+  TailParams p{L1, L2, A / 32, (A / 32) * C};
+  const int grid = static_cast<int>(p.tiles < h->num_sms ? p.tiles : h->num_sms);
+  auto k = tail_pair_kernel<MU>;
+  MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
+  k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mx, *ms, p);
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return MUMODE_OK;
+}
+
+// The tail kernel pays off once the a-stride makes every tile row a new page
+// (policy 9 forces it wherever the shape allows, 10 disables it).
+static constexpr int64_t kTailMinA = 512;
+
 template <int MU>
 static int launch_fused_mu(mumode_handle_s* h, bool first, const double* T, double* S,
                            const double* L1, const double* L2, int64_t A, int64_t C) {
   if (first) return launch_fused<MU, true, 8>(h, T, S, L1, L2, A, C);
+  if constexpr (MU <= 24) {
+    if (A % 32 == 0 && h->policy != 10 && (h->policy == 9 || A >= kTailMinA))
+      return launch_tail<MU>(h, T, S, L1, L2, A, C);
+  }
   // 16 a's per tile when shared memory allows it and A tiles evenly
   constexpr bool wide_fits = FusedCfg<MU, false, 16>::SMEM_BYTES <= 227 * 1024 &&
                              FusedCfg<MU, false, 16>::NBUF >= 2;
@@ -589,7 +620,8 @@ static int launch_fused_mu(mumode_handle_s* h, bool first, const double* T, doub
 static int fused_extent(int d, const int64_t* m, const int64_t* n, bool cplx, bool adjoint,
                         int policy, int mu_lo, int mu_hi, const double* T, const double* S,
                         const double* const* L) {
-  if (cplx || adjoint || !(policy == 0 || policy == 7) || mu_hi - mu_lo < 1) return 0;
+  if (cplx || adjoint || !(policy == 0 || policy == 7 || policy == 9 || policy == 10) || mu_hi - mu_lo < 1)
+    return 0;
   const int64_t MU = m[0];
   if (MU != 8 && MU != 16 && MU != 24 && MU != 32) return 0;
   for (int k = 0; k < d; ++k)
@@ -786,7 +818,7 @@ void* mumode_get_stream(mumode_handle_t h) { return h ? static_cast<void*>(h->st
 int64_t mumode_launch_count(mumode_handle_t h) { return h ? h->launches : -1; }
 
 int mumode_set_kernel_policy(mumode_handle_t h, int policy) {
-  if (!h || policy < 0 || policy > 8) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
+  if (!h || policy < 0 || policy > 10) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
   // 3..6 force real tile configuration 0..3 / complex configuration 0..3
   h->policy = policy;
   return MUMODE_OK;

@@ -40,8 +40,9 @@ def _require_gpu():
         pytest.fail("GPU test run without a GPU")
 
 
-@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8],
-                ids=["auto", "generic", "tma", "tma_big", "tma_tm", "tma_lm", "tma_mid", "fused", "ldg"])
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10],
+                ids=["auto", "generic", "tma", "tma_big", "tma_tm", "tma_lm", "tma_mid", "fused", "ldg", "tail",
+                     "no_tail"])
 def policy(request):
     h = mm.get_handle(0)
     h.set_kernel_policy(request.param)
@@ -304,9 +305,11 @@ def test_complex_medium_shapes_all_modes(policy):
         assert O.rel_fro(host(mm.cttucker(dev(T), [dev(P) for P in Ps])), O.port_tucker(T, Ps, adjoint=True)) < 1e-14
 
 
-@pytest.mark.parametrize("shape", [(8,) * 6, (16,) * 4, (24,) * 4, (24,) * 5, (24,) * 3, (32,) * 3, (16, 16)])
+@pytest.mark.parametrize("shape", [(8,) * 6, (16,) * 4, (24,) * 4, (24,) * 5, (24,) * 3, (32,) * 3, (16, 16),
+                                   (8,) * 4, (16,) * 5, (8,) * 8])
 def test_fused_small_square_modes(policy, shape):
-    # the fused two-mode passes (config C5-class shapes): even and odd orders
+    # the fused two-mode passes (config C5-class shapes): even and odd orders;
+    # (8,)*8 reaches the 32-wide strided-pair (tail) kernel under auto (A = 8^6)
     rng = np.random.default_rng(len(shape) * 100 + shape[0])
     T = rnd(rng, shape)
     Ls = [rnd(rng, (e, e)) for e in shape]

@@ -12,6 +12,8 @@ from paper_2112_11238_b200 import _lib  # noqa: E402
 lib = _lib.lib()
 h = mm.get_handle(0)
 h.bind_torch_stream()
+policy = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+h.set_kernel_policy(policy)
 shape = (24,) * 6
 T = mm.colmajor_empty(shape, torch.float64, "cuda").normal_()
 S = torch.empty_like(T)
@@ -32,4 +34,4 @@ for lo in (1, 3, 5):
         ts.append(a.elapsed_time(b))
     ts.sort()
     gb = 2 * T.numel() * 8 / 1e9
-    print(f"pass modes {lo},{lo+1}: {ts[len(ts)//2]*1e3:.1f} us  -> {gb / (ts[len(ts)//2]*1e-3):.0f} GB/s")
+    print(f"policy {policy} pass modes {lo},{lo+1}: {ts[len(ts)//2]*1e3:.1f} us  -> {gb / (ts[len(ts)//2]*1e-3):.0f} GB/s")
