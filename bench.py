@@ -164,8 +164,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the C1/C3/C4/C5 side measurements")
     ap.add_argument("--force-dist", action="store_true", help="run the slab/NCCL path even at N=1 (testing)")
-    ap.add_argument("--overlap", action="store_true",
-                    help="N>1: overlap the slab exchange with the local modes (chunked grouped send/recv)")
+    ap.add_argument("--chunks", type=int, default=0,
+                    help="N>1: sub-slabs per rank in mumode_dist_tucker_f64 (exchange of one overlaps the "
+                         "next; 0 = auto)")
+    ap.add_argument("--py-dist", action="store_true",
+                    help="N>1: the Python slab algorithm with a torch all-to-all instead of the C-ABI")
+    ap.add_argument("--overlap", action="store_true", help="with --py-dist: chunked grouped send/recv")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -344,16 +348,20 @@ def main():
 
 def run_distributed(args, world, rank, local):
     """C2 slab-partitioned over the last mode across `world` GPUs (strong
-    scaling: the same 256^3 Tucker application, split): local modes 1-2, pack,
-    one NCCL all-to-all, local mode 3 (paper_2112_11238_b200/dist.py)."""
+    scaling: the same 256^3 Tucker application, split) through the C-ABI
+    mumode_dist_tucker_f64: per sub-slab local modes 1-2 + pack on the compute
+    stream, grouped NCCL send/recv on the exchange stream (overlapping the next
+    sub-slab), then local mode 3 (csrc/slab_dist.cuh). --py-dist runs the
+    Python algorithm of paper_2112_11238_b200/dist.py with a torch all-to-all."""
     import torch
     import torch.distributed as dist
     import paper_2112_11238_b200 as mm
     from paper_2112_11238_b200 import _lib
-    from paper_2112_11238_b200.dist import (CudaSlabBackend, SlabPlan, scatter_slabs, slab_tucker,
-                                            slab_tucker_overlapped)
+    from paper_2112_11238_b200.dist import (Comm, CudaSlabBackend, SlabPlan, dist_tucker, scatter_slabs,
+                                            slab_tucker, slab_tucker_overlapped)
 
     dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
     h = mm.get_handle(local)
     lib = _lib.lib()
     stream = torch.cuda.current_stream(dev)
@@ -365,42 +373,57 @@ def run_distributed(args, world, rank, local):
     T_r_host = scatter_slabs(plan, T_host)[rank]
     T_r = torch.from_numpy(T_r_host).to(dev)
     Ls = [torch.from_numpy(L).to(dev) for L in L_host]
-    be = CudaSlabBackend(local)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    S_out = torch.empty(plan.a_sizes[rank] * 256, dtype=torch.float64, device=dev)
+    if args.py_dist:
+        be = CudaSlabBackend(local)
+        if args.overlap:
+            def run_slab(T_in):
+                return slab_tucker_overlapped(plan, rank, T_in, Ls, be, chunks=4)
+        else:
+            def run_slab(T_in):
+                return slab_tucker(plan, rank, T_in, Ls, be)
+        path = "python slab algorithm, torch " + ("grouped send/recv (4 chunks)" if args.overlap else "all-to-all")
+    else:
+        comm = Comm.from_torch(device=local)
+
+        def run_slab(T_in):
+            return dist_tucker(comm, T_in, Ls, C2, chunks=args.chunks, out=S_out)
+        path = ("C-ABI mumode_dist_tucker_f64, NCCL grouped send/recv, "
+                + (f"{args.chunks} overlapped sub-slabs" if args.chunks else "auto sub-slabs"))
     clocks = ClockSampler(local)
     clocks.start()
-    if args.overlap:
-        def run_slab(T_in):
-            return slab_tucker_overlapped(plan, rank, T_in, Ls, be, chunks=4)
-    else:
-        def run_slab(T_in):
-            return slab_tucker(plan, rank, T_in, Ls, be)
     for _ in range(args.warmup):
         run_slab(T_r)
     torch.cuda.synchronize()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    d = 3
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     dist.barrier()
     torch.cuda.synchronize()
     l0 = h.launches
-    for e0, e1, e2 in ev:
+    for e0, e1 in ev:
         flush.fill_(1.0)
         e0.record(stream)
-        if args.overlap:
-            run_slab(T_r)
-            e1.record(stream)
-        else:
-            Y = be.local_modes(T_r, plan.local_in_extents(rank), plan.n, Ls, 1, d - 1)
-            e1.record(stream)
-            send = be.pack(Y, plan.A, plan.c_sizes[rank], plan.a_off)
-            recv = be.alltoall(send, plan.send_counts(rank), plan.recv_counts(rank))
-            be.last_mode(recv, plan.a_sizes[rank], plan.m[-1], Ls[-1])
-        e2.record(stream)
+        run_slab(T_r)
+        e1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
     launches = h.launches - l0
-    total_ms = sum(e0.elapsed_time(e2) for e0, _, e2 in ev)
-    local_ms = sum(e0.elapsed_time(e1) for e0, e1, _ in ev)
+    total_ms = sum(e0.elapsed_time(e1) for e0, e1 in ev)
+    # the dominant kernel alone: local modes 1-2 on this rank's slab
+    Y = torch.empty(256 * 256 * plan.c_sizes[rank], dtype=torch.float64, device=dev)
+    ext = _lib.i64_array(plan.local_in_extents(rank))
+    nn = _lib.i64_array([256, 256, plan.c_sizes[rank]])
+    P = _lib.ptr_array([L.data_ptr() for L in Ls])
+    lev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+    for _ in range(2):  # descriptors and workspace for this shape
+        lib.mumode_tucker_range_f64(h.h, 3, ext, nn, T_r.data_ptr(), P, Y.data_ptr(), 1, 2)
+    for e0, e1 in lev:
+        flush.fill_(1.0)
+        e0.record(stream)
+        lib.mumode_tucker_range_f64(h.h, 3, ext, nn, T_r.data_ptr(), P, Y.data_ptr(), 1, 2)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    local_ms = sum(e0.elapsed_time(e1) for e0, e1 in lev)
     t = torch.tensor([total_ms, local_ms], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms, local_ms = float(t[0]), float(t[1])
@@ -423,6 +446,8 @@ def run_distributed(args, world, rank, local):
     t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_value = plan.flops() * args.steps / float(t[0]) / 1e9
+    if not args.py_dist:
+        comm.close()
     if rank != 0:
         return
     line = {
@@ -432,19 +457,18 @@ def run_distributed(args, world, rank, local):
         "vs_baseline": round(value / PAPER_C2_GFLOPS, 3), "dtype": "f64",
         "data": "synthetic (mt19937_64 seed 1234, standard normal, reference draw order)",
         "config": {"workload": WORKLOAD, "seed": SEED,
-                   "parallelism": f"slab x{world} (last mode) + NCCL " +
-                                  ("grouped send/recv overlapped in 4 chunks" if args.overlap else "all-to-all"),
+                   "parallelism": f"slab x{world} (last mode): {path}",
                    "l2": "flushed between steps (256 MiB write outside the step events)",
                    "exchange_bytes_per_rank": plan.exchange_bytes(rank),
                    "local_ms_per_step": round(local_ms / args.steps, 4),
                    "pct_fp64_roofline_per_gpu": round(100.0 * value / world / (peak * 1e3), 2)},
         "roofline": {"bound": "tensor", "achieved": round(achieved_tf, 3), "peak": round(peak, 3),
                      "unit": "TFLOP/s", "frac": round(achieved_tf / peak, 4), "traffic": None,
-                     "kernel": "modeprod_tma_kernel, local modes 1-2 on the rank's slab",
+                     "kernel": "modeprod_tma_kernel, local modes 1-2 on the rank's slab (timed alone)",
                      "peak_source": "fp64 DMMA probe measured live (mumode_probe_fp64_peak)"},
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": int(T_pin.numel() * 8),
                 "d2h_bytes_per_step": int(out_pin.numel() * 8),
-                "path": "per rank: pinned slab H2D, slab_tucker, result rows D2H"},
+                "path": "per rank: pinned slab H2D, slab-partitioned Tucker, result rows D2H"},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }

@@ -110,6 +110,38 @@ int mumode_tucker_range_f64(mumode_handle_t h, int d, const int64_t* m, const in
 int mumode_slab_pack_f64(mumode_handle_t h, int64_t A, int64_t C, int P, const int64_t* a_off,
                          const double* Y, double* send);
 
+/* ---- multi-GPU: slab-partitioned Tucker (SURVEY 8b "mumode_dist_tucker_f64(h,
+ * comm, ...)", 8e) ---------------------------------------------------------
+ * A communicator wraps an NCCL communicator (NCCL is loaded at run time,
+ * libnccl.so.2) plus an exchange stream and the exchange buffers. */
+typedef struct mumode_comm_s* mumode_comm_t;
+/* 128-byte NCCL unique id: rank 0 creates it, the caller broadcasts it. */
+int mumode_comm_unique_id(void* id_out);
+int mumode_comm_create(mumode_comm_t* c, int device, const void* id, int nranks, int rank);
+/* Wrap a caller-owned ncclComm_t (not destroyed by mumode_comm_destroy);
+ * nccl_comm may be NULL when nranks == 1. */
+int mumode_comm_wrap(mumode_comm_t* c, int device, void* nccl_comm, int nranks, int rank);
+int mumode_comm_destroy(mumode_comm_t c);
+/* The partition (host only): c_off[P+1] = last-mode slab offsets (rank r
+ * holds T[..., c_off[r]:c_off[r+1]]), a_off[P+1] = output row blocks over
+ * A = n_1...n_{d-1} (rank r returns rows a_off[r]:a_off[r+1] of the result
+ * flattened to A x n_d). Even splits; MUMODE_ERR_SIZE if m_d < P. */
+int mumode_slab_plan(int nranks, int d, const int64_t* m, const int64_t* n, int64_t* c_off,
+                     int64_t* a_off);
+/* One slab-partitioned Tucker application (replaces ops::tucker across
+ * ranks, tucker.hpp:129-144). m, n: GLOBAL extents. T: this rank's slab
+ * (m_1 x ... x m_{d-1} x c_r, column-major); S: this rank's (A_r x n_d)
+ * column-major output rows. The slab is processed in `chunks` sub-slabs whose
+ * NCCL exchange overlaps the next sub-slab's contraction (0 = auto: split only
+ * while each sub-slab keeps >= 4M elements, at most 4). All ranks call it
+ * with the same extents and chunks. Stream-ordered on the handle's stream. */
+int mumode_dist_tucker_f64(mumode_handle_t h, mumode_comm_t c, int d, const int64_t* m,
+                           const int64_t* n, const double* T, const double* const* L, double* S,
+                           int chunks);
+int mumode_dist_tucker_c128(mumode_handle_t h, mumode_comm_t c, int d, const int64_t* m,
+                            const int64_t* n, const double* T, const double* const* L, double* S,
+                            int chunks);
+
 /* Replaces ops::kronsumv (tucker.hpp:209-232): W = sum_mu V x_mu A_mu with
  * square A_mu of size m[mu]. */
 int mumode_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double* V,

@@ -8,7 +8,9 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
+#include <type_traits>
 #include <map>
 #include <unordered_map>
 #include <memory>
@@ -1263,3 +1265,5 @@ int mumode_host_expint_f64(mumode_handle_t h, int d, const int64_t* m, const dou
 }
 
 }  // extern "C"
+
+#include "slab_dist.cuh"

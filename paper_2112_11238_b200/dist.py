@@ -231,6 +231,108 @@ class CudaSlabBackend:
         return S
 
 
+# ------------------------------------------------------------------ C-ABI path
+class Comm:
+    """A ``mumode_comm_t``: NCCL communicator + exchange stream + buffers of the
+    C-ABI slab-partitioned Tucker (``mumode_dist_tucker_{f64,c128}``)."""
+
+    NCCL_ID_BYTES = 128
+
+    def __init__(self, nranks: int, rank: int, unique_id: bytes | None, device: int = 0):
+        import ctypes
+
+        from . import _lib
+        from .api import _check
+        self.nranks, self.rank, self.device = int(nranks), int(rank), int(device)
+        c = ctypes.c_void_p()
+        if unique_id is None:  # single rank without NCCL
+            if self.nranks != 1:
+                raise ValueError("a multi-rank communicator needs an NCCL unique id")
+            _check(_lib.lib().mumode_comm_wrap(ctypes.byref(c), self.device, None, 1, 0))
+        else:
+            buf = ctypes.create_string_buffer(bytes(unique_id), self.NCCL_ID_BYTES)
+            _check(_lib.lib().mumode_comm_create(ctypes.byref(c), self.device, buf, self.nranks, self.rank))
+        self.c = c
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes
+
+        from . import _lib
+        from .api import _check
+        buf = ctypes.create_string_buffer(Comm.NCCL_ID_BYTES)
+        _check(_lib.lib().mumode_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_torch(cls, group=None, device: int | None = None) -> "Comm":
+        """Collective over a torch.distributed group: its first rank creates the
+        NCCL id and broadcasts it through the group."""
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=src, group=group)
+        dev = torch.cuda.current_device() if device is None else device
+        return cls(world, rank, obj[0], dev)
+
+    def close(self) -> None:
+        if getattr(self, "c", None):
+            from . import _lib
+            _lib.lib().mumode_comm_destroy(self.c)
+            self.c = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def slab_plan_offsets(P: int, m: Sequence[int], n: Sequence[int]) -> tuple[list[int], list[int]]:
+    """(c_off, a_off) from the C-ABI's mumode_slab_plan (host only)."""
+    import ctypes
+
+    from . import _lib
+    from .api import _check
+    c_off = (ctypes.c_int64 * (P + 1))()
+    a_off = (ctypes.c_int64 * (P + 1))()
+    _check(_lib.lib().mumode_slab_plan(int(P), len(m), _lib.i64_array(m), _lib.i64_array(n), c_off, a_off))
+    return list(c_off), list(a_off)
+
+
+def dist_tucker(comm: Comm, T_local, Ls, m: Sequence[int], n: Sequence[int] | None = None, chunks: int = 4,
+                out=None):
+    """One slab-partitioned Tucker application through the C-ABI
+    (``mumode_dist_tucker_{f64,c128}``). ``T_local``: this rank's column-major
+    last-mode slab on its GPU; ``Ls``: all d factors on the same GPU; ``m``,
+    ``n``: GLOBAL extents. Returns this rank's (A_r x n_d) rows of the result as
+    a flat column-major tensor (``gather_rows`` reassembles)."""
+    import torch
+
+    from . import _lib
+    from .api import _check, get_handle, is_colmajor
+    d = len(m)
+    n = [int(L.shape[0]) for L in Ls] if n is None else [int(e) for e in n]
+    cplx = T_local.is_complex() or any(L.is_complex() for L in Ls)
+    dt = torch.complex128 if cplx else torch.float64
+    if T_local.dtype != dt or not is_colmajor(T_local):
+        raise ValueError("dist_tucker: T_local must be a column-major float64/complex128 slab "
+                         "(complex factors need a complex slab)")
+    Ls = [L.to(dt) for L in Ls]
+    Ls = [L if is_colmajor(L) else L.t().contiguous().t() for L in Ls]
+    c_off, a_off = slab_plan_offsets(comm.nranks, m, n)
+    A_r = a_off[comm.rank + 1] - a_off[comm.rank]
+    S = out if out is not None else torch.empty(A_r * n[-1], dtype=dt, device=T_local.device)
+    h = get_handle(T_local.device.index)
+    h.bind_torch_stream()
+    fn = _lib.lib().mumode_dist_tucker_c128 if cplx else _lib.lib().mumode_dist_tucker_f64
+    _check(fn(h.h, comm.c, d, _lib.i64_array(m), _lib.i64_array(n), T_local.data_ptr(),
+              _lib.ptr_array([L.data_ptr() for L in Ls]), S.data_ptr(), int(chunks)))
+    return S
+
+
 def gather_rows(plan: SlabPlan, blocks: Sequence[np.ndarray]) -> np.ndarray:
     """Reassemble the full column-major result from the per-rank (A_r x n_d)
     row blocks (flat column-major arrays)."""

@@ -17,7 +17,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle as O
-from paper_2112_11238_b200.dist import (SlabPlan, gather_rows, scatter_slabs, slab_tucker,
+import paper_2112_11238_b200 as mm
+from paper_2112_11238_b200.dist import (SlabPlan, gather_rows, scatter_slabs, slab_plan_offsets, slab_tucker,
                                         slab_tucker_overlapped)
 
 
@@ -132,6 +133,19 @@ def test_plan_bookkeeping():
         SlabPlan((4, 2), (4, 2), 3)
 
 
+def test_c_abi_slab_plan_matches_python_plan():
+    # mumode_slab_plan (host-only C-ABI) == SlabPlan, the partition the gloo
+    # tests exercise, so both multi-GPU paths agree on who holds what
+    from paper_2112_11238_b200.api import SizeError
+    for m, n, P in [((256, 256, 256), (256, 256, 256), 8), ((5, 7), (4, 3), 3), ((24,) * 6, (24,) * 6, 8),
+                    ((6, 5, 4), (3, 7, 5), 2), ((2, 3, 2, 3, 4), (3, 2, 3, 2, 5), 3), ((3, 64), (2, 64), 64)]:
+        plan = SlabPlan(m, n, P)
+        c_off, a_off = slab_plan_offsets(P, m, n)
+        assert c_off == plan.c_off and a_off == plan.a_off, (m, n, P)
+    with pytest.raises(SizeError, match="last mode extent 2 < 3 ranks"):
+        slab_plan_offsets(3, (4, 2), (4, 2))
+
+
 # ------------------------------------------------------------------ GPU
 class SimulatedExchange:
     """Wraps the CUDA backend for P ranks simulated on one GPU: the exchange
@@ -222,3 +236,61 @@ def test_slab_tucker_nccl_single_rank():
         assert O.rel_fro(S, O.port_tucker(T, Ls)) < 1e-13
     finally:
         dist.destroy_process_group()
+
+
+DIST_CASES = [((48, 40, 32), (40, 56, 24), False), ((24, 24, 24, 24), (24, 24, 24, 24), False),
+              ((16, 12, 10), (12, 14, 9), True), ((30, 7), (11, 13), False), ((64, 48, 40), (56, 48, 72), False)]
+
+
+def _dist_case(comm, m, n, cplx, chunks, seed):
+    from paper_2112_11238_b200.dist import dist_tucker
+    rng = np.random.default_rng(seed)
+    def rnd(shape):
+        x = rng.standard_normal(shape)
+        if cplx:
+            x = x + 1j * rng.standard_normal(shape)
+        return np.asfortranarray(x)
+    T = rnd(m)
+    Ls = [rnd((n[k], m[k])) for k in range(len(m))]
+    plan = SlabPlan(m, n, 1)
+    Td = torch.from_numpy(T).cuda()
+    S_r = dist_tucker(comm, Td, [torch.from_numpy(L).cuda() for L in Ls], m, n, chunks=chunks)
+    S = gather_rows(plan, [S_r.cpu().numpy()])
+    return O.rel_fro(S, O.port_tucker(T, Ls))
+
+
+@pytest.mark.gpu
+def test_dist_tucker_c_abi_nccl_single_rank():
+    # the C-ABI slab-partitioned Tucker with a real (1-rank) NCCL communicator:
+    # chunked local modes, pack, grouped exchange stream, last mode
+    from paper_2112_11238_b200.dist import Comm
+    comm = Comm(1, 0, Comm.unique_id(), 0)
+    try:
+        for i, (m, n, cplx) in enumerate(DIST_CASES):
+            for chunks in (1, 3, 8):
+                assert _dist_case(comm, m, n, cplx, chunks, 100 + i) < 1e-14, (m, n, cplx, chunks)
+    finally:
+        comm.close()
+
+
+@pytest.mark.gpu
+def test_dist_tucker_c_abi_wrapped_single_rank_matches_tucker_bitwise():
+    from paper_2112_11238_b200.dist import Comm, dist_tucker
+    comm = Comm(1, 0, None, 0)
+    try:
+        assert _dist_case(comm, (40, 32, 24), (24, 40, 32), False, 2, 7) < 1e-14
+        # 1 rank, 1 chunk: same kernels and accumulation order as tucker()
+        g = mm.Rng(1234)
+        T = torch.from_numpy(g.normal((96, 64, 48))).cuda()
+        Ls = [torch.from_numpy(g.normal((64, e))).cuda() for e in (96, 64, 48)]
+        S_r = dist_tucker(comm, T, Ls, (96, 64, 48), chunks=1)
+        ref = mm.tucker(T, Ls)
+        assert np.array_equal(S_r.cpu().numpy(), ref.cpu().numpy().reshape(-1, order="F"))
+    finally:
+        comm.close()
+
+
+def test_multi_rank_comm_requires_nccl_id():
+    from paper_2112_11238_b200.dist import Comm
+    with pytest.raises(ValueError):
+        Comm(2, 0, None, 0)
