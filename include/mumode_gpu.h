@@ -128,6 +128,15 @@ int mumode_comm_destroy(mumode_comm_t c);
  * flattened to A x n_d). Even splits; MUMODE_ERR_SIZE if m_d < P. */
 int mumode_slab_plan(int nranks, int d, const int64_t* m, const int64_t* n, int64_t* c_off,
                      int64_t* a_off);
+/* The schedule mumode_dist_tucker_* executes on rank `rank` (host only):
+ * chunk_tab rows (col0, width, send_offset) per sub-slab, op_tab rows
+ * (chunk, kind, peer, send_offset, z_offset, count) with kind 0 = NCCL send,
+ * 1 = NCCL receive, 2 = own block device copy; offsets/counts in doubles.
+ * Lets the multi-rank logic be checked without GPUs. Tables too small ->
+ * MUMODE_ERR_ARGUMENT with the needed sizes in n_chunks / n_ops. */
+int mumode_dist_plan(int nranks, int rank, int d, const int64_t* m, const int64_t* n, int chunks,
+                     int cplx, int64_t* chunk_tab, int max_chunks, int* n_chunks, int64_t* op_tab,
+                     int max_ops, int* n_ops);
 /* One slab-partitioned Tucker application (replaces ops::tucker across
  * ranks, tucker.hpp:129-144). m, n: GLOBAL extents. T: this rank's slab
  * (m_1 x ... x m_{d-1} x c_r, column-major); S: this rank's (A_r x n_d)

@@ -98,6 +98,87 @@ static int slab_plan(int P, int d, const int64_t* m, const int64_t* n, int64_t* 
   return MUMODE_OK;
 }
 
+// The complete per-rank schedule of one slab-partitioned application, built
+// on the host (and exposed as mumode_dist_plan so the multi-rank logic is
+// verified on CPU: tests/test_dist.py simulates every rank executing it).
+struct DistChunk {
+  int64_t col0;      // first slab column of the sub-slab
+  int64_t w;         // its width (0: this rank has no sub-slab j)
+  int64_t send_off;  // doubles: where the packed sub-slab sits in the send buffer
+};
+struct DistOp {
+  int64_t chunk, kind, peer;  // kind 0 = send, 1 = receive, 2 = own block (device copy)
+  int64_t buf_off;            // send buffer offset (send, copy source)
+  int64_t z_off;              // Z offset (receive, copy destination)
+  int64_t count;              // doubles
+};
+struct DistPlan {
+  int64_t c_off[kMaxRanks + 1], a_off[kMaxRanks + 1];
+  int64_t rows_in = 0, A = 0, A_r = 0, m_d = 0, n_d = 0, wmax = 0, send_elems = 0, z_elems = 0;
+  std::vector<DistChunk> ch;
+  std::vector<DistOp> ops;  // grouped by chunk; within a chunk: copy, sends (q order), receives (s order)
+};
+
+static int dist_plan(int P, int r, int d, const int64_t* m, const int64_t* n, int chunks, int el, DistPlan& pl) {
+  if (r < 0 || r >= P) return fail(MUMODE_ERR_ARGUMENT, "dist plan: bad rank");
+  if (chunks < 0) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: chunks must be >= 0 (0 = auto)");
+  MM_TRY(slab_plan(P, d, m, n, pl.c_off, pl.a_off));
+  pl.rows_in = prod(m, 0, d - 1);
+  pl.A = prod(n, 0, d - 1);
+  pl.A_r = pl.a_off[r + 1] - pl.a_off[r];
+  pl.m_d = m[d - 1];
+  pl.n_d = n[d - 1];
+  // auto: split a slab only while every sub-slab keeps >= 4M elements, so the
+  // per-chunk kernels still fill the GPU (at most 4 sub-slabs); the same on
+  // every rank (smallest slab)
+  if (chunks == 0) {
+    const int64_t c_min = pl.c_off[1] - pl.c_off[0] - ((m[d - 1] % P) ? 1 : 0);
+    chunks = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(4, pl.rows_in * std::max<int64_t>(c_min, 1) / (int64_t(1) << 22))));
+  }
+  // every rank's sub-slab split (all ranks derive all of them, so the posted
+  // sends and receives match)
+  int nch = 0;
+  std::vector<std::vector<int64_t>> sub(P);
+  for (int s = 0; s < P; ++s) {
+    const int64_t cs = pl.c_off[s + 1] - pl.c_off[s];
+    const int k = static_cast<int>(std::min<int64_t>(chunks, cs));
+    sub[s].assign(k + 1, 0);
+    even_splits(cs, k, sub[s].data());
+    nch = std::max(nch, k);
+  }
+  auto width = [&](int s, int j) -> int64_t {
+    return j + 1 < static_cast<int>(sub[s].size()) ? sub[s][j + 1] - sub[s][j] : 0;
+  };
+  const int64_t A = pl.A, A_r = pl.A_r;
+  pl.ch.clear();
+  pl.ops.clear();
+  pl.wmax = 0;
+  for (int j = 0; j < nch; ++j) {
+    const int64_t w = width(r, j);
+    const int64_t c0 = w > 0 ? sub[r][j] : 0;
+    pl.ch.push_back({c0, w, A * c0 * el});
+    pl.wmax = std::max(pl.wmax, w);
+    const int64_t sbase = A * c0 * el;
+    if (w > 0 && A_r > 0)  // own row block: straight into its final columns
+      pl.ops.push_back({j, 2, r, sbase + pl.a_off[r] * w * el, A_r * (pl.c_off[r] + c0) * el, A_r * w * el});
+    if (w > 0)
+      for (int q = 0; q < P; ++q) {
+        const int64_t rows = pl.a_off[q + 1] - pl.a_off[q];
+        if (q == r || rows == 0) continue;
+        pl.ops.push_back({j, 0, q, sbase + pl.a_off[q] * w * el, 0, rows * w * el});
+      }
+    for (int s = 0; s < P; ++s) {
+      const int64_t ws = width(s, j);
+      if (s == r || ws == 0 || A_r == 0) continue;
+      pl.ops.push_back({j, 1, s, 0, A_r * (pl.c_off[s] + sub[s][j]) * el, A_r * ws * el});
+    }
+  }
+  pl.send_elems = A * (pl.c_off[r + 1] - pl.c_off[r]) * el;
+  pl.z_elems = A_r * pl.m_d * el;
+  return MUMODE_OK;
+}
+
 }  // namespace mumode_gpu
 
 struct mumode_comm_s {
@@ -135,96 +216,67 @@ static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64
                        const double* T, const double* const* L, double* S, int chunks, bool cplx) {
   const int P = cm->nranks, r = cm->rank;
   if (cm->device != h->device) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: handle and comm on different devices");
-  if (chunks < 0) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: chunks must be >= 0 (0 = auto)");
-  int64_t c_off[kMaxRanks + 1], a_off[kMaxRanks + 1];
-  MM_TRY(slab_plan(P, d, m, n, c_off, a_off));
   if (!T || !L || !S) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: null pointer");
   for (int k = 0; k < d; ++k)
     if (!L[k]) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: null matrix for mode " + std::to_string(k + 1));
   const int el = cplx ? 2 : 1;
-  const int64_t rows_in = prod(m, 0, d - 1);       // slab rows per last-mode column
-  const int64_t A = prod(n, 0, d - 1);             // rows after modes 1..d-1
-  const int64_t A_r = a_off[r + 1] - a_off[r];
-  const int64_t m_d = m[d - 1], n_d = n[d - 1];
+  DistPlan pl;
+  MM_TRY(dist_plan(P, r, d, m, n, chunks, el, pl));
+  const int64_t A = pl.A, A_r = pl.A_r, m_d = pl.m_d, n_d = pl.n_d;
   if (P == 1 && chunks <= 1) {
     // one rank: no exchange; modes 1..d-1 straight into Z, then mode d
     // (explicit chunks > 1 still take the general path: exercised by tests)
-    MM_TRY(cm->z.ensure(size_t(std::max<int64_t>(A * m_d * el, 1)) * sizeof(double)));
+    MM_TRY(cm->z.ensure(size_t(std::max<int64_t>(pl.z_elems, 1)) * sizeof(double)));
     auto* Z = static_cast<double*>(cm->z.p);
     MM_TRY(tucker_dev(h, d, m, n, T, L, Z, false, cplx, 1, d - 1));
     const int64_t zext[2] = {A, m_d};
     return mode_product_dev(h, 2, zext, 2, n_d, Z, L[d - 1], 1, n_d, cplx, false, S);
   }
-  // auto: split a slab only while every sub-slab keeps >= 4M elements, so the
-  // per-chunk kernels still fill the GPU (at most 4 sub-slabs)
-  if (chunks == 0) {
-    const int64_t c_min = c_off[1] - c_off[0] - ((m[d - 1] % P) ? 1 : 0);
-    chunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(4, rows_in * std::max<int64_t>(c_min, 1) / (int64_t(1) << 22))));
-  }
-  // every rank's sub-slab split (all ranks derive all of them, so the posted
-  // sends and receives match)
-  int nch = 0;
-  std::vector<std::vector<int64_t>> sub(P);
-  for (int s = 0; s < P; ++s) {
-    const int64_t cs = c_off[s + 1] - c_off[s];
-    const int k = static_cast<int>(std::min<int64_t>(chunks, cs));
-    sub[s].assign(k + 1, 0);
-    even_splits(cs, k, sub[s].data());
-    nch = std::max(nch, k);
-  }
-  auto width = [&](int s, int j) -> int64_t {
-    return j + 1 < static_cast<int>(sub[s].size()) ? sub[s][j + 1] - sub[s][j] : 0;
-  };
-  int64_t wmax = 0;
-  for (int j = 0; j < nch; ++j) wmax = std::max(wmax, width(r, j));
-  const int64_t c_r = c_off[r + 1] - c_off[r];
-  MM_TRY(cm->y.ensure(size_t(std::max<int64_t>(A * wmax * el, 1)) * sizeof(double)));
-  MM_TRY(cm->send.ensure(size_t(std::max<int64_t>(A * c_r * el, 1)) * sizeof(double)));
-  MM_TRY(cm->z.ensure(size_t(std::max<int64_t>(A_r * m_d * el, 1)) * sizeof(double)));
+  const int nch = static_cast<int>(pl.ch.size());
+  MM_TRY(cm->y.ensure(size_t(std::max<int64_t>(A * pl.wmax * el, 1)) * sizeof(double)));
+  MM_TRY(cm->send.ensure(size_t(std::max<int64_t>(pl.send_elems, 1)) * sizeof(double)));
+  MM_TRY(cm->z.ensure(size_t(std::max<int64_t>(pl.z_elems, 1)) * sizeof(double)));
   MM_TRY(comm_events(cm, size_t(nch) + 2));
   auto* Y = static_cast<double*>(cm->y.p);
   auto* send = static_cast<double*>(cm->send.p);
   auto* Z = static_cast<double*>(cm->z.p);
-  const ncclDataType_t f64 = ncclFloat64;
 
   // Z (and send) may still be read by the previous call's work on h->stream
   MM_CUDA(cudaEventRecord(cm->events[nch], h->stream));
   MM_CUDA(cudaStreamWaitEvent(cm->stream, cm->events[nch], 0));
   std::vector<int64_t> ext(m, m + d);
   PackOffsets off{};
-  for (int q = 0; q <= P; ++q) off.a[q] = a_off[q] * el;
+  for (int q = 0; q <= P; ++q) off.a[q] = pl.a_off[q] * el;
+  size_t op = 0;
   for (int j = 0; j < nch; ++j) {
-    const int64_t w = width(r, j);
-    double* sj = send + A * sub[r][std::min<size_t>(j, sub[r].size() - 1)] * el;
-    if (w > 0) {
-      ext[d - 1] = w;
-      const double* Tj = T + rows_in * sub[r][j] * el;
-      MM_TRY(tucker_dev(h, d, ext.data(), n, Tj, L, Y, false, cplx, 1, d - 1));
-      slab_pack_kernel<<<grid_for(A * el * w, h->num_sms), 256, 0, h->stream>>>(Y, sj, A * el, w, P, off);
+    const DistChunk& c = pl.ch[j];
+    if (c.w > 0) {
+      ext[d - 1] = c.w;
+      MM_TRY(tucker_dev(h, d, ext.data(), n, T + pl.rows_in * c.col0 * el, L, Y, false, cplx, 1, d - 1));
+      slab_pack_kernel<<<grid_for(A * el * c.w, h->num_sms), 256, 0, h->stream>>>(Y, send + c.send_off, A * el,
+                                                                                 c.w, P, off);
       MM_CUDA(cudaGetLastError());
       h->launches++;
       MM_CUDA(cudaEventRecord(cm->events[j], h->stream));
       MM_CUDA(cudaStreamWaitEvent(cm->stream, cm->events[j], 0));
-      // own row block: straight into its final columns
-      const int64_t col0 = c_off[r] + sub[r][j];
-      if (A_r > 0)
-        MM_CUDA(cudaMemcpyAsync(Z + A_r * col0 * el, sj + a_off[r] * w * el, size_t(A_r * w * el) * sizeof(double),
-                                cudaMemcpyDeviceToDevice, cm->stream));
     }
+    const size_t first = op;
+    while (op < pl.ops.size() && pl.ops[op].chunk == j) ++op;
+    for (size_t k = first; k < op; ++k)
+      if (pl.ops[k].kind == 2)
+        MM_CUDA(cudaMemcpyAsync(Z + pl.ops[k].z_off, send + pl.ops[k].buf_off, size_t(pl.ops[k].count) * sizeof(double),
+                                cudaMemcpyDeviceToDevice, cm->stream));
     if (P > 1) {
       auto& api = nccl_api();
       MM_NCCL(api.group_start());
-      if (w > 0)
-        for (int q = 0; q < P; ++q) {
-          const int64_t rows = a_off[q + 1] - a_off[q];
-          if (q == r || rows == 0) continue;
-          MM_NCCL(api.send(sj + a_off[q] * w * el, size_t(rows * w * el), f64, q, cm->comm, cm->stream));
-        }
-      for (int s = 0; s < P; ++s) {
-        const int64_t ws = width(s, j);
-        if (s == r || ws == 0 || A_r == 0) continue;
-        const int64_t col0 = c_off[s] + sub[s][j];
-        MM_NCCL(api.recv(Z + A_r * col0 * el, size_t(A_r * ws * el), f64, s, cm->comm, cm->stream));
+      for (size_t k = first; k < op; ++k) {
+        const DistOp& o = pl.ops[k];
+        if (o.kind == 0)
+          MM_NCCL(api.send(send + o.buf_off, size_t(o.count), ncclFloat64, static_cast<int>(o.peer), cm->comm,
+                           cm->stream));
+        else if (o.kind == 1)
+          MM_NCCL(api.recv(Z + o.z_off, size_t(o.count), ncclFloat64, static_cast<int>(o.peer), cm->comm,
+                           cm->stream));
       }
       MM_NCCL(api.group_end());
     }
@@ -307,6 +359,29 @@ int mumode_slab_plan(int nranks, int d, const int64_t* m, const int64_t* n, int6
   using namespace mumode_gpu;
   if (!m || !n || !c_off || !a_off) return fail(MUMODE_ERR_ARGUMENT, "slab plan: null pointer");
   return slab_plan(nranks, d, m, n, c_off, a_off);
+}
+
+int mumode_dist_plan(int nranks, int rank, int d, const int64_t* m, const int64_t* n, int chunks, int cplx,
+                     int64_t* chunk_tab, int max_chunks, int* n_chunks, int64_t* op_tab, int max_ops, int* n_ops) {
+  using namespace mumode_gpu;
+  if (!m || !n || !n_chunks || !n_ops) return fail(MUMODE_ERR_ARGUMENT, "dist plan: null pointer");
+  DistPlan pl;
+  MM_TRY(dist_plan(nranks, rank, d, m, n, chunks, cplx ? 2 : 1, pl));
+  *n_chunks = static_cast<int>(pl.ch.size());
+  *n_ops = static_cast<int>(pl.ops.size());
+  if (*n_chunks > max_chunks || *n_ops > max_ops || (max_chunks > 0 && !chunk_tab) || (max_ops > 0 && !op_tab))
+    return fail(MUMODE_ERR_ARGUMENT, "dist plan: tables too small (sizes returned in n_chunks / n_ops)");
+  for (size_t j = 0; j < pl.ch.size(); ++j) {
+    chunk_tab[3 * j] = pl.ch[j].col0;
+    chunk_tab[3 * j + 1] = pl.ch[j].w;
+    chunk_tab[3 * j + 2] = pl.ch[j].send_off;
+  }
+  for (size_t k = 0; k < pl.ops.size(); ++k) {
+    const DistOp& o = pl.ops[k];
+    const int64_t row[6] = {o.chunk, o.kind, o.peer, o.buf_off, o.z_off, o.count};
+    std::memcpy(op_tab + 6 * k, row, sizeof(row));
+  }
+  return MUMODE_OK;
 }
 
 int mumode_dist_tucker_f64(mumode_handle_t h, mumode_comm_t c, int d, const int64_t* m, const int64_t* n,

@@ -302,6 +302,29 @@ def slab_plan_offsets(P: int, m: Sequence[int], n: Sequence[int]) -> tuple[list[
     return list(c_off), list(a_off)
 
 
+def dist_plan(P: int, rank: int, m: Sequence[int], n: Sequence[int], chunks: int = 0, cplx: bool = False):
+    """The exact schedule ``mumode_dist_tucker_*`` runs on ``rank`` (host-only
+    C-ABI ``mumode_dist_plan``): ([(col0, width, send_off)] per sub-slab,
+    [(chunk, kind, peer, send_off, z_off, count)] with kind 0 send, 1 receive,
+    2 own-block copy; offsets and counts in doubles)."""
+    import ctypes
+
+    from . import _lib
+    from .api import _check
+    lib = _lib.lib()
+    nc, no = ctypes.c_int(), ctypes.c_int()
+    args = (int(P), int(rank), len(m), _lib.i64_array(m), _lib.i64_array(n), int(chunks), int(cplx))
+    rc = lib.mumode_dist_plan(*args, None, 0, ctypes.byref(nc), None, 0, ctypes.byref(no))
+    if rc != 0 and nc.value == 0 and no.value == 0:
+        _check(rc)
+    ct = (ctypes.c_int64 * max(1, 3 * nc.value))()
+    ot = (ctypes.c_int64 * max(1, 6 * no.value))()
+    _check(lib.mumode_dist_plan(*args, ct, nc.value, ctypes.byref(nc), ot, no.value, ctypes.byref(no)))
+    chunks_ = [tuple(ct[3 * j:3 * j + 3]) for j in range(nc.value)]
+    ops = [tuple(ot[6 * k:6 * k + 6]) for k in range(no.value)]
+    return chunks_, ops
+
+
 def dist_tucker(comm: Comm, T_local, Ls, m: Sequence[int], n: Sequence[int] | None = None, chunks: int = 4,
                 out=None):
     """One slab-partitioned Tucker application through the C-ABI

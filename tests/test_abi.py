@@ -155,3 +155,15 @@ def test_factorized_stack_refuses_singular_matrices():
         mm.FactorizedStack([np.zeros((2, 2))])
     F = mm.FactorizedStack([np.array([[4.0, 1.0], [2.0, 3.0]])])
     np.testing.assert_allclose(F.inverses[0] @ np.array([[4.0, 1.0], [2.0, 3.0]]), np.eye(2), atol=1e-15)
+
+
+def test_empty_tensors_rejected_like_reference():
+    # Shape({2, 0, 3}) and Shape({}) throw ArgumentError (test_tensor_core.cpp:17-20);
+    # the engine rejects them before touching a device, at both layers
+    with pytest.raises(mm.ArgumentError, match="extents must be positive"):
+        mm.tucker(np.zeros((2, 0, 3), order="F"), [np.eye(2), np.zeros((1, 0)), np.eye(3)])
+    with pytest.raises(mm.ArgumentError, match="order must be >= 1"):
+        mm.mode_product(np.zeros(()), np.eye(1), 1)
+    from paper_2112_11238_b200.dist import slab_plan_offsets
+    with pytest.raises(mm.ArgumentError, match="extents must be positive"):
+        slab_plan_offsets(1, (2, 0, 3), (2, 1, 3))

@@ -146,6 +146,101 @@ def test_c_abi_slab_plan_matches_python_plan():
         slab_plan_offsets(3, (4, 2), (4, 2))
 
 
+def _simulate_c_schedule(m, n, P, chunks, cplx, seed):
+    """Every rank executes its mumode_dist_plan schedule on numpy buffers:
+    local modes per sub-slab (oracle), the slab_pack layout, sends matched to
+    receives in NCCL order per peer pair, own-block copies, then the last
+    mode. Returns the relative error against the oracle Tucker."""
+    from paper_2112_11238_b200.dist import dist_plan
+    rng = np.random.default_rng(seed)
+
+    def rnd(shape):
+        x = rng.standard_normal(shape)
+        return np.asfortranarray(x + 1j * rng.standard_normal(shape) if cplx else x)
+    d = len(m)
+    T = rnd(m)
+    Ls = [rnd((n[k], m[k])) for k in range(d)]
+    plan = SlabPlan(m, n, P)
+    el = 2 if cplx else 1
+    A = plan.A
+    slabs = scatter_slabs(plan, T)
+    sends, zs, sched = [], [], []
+    for r in range(P):
+        ch, ops = dist_plan(P, r, m, n, chunks, cplx)
+        sched.append((ch, ops))
+        send = np.full(A * plan.c_sizes[r] * el, np.nan)
+        for col0, w, soff in ch:
+            if w == 0:
+                continue
+            Tj = np.asfortranarray(slabs[r][..., col0:col0 + w])
+            Y = Tj
+            for mu in range(1, d):
+                Y = O.port_mode_product(Y, Ls[mu - 1], mu)
+            Yd = Y.reshape((A, w), order="F")
+            Yd = np.stack([Yd.real, Yd.imag], axis=0).transpose(1, 0, 2).reshape(A * el, w) if cplx else Yd
+            for q in range(P):  # slab_pack_kernel layout
+                lo, hi = plan.a_off[q] * el, plan.a_off[q + 1] * el
+                blk = Yd[lo:hi, :].reshape(-1, order="F")
+                send[soff + lo * w: soff + lo * w + blk.size] = blk
+        sends.append(send)
+        zs.append(np.full(plan.a_sizes[r] * m[-1] * el, np.nan))
+    # exchange: per (chunk, sender, receiver) the k-th send pairs with the k-th receive
+    from collections import defaultdict
+    sq, rq = defaultdict(list), defaultdict(list)
+    for r, (ch, ops) in enumerate(sched):
+        for (j, kind, peer, boff, zoff, cnt) in ops:
+            if kind == 0:
+                sq[(r, peer)].append((j, boff, cnt))
+            elif kind == 1:
+                rq[(peer, r)].append((j, zoff, cnt))
+            else:
+                assert peer == r
+                assert np.isnan(zs[r][zoff:zoff + cnt]).all(), "own block overlaps"
+                zs[r][zoff:zoff + cnt] = sends[r][boff:boff + cnt]
+    assert set(sq) == set(rq)
+    for key in sq:
+        assert len(sq[key]) == len(rq[key])
+        for (j, boff, cnt), (j2, zoff, cnt2) in zip(sq[key], rq[key]):
+            assert j == j2 and cnt == cnt2, (key, j, j2, cnt, cnt2)
+            src, dst = key
+            assert np.isnan(zs[dst][zoff:zoff + cnt]).all(), "receive regions overlap"
+            zs[dst][zoff:zoff + cnt] = sends[src][boff:boff + cnt]
+    blocks = []
+    for r in range(P):
+        assert not np.isnan(zs[r]).any(), "Z not fully written"
+        Z = zs[r]
+        if cplx:
+            Z = Z[0::2] + 1j * Z[1::2]
+        Zm = Z.reshape((plan.a_sizes[r], m[-1]), order="F")
+        blocks.append(O.port_mode_product(np.asfortranarray(Zm), Ls[-1], 2).reshape(-1, order="F"))
+    return O.rel_fro(gather_rows(plan, blocks), O.port_tucker(T, Ls))
+
+
+@pytest.mark.parametrize("P", [2, 3, 5, 8])
+def test_c_abi_dist_schedule_simulated_ranks(P):
+    # the C++ multi-rank schedule (offsets, chunking, send/receive matching)
+    # executed by P simulated ranks on CPU reproduces the Tucker operator
+    cases = [((6, 5, 8), (3, 7, 5), False), ((4, 4, 4, 9), (4, 4, 4, 6), False), ((7, 3, 17), (5, 4, 2), True),
+             ((5, 13), (8, 3), False), ((2, 3, 2, 3, 8), (3, 2, 3, 2, 5), True), ((3, 2, 11), (1, 1, 4), False)]
+    for i, (m, n, cplx) in enumerate(cases):
+        if m[-1] < P:
+            continue
+        for chunks in (0, 1, 2, 3, 16):
+            err = _simulate_c_schedule(m, n, P, chunks, cplx, 1000 * P + i)
+            assert err < 1e-13, (m, n, P, chunks, cplx, err)
+
+
+def test_c_abi_dist_plan_auto_chunks_and_sizes():
+    from paper_2112_11238_b200.dist import dist_plan
+    # C2 on 2 ranks: slabs of 128 columns x 65536 rows -> 2 auto sub-slabs; 8 ranks -> 1
+    ch, ops = dist_plan(2, 0, (256, 256, 256), (256, 256, 256))
+    assert [w for _, w, _ in ch] == [64, 64]
+    assert sum(c for (_, k, _, _, _, c) in ops if k == 0) == 65536 // 2 * 128  # half the rows leave
+    ch, ops = dist_plan(8, 3, (256, 256, 256), (256, 256, 256))
+    assert [w for _, w, _ in ch] == [32]
+    assert sum(1 for o in ops if o[1] == 0) == 7 and sum(1 for o in ops if o[1] == 1) == 7
+
+
 # ------------------------------------------------------------------ GPU
 class SimulatedExchange:
     """Wraps the CUDA backend for P ranks simulated on one GPU: the exchange
