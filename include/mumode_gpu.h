@@ -150,6 +150,18 @@ int mumode_dist_tucker_f64(mumode_handle_t h, mumode_comm_t c, int d, const int6
 int mumode_dist_tucker_c128(mumode_handle_t h, mumode_comm_t c, int d, const int64_t* m,
                             const int64_t* n, const double* T, const double* const* L, double* S,
                             int chunks);
+/* Return exchange after an application with output extents n (host only):
+ * rank r's output rows (A_r x n_d) -> the last-mode slabs of the output for
+ * the next application. op_tab rows as in mumode_dist_plan (send_offset into
+ * the rows, z_offset into a [s][A_s x c_r] staging buffer). */
+int mumode_dist_return_plan(int nranks, int rank, int d, const int64_t* n, int64_t* op_tab,
+                            int max_ops, int* n_ops);
+/* `steps` exponential-integrator steps u <- tucker(u, {E_1..E_d}) across ranks
+ * (apps::linear_evolution_exact, src/evolution.cpp:70-82): each step is a
+ * slab-partitioned Tucker, a return exchange and an unpack, in the
+ * reference's mode order. u0, u: this rank's last-mode slabs (E square). */
+int mumode_dist_expint_f64(mumode_handle_t h, mumode_comm_t c, int d, const int64_t* m,
+                           const double* const* E, const double* u0, double* u, int steps);
 
 /* Replaces ops::kronsumv (tucker.hpp:209-232): W = sum_mu V x_mu A_mu with
  * square A_mu of size m[mu]. */

@@ -44,6 +44,9 @@ SIGNATURES = {
     "mumode_dist_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, I64P, I64P, ctypes.c_int, ctypes.c_int,
                                         I64P, ctypes.c_int, ctypes.POINTER(ctypes.c_int), I64P, ctypes.c_int,
                                         ctypes.POINTER(ctypes.c_int)]),
+    "mumode_dist_return_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, I64P, I64P, ctypes.c_int,
+                                               ctypes.POINTER(ctypes.c_int)]),
+    "mumode_dist_expint_f64": (ctypes.c_int, [H, VP, ctypes.c_int, I64P, ctypes.POINTER(VP), VP, VP, ctypes.c_int]),
     "mumode_dist_tucker_f64": (ctypes.c_int, [H, VP, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
     "mumode_dist_tucker_c128": (ctypes.c_int, [H, VP, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
     "mumode_kronsumv_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, VP, ctypes.POINTER(VP), VP]),

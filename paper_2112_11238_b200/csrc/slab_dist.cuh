@@ -179,6 +179,33 @@ static int dist_plan(int P, int r, int d, const int64_t* m, const int64_t* n, in
   return MUMODE_OK;
 }
 
+// Return exchange after an application: rank r's output rows (A_r x n_d,
+// column-major, the rows buffer R) become the last-mode slabs of the output
+// tensor for the next application (A x c'_r). Rank r sends R's columns of
+// slab q (contiguous: A_r x c'_q) to q and receives (A_s x c'_r) from every s
+// into a staging buffer laid out like the pack ([s][A_s x c'_r]), which
+// slab_unpack_kernel turns into the slab. ops: buf_off into R, z_off into the
+// staging buffer.
+static int return_plan(int P, int r, int d, const int64_t* n, std::vector<DistOp>& ops, int64_t* c_off,
+                       int64_t* a_off, int el) {
+  if (r < 0 || r >= P) return fail(MUMODE_ERR_ARGUMENT, "dist plan: bad rank");
+  MM_TRY(slab_plan(P, d, n, n, c_off, a_off));
+  ops.clear();
+  const int64_t A_r = a_off[r + 1] - a_off[r], c_r = c_off[r + 1] - c_off[r];
+  if (A_r > 0) ops.push_back({0, 2, r, A_r * c_off[r] * el, a_off[r] * c_r * el, A_r * c_r * el});
+  for (int q = 0; q < P; ++q) {
+    const int64_t c_q = c_off[q + 1] - c_off[q];
+    if (q == r || A_r == 0 || c_q == 0) continue;
+    ops.push_back({0, 0, q, A_r * c_off[q] * el, 0, A_r * c_q * el});
+  }
+  for (int s = 0; s < P; ++s) {
+    const int64_t A_s = a_off[s + 1] - a_off[s];
+    if (s == r || A_s == 0) continue;
+    ops.push_back({0, 1, s, 0, a_off[s] * c_r * el, A_s * c_r * el});
+  }
+  return MUMODE_OK;
+}
+
 }  // namespace mumode_gpu
 
 struct mumode_comm_s {
@@ -188,6 +215,8 @@ struct mumode_comm_s {
   cudaStream_t stream = nullptr;          // exchange stream
   std::vector<cudaEvent_t> events;        // per-chunk "packed" + start/done
   mumode_gpu::DevBuf y, send, z;          // chunk intermediate, packed slab, received (A_r x m_d)
+  mumode_gpu::DevBuf rows, stage, spare;  // expint: output rows, return staging, slab ping-pong
+  cudaEvent_t ret_in = nullptr, ret_out = nullptr;  // expint: return exchange
 };
 
 namespace mumode_gpu {
@@ -288,6 +317,94 @@ static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64
   return mode_product_dev(h, 2, zext, 2, n_d, Z, L[d - 1], 1, n_d, cplx, false, S);
 }
 
+// Inverse of slab_pack_kernel: staging ([q][|A_q| x C] blocks) -> Y (A x C).
+__global__ void slab_unpack_kernel(const double* __restrict__ stage, double* __restrict__ Y, int64_t A, int64_t C,
+                                   int P, PackOffsets off) {
+  const int64_t total = A * C;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t a = e % A, c = e / A;
+    int q = 0;
+    while (q + 1 < P && a >= off.a[q + 1]) ++q;
+    const int64_t rows = off.a[q + 1] - off.a[q];
+    Y[e] = stage[off.a[q] * C + (a - off.a[q]) + c * rows];
+  }
+}
+
+// Copies and one NCCL group of a schedule on the exchange stream.
+static int run_ops(mumode_comm_s* cm, const DistOp* ops, size_t nops, const double* src, double* dst) {
+  for (size_t k = 0; k < nops; ++k)
+    if (ops[k].kind == 2)
+      MM_CUDA(cudaMemcpyAsync(dst + ops[k].z_off, src + ops[k].buf_off, size_t(ops[k].count) * sizeof(double),
+                              cudaMemcpyDeviceToDevice, cm->stream));
+  if (cm->nranks == 1) return MUMODE_OK;
+  auto& api = nccl_api();
+  MM_NCCL(api.group_start());
+  for (size_t k = 0; k < nops; ++k) {
+    const DistOp& o = ops[k];
+    if (o.kind == 0)
+      MM_NCCL(api.send(src + o.buf_off, size_t(o.count), ncclFloat64, static_cast<int>(o.peer), cm->comm, cm->stream));
+    else if (o.kind == 1)
+      MM_NCCL(api.recv(dst + o.z_off, size_t(o.count), ncclFloat64, static_cast<int>(o.peer), cm->comm, cm->stream));
+  }
+  MM_NCCL(api.group_end());
+  return MUMODE_OK;
+}
+
+// steps x (slab-partitioned Tucker with E, return exchange, unpack): the
+// exponential-integrator step (evolution.cpp:70-82) across ranks; modes in the
+// reference order every step. u0 / u: this rank's last-mode slabs.
+static int dist_expint(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64_t* m, const double* const* E,
+                       const double* u0, double* u, int steps) {
+  const int P = cm->nranks, r = cm->rank;
+  if (cm->device != h->device) return fail(MUMODE_ERR_ARGUMENT, "dist_expint: handle and comm on different devices");
+  if (steps < 0) return fail(MUMODE_ERR_ARGUMENT, "expint: steps must be non-negative");
+  if (!u0 || !u || !E) return fail(MUMODE_ERR_ARGUMENT, "dist_expint: null pointer");
+  int64_t c_off[kMaxRanks + 1], a_off[kMaxRanks + 1];
+  std::vector<DistOp> ops;
+  MM_TRY(return_plan(P, r, d, m, ops, c_off, a_off, 1));
+  const int64_t A = prod(m, 0, d - 1), c_r = c_off[r + 1] - c_off[r], A_r = a_off[r + 1] - a_off[r];
+  const size_t slab_bytes = size_t(A * c_r) * sizeof(double);
+  if (steps == 0) {
+    if (u != u0) MM_CUDA(cudaMemcpyAsync(u, u0, slab_bytes, cudaMemcpyDeviceToDevice, h->stream));
+    return MUMODE_OK;
+  }
+  MM_TRY(cm->spare.ensure(std::max<size_t>(slab_bytes, 8)));
+  if (P > 1) {
+    MM_TRY(cm->rows.ensure(std::max<size_t>(size_t(A_r * m[d - 1]) * sizeof(double), 8)));
+    MM_TRY(cm->stage.ensure(std::max<size_t>(slab_bytes, 8)));
+  }
+  if (!cm->ret_in) MM_CUDA(cudaEventCreateWithFlags(&cm->ret_in, cudaEventDisableTiming));
+  if (!cm->ret_out) MM_CUDA(cudaEventCreateWithFlags(&cm->ret_out, cudaEventDisableTiming));
+  cudaEvent_t ev_in = cm->ret_in, ev_out = cm->ret_out;
+  auto* spare = static_cast<double*>(cm->spare.p);
+  PackOffsets off{};
+  for (int q = 0; q <= P; ++q) off.a[q] = a_off[q];
+  const double* cur = u0;
+  for (int s = 0; s < steps; ++s) {
+    double* dst = ((steps - 1 - s) % 2 == 0) ? u : spare;
+    if (dst == cur) dst = (dst == u) ? spare : u;
+    if (P == 1) {  // the output rows ARE the slab
+      MM_TRY(dist_tucker(h, cm, d, m, m, cur, E, dst, 0, false));
+    } else {
+      auto* R = static_cast<double*>(cm->rows.p);
+      auto* stage = static_cast<double*>(cm->stage.p);
+      MM_TRY(dist_tucker(h, cm, d, m, m, cur, E, R, 0, false));
+      MM_CUDA(cudaEventRecord(ev_in, h->stream));
+      MM_CUDA(cudaStreamWaitEvent(cm->stream, ev_in, 0));
+      MM_TRY(run_ops(cm, ops.data(), ops.size(), R, stage));
+      MM_CUDA(cudaEventRecord(ev_out, cm->stream));
+      MM_CUDA(cudaStreamWaitEvent(h->stream, ev_out, 0));
+      slab_unpack_kernel<<<grid_for(A * c_r, h->num_sms), 256, 0, h->stream>>>(stage, dst, A, c_r, P, off);
+      MM_CUDA(cudaGetLastError());
+      h->launches++;
+    }
+    cur = dst;
+  }
+  if (cur != u) MM_CUDA(cudaMemcpyAsync(u, cur, slab_bytes, cudaMemcpyDeviceToDevice, h->stream));
+  return MUMODE_OK;
+}
+
 }  // namespace mumode_gpu
 
 extern "C" {
@@ -349,6 +466,8 @@ int mumode_comm_destroy(mumode_comm_t c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto e : c->events) cudaEventDestroy(e);
+  if (c->ret_in) cudaEventDestroy(c->ret_in);
+  if (c->ret_out) cudaEventDestroy(c->ret_out);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->owned && c->comm) mumode_gpu::nccl_api().comm_destroy(c->comm);
   delete c;
@@ -382,6 +501,32 @@ int mumode_dist_plan(int nranks, int rank, int d, const int64_t* m, const int64_
     std::memcpy(op_tab + 6 * k, row, sizeof(row));
   }
   return MUMODE_OK;
+}
+
+int mumode_dist_return_plan(int nranks, int rank, int d, const int64_t* n, int64_t* op_tab, int max_ops,
+                            int* n_ops) {
+  using namespace mumode_gpu;
+  if (!n || !n_ops) return fail(MUMODE_ERR_ARGUMENT, "dist plan: null pointer");
+  int64_t c_off[kMaxRanks + 1], a_off[kMaxRanks + 1];
+  std::vector<DistOp> ops;
+  MM_TRY(return_plan(nranks, rank, d, n, ops, c_off, a_off, 1));
+  *n_ops = static_cast<int>(ops.size());
+  if (*n_ops > max_ops || (max_ops > 0 && !op_tab))
+    return fail(MUMODE_ERR_ARGUMENT, "dist plan: tables too small (size returned in n_ops)");
+  for (size_t k = 0; k < ops.size(); ++k) {
+    const int64_t row[6] = {ops[k].chunk, ops[k].kind, ops[k].peer, ops[k].buf_off, ops[k].z_off, ops[k].count};
+    std::memcpy(op_tab + 6 * k, row, sizeof(row));
+  }
+  return MUMODE_OK;
+}
+
+int mumode_dist_expint_f64(mumode_handle_t h, mumode_comm_t c, int d, const int64_t* m, const double* const* E,
+                           const double* u0, double* u, int steps) {
+  using namespace mumode_gpu;
+  if (!h || !c) return fail(MUMODE_ERR_ARGUMENT, "dist_expint: null handle / comm");
+  if (!m) return fail(MUMODE_ERR_ARGUMENT, "dist_expint: null extents");
+  MM_CUDA(cudaSetDevice(h->device));
+  return dist_expint(h, c, d, m, E, u0, u, steps);
 }
 
 int mumode_dist_tucker_f64(mumode_handle_t h, mumode_comm_t c, int d, const int64_t* m, const int64_t* n,

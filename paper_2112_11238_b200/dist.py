@@ -356,6 +356,45 @@ def dist_tucker(comm: Comm, T_local, Ls, m: Sequence[int], n: Sequence[int] | No
     return S
 
 
+def dist_return_plan(P: int, rank: int, n: Sequence[int]):
+    """Schedule of the return exchange (host-only C-ABI mumode_dist_return_plan):
+    [(0, kind, peer, rows_off, stage_off, count)]."""
+    import ctypes
+
+    from . import _lib
+    from .api import _check
+    lib = _lib.lib()
+    no = ctypes.c_int()
+    args = (int(P), int(rank), len(n), _lib.i64_array(n))
+    rc = lib.mumode_dist_return_plan(*args, None, 0, ctypes.byref(no))
+    if rc != 0 and no.value == 0:
+        _check(rc)
+    ot = (ctypes.c_int64 * max(1, 6 * no.value))()
+    _check(lib.mumode_dist_return_plan(*args, ot, no.value, ctypes.byref(no)))
+    return [tuple(ot[6 * k:6 * k + 6]) for k in range(no.value)]
+
+
+def dist_expint(comm: Comm, u0_local, Es, m: Sequence[int], steps: int, out=None):
+    """``steps`` exponential-integrator steps across ranks through the C-ABI
+    (``mumode_dist_expint_f64``); ``u0_local`` / result: this rank's
+    column-major last-mode slab."""
+    import torch
+
+    from . import _lib
+    from .api import _check, get_handle, is_colmajor
+    if u0_local.dtype != torch.float64 or not is_colmajor(u0_local):
+        raise ValueError("dist_expint: u0_local must be a column-major float64 slab")
+    Es = [E.to(torch.float64) for E in Es]
+    Es = [E if is_colmajor(E) else E.t().contiguous().t() for E in Es]
+    u = out if out is not None else torch.empty_like(u0_local)
+    h = get_handle(u0_local.device.index)
+    h.bind_torch_stream()
+    _check(_lib.lib().mumode_dist_expint_f64(h.h, comm.c, len(m), _lib.i64_array(m),
+                                            _lib.ptr_array([E.data_ptr() for E in Es]), u0_local.data_ptr(),
+                                            u.data_ptr(), int(steps)))
+    return u
+
+
 def gather_rows(plan: SlabPlan, blocks: Sequence[np.ndarray]) -> np.ndarray:
     """Reassemble the full column-major result from the per-rank (A_r x n_d)
     row blocks (flat column-major arrays)."""

@@ -146,6 +146,100 @@ def test_c_abi_slab_plan_matches_python_plan():
         slab_plan_offsets(3, (4, 2), (4, 2))
 
 
+def _simulate_return(n, P, blocks):
+    """Every rank executes its mumode_dist_return_plan schedule: output rows ->
+    staging ([s][A_s x c_r]) -> slab (the slab_unpack_kernel mapping)."""
+    from paper_2112_11238_b200.dist import dist_return_plan
+    plan = SlabPlan(n, n, P)  # the output's own partition
+    stages = [np.full(plan.A * plan.c_sizes[r], np.nan) for r in range(P)]
+    from collections import defaultdict
+    sq, rq = defaultdict(list), defaultdict(list)
+    for r in range(P):
+        for (_, kind, peer, boff, zoff, cnt) in dist_return_plan(P, r, n):
+            if kind == 0:
+                sq[(r, peer)].append((boff, cnt))
+            elif kind == 1:
+                rq[(peer, r)].append((zoff, cnt))
+            else:
+                stages[r][zoff:zoff + cnt] = blocks[r][boff:boff + cnt]
+    assert set(sq) == set(rq)
+    for (src, dst), lst in sq.items():
+        assert len(lst) == len(rq[(src, dst)]) == 1
+        (boff, cnt), (zoff, cnt2) = lst[0], rq[(src, dst)][0]
+        assert cnt == cnt2
+        assert np.isnan(stages[dst][zoff:zoff + cnt]).all()
+        stages[dst][zoff:zoff + cnt] = blocks[src][boff:boff + cnt]
+    slabs = []
+    for r in range(P):
+        assert not np.isnan(stages[r]).any()
+        c_r = plan.c_sizes[r]
+        Y = np.empty((plan.A, c_r))
+        for q in range(P):
+            lo, hi = plan.a_off[q], plan.a_off[q + 1]
+            Y[lo:hi, :] = stages[r][lo * c_r: hi * c_r].reshape((hi - lo, c_r), order="F")
+        slabs.append(Y.reshape(n[:-1] + (c_r,), order="F"))
+    return slabs
+
+
+def _simulate_tucker_blocks(T_slabs, Ls, m, n, P, chunks):
+    """Row blocks of one slab-partitioned application (real) executed from the
+    mumode_dist_plan schedules."""
+    from paper_2112_11238_b200.dist import dist_plan
+    d = len(m)
+    plan = SlabPlan(m, n, P)
+    A = plan.A
+    sends, zs, sched = [], [], []
+    for r in range(P):
+        ch, ops = dist_plan(P, r, m, n, chunks, False)
+        sched.append(ops)
+        send = np.full(A * plan.c_sizes[r], np.nan)
+        for col0, w, soff in ch:
+            if w == 0:
+                continue
+            Y = np.asfortranarray(T_slabs[r][..., col0:col0 + w])
+            for mu in range(1, d):
+                Y = O.port_mode_product(Y, Ls[mu - 1], mu)
+            Yd = Y.reshape((A, w), order="F")
+            for q in range(P):
+                lo, hi = plan.a_off[q], plan.a_off[q + 1]
+                send[soff + lo * w: soff + hi * w] = Yd[lo:hi, :].reshape(-1, order="F")
+        sends.append(send)
+        zs.append(np.full(plan.a_sizes[r] * m[-1], np.nan))
+    from collections import defaultdict
+    sq, rq = defaultdict(list), defaultdict(list)
+    for r, ops in enumerate(sched):
+        for (j, kind, peer, boff, zoff, cnt) in ops:
+            if kind == 0:
+                sq[(r, peer)].append((j, boff, cnt))
+            elif kind == 1:
+                rq[(peer, r)].append((j, zoff, cnt))
+            else:
+                zs[r][zoff:zoff + cnt] = sends[r][boff:boff + cnt]
+    for key in sq:
+        for (j, boff, cnt), (j2, zoff, cnt2) in zip(sq[key], rq[key]):
+            zs[key[1]][zoff:zoff + cnt] = sends[key[0]][boff:boff + cnt]
+    return [O.port_mode_product(np.asfortranarray(zs[r].reshape((plan.a_sizes[r], m[-1]), order="F")), Ls[-1],
+                                2).reshape(-1, order="F") for r in range(P)]
+
+
+@pytest.mark.parametrize("P", [2, 3, 5])
+def test_c_abi_return_exchange_and_two_integrator_steps_simulated(P):
+    # mumode_dist_expint's step = dist_tucker schedule + return schedule +
+    # unpack; two steps over P simulated ranks equal two oracle Tuckers
+    for i, m in enumerate([(6, 5, 10), (4, 3, 4, 7), (9, 11)]):
+        rng = np.random.default_rng(10 * P + i)
+        u0 = np.asfortranarray(rng.standard_normal(m))
+        Es = [np.asfortranarray(rng.standard_normal((e, e)) / e) for e in m]
+        plan = SlabPlan(m, m, P)
+        slabs = scatter_slabs(plan, u0)
+        ref = u0
+        for step in range(2):
+            blocks = _simulate_tucker_blocks(slabs, Es, m, m, P, 2)
+            slabs = _simulate_return(m, P, blocks)
+            ref = O.port_tucker(ref, Es)
+            assert O.rel_fro(np.concatenate(slabs, axis=-1), ref) < 1e-13, (m, P, step)
+
+
 def _simulate_c_schedule(m, n, P, chunks, cplx, seed):
     """Every rank executes its mumode_dist_plan schedule on numpy buffers:
     local modes per sub-slab (oracle), the slab_pack layout, sends matched to
@@ -389,3 +483,21 @@ def test_multi_rank_comm_requires_nccl_id():
     from paper_2112_11238_b200.dist import Comm
     with pytest.raises(ValueError):
         Comm(2, 0, None, 0)
+
+
+@pytest.mark.gpu
+def test_dist_expint_c_abi_single_rank_matches_expint_bitwise():
+    from paper_2112_11238_b200.dist import Comm, dist_expint
+    comm = Comm(1, 0, Comm.unique_id(), 0)
+    try:
+        g = mm.Rng(77)
+        for m in [(40, 32, 24), (24, 24, 24, 24)]:
+            u0 = torch.from_numpy(g.normal(m)).cuda()
+            Es = [torch.from_numpy(mm.expm(-1e-3 * np.diag(np.arange(1.0, e + 1)) + 1e-4 * g.normal((e, e)))).cuda()
+                  for e in m]
+            for steps in (0, 1, 4):
+                u = dist_expint(comm, u0, Es, m, steps)
+                ref = mm.expint(u0, Es, steps)
+                assert torch.equal(u, ref), (m, steps)
+    finally:
+        comm.close()
