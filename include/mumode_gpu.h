@@ -109,6 +109,10 @@ int mumode_tucker_range_f64(mumode_handle_t h, int d, const int64_t* m, const in
  * entries, a_off[0] = 0, a_off[P] = A, P <= 64). */
 int mumode_slab_pack_f64(mumode_handle_t h, int64_t A, int64_t C, int P, const int64_t* a_off,
                          const double* Y, double* send);
+/* Inverse of mumode_slab_pack_f64 (send layout -> Y); the receive side of the
+ * integrator's return exchange. */
+int mumode_slab_unpack_f64(mumode_handle_t h, int64_t A, int64_t C, int P, const int64_t* a_off,
+                           const double* send, double* Y);
 
 /* ---- multi-GPU: slab-partitioned Tucker (SURVEY 8b "mumode_dist_tucker_f64(h,
  * comm, ...)", 8e) ---------------------------------------------------------

@@ -36,6 +36,7 @@ SIGNATURES = {
     "mumode_tucker_promote": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
     "mumode_tucker_range_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int, ctypes.c_int]),
     "mumode_slab_pack_f64": (ctypes.c_int, [H, I64, I64, ctypes.c_int, I64P, VP, VP]),
+    "mumode_slab_unpack_f64": (ctypes.c_int, [H, I64, I64, ctypes.c_int, I64P, VP, VP]),
     "mumode_comm_unique_id": (ctypes.c_int, [VP]),
     "mumode_comm_create": (ctypes.c_int, [ctypes.POINTER(VP), ctypes.c_int, VP, ctypes.c_int, ctypes.c_int]),
     "mumode_comm_wrap": (ctypes.c_int, [ctypes.POINTER(VP), ctypes.c_int, VP, ctypes.c_int, ctypes.c_int]),

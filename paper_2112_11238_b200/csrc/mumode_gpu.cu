@@ -207,34 +207,59 @@ __global__ void real_to_complex_kernel(const double* __restrict__ x, double* __r
 
 // Slab-transpose pack: Y (A x C, column-major) -> send buffer holding, for
 // each destination q, the row block Y[a_off[q] : a_off[q+1], 0:C] as a
-// contiguous column-major (|A_q| x C) matrix, blocks in q order.
+// contiguous column-major (|A_q| x C) matrix, blocks in q order. One CTA per
+// (column, destination) pair copies one contiguous run to one contiguous run
+// (no per-element index arithmetic: the kernel runs at copy bandwidth).
+// UNPACK = true is the inverse (send layout -> Y).
 constexpr int kMaxRanks = 64;
 struct PackOffsets {
   int64_t a[kMaxRanks + 1];
 };
-__global__ void slab_pack_kernel(const double* __restrict__ Y, double* __restrict__ send, int64_t A,
-                                 int64_t C, int P, PackOffsets off) {
-  const int64_t total = A * C;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t a = e % A, c = e / A;
-    int q = 0;
-    while (q + 1 < P && a >= off.a[q + 1]) ++q;
-    const int64_t rows = off.a[q + 1] - off.a[q];
-    send[off.a[q] * C + (a - off.a[q]) + c * rows] = Y[e];
+template <bool UNPACK>
+__global__ void __launch_bounds__(256) slab_pack_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                                        int64_t A, int64_t C, int P, PackOffsets off) {
+  constexpr int64_t SEG = 4096;  // doubles per CTA work item (long runs are split over CTAs)
+  const int64_t pairs = C * P;
+  for (int64_t pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
+    const int64_t c = pr / P;
+    const int q = static_cast<int>(pr - c * P);
+    const int64_t lo = off.a[q], rows = off.a[q + 1] - lo;
+    const int64_t y0 = lo + c * A, s0 = lo * C + c * rows;
+    for (int64_t seg = blockIdx.y * SEG; seg < rows; seg += int64_t(gridDim.y) * SEG) {
+      const int64_t len = rows - seg < SEG ? rows - seg : SEG;
+      const double* src = in + (UNPACK ? s0 : y0) + seg;
+      double* dst = out + (UNPACK ? y0 : s0) + seg;
+      if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15u) == 0) {
+        const int64_t n2 = len / 2;
+        for (int64_t i = threadIdx.x; i < n2; i += blockDim.x)
+          reinterpret_cast<double2*>(dst)[i] = reinterpret_cast<const double2*>(src)[i];
+        if ((len & 1) && threadIdx.x == 0) dst[len - 1] = src[len - 1];
+      } else {
+        for (int64_t i = threadIdx.x; i < len; i += blockDim.x) dst[i] = src[i];
+      }
+    }
   }
 }
 
 // w(a, n) /= (esum_front[a] + ev_last[n]) for the direct Kronecker-sum solve;
-// denominators summed in the reference's order (imex.cpp:70-77).
-__global__ void eigsum_divide_kernel(double* __restrict__ w, const double* __restrict__ esum_front,
-                                     const double* __restrict__ ev_last, int64_t A, int64_t N) {
-  const int64_t total = A * N;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t a = e % A, n = e / A;
-    w[e] /= (esum_front[a] + ev_last[n]);
+// denominators summed in the reference's order (imex.cpp:70-77). One CTA row
+// per column n (no per-element division).
+__global__ void __launch_bounds__(256) eigsum_divide_kernel(double* __restrict__ w, const double* __restrict__ esum_front,
+                                                            const double* __restrict__ ev_last, int64_t A, int64_t N) {
+  for (int64_t n = blockIdx.y; n < N; n += gridDim.y) {
+    const double en = ev_last[n];
+    double* col = w + n * A;
+    for (int64_t a = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; a < A; a += int64_t(gridDim.x) * blockDim.x)
+      col[a] /= (esum_front[a] + en);
   }
+}
+
+// (column, destination) pairs on x, 4096-double segments of long runs on y
+static dim3 pack_grid(int64_t A, int64_t C, int P, int sms) {
+  const int64_t pairs = C * P, cap = int64_t(sms) * 16;
+  const int64_t segs = std::min<int64_t>((A / P + 4095) / 4096 + 1, 64);
+  const int64_t gx = std::max<int64_t>(1, std::min(pairs, std::max<int64_t>(cap / segs, 1)));
+  return dim3(static_cast<unsigned>(gx), static_cast<unsigned>(segs));
 }
 
 static int grid_for(int64_t n, int sms) {
@@ -898,7 +923,21 @@ int mumode_slab_pack_f64(mumode_handle_t h, int64_t A, int64_t C, int P, const i
   PackOffsets off{};
   for (int q = 0; q <= P; ++q) off.a[q] = a_off[q];
   MM_CUDA(cudaSetDevice(h->device));
-  slab_pack_kernel<<<grid_for(A * C, h->num_sms), 256, 0, h->stream>>>(Y, send, A, C, P, off);
+  slab_pack_kernel<false><<<pack_grid(A, C, P, h->num_sms), 256, 0, h->stream>>>(Y, send, A, C, P, off);
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return MUMODE_OK;
+}
+
+int mumode_slab_unpack_f64(mumode_handle_t h, int64_t A, int64_t C, int P, const int64_t* a_off,
+                           const double* send, double* Y) {
+  if (!h || !a_off || !Y || !send) return fail(MUMODE_ERR_ARGUMENT, "slab_unpack: null pointer");
+  if (P < 1 || P > kMaxRanks) return fail(MUMODE_ERR_ARGUMENT, "slab_unpack: 1..64 ranks");
+  if (a_off[0] != 0 || a_off[P] != A) return fail(MUMODE_ERR_SIZE, "slab_unpack: row offsets must cover 0..A");
+  PackOffsets off{};
+  for (int q = 0; q <= P; ++q) off.a[q] = a_off[q];
+  MM_CUDA(cudaSetDevice(h->device));
+  slab_pack_kernel<true><<<pack_grid(A, C, P, h->num_sms), 256, 0, h->stream>>>(send, Y, A, C, P, off);
   MM_CUDA(cudaGetLastError());
   h->launches++;
   return MUMODE_OK;
@@ -940,7 +979,11 @@ int mumode_kronsum_solve_f64(mumode_handle_t h, int d, const int64_t* m, const d
   double* dsum = static_cast<double*>(h->lbuf.p);
   MM_CUDA(cudaMemcpyAsync(dsum, esum.data(), esum.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream));
   MM_TRY(tucker_dev(h, d, m, m, b, Qt, w, false, false));
-  eigsum_divide_kernel<<<grid_for(numel, h->num_sms), 256, 0, h->stream>>>(w, dsum, dsum + A, A, N);
+  {
+    const int gx = static_cast<int>(std::min<int64_t>((A + 255) / 256, 64));
+    const int gy = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(N, int64_t(h->num_sms) * 16 / gx)));
+    eigsum_divide_kernel<<<dim3(gx, gy), 256, 0, h->stream>>>(w, dsum, dsum + A, A, N);
+  }
   MM_CUDA(cudaGetLastError());
   h->launches++;
   MM_TRY(tucker_dev(h, d, m, m, w, Q, x, false, false));

@@ -184,7 +184,7 @@ static int dist_plan(int P, int r, int d, const int64_t* m, const int64_t* n, in
 // tensor for the next application (A x c'_r). Rank r sends R's columns of
 // slab q (contiguous: A_r x c'_q) to q and receives (A_s x c'_r) from every s
 // into a staging buffer laid out like the pack ([s][A_s x c'_r]), which
-// slab_unpack_kernel turns into the slab. ops: buf_off into R, z_off into the
+// slab_pack_kernel<true> (the unpack) turns into the slab. ops: buf_off into R, z_off into the
 // staging buffer.
 static int return_plan(int P, int r, int d, const int64_t* n, std::vector<DistOp>& ops, int64_t* c_off,
                        int64_t* a_off, int el) {
@@ -282,8 +282,8 @@ static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64
     if (c.w > 0) {
       ext[d - 1] = c.w;
       MM_TRY(tucker_dev(h, d, ext.data(), n, T + pl.rows_in * c.col0 * el, L, Y, false, cplx, 1, d - 1));
-      slab_pack_kernel<<<grid_for(A * el * c.w, h->num_sms), 256, 0, h->stream>>>(Y, send + c.send_off, A * el,
-                                                                                 c.w, P, off);
+      slab_pack_kernel<false><<<pack_grid(A * el, c.w, P, h->num_sms), 256, 0, h->stream>>>(Y, send + c.send_off, A * el,
+                                                                                      c.w, P, off);
       MM_CUDA(cudaGetLastError());
       h->launches++;
       MM_CUDA(cudaEventRecord(cm->events[j], h->stream));
@@ -315,20 +315,6 @@ static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64
   if (A_r == 0) return MUMODE_OK;
   const int64_t zext[2] = {A_r, m_d};
   return mode_product_dev(h, 2, zext, 2, n_d, Z, L[d - 1], 1, n_d, cplx, false, S);
-}
-
-// Inverse of slab_pack_kernel: staging ([q][|A_q| x C] blocks) -> Y (A x C).
-__global__ void slab_unpack_kernel(const double* __restrict__ stage, double* __restrict__ Y, int64_t A, int64_t C,
-                                   int P, PackOffsets off) {
-  const int64_t total = A * C;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t a = e % A, c = e / A;
-    int q = 0;
-    while (q + 1 < P && a >= off.a[q + 1]) ++q;
-    const int64_t rows = off.a[q + 1] - off.a[q];
-    Y[e] = stage[off.a[q] * C + (a - off.a[q]) + c * rows];
-  }
 }
 
 // Copies and one NCCL group of a schedule on the exchange stream.
@@ -395,7 +381,7 @@ static int dist_expint(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64
       MM_TRY(run_ops(cm, ops.data(), ops.size(), R, stage));
       MM_CUDA(cudaEventRecord(ev_out, cm->stream));
       MM_CUDA(cudaStreamWaitEvent(h->stream, ev_out, 0));
-      slab_unpack_kernel<<<grid_for(A * c_r, h->num_sms), 256, 0, h->stream>>>(stage, dst, A, c_r, P, off);
+      slab_pack_kernel<true><<<pack_grid(A, c_r, P, h->num_sms), 256, 0, h->stream>>>(stage, dst, A, c_r, P, off);
       MM_CUDA(cudaGetLastError());
       h->launches++;
     }

@@ -501,3 +501,22 @@ def test_dist_expint_c_abi_single_rank_matches_expint_bitwise():
                 assert torch.equal(u, ref), (m, steps)
     finally:
         comm.close()
+
+
+@pytest.mark.gpu
+def test_slab_pack_unpack_kernels_against_numpy():
+    from paper_2112_11238_b200 import _lib
+    from paper_2112_11238_b200.dist import even_splits, offsets
+    lib, h = _lib.lib(), mm.get_handle(0)
+    h.bind_torch_stream()
+    for A, C, P in [(65536, 32, 8), (1000, 7, 3), (5, 9, 5), (40000, 25, 8), (7, 1, 1), (130, 64, 64)]:
+        a_off = offsets(even_splits(A, P))
+        Y = torch.randn(A * C, dtype=torch.float64, device="cuda")
+        send = torch.full_like(Y, float("nan"))
+        assert lib.mumode_slab_pack_f64(h.h, A, C, P, _lib.i64_array(a_off), Y.data_ptr(), send.data_ptr()) == 0
+        Yn = Y.cpu().numpy().reshape((A, C), order="F")
+        ref = np.concatenate([Yn[a_off[q]:a_off[q + 1], :].reshape(-1, order="F") for q in range(P)])
+        np.testing.assert_array_equal(send.cpu().numpy(), ref)
+        back = torch.full_like(Y, float("nan"))
+        assert lib.mumode_slab_unpack_f64(h.h, A, C, P, _lib.i64_array(a_off), send.data_ptr(), back.data_ptr()) == 0
+        assert torch.equal(back, Y)
