@@ -143,45 +143,59 @@ __global__ void __launch_bounds__(FusedCfg<MU, FIRST, RA>::THREADS, 1)
     mbar_wait(&full_bar[buf], phase);
     const uint8_t* X = smem + buf * Cfg::X_BYTES;
 
-    // ---- mode mu: X -> Y
+    // ---- mode mu: X -> Y. For FIRST a warp's UPW (3) units advance together
+    // (9 independent accumulator chains hide the DMMA latency: pass 1 of C5
+    // 619 -> 602 us); with 16-wide a tiles (6 units) that costs more than it
+    // hides, so the others go one unit at a time.
+    constexpr int GROUP = FIRST ? Cfg::UNITS / 8 : 1;
 #pragma unroll
-    for (int uu = 0; uu < Cfg::UNITS / 8; ++uu) {
-      const int u = warp + 8 * uu;  // FIRST: fibre fragment; else (a-half, b2) = (u / MU, u % MU)
-      double acc[NF][2];
+    for (int grp = 0; grp < (Cfg::UNITS / 8) / GROUP; ++grp) {
+      constexpr int UPW = GROUP;
+      double acc[UPW][NF][2];
 #pragma unroll
-      for (int nf = 0; nf < NF; ++nf) acc[nf][0] = acc[nf][1] = 0.0;
+      for (int uu = 0; uu < UPW; ++uu)
+#pragma unroll
+        for (int nf = 0; nf < NF; ++nf) acc[uu][nf][0] = acc[uu][nf][1] = 0.0;
 #pragma unroll
       for (int s = 0; s < KS; ++s) {
         const uint32_t Js = J0 ^ (32u * static_cast<uint32_t>(s & 1));
-        if constexpr (FIRST) {
-          // A = X^T fragment (fibres 8u + xmap8(g), k = 4s + t), KX layout
-          const double xf = *reinterpret_cast<const double*>(X + (s >> 1) * (8 * MU * 64) + (8 * u) * 64 +
-                                                             kx_off + Js);
 #pragma unroll
-          for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[nf][0], acc[nf][1], xf, l1[nf][s]);
-        } else {
-          // B = X fragment (k = b1 = 4s + t, a = xmap8(g)) in slab (a-half, b2) = u, XK layout
-          const double xf = *reinterpret_cast<const double*>(X + u * (MU * 64) + (4 * s) * 64 + xk_off + Js);
+        for (int uu = 0; uu < UPW; ++uu) {
+          const int u = warp + 8 * (grp * GROUP + uu);  // FIRST: fibre fragment; else (a-half, b2)
+          if constexpr (FIRST) {
+            // A = X^T fragment (fibres 8u + xmap8(g), k = 4s + t), KX layout
+            const double xf = *reinterpret_cast<const double*>(X + (s >> 1) * (8 * MU * 64) + (8 * u) * 64 +
+                                                               kx_off + Js);
 #pragma unroll
-          for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[nf][0], acc[nf][1], l1[nf][s], xf);
+            for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[uu][nf][0], acc[uu][nf][1], xf, l1[nf][s]);
+          } else {
+            // B = X fragment (k = b1 = 4s + t, a = xmap8(g)) in slab (a-half, b2) = u, XK layout
+            const double xf = *reinterpret_cast<const double*>(X + u * (MU * 64) + (4 * s) * 64 + xk_off + Js);
+#pragma unroll
+            for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[uu][nf][0], acc[uu][nf][1], l1[nf][s], xf);
+          }
         }
       }
-      if constexpr (FIRST) {
-        // D[g <-> fibre f = 8u + xmap8(g)][i pair = 8nf + xmap8(2t)] -> Y row (cl, nf, j2)
-        const int f = 8 * u + xmap8(g);
-        const int j2 = f % MU, cl = f / MU;
 #pragma unroll
-        for (int nf = 0; nf < NF; ++nf) {
-          const int r = (cl * NF + nf) * (MU + 1) + j2;
-          *reinterpret_cast<double2*>(Y + y_off(r, xmap8(2 * t))) = make_double2(acc[nf][0], acc[nf][1]);
-        }
-      } else {
-        // D[g <-> i = 8nf + g][a pair = xmap8(2t)] -> Y row (a-half, i, b2)
-        const int ah = u / MU, b2 = u % MU;
+      for (int uu = 0; uu < UPW; ++uu) {
+        const int u = warp + 8 * (grp * GROUP + uu);
+        if constexpr (FIRST) {
+          // D[g <-> fibre f = 8u + xmap8(g)][i pair = 8nf + xmap8(2t)] -> Y row (cl, nf, j2)
+          const int f = 8 * u + xmap8(g);
+          const int j2 = f % MU, cl = f / MU;
 #pragma unroll
-        for (int nf = 0; nf < NF; ++nf) {
-          const int r = (ah * MU + 8 * nf + g) * (MU + 1) + b2;
-          *reinterpret_cast<double2*>(Y + y_off(r, xmap8(2 * t))) = make_double2(acc[nf][0], acc[nf][1]);
+          for (int nf = 0; nf < NF; ++nf) {
+            const int r = (cl * NF + nf) * (MU + 1) + j2;
+            *reinterpret_cast<double2*>(Y + y_off(r, xmap8(2 * t))) = make_double2(acc[uu][nf][0], acc[uu][nf][1]);
+          }
+        } else {
+          // D[g <-> i = 8nf + g][a pair = xmap8(2t)] -> Y row (a-half, i, b2)
+          const int ah = u / MU, b2 = u % MU;
+#pragma unroll
+          for (int nf = 0; nf < NF; ++nf) {
+            const int r = (ah * MU + 8 * nf + g) * (MU + 1) + b2;
+            *reinterpret_cast<double2*>(Y + y_off(r, xmap8(2 * t))) = make_double2(acc[uu][nf][0], acc[uu][nf][1]);
+          }
         }
       }
     }
@@ -197,39 +211,50 @@ __global__ void __launch_bounds__(FusedCfg<MU, FIRST, RA>::THREADS, 1)
       c_base = tile / ablks;
       a_base = RA * (tile - c_base * ablks);
     }
+    // one unit at a time here: advancing FIRST's three units together
+    // bunches their 16-B store bursts (pass 1 of C5 602 -> 688 us)
+    constexpr int GROUP2 = 1;
 #pragma unroll
-    for (int uu = 0; uu < Cfg::UNITS / 8; ++uu) {
-      const int u = warp + 8 * uu;  // FIRST: (cl, ib) = (u / NF, u % NF); else (a-half, i)
-      double acc[NF][2];
+    for (int grp = 0; grp < (Cfg::UNITS / 8) / GROUP2; ++grp) {
+      constexpr int UPW = GROUP2;
+      double acc[UPW][NF][2];
 #pragma unroll
-      for (int nf = 0; nf < NF; ++nf) acc[nf][0] = acc[nf][1] = 0.0;
-      const int rbase = u * (MU + 1);
+      for (int uu = 0; uu < UPW; ++uu)
 #pragma unroll
-      for (int s = 0; s < KS; ++s) {
-        const double yf = *reinterpret_cast<const double*>(Y + y_off(rbase + 4 * s + t, xmap8(g)));
+        for (int nf = 0; nf < NF; ++nf) acc[uu][nf][0] = acc[uu][nf][1] = 0.0;
 #pragma unroll
-        for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[nf][0], acc[nf][1], l2[nf][s], yf);
-      }
+      for (int s = 0; s < KS; ++s)
+#pragma unroll
+        for (int uu = 0; uu < UPW; ++uu) {
+          const int u = warp + 8 * (grp * GROUP2 + uu);  // FIRST: (cl, ib) = (u / NF, u % NF); else (a-half, i)
+          const double yf = *reinterpret_cast<const double*>(Y + y_off(u * (MU + 1) + 4 * s + t, xmap8(g)));
+#pragma unroll
+          for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[uu][nf][0], acc[uu][nf][1], l2[nf][s], yf);
+        }
       const int x = xmap8(2 * t);  // output pair along the contiguous index
-      if constexpr (FIRST) {
-        const int cl = u / NF, ib = u % NF;
-        const int64_t c = c_base + cl;
-        if (c < p.C) {
+#pragma unroll
+      for (int uu = 0; uu < UPW; ++uu) {
+        const int u = warp + 8 * (grp * GROUP2 + uu);
+        if constexpr (FIRST) {
+          const int cl = u / NF, ib = u % NF;
+          const int64_t c = c_base + cl;
+          if (c < p.C) {
+#pragma unroll
+            for (int nf = 0; nf < NF; ++nf) {
+              const int j = 8 * nf + g;
+              stg_f64x2(p.S + (8 * ib + x) + static_cast<int64_t>(MU) * (j + static_cast<int64_t>(MU) * c),
+                        acc[uu][nf][0], acc[uu][nf][1]);
+            }
+          }
+        } else {
+          const int ah = u / MU, i = u % MU;
 #pragma unroll
           for (int nf = 0; nf < NF; ++nf) {
             const int j = 8 * nf + g;
-            stg_f64x2(p.S + (8 * ib + x) + static_cast<int64_t>(MU) * (j + static_cast<int64_t>(MU) * c),
-                      acc[nf][0], acc[nf][1]);
+            stg_f64x2(p.S + a_base + 8 * ah + x +
+                          p.A * (i + static_cast<int64_t>(MU) * (j + static_cast<int64_t>(MU) * c_base)),
+                      acc[uu][nf][0], acc[uu][nf][1]);
           }
-        }
-      } else {
-        const int ah = u / MU, i = u % MU;
-#pragma unroll
-        for (int nf = 0; nf < NF; ++nf) {
-          const int j = 8 * nf + g;
-          stg_f64x2(p.S + a_base + 8 * ah + x +
-                        p.A * (i + static_cast<int64_t>(MU) * (j + static_cast<int64_t>(MU) * c_base)),
-                    acc[nf][0], acc[nf][1]);
         }
       }
     }

@@ -624,7 +624,7 @@ static int launch_tail(mumode_handle_s* h, const double* T, double* S, const dou
 
 // The tail kernel pays off once the a-stride makes every tile row a new page
 // (policy 9 forces it wherever the shape allows, 10 disables it).
-static constexpr int64_t kTailMinA = 512;
+static constexpr int64_t kTailMinA = 16384;
 
 template <int MU>
 static int launch_fused_mu(mumode_handle_s* h, bool first, const double* T, double* S,
