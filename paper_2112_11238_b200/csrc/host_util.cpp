@@ -62,15 +62,17 @@ namespace {
 
 using Mat = std::vector<double>;  // column-major n x n
 
-void matmul(const Mat& A, const Mat& B, Mat& C, int64_t n) {
+// C = A B with every element one k-ordered fused-multiply-add chain from 0:
+// the arithmetic of the reference's la::gemm (cblas_dgemm, src/gemm.cpp:53-66)
+// on OpenBLAS's x86 kernels, so products round like the reference's.
+__attribute__((target("avx2,fma"))) void matmul(const Mat& A, const Mat& B, Mat& C, int64_t n) {
   std::fill(C.begin(), C.end(), 0.0);
   for (int64_t j = 0; j < n; ++j)
     for (int64_t k = 0; k < n; ++k) {
       const double b = B[k + j * n];
-      if (b == 0.0) continue;
       const double* a = &A[k * n];
       double* c = &C[j * n];
-      for (int64_t i = 0; i < n; ++i) c[i] += a[i] * b;
+      for (int64_t i = 0; i < n; ++i) c[i] = std::fma(a[i], b, c[i]);
     }
 }
 
@@ -97,10 +99,11 @@ bool solve(Mat Q, Mat& P, int64_t n) {
     piv[static_cast<size_t>(k)] = p;
     if (p != k)
       for (int64_t j = 0; j < n; ++j) std::swap(Q[k + j * n], Q[p + j * n]);
+    // multiplier by the reciprocal pivot, as lu.hpp:41-46 does
+    const double inv_pivot = 1.0 / Q[k + k * n];
     for (int64_t i = k + 1; i < n; ++i) {
-      const double f = Q[i + k * n] / Q[k + k * n];
+      const double f = Q[i + k * n] * inv_pivot;
       Q[i + k * n] = f;
-      if (f == 0.0) continue;
       for (int64_t j = k + 1; j < n; ++j) Q[i + j * n] -= f * Q[k + j * n];
     }
   }
