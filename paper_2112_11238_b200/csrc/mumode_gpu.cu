@@ -98,6 +98,8 @@ struct mumode_handle_s {
   int policy = 0;
   int64_t launches = 0;
   mumode_gpu::DevBuf ws[3];     // Tucker ping-pong intermediates + expint buffer
+  mumode_gpu::DevBuf pad_in, pad_out, lpad;  // odd-leading-extent chains run on an even-padded copy
+  mumode_gpu::DevBuf lstage;    // a factor with an odd leading dimension, re-laid with an even one
   mumode_gpu::DevBuf lbuf;      // materialised op(L) for adjoint / promotion
   mumode_gpu::DevBuf host_in, host_out, host_mats, host_mid;  // host drop-in staging
   cudaStream_t copy_in = nullptr, copy_out = nullptr;         // host drop-in copy engines
@@ -255,6 +257,20 @@ __global__ void __launch_bounds__(256) eigsum_divide_kernel(double* __restrict__
 }
 
 // (column, destination) pairs on x, 4096-double segments of long runs on y
+// dst (rd x cd) = src (rs x cs) zero-extended / cropped, column-major.
+__global__ void __launch_bounds__(256) pad2d_kernel(const double* __restrict__ src, int64_t rs, int64_t cs,
+                                                    double* __restrict__ dst, int64_t rd, int64_t cd) {
+  for (int64_t c = blockIdx.y; c < cd; c += gridDim.y)
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < rd; r += int64_t(gridDim.x) * blockDim.x)
+      dst[r + c * rd] = (r < rs && c < cs) ? src[r + c * rs] : 0.0;
+}
+
+static dim3 pad_grid(int64_t rows, int64_t cols, int sms) {
+  const int64_t gx = std::min<int64_t>((rows + 255) / 256, 8);
+  const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(cols, int64_t(sms) * 16 / gx));
+  return dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
+}
+
 static dim3 pack_grid(int64_t A, int64_t C, int P, int sms) {
   const int64_t pairs = C * P, cap = int64_t(sms) * 16;
   const int64_t segs = std::min<int64_t>((A / P + 4095) / 4096 + 1, 64);
@@ -562,7 +578,25 @@ static bool ldg_worthwhile(const ModeJob& j) {
   return M >= 16 && j.K >= 8 && ((j.A == 1) ? j.C : j.N) >= 16;
 }
 
-static int run_job(mumode_handle_s* h, const ModeJob& j) {
+static int run_job(mumode_handle_s* h, const ModeJob& j0) {
+  ModeJob j = j0;
+  // A real mu > 1 product whose factor has an odd leading dimension (odd n_mu)
+  // is TMA-describable once the factor is re-laid with ld = n_mu + 1 (a tiny
+  // copy; the tensor strides are what they are).
+  if (!j.cplx && !j.conj && j.A != 1 && j.sLi == 1 && (j.sLk & 1) && h->policy != 1 && h->policy != 8) {
+    ModeJob jp = j;
+    jp.sLk = j.sLk + 1;
+    jp.L = reinterpret_cast<const double*>(uintptr_t(256));  // the staged copy is 256-B aligned
+    if (tma_ok(jp) && tma_worthwhile(jp)) {
+      MM_TRY(h->lstage.ensure(size_t(jp.sLk * j.K) * sizeof(double)));
+      auto* Lp = static_cast<double*>(h->lstage.p);
+      pad2d_kernel<<<pad_grid(jp.sLk, j.K, h->num_sms), 256, 0, h->stream>>>(j.L, j.sLk, j.K, Lp, jp.sLk, j.K);
+      MM_CUDA(cudaGetLastError());
+      h->launches++;
+      jp.L = Lp;
+      j = jp;
+    }
+  }
   // accumulating products: real mu > 1 have a TMA instantiation; others generic
   const bool can_tma = tma_ok(j) && !(j.accumulate && (j.A == 1 || j.cplx));
   if (h->policy == 8 && !j.cplx) return launch_ldg(h, j);
@@ -694,6 +728,56 @@ static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t
   if (mu_hi == 0) mu_hi = d;
   const int el = cplx ? 2 : 1;
   const int nmodes = mu_hi - mu_lo + 1;
+  // An odd real leading extent gives 8-byte strides, which TMA cannot
+  // describe (every stride is a multiple of the mode-1 extent). A whole
+  // chain then runs on a copy whose mode 1 is padded by one zero row (and
+  // mode-1 factor by a zero column / row): zero k-terms leave the FMA chains
+  // unchanged, the pad row of the output is dropped. Two copy passes buy the
+  // TMA/DMMA kernels for every mode.
+  if (!cplx && !adjoint && mu_lo == 1 && mu_hi == d && d >= 2 && h->policy == 0 && ((m[0] | n[0]) & 1) &&
+      aligned16_ptr(T) && aligned16_ptr(S)) {
+    // measured (tools/odd_sweep.py): the padded chain wins from ~223^3 up
+    // (255^3: 26.5 -> 28.7 TF/s); below ~208 the LDG-staged kernel's smaller
+    // tiles quantise better
+    bool big = true;
+    for (int k = 0; k < d; ++k) big = big && m[k] >= 208 && n[k] >= 208;
+    const int64_t numel_in = prod(m, 0, d), numel_out = prod(n, 0, d);
+    if (big && std::max(numel_in, numel_out) >= (int64_t(1) << 20)) {
+      std::vector<int64_t> mp(m, m + d), np(n, n + d);
+      mp[0] += m[0] & 1;
+      np[0] += n[0] & 1;
+      const int64_t rest_in = numel_in / m[0], rest_out = numel_out / n[0];
+      const bool ok = (mp[0] == m[0] || h->pad_in.ensure(size_t(mp[0] * rest_in) * sizeof(double)) == MUMODE_OK) &&
+                      h->lpad.ensure(size_t(np[0] * mp[0]) * sizeof(double)) == MUMODE_OK &&
+                      (np[0] == n[0] || h->pad_out.ensure(size_t(np[0] * rest_out) * sizeof(double)) == MUMODE_OK);
+      if (ok) {
+        const double* Tp = T;
+        auto* Lp = static_cast<double*>(h->lpad.p);
+        double* Sp = np[0] == n[0] ? S : static_cast<double*>(h->pad_out.p);
+        if (mp[0] != m[0]) {
+          auto* Tpad = static_cast<double*>(h->pad_in.p);
+          pad2d_kernel<<<pad_grid(mp[0], rest_in, h->num_sms), 256, 0, h->stream>>>(T, m[0], rest_in, Tpad, mp[0],
+                                                                                    rest_in);
+          h->launches++;
+          Tp = Tpad;
+        }
+        pad2d_kernel<<<pad_grid(np[0], mp[0], h->num_sms), 256, 0, h->stream>>>(L[0], n[0], m[0], Lp, np[0], mp[0]);
+        MM_CUDA(cudaGetLastError());
+        h->launches++;
+        std::vector<const double*> Lpad(L, L + d);
+        Lpad[0] = Lp;
+        MM_TRY(tucker_dev(h, d, mp.data(), np.data(), Tp, Lpad.data(), Sp, false, false));
+        if (Sp != S) {
+          pad2d_kernel<<<pad_grid(n[0], rest_out, h->num_sms), 256, 0, h->stream>>>(Sp, np[0], rest_out, S, n[0],
+                                                                                 rest_out);
+          MM_CUDA(cudaGetLastError());
+          h->launches++;
+        }
+        return MUMODE_OK;
+      }
+      g_err.clear();  // not enough memory for the padded copies: run unpadded
+    }
+  }
   // workspace: largest intermediate
   std::vector<int64_t> ext(m, m + d);
   size_t maxel = 0;

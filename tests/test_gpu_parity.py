@@ -457,3 +457,25 @@ def test_aliasing_output_rejected_by_the_abi():
     rc = _lib.lib().mumode_mode_product_f64(h.h, 3, _lib.i64_array((32, 32, 32)), 2, 32,
                                             T.data_ptr(), L.data_ptr(), T.data_ptr())
     assert rc == 2 and b"overlaps" in _lib.lib().mumode_last_error()
+
+
+@pytest.mark.parametrize("m,n", [((209, 211, 213), (211, 215, 209)), ((209, 216, 210), (208, 216, 210)),
+                                 ((208, 216, 210), (209, 216, 210)), ((255, 255, 255), (255, 255, 255)),
+                                 ((101, 103, 105), (103, 99, 101))])
+def test_odd_leading_extent_padded_chain_bitwise(m, n):
+    # auto runs odd leading extents as an even-padded TMA/DMMA chain; it must
+    # equal the unpadded LDG-staged path bit for bit (zero k-terms leave the
+    # FMA chains unchanged) and the oracle
+    rng = np.random.default_rng(sum(m) + sum(n))
+    T = rnd(rng, m)
+    Ls = [rnd(rng, (n[k], m[k])) for k in range(3)]
+    h = mm.get_handle(0)
+    got = {}
+    for pol in (0, 8):
+        h.set_kernel_policy(pol)
+        try:
+            got[pol] = host(mm.tucker(dev(T), [dev(L) for L in Ls]))
+        finally:
+            h.set_kernel_policy(0)
+    np.testing.assert_array_equal(got[0], got[8])
+    assert O.rel_fro(got[0], O.port_tucker(T, Ls)) < 1e-14

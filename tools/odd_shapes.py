@@ -28,3 +28,13 @@ for n in (255, 256, 201, 200, 129):
     Ls = [mm.to_colmajor(torch.randn(n, n, dtype=torch.float64, device="cuda")) for _ in range(3)]
     ms = timeit(lambda: mm.tucker(T, Ls))
     print(json.dumps({"n": n, "tucker_ms": round(ms, 4), "tflops": round(3 * 2 * n ** 4 / ms / 1e9, 2)}))
+
+# complex: odd extents (SIMT generic kernel today) vs even (TMA/DMMA)
+for m, nn in ((127, 191), (128, 192), (99, 101)):
+    T = mm.colmajor_empty((m, m, m), torch.complex128, "cuda")
+    T.real.normal_()
+    T.imag.normal_()
+    Ls = [mm.to_colmajor(torch.randn(nn, m, dtype=torch.complex128, device="cuda")) for _ in range(3)]
+    ms = timeit(lambda: mm.tucker(T, Ls))
+    fl = 8 * (nn * m ** 3 + nn * nn * m ** 2 + nn ** 3 * m)
+    print(json.dumps({"complex": [m, nn], "tucker_ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 2)}))
