@@ -103,6 +103,16 @@ int mumode_tucker_range_f64(mumode_handle_t h, int d, const int64_t* m, const in
                             const double* T, const double* const* L, double* S, int mu_lo,
                             int mu_hi);
 
+/* Modes mu_lo..mu_hi of the Tucker chain with the LAST one's result (viewed
+ * as rows x cols: rows = every extent up to mode mu_hi, cols = the extents
+ * after it) scattered by row blocks: rows a_off[q]..a_off[q+1] go to
+ * dst[q], a column-major (a_off[q+1]-a_off[q]) x (col0 + cols ...) matrix,
+ * at column col0 + c. The TMA kernel's epilogue stores straight to dst[q]
+ * (the fused exchange of mumode_dist_tucker_* with peer pointers); other
+ * paths compute then copy. Real, forward. */
+int mumode_tucker_range_scatter_f64(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                                    const double* T, const double* const* L, int mu_lo, int mu_hi,
+                                    int P, const int64_t* a_off, int64_t col0, double* const* dst);
 /* Slab-transpose pack for the all-to-all: Y is A x C column-major; for each
  * destination rank q the row block Y[a_off[q]:a_off[q+1], :] is written as a
  * contiguous column-major block, blocks in rank order (a_off has P+1

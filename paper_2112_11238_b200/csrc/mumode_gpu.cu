@@ -100,6 +100,7 @@ struct mumode_handle_s {
   mumode_gpu::DevBuf ws[3];     // Tucker ping-pong intermediates + expint buffer
   mumode_gpu::DevBuf pad_in, pad_out, lpad;  // odd-leading-extent chains run on an even-padded copy
   mumode_gpu::DevBuf lstage;    // a factor with an odd leading dimension, re-laid with an even one
+  mumode_gpu::DevBuf scat_params, scat_tmp, scat_mid;  // scatter table; fallback output; chain intermediate
   mumode_gpu::DevBuf lbuf;      // materialised op(L) for adjoint / promotion
   mumode_gpu::DevBuf host_in, host_out, host_mats, host_mid;  // host drop-in staging
   cudaStream_t copy_in = nullptr, copy_out = nullptr;         // host drop-in copy engines
@@ -243,6 +244,22 @@ __global__ void __launch_bounds__(256) slab_pack_kernel(const double* __restrict
   }
 }
 
+// Fallback of the scatter epilogue: Y (A x C) -> dst[q] rows (A_q x ...) at
+// column col0 + c, one contiguous run per (column, rank).
+__global__ void __launch_bounds__(256) scatter_copy_kernel(const double* __restrict__ Y, int64_t A, int64_t C,
+                                                           const ScatterParams* __restrict__ sp) {
+  const int P = sp->P;
+  for (int64_t pr = blockIdx.x; pr < C * P; pr += gridDim.x) {
+    const int64_t c = pr / P;
+    const int q = static_cast<int>(pr - c * P);
+    const int64_t lo = sp->a_off[q], rows = sp->a_off[q + 1] - lo;
+    const double* src = Y + c * A + lo;
+    double* dst = sp->dst[q] + rows * (sp->col0 + c);
+    for (int64_t i = blockIdx.y * int64_t(blockDim.x) + threadIdx.x; i < rows; i += int64_t(gridDim.y) * blockDim.x)
+      dst[i] = src[i];
+  }
+}
+
 // w(a, n) /= (esum_front[a] + ev_last[n]) for the direct Kronecker-sum solve;
 // denominators summed in the reference's order (imex.cpp:70-77). One CTA row
 // per column n (no per-element division).
@@ -312,6 +329,7 @@ struct ModeJob {
   bool cplx;
   bool conj;
   bool accumulate = false;  // S += T x_mu op(L)
+  const ScatterParams* scat = nullptr;  // device table: scatter the (rows x C) result to ranks (S unused)
 };
 
 // Compiled tile configurations (BM, BN, BK, stages, warps along M, along N).
@@ -474,13 +492,22 @@ static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
   p.nt = (p.N + Cfg::BN - 1) / Cfg::BN;
   p.tiles = int64_t(p.mt) * p.nt;
   const int grid = static_cast<int>(p.tiles < h->num_sms ? p.tiles : h->num_sms);
-  if (mode1) {
+  p.scat = j.scat;
+  if (j.scat) {
+    if constexpr (Cfg::E == 1) {
+      auto k = mode1 ? modeprod_tma_kernel<Cfg, true, 2> : modeprod_tma_kernel<Cfg, false, 2>;
+      MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
+      k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mp, *mq, p);
+    } else {
+      return fail(MUMODE_ERR_ARGUMENT, "scatter epilogue is real-only");
+    }
+  } else if (mode1) {
     auto k = modeprod_tma_kernel<Cfg, true>;
     MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
     k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mp, *mq, p);
   } else if (j.accumulate) {
     if constexpr (Cfg::E == 1) {
-      auto k = modeprod_tma_kernel<Cfg, false, true>;
+      auto k = modeprod_tma_kernel<Cfg, false, 1>;
       MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
       k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mp, *mq, p);
     } else {
@@ -597,6 +624,26 @@ static int run_job(mumode_handle_s* h, const ModeJob& j0) {
       j = jp;
     }
   }
+  if (j.scat) {
+    // fused exchange: the TMA kernel's epilogue scatters to the ranks; any
+    // other path computes the (rows x C) result and scatter-copies it
+    if (!j.cplx && !j.accumulate && tma_ok(j) && h->policy != 1 && h->policy != 8 &&
+        (h->policy >= 2 || tma_worthwhile(j)))
+      return launch_tma_auto(h, j);
+    ModeJob jt = j;
+    jt.scat = nullptr;
+    const int64_t rows = (j.A == 1) ? j.N : j.A * j.N, cols = (j.A == 1) ? j.C : j.C;
+    MM_TRY(h->scat_tmp.ensure(size_t(rows * cols * (j.cplx ? 2 : 1)) * sizeof(double)));
+    jt.S = static_cast<double*>(h->scat_tmp.p);
+    MM_TRY(run_job(h, jt));
+    if (j.cplx) return fail(MUMODE_ERR_ARGUMENT, "scatter of complex products is not supported");
+    const unsigned gy = static_cast<unsigned>(std::min<int64_t>(8, (rows + 255) / 256));
+    scatter_copy_kernel<<<dim3(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cols * 64, int64_t(h->num_sms) * 8))), gy),
+                          256, 0, h->stream>>>(static_cast<const double*>(h->scat_tmp.p), rows, cols, j.scat);
+    MM_CUDA(cudaGetLastError());
+    h->launches++;
+    return MUMODE_OK;
+  }
   // accumulating products: real mu > 1 have a TMA instantiation; others generic
   const bool can_tma = tma_ok(j) && !(j.accumulate && (j.A == 1 || j.cplx));
   if (h->policy == 8 && !j.cplx) return launch_ldg(h, j);
@@ -700,9 +747,11 @@ static int fused_extent(int d, const int64_t* m, const int64_t* n, bool cplx, bo
 // n_mu x m_mu given by (L, sLi, sLk, conj).
 static int mode_product_dev(mumode_handle_s* h, int d, const int64_t* m, int mu, int64_t n_mu,
                             const double* T, const double* L, int64_t sLi, int64_t sLk,
-                            bool cplx, bool conj, double* S, bool accumulate = false) {
+                            bool cplx, bool conj, double* S, bool accumulate = false,
+                            const ScatterParams* scat = nullptr) {
   ModeJob j;
   j.accumulate = accumulate;
+  j.scat = scat;
   j.T = T;
   j.L = L;
   j.S = S;
@@ -724,10 +773,26 @@ static int mode_product_dev(mumode_handle_s* h, int d, const int64_t* m, int mu,
 // access, or a materialised op(L) when the TMA path applies.
 static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t* n,
                       const double* T, const double* const* L, double* S, bool adjoint,
-                      bool cplx, int mu_lo = 1, int mu_hi = 0) {
+                      bool cplx, int mu_lo = 1, int mu_hi = 0, const ScatterParams* scat = nullptr) {
   if (mu_hi == 0) mu_hi = d;
   const int el = cplx ? 2 : 1;
   const int nmodes = mu_hi - mu_lo + 1;
+  if (scat) {
+    // the range's last mode scatters its (rows x cols) result to the ranks
+    // (fused exchange, csrc/slab_dist.cuh); the modes before it run as usual
+    if (adjoint) return fail(MUMODE_ERR_ARGUMENT, "scatter: forward chains only");
+    std::vector<int64_t> ext(m, m + d);
+    const double* src = T;
+    if (nmodes > 1) {
+      for (int k = mu_lo - 1; k < mu_hi - 1; ++k) ext[k] = n[k];
+      MM_TRY(h->scat_mid.ensure(size_t(prod(ext.data(), 0, d) * el) * sizeof(double)));
+      auto* mid = static_cast<double*>(h->scat_mid.p);
+      MM_TRY(tucker_dev(h, d, m, n, T, L, mid, false, cplx, mu_lo, mu_hi - 1));
+      src = mid;
+    }
+    return mode_product_dev(h, d, ext.data(), mu_hi, n[mu_hi - 1], src, L[mu_hi - 1], 1, n[mu_hi - 1], cplx,
+                            false, nullptr, false, scat);
+  }
   // An odd real leading extent gives 8-byte strides, which TMA cannot
   // describe (every stride is a multiple of the mode-1 extent). A whole
   // chain then runs on a copy whose mode 1 is padded by one zero row (and
@@ -997,6 +1062,40 @@ int mumode_tucker_range_f64(mumode_handle_t h, int d, const int64_t* m, const in
     if (!L[k] || n[k] < 1) return fail(MUMODE_ERR_ARGUMENT, "tucker_range: bad matrix for mode " + std::to_string(k + 1));
   MM_CUDA(cudaSetDevice(h->device));
   return tucker_dev(h, d, m, n, T, L, S, false, false, mu_lo, mu_hi);
+}
+
+int mumode_tucker_range_scatter_f64(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                                    const double* T, const double* const* L, int mu_lo, int mu_hi, int P,
+                                    const int64_t* a_off, int64_t col0, double* const* dst) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  MM_TRY(check_shape(d, m, "tucker_range_scatter"));
+  if (mu_lo < 1 || mu_hi > d || mu_lo > mu_hi)
+    return fail(MUMODE_ERR_ARGUMENT, "tucker_range_scatter: bad mode range");
+  if (!T || !L || !n || !a_off || !dst) return fail(MUMODE_ERR_ARGUMENT, "tucker_range_scatter: null pointer");
+  if (P < 1 || P > kScatterMaxRanks) return fail(MUMODE_ERR_ARGUMENT, "tucker_range_scatter: 1..64 ranks");
+  for (int k = mu_lo - 1; k < mu_hi; ++k)
+    if (!L[k] || n[k] < 1)
+      return fail(MUMODE_ERR_ARGUMENT, "tucker_range_scatter: bad matrix for mode " + std::to_string(k + 1));
+  // rows of the scattered matrix: every extent up to mode mu_hi (outputs
+  // for modes in the range), columns: the extents after it
+  int64_t rows = 1;
+  for (int k = 0; k < mu_hi; ++k) rows *= (k >= mu_lo - 1) ? n[k] : m[k];
+  if (a_off[0] != 0 || a_off[P] != rows)
+    return fail(MUMODE_ERR_SIZE, "tucker_range_scatter: row offsets must cover the result's rows");
+  for (int q = 0; q < P; ++q) {
+    if (a_off[q + 1] < a_off[q]) return fail(MUMODE_ERR_ARGUMENT, "tucker_range_scatter: offsets must ascend");
+    if (!dst[q] && a_off[q + 1] > a_off[q]) return fail(MUMODE_ERR_ARGUMENT, "tucker_range_scatter: null destination");
+  }
+  MM_CUDA(cudaSetDevice(h->device));
+  ScatterParams sp{};
+  sp.P = P;
+  sp.col0 = col0;
+  for (int q = 0; q <= P; ++q) sp.a_off[q] = a_off[q];
+  for (int q = 0; q < P; ++q) sp.dst[q] = dst[q];
+  MM_TRY(h->scat_params.ensure(sizeof(ScatterParams)));
+  auto* dsp = static_cast<ScatterParams*>(h->scat_params.p);
+  MM_CUDA(cudaMemcpyAsync(dsp, &sp, sizeof(sp), cudaMemcpyHostToDevice, h->stream));
+  return tucker_dev(h, d, m, n, T, L, nullptr, false, false, mu_lo, mu_hi, dsp);
 }
 
 int mumode_slab_pack_f64(mumode_handle_t h, int64_t A, int64_t C, int P, const int64_t* a_off,

@@ -23,7 +23,52 @@
 
 namespace mumode_gpu {
 
+// Scatter epilogue (EPI 2): the output is the (rows x w) matrix of a slab's
+// last local mode; row rho belongs to rank q with a_off[q] <= rho < a_off[q+1]
+// and lands at dst[q][(rho - a_off[q]) + (a_off[q+1] - a_off[q]) * (col0 + c)]
+// -- the rank's received (A_q x m_d) matrix, written in place over NVLink
+// peer pointers (csrc/slab_dist.cuh) instead of pack + exchange.
+constexpr int kScatterMaxRanks = 64;
+struct ScatterParams {
+  int P;
+  int64_t col0;
+  int64_t a_off[kScatterMaxRanks + 1];
+  double* dst[kScatterMaxRanks];
+};
+
+// owner rank of row rho (binary search over P + 1 offsets)
+__device__ __forceinline__ int scatter_owner(const ScatterParams* sp, int64_t rho) {
+  int lo = 0, hi = sp->P - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(&sp->a_off[mid]) <= rho) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void scatter_store(const ScatterParams* sp, int64_t rho, int64_t col, double v0,
+                                              double v1) {
+  const int64_t gcol = sp->col0 + col;
+  const int q = scatter_owner(sp, rho);
+  const int64_t lo = __ldg(&sp->a_off[q]), hi = __ldg(&sp->a_off[q + 1]);
+  double* d0 = sp->dst[q] + (rho - lo) + (hi - lo) * gcol;
+  if (rho + 1 < hi) {  // both rows on rank q
+    if ((reinterpret_cast<uintptr_t>(d0) & 15u) == 0) {
+      stg_f64x2(d0, v0, v1);
+    } else {
+      d0[0] = v0;
+      d0[1] = v1;
+    }
+  } else {  // the pair straddles two ranks
+    d0[0] = v0;
+    const int q1 = scatter_owner(sp, rho + 1);
+    const int64_t lo1 = __ldg(&sp->a_off[q1]), hi1 = __ldg(&sp->a_off[q1 + 1]);
+    sp->dst[q1][(rho + 1 - lo1) + (hi1 - lo1) * gcol] = v1;
+  }
+}
+
 struct TmaParams {
+  const ScatterParams* scat;  // EPI 2 only (device memory)
   double* D;
   int64_t ldD;      // stride of D between consecutive n (elements)
   int64_t bstride;  // stride of D between batches c (elements)
@@ -99,15 +144,18 @@ struct TmaCfg {
 
 // QK == true  (mu == 1): P = L (XK), Q = T (KX)
 // QK == false (mu  > 1): P = T (XK, fragment list over (a-block, c)), Q = L (XK)
-// ACC: D += result (kronsumv term accumulation, tucker.hpp:222-231); a
+// EPI: 0 = store; 1 = D += result (kronsumv term accumulation,
+// tucker.hpp:222-231); 2 = scatter to the owning ranks (real only). A
 // compile-time switch -- a runtime branch in the epilogue costs ~2 % on C2.
-template <class Cfg, bool QK, bool ACC = false>
+template <class Cfg, bool QK, int EPI = 0>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
     modeprod_tma_kernel(const __grid_constant__ CUtensorMap mapP,
                         const __grid_constant__ CUtensorMap mapQ, const TmaParams p) {
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
   constexpr int FM = Cfg::FM, FN = Cfg::FN, E = Cfg::E, ROW = Cfg::ROW;
   constexpr bool CPLX = (E == 2);
+  constexpr bool ACC = (EPI == 1);
+  static_assert(EPI != 2 || !CPLX, "scatter epilogue is real-only");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment by pointer arithmetic so the compiler keeps the shared
   // address space (LDS, not generic LD).
@@ -335,6 +383,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         for (int fn = 0; fn < FN; ++fn) {
           const int n = ntile * BN + nw + 8 * fn + xmap8(g);
           if (n >= p.N) continue;
+          if constexpr (EPI == 2) {
+            // row of the (rows x w) matrix and its column (m even, Mlim even)
+            if constexpr (QK)
+              scatter_store(p.scat, m, n, acc[fm][fn][0], acc[fm][fn][1]);
+            else
+              scatter_store(p.scat, m + static_cast<int64_t>(n) * p.ldD, c, acc[fm][fn][0], acc[fm][fn][1]);
+            continue;
+          }
           double* dst = base + static_cast<int64_t>(n) * p.ldD;
           if constexpr (ACC) {
             const double2 o = *reinterpret_cast<const double2*>(dst);

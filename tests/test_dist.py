@@ -520,3 +520,49 @@ def test_slab_pack_unpack_kernels_against_numpy():
         back = torch.full_like(Y, float("nan"))
         assert lib.mumode_slab_unpack_f64(h.h, A, C, P, _lib.i64_array(a_off), send.data_ptr(), back.data_ptr()) == 0
         assert torch.equal(back, Y)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("policy", [0, 8, 1])
+def test_scatter_epilogue_to_rank_buffers(policy):
+    # the fused exchange's epilogue (EPI 2), simulated with P destination
+    # buffers on one GPU: rows a_off[q]..a_off[q+1] of the range's result land
+    # in buffer q at column col0 + c; odd offsets split 16-B pairs and
+    # misalign rows, one rank is empty. policy 8 / 1: compute + scatter-copy.
+    from paper_2112_11238_b200 import _lib
+    lib, h = _lib.lib(), mm.get_handle(0)
+    h.bind_torch_stream()
+    h.set_kernel_policy(policy)
+    try:
+        for m, n, lo, hi in [((48, 40, 32), (40, 56, 24), 1, 2), ((64, 48, 20), (56, 48, 20), 1, 2),
+                             ((40, 30), (64, 30), 1, 1), ((16, 16, 16, 16), (16, 16, 16, 16), 1, 3)]:
+            rng = np.random.default_rng(sum(m))
+            T = np.asfortranarray(rng.standard_normal(m))
+            Ls = [np.asfortranarray(rng.standard_normal((n[k], m[k]))) for k in range(len(m))]
+            Y = T
+            for mu in range(lo, hi + 1):
+                Y = O.port_mode_product(Y, Ls[mu - 1], mu)
+            rows = int(np.prod(Y.shape[:hi]))
+            cols = Y.size // rows
+            Y2 = Y.reshape((rows, cols), order="F")
+            cuts = sorted({0, 37, 101 % rows, rows // 2 + 1, rows})
+            a_off = [0, 37, 37] + [c for c in cuts if c > 37]  # rank 1 empty
+            P = len(a_off) - 1
+            col0 = 3
+            bufs = [torch.full(((a_off[q + 1] - a_off[q]) * (col0 + cols + 2),), float("nan"), dtype=torch.float64,
+                               device="cuda") for q in range(P)]
+            Td = torch.from_numpy(T).cuda()
+            Lds = [torch.from_numpy(L).cuda() for L in Ls]
+            rc = lib.mumode_tucker_range_scatter_f64(
+                h.h, len(m), _lib.i64_array(m), _lib.i64_array(n), Td.data_ptr(), _lib.ptr_array([L.data_ptr() for L in Lds]),
+                lo, hi, P, _lib.i64_array(a_off), col0, _lib.ptr_array([b.data_ptr() if b.numel() else 0 for b in bufs]))
+            assert rc == 0, lib.mumode_last_error()
+            for q in range(P):
+                r = a_off[q + 1] - a_off[q]
+                got = bufs[q].cpu().numpy().reshape((r, col0 + cols + 2), order="F")
+                assert np.isnan(got[:, :col0]).all() and np.isnan(got[:, col0 + cols:]).all()
+                ref = Y2[a_off[q]:a_off[q + 1], :]
+                if r:
+                    assert O.rel_max(got[:, col0:col0 + cols], ref) < 1e-13, (m, q)
+    finally:
+        h.set_kernel_policy(0)
