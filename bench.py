@@ -167,6 +167,8 @@ def main():
     ap.add_argument("--chunks", type=int, default=0,
                     help="N>1: sub-slabs per rank in mumode_dist_tucker_f64 (exchange of one overlaps the "
                          "next; 0 = auto)")
+    ap.add_argument("--exchange", choices=["nccl", "p2p"], default="nccl",
+                    help="N>1: NCCL grouped send/recv, or peer stores from the last local mode's epilogue")
     ap.add_argument("--py-dist", action="store_true",
                     help="N>1: the Python slab algorithm with a torch all-to-all instead of the C-ABI")
     ap.add_argument("--overlap", action="store_true", help="with --py-dist: chunked grouped send/recv")
@@ -386,10 +388,13 @@ def run_distributed(args, world, rank, local):
         path = "python slab algorithm, torch " + ("grouped send/recv (4 chunks)" if args.overlap else "all-to-all")
     else:
         comm = Comm.from_torch(device=local)
+        comm.set_exchange(args.exchange)
 
         def run_slab(T_in):
             return dist_tucker(comm, T_in, Ls, C2, chunks=args.chunks, out=S_out)
-        path = ("C-ABI mumode_dist_tucker_f64, NCCL grouped send/recv, "
+        path = ("C-ABI mumode_dist_tucker_f64, peer stores from the mode-2 epilogue (NVLink, CUDA IPC)"
+                if args.exchange == "p2p" else
+                "C-ABI mumode_dist_tucker_f64, NCCL grouped send/recv, "
                 + (f"{args.chunks} overlapped sub-slabs" if args.chunks else "auto sub-slabs"))
     clocks = ClockSampler(local)
     clocks.start()

@@ -136,6 +136,12 @@ int mumode_comm_create(mumode_comm_t* c, int device, const void* id, int nranks,
  * nccl_comm may be NULL when nranks == 1. */
 int mumode_comm_wrap(mumode_comm_t* c, int device, void* nccl_comm, int nranks, int rank);
 int mumode_comm_destroy(mumode_comm_t c);
+/* Exchange used by mumode_dist_tucker_f64: 0 = NCCL grouped send/recv
+ * (default), 1 = peer stores: the last local mode's epilogue writes every row
+ * straight into the owning rank's matrix through CUDA-IPC peer pointers
+ * (NVLink), then a system-scope flag handshake (csrc/slab_dist.cuh). The
+ * first call per shape maps the peers (collective). Complex stays on NCCL. */
+int mumode_comm_set_exchange(mumode_comm_t c, int mode);
 /* The partition (host only): c_off[P+1] = last-mode slab offsets (rank r
  * holds T[..., c_off[r]:c_off[r+1]]), a_off[P+1] = output row blocks over
  * A = n_1...n_{d-1} (rank r returns rows a_off[r]:a_off[r+1] of the result

@@ -35,6 +35,7 @@ struct NcclApi {
   decltype(&ncclRecv) recv = nullptr;
   decltype(&ncclGetErrorString) error_string = nullptr;
   decltype(&ncclGetVersion) get_version = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
 };
 
 static NcclApi& nccl_api() {
@@ -61,6 +62,7 @@ static NcclApi& nccl_api() {
     sym(a.recv, "ncclRecv");
     sym(a.error_string, "ncclGetErrorString");
     sym(a.get_version, "ncclGetVersion");
+    sym(a.all_gather, "ncclAllGather");
     a.ok = all;
     if (!all) a.why = "NCCL library lacks the point-to-point API";
     return a;
@@ -217,6 +219,14 @@ struct mumode_comm_s {
   mumode_gpu::DevBuf y, send, z;          // chunk intermediate, packed slab, received (A_r x m_d)
   mumode_gpu::DevBuf rows, stage, spare;  // expint: output rows, return staging, slab ping-pong
   cudaEvent_t ret_in = nullptr, ret_out = nullptr;  // expint: return exchange
+  // exchange 1 (peer stores): double-buffered Z and epoch flags, mapped into
+  // every peer with CUDA IPC; the scatter table for the epilogue
+  int exchange = 0;
+  int64_t epoch = 0;
+  mumode_gpu::DevBuf pz[2], flags, handles, scat;
+  size_t mapped_bytes = 0;                 // Z size the peer mappings were made for
+  std::vector<double*> peer_z[2];          // [parity][rank] (own rank: local pointer)
+  std::vector<int64_t*> peer_flags;        // [rank] flag array of that rank
 };
 
 namespace mumode_gpu {
@@ -241,6 +251,121 @@ static int comm_events(mumode_comm_s* c, size_t want) {
   return MUMODE_OK;
 }
 
+// ---- exchange 1: peer stores over NVLink (CUDA IPC mappings)
+// Signal: every earlier write of this stream (the scatter kernel's peer
+// stores) is ordered before the flags by a system-scope fence, then each peer
+// q gets flags_q[r] = epoch (release, system scope).
+__global__ void p2p_signal_kernel(int64_t* const* __restrict__ peer_flags, int P, int r, int64_t epoch) {
+  asm volatile("fence.sc.sys;\n" ::: "memory");
+  for (int q = threadIdx.x; q < P; q += blockDim.x)
+    asm volatile("st.release.sys.global.b64 [%0], %1;\n" ::"l"(peer_flags[q] + r), "l"(epoch) : "memory");
+}
+// Wait until every rank's flag in the local array reached epoch (acquire,
+// system scope), with the watchdog of the mbarrier waits: a lost peer
+// surfaces as a launch failure, not a hung GPU.
+__global__ void p2p_wait_kernel(const int64_t* __restrict__ flags, int P, int64_t epoch) {
+  for (int s = threadIdx.x; s < P; s += blockDim.x) {
+    uint32_t polls = 0;
+    int64_t v;
+    do {
+      asm volatile("ld.acquire.sys.global.b64 %0, [%1];\n" : "=l"(v) : "l"(flags + s) : "memory");
+      if (++polls == (1u << 30)) __trap();
+    } while (v < epoch);
+  }
+  __syncthreads();
+  asm volatile("fence.sc.sys;\n" ::: "memory");
+}
+
+// (Re)map the peers' Z buffers and flag arrays: a collective -- every rank
+// calls it with the same byte size in the same dist_tucker call.
+static int p2p_map(mumode_comm_s* cm, size_t zbytes) {
+  const int P = cm->nranks, r = cm->rank;
+  for (int b = 0; b < 2; ++b)
+    for (int q = 0; q < static_cast<int>(cm->peer_z[b].size()); ++q)
+      if (q != r && cm->peer_z[b][q]) cudaIpcCloseMemHandle(cm->peer_z[b][q]);
+  for (int q = 0; q < static_cast<int>(cm->peer_flags.size()); ++q)
+    if (q != r && cm->peer_flags[q]) cudaIpcCloseMemHandle(cm->peer_flags[q]);
+  MM_TRY(cm->pz[0].ensure(zbytes));
+  MM_TRY(cm->pz[1].ensure(zbytes));
+  if (!cm->flags.p) {
+    MM_TRY(cm->flags.ensure(sizeof(int64_t) * kMaxRanks));
+    MM_CUDA(cudaMemset(cm->flags.p, 0, sizeof(int64_t) * kMaxRanks));
+  }
+  constexpr size_t HB = sizeof(cudaIpcMemHandle_t);
+  std::vector<cudaIpcMemHandle_t> mine(3);
+  MM_CUDA(cudaIpcGetMemHandle(&mine[0], cm->pz[0].p));
+  MM_CUDA(cudaIpcGetMemHandle(&mine[1], cm->pz[1].p));
+  MM_CUDA(cudaIpcGetMemHandle(&mine[2], cm->flags.p));
+  MM_TRY(cm->handles.ensure(3 * HB * (P + 1)));
+  auto* dh = static_cast<uint8_t*>(cm->handles.p);
+  MM_CUDA(cudaMemcpy(dh, mine.data(), 3 * HB, cudaMemcpyHostToDevice));
+  auto& api = nccl_api();
+  MM_NCCL(api.all_gather(dh, dh + 3 * HB, 3 * HB, ncclUint8, cm->comm, cm->stream));
+  MM_CUDA(cudaStreamSynchronize(cm->stream));
+  std::vector<cudaIpcMemHandle_t> all(3 * P);
+  MM_CUDA(cudaMemcpy(all.data(), dh + 3 * HB, 3 * HB * P, cudaMemcpyDeviceToHost));
+  for (int b = 0; b < 2; ++b) cm->peer_z[b].assign(P, nullptr);
+  cm->peer_flags.assign(P, nullptr);
+  for (int q = 0; q < P; ++q) {
+    if (q == r) {
+      cm->peer_z[0][q] = static_cast<double*>(cm->pz[0].p);
+      cm->peer_z[1][q] = static_cast<double*>(cm->pz[1].p);
+      cm->peer_flags[q] = static_cast<int64_t*>(cm->flags.p);
+      continue;
+    }
+    void* ptr = nullptr;
+    for (int b = 0; b < 2; ++b) {
+      MM_CUDA(cudaIpcOpenMemHandle(&ptr, all[3 * q + b], cudaIpcMemLazyEnablePeerAccess));
+      cm->peer_z[b][q] = static_cast<double*>(ptr);
+    }
+    MM_CUDA(cudaIpcOpenMemHandle(&ptr, all[3 * q + 2], cudaIpcMemLazyEnablePeerAccess));
+    cm->peer_flags[q] = static_cast<int64_t*>(ptr);
+  }
+  cm->mapped_bytes = zbytes;
+  return MUMODE_OK;
+}
+
+// One application with the exchange fused into the last local mode's
+// epilogue: the TMA kernel stores every row pair straight into the owning
+// rank's Z (peer pointers), then signal / wait, then mode d on the local Z.
+static int dist_tucker_p2p(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64_t* m, const int64_t* n,
+                           const double* T, const double* const* L, double* S, const DistPlan& pl) {
+  const int P = cm->nranks, r = cm->rank;
+  // all ranks see the same shapes, so they remap in the same call
+  size_t want = 0;
+  for (int q = 0; q < P; ++q)
+    want = std::max(want, size_t((pl.a_off[q + 1] - pl.a_off[q]) * pl.m_d) * sizeof(double));
+  want = std::max(want, size_t(8));
+  if (P > 1 && want > cm->mapped_bytes) MM_TRY(p2p_map(cm, want));
+  if (P == 1) {
+    MM_TRY(cm->pz[0].ensure(want));
+    MM_TRY(cm->pz[1].ensure(want));
+    for (int b = 0; b < 2; ++b) cm->peer_z[b].assign(1, static_cast<double*>(cm->pz[b].p));
+  }
+  const int par = static_cast<int>(++cm->epoch & 1);
+  ScatterParams sp{};
+  sp.P = P;
+  sp.col0 = pl.c_off[r];
+  for (int q = 0; q <= P; ++q) sp.a_off[q] = pl.a_off[q];
+  for (int q = 0; q < P; ++q) sp.dst[q] = cm->peer_z[par][q];
+  MM_TRY(cm->scat.ensure(sizeof(ScatterParams) + sizeof(int64_t*) * kMaxRanks));
+  auto* dsp = static_cast<ScatterParams*>(cm->scat.p);
+  auto** dflags = reinterpret_cast<int64_t**>(static_cast<uint8_t*>(cm->scat.p) + sizeof(ScatterParams));
+  MM_CUDA(cudaMemcpyAsync(dsp, &sp, sizeof(sp), cudaMemcpyHostToDevice, h->stream));
+  if (P > 1)
+    MM_CUDA(cudaMemcpyAsync(dflags, cm->peer_flags.data(), sizeof(int64_t*) * P, cudaMemcpyHostToDevice, h->stream));
+  MM_TRY(tucker_dev(h, d, m, n, T, L, nullptr, false, false, 1, d - 1, dsp));
+  if (P > 1) {
+    p2p_signal_kernel<<<1, 64, 0, h->stream>>>(dflags, P, r, cm->epoch);
+    p2p_wait_kernel<<<1, 64, 0, h->stream>>>(static_cast<const int64_t*>(cm->flags.p), P, cm->epoch);
+    MM_CUDA(cudaGetLastError());
+    h->launches += 2;
+  }
+  if (pl.A_r == 0) return MUMODE_OK;
+  const int64_t zext[2] = {pl.A_r, pl.m_d};
+  return mode_product_dev(h, 2, zext, 2, pl.n_d, cm->peer_z[par][r], L[d - 1], 1, pl.n_d, false, false, S);
+}
+
 static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64_t* m, const int64_t* n,
                        const double* T, const double* const* L, double* S, int chunks, bool cplx) {
   const int P = cm->nranks, r = cm->rank;
@@ -252,6 +377,7 @@ static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64
   DistPlan pl;
   MM_TRY(dist_plan(P, r, d, m, n, chunks, el, pl));
   const int64_t A = pl.A, A_r = pl.A_r, m_d = pl.m_d, n_d = pl.n_d;
+  if (cm->exchange == 1 && !cplx) return dist_tucker_p2p(h, cm, d, m, n, T, L, S, pl);
   if (P == 1 && chunks <= 1) {
     // one rank: no exchange; modes 1..d-1 straight into Z, then mode d
     // (explicit chunks > 1 still take the general path: exercised by tests)
@@ -452,11 +578,26 @@ int mumode_comm_destroy(mumode_comm_t c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto e : c->events) cudaEventDestroy(e);
+  for (int b = 0; b < 2; ++b)
+    for (int q = 0; q < static_cast<int>(c->peer_z[b].size()); ++q)
+      if (q != c->rank && c->peer_z[b][q]) cudaIpcCloseMemHandle(c->peer_z[b][q]);
+  for (int q = 0; q < static_cast<int>(c->peer_flags.size()); ++q)
+    if (q != c->rank && c->peer_flags[q]) cudaIpcCloseMemHandle(c->peer_flags[q]);
   if (c->ret_in) cudaEventDestroy(c->ret_in);
   if (c->ret_out) cudaEventDestroy(c->ret_out);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->owned && c->comm) mumode_gpu::nccl_api().comm_destroy(c->comm);
   delete c;
+  return MUMODE_OK;
+}
+
+int mumode_comm_set_exchange(mumode_comm_t c, int mode) {
+  using namespace mumode_gpu;
+  if (!c) return fail(MUMODE_ERR_ARGUMENT, "null comm");
+  if (mode != 0 && mode != 1) return fail(MUMODE_ERR_ARGUMENT, "exchange: 0 = NCCL send/recv, 1 = peer stores");
+  if (mode == 1 && c->nranks > 1 && (!c->comm || !nccl_api().ok))
+    return fail(MUMODE_ERR_NCCL, "peer-store exchange needs an NCCL communicator to map the peers");
+  c->exchange = mode;
   return MUMODE_OK;
 }
 

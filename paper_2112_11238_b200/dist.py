@@ -277,6 +277,13 @@ class Comm:
         dev = torch.cuda.current_device() if device is None else device
         return cls(world, rank, obj[0], dev)
 
+    def set_exchange(self, mode: str) -> None:
+        """'nccl' (grouped send/recv, default) or 'p2p' (the last local mode's
+        epilogue stores rows straight into the owning ranks' memory)."""
+        from . import _lib
+        from .api import _check
+        _check(_lib.lib().mumode_comm_set_exchange(self.c, {"nccl": 0, "p2p": 1}[mode]))
+
     def close(self) -> None:
         if getattr(self, "c", None):
             from . import _lib

@@ -566,3 +566,23 @@ def test_scatter_epilogue_to_rank_buffers(policy):
                     assert O.rel_max(got[:, col0:col0 + cols], ref) < 1e-13, (m, q)
     finally:
         h.set_kernel_policy(0)
+
+
+@pytest.mark.gpu
+def test_dist_tucker_peer_store_exchange_single_rank():
+    # exchange 1 at one rank: the scatter epilogue writes into the comm's
+    # double-buffered Z (own pointer), then mode d; bitwise equal to tucker()
+    from paper_2112_11238_b200.dist import Comm, dist_tucker
+    comm = Comm(1, 0, Comm.unique_id(), 0)
+    try:
+        comm.set_exchange("p2p")
+        g = mm.Rng(5)
+        for m, n in [((96, 64, 48), (64, 96, 40)), ((24, 24, 24, 24, 24), (24, 24, 24, 24, 24)), ((60, 40), (30, 50))]:
+            T = torch.from_numpy(g.normal(m)).cuda()
+            Ls = [torch.from_numpy(g.normal((n[k], m[k]))).cuda() for k in range(len(m))]
+            ref = mm.tucker(T, Ls).cpu().numpy().reshape(-1, order="F")
+            for _ in range(3):  # both Z parities
+                S_r = dist_tucker(comm, T, Ls, m, n)
+                assert np.array_equal(S_r.cpu().numpy(), ref), m
+    finally:
+        comm.close()
