@@ -137,6 +137,14 @@ __device__ __forceinline__ void bulk_wait_read_all() {
 // all committed stores are complete (globally visible)
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
+// Programmatic dependent launch: let the next kernel in the stream start
+// launching now, and (before touching global memory) wait until the previous
+// grid has completed and its writes are visible. No-ops without PDL.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 // Named barrier among `count` threads (warps that do not take part skip it).
 __device__ __forceinline__ void named_barrier_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");

@@ -111,6 +111,25 @@ struct mumode_handle_s {
 
 namespace mumode_gpu {
 
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while its predecessor in the stream drains; it calls griddepcontrol.wait
+// before its first global access.
+template <class K, class... Args>
+static int launch_pdl(K kernel, int grid, int threads, int smem, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(static_cast<unsigned>(threads));
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MM_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
+  return MUMODE_OK;
+}
+
 // Opt a kernel instance into its dynamic shared memory once per process
 // (keyed by the kernel's address; attributes are per function, not per device
 // for the single-architecture build).
@@ -497,26 +516,26 @@ static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
     if constexpr (Cfg::E == 1) {
       auto k = mode1 ? modeprod_tma_kernel<Cfg, true, 2> : modeprod_tma_kernel<Cfg, false, 2>;
       MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
-      k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mp, *mq, p);
+      MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, *mq, p));
     } else {
       return fail(MUMODE_ERR_ARGUMENT, "scatter epilogue is real-only");
     }
   } else if (mode1) {
     auto k = modeprod_tma_kernel<Cfg, true>;
     MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
-    k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mp, *mq, p);
+    MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, *mq, p));
   } else if (j.accumulate) {
     if constexpr (Cfg::E == 1) {
       auto k = modeprod_tma_kernel<Cfg, false, 1>;
       MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
-      k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mp, *mq, p);
+      MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, *mq, p));
     } else {
       return fail(MUMODE_ERR_ARGUMENT, "accumulating complex mode product is not compiled");
     }
   } else {
     auto k = modeprod_tma_kernel<Cfg, false>;
     MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
-    k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mp, *mq, p);
+    MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, *mq, p));
   }
   MM_CUDA(cudaGetLastError());
   h->launches++;

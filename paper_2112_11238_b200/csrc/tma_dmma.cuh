@@ -174,6 +174,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     fence_barrier_init();
   }
   __syncthreads();
+  // the successor may launch (its CTAs take SMs as ours exit); nothing below
+  // reads or writes global memory before the predecessor grid is complete
+  pdl_launch_dependents();
+  pdl_wait();
 
   // Tile order: the CTAs that share the big tensor's slab run together (mode
   // 1: T is Q, so m fastest; otherwise T is P, so n fastest) -> T streams
