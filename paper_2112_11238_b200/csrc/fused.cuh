@@ -86,6 +86,8 @@ __global__ void __launch_bounds__(FusedCfg<MU, FIRST, RA>::THREADS, 1)
     fence_barrier_init();
   }
   __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();  // before any global access (factors included)
 
   if (warp == Cfg::WARPS) {
     // ------------------------------------------------------------ producer

@@ -694,7 +694,7 @@ static int launch_fused(mumode_handle_s* h, const double* T, double* S, const do
   const int grid = static_cast<int>(p.tiles < h->num_sms ? p.tiles : h->num_sms);
   auto k = fused_pair_kernel<MU, FIRST, RA>;
   MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
-  k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mp, p);
+  MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, p));
   MM_CUDA(cudaGetLastError());
   h->launches++;
   return MUMODE_OK;
@@ -716,7 +716,7 @@ static int launch_tail(mumode_handle_s* h, const double* T, double* S, const dou
   const int grid = static_cast<int>(p.tiles < h->num_sms ? p.tiles : h->num_sms);
   auto k = tail_pair_kernel<MU>;
   MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
-  k<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream>>>(*mx, *ms, p);
+  MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mx, *ms, p));
   MM_CUDA(cudaGetLastError());
   h->launches++;
   return MUMODE_OK;

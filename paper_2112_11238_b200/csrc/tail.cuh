@@ -95,6 +95,8 @@ __global__ void __launch_bounds__(TailCfg<MU>::THREADS, 1)
     fence_barrier_init();
   }
   __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();  // before any global access (factors included)
 
   if (warp == Cfg::WARPS) {
     // ------------------------------------------------------------ producer
