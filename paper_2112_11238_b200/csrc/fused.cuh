@@ -34,9 +34,12 @@ template <int MU, bool FIRST, int RA = 8>
 struct FusedCfg {
   static constexpr int NF = MU / 8;   // 8-wide output fragments per mode
   static constexpr int KS = MU / 4;   // k-steps per contraction
-  static constexpr int WARPS = 8;     // consumer warps
   static constexpr int AH = FIRST ? 1 : RA / 8;  // 8-a halves per tile
-  static constexpr int UNITS = MU * AH;          // units per mode (UNITS / 8 per warp)
+  static constexpr int UNITS = MU * AH;          // units per mode (UNITS / WARPS per warp)
+  // consumer warps: 12 where the units split evenly (MU = 24: pass 1 of C5
+  // 600 -> 580 us, pass 2 649 -> 614 us), else 8; one producer warp. (A
+  // 4-warp producer group donating registers via setmaxnreg was slower.)
+  static constexpr int WARPS = (UNITS % 12 == 0) ? 12 : 8;
   static constexpr int THREADS = (WARPS + 1) * 32;
   static constexpr int X_BYTES = 8 * AH * MU * MU * 8;
   static constexpr int Y_ROWS = (FIRST ? 8 * NF : AH * MU) * (MU + 1);
@@ -149,9 +152,9 @@ __global__ void __launch_bounds__(FusedCfg<MU, FIRST, RA>::THREADS, 1)
     // (9 independent accumulator chains hide the DMMA latency: pass 1 of C5
     // 619 -> 602 us); with 16-wide a tiles (6 units) that costs more than it
     // hides, so the others go one unit at a time.
-    constexpr int GROUP = FIRST ? Cfg::UNITS / 8 : 1;
+    constexpr int GROUP = FIRST ? Cfg::UNITS / Cfg::WARPS : 1;
 #pragma unroll
-    for (int grp = 0; grp < (Cfg::UNITS / 8) / GROUP; ++grp) {
+    for (int grp = 0; grp < (Cfg::UNITS / Cfg::WARPS) / GROUP; ++grp) {
       constexpr int UPW = GROUP;
       double acc[UPW][NF][2];
 #pragma unroll
@@ -163,7 +166,7 @@ __global__ void __launch_bounds__(FusedCfg<MU, FIRST, RA>::THREADS, 1)
         const uint32_t Js = J0 ^ (32u * static_cast<uint32_t>(s & 1));
 #pragma unroll
         for (int uu = 0; uu < UPW; ++uu) {
-          const int u = warp + 8 * (grp * GROUP + uu);  // FIRST: fibre fragment; else (a-half, b2)
+          const int u = warp + Cfg::WARPS * (grp * GROUP + uu);  // FIRST: fibre fragment; else (a-half, b2)
           if constexpr (FIRST) {
             // A = X^T fragment (fibres 8u + xmap8(g), k = 4s + t), KX layout
             const double xf = *reinterpret_cast<const double*>(X + (s >> 1) * (8 * MU * 64) + (8 * u) * 64 +
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(FusedCfg<MU, FIRST, RA>::THREADS, 1)
       }
 #pragma unroll
       for (int uu = 0; uu < UPW; ++uu) {
-        const int u = warp + 8 * (grp * GROUP + uu);
+        const int u = warp + Cfg::WARPS * (grp * GROUP + uu);
         if constexpr (FIRST) {
           // D[g <-> fibre f = 8u + xmap8(g)][i pair = 8nf + xmap8(2t)] -> Y row (cl, nf, j2)
           const int f = 8 * u + xmap8(g);
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(FusedCfg<MU, FIRST, RA>::THREADS, 1)
     // bunches their 16-B store bursts (pass 1 of C5 602 -> 688 us)
     constexpr int GROUP2 = 1;
 #pragma unroll
-    for (int grp = 0; grp < (Cfg::UNITS / 8) / GROUP2; ++grp) {
+    for (int grp = 0; grp < (Cfg::UNITS / Cfg::WARPS) / GROUP2; ++grp) {
       constexpr int UPW = GROUP2;
       double acc[UPW][NF][2];
 #pragma unroll
@@ -228,7 +231,7 @@ __global__ void __launch_bounds__(FusedCfg<MU, FIRST, RA>::THREADS, 1)
       for (int s = 0; s < KS; ++s)
 #pragma unroll
         for (int uu = 0; uu < UPW; ++uu) {
-          const int u = warp + 8 * (grp * GROUP2 + uu);  // FIRST: (cl, ib) = (u / NF, u % NF); else (a-half, i)
+          const int u = warp + Cfg::WARPS * (grp * GROUP2 + uu);  // FIRST: (cl, ib) = (u / NF, u % NF); else (a-half, i)
           const double yf = *reinterpret_cast<const double*>(Y + y_off(u * (MU + 1) + 4 * s + t, xmap8(g)));
 #pragma unroll
           for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[uu][nf][0], acc[uu][nf][1], l2[nf][s], yf);
@@ -236,7 +239,7 @@ __global__ void __launch_bounds__(FusedCfg<MU, FIRST, RA>::THREADS, 1)
       const int x = xmap8(2 * t);  // output pair along the contiguous index
 #pragma unroll
       for (int uu = 0; uu < UPW; ++uu) {
-        const int u = warp + 8 * (grp * GROUP2 + uu);
+        const int u = warp + Cfg::WARPS * (grp * GROUP2 + uu);
         if constexpr (FIRST) {
           const int cl = u / NF, ib = u % NF;
           const int64_t c = c_base + cl;
