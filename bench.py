@@ -169,6 +169,8 @@ def main():
                          "next; 0 = auto)")
     ap.add_argument("--exchange", choices=["nccl", "p2p"], default="nccl",
                     help="N>1: NCCL grouped send/recv, or peer stores from the last local mode's epilogue")
+    ap.add_argument("--overlap-sms", type=int, default=16,
+                    help="N>1: SMs the compute leaves to NCCL while sub-slabs overlap the exchange")
     ap.add_argument("--py-dist", action="store_true",
                     help="N>1: the Python slab algorithm with a torch all-to-all instead of the C-ABI")
     ap.add_argument("--overlap", action="store_true", help="with --py-dist: chunked grouped send/recv")
@@ -389,6 +391,7 @@ def run_distributed(args, world, rank, local):
     else:
         comm = Comm.from_torch(device=local)
         comm.set_exchange(args.exchange)
+        comm.set_overlap_sms(args.overlap_sms)
 
         def run_slab(T_in):
             return dist_tucker(comm, T_in, Ls, C2, chunks=args.chunks, out=S_out)

@@ -142,6 +142,9 @@ int mumode_comm_destroy(mumode_comm_t c);
  * (NVLink), then a system-scope flag handshake (csrc/slab_dist.cuh). The
  * first call per shape maps the peers (collective). Complex stays on NCCL. */
 int mumode_comm_set_exchange(mumode_comm_t c, int mode);
+/* SMs the persistent compute kernels leave free while sub-slabs overlap the
+ * NCCL exchange (default 16; NCCL's kernels need SMs to run beside them). */
+int mumode_comm_set_overlap_sms(mumode_comm_t c, int sms);
 /* The partition (host only): c_off[P+1] = last-mode slab offsets (rank r
  * holds T[..., c_off[r]:c_off[r+1]]), a_off[P+1] = output row blocks over
  * A = n_1...n_{d-1} (rank r returns rows a_off[r]:a_off[r+1] of the result

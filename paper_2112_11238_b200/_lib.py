@@ -44,6 +44,7 @@ SIGNATURES = {
     "mumode_comm_wrap": (ctypes.c_int, [ctypes.POINTER(VP), ctypes.c_int, VP, ctypes.c_int, ctypes.c_int]),
     "mumode_comm_destroy": (ctypes.c_int, [VP]),
     "mumode_comm_set_exchange": (ctypes.c_int, [VP, ctypes.c_int]),
+    "mumode_comm_set_overlap_sms": (ctypes.c_int, [VP, ctypes.c_int]),
     "mumode_slab_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, I64P, I64P, I64P, I64P]),
     "mumode_dist_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, I64P, I64P, ctypes.c_int, ctypes.c_int,
                                         I64P, ctypes.c_int, ctypes.POINTER(ctypes.c_int), I64P, ctypes.c_int,

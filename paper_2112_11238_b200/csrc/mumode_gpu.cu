@@ -96,6 +96,7 @@ struct mumode_handle_s {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   int policy = 0;
+  int sm_reserve = 0;           // SMs left free by the persistent kernels (dist exchange overlap)
   int64_t launches = 0;
   mumode_gpu::DevBuf ws[3];     // Tucker ping-pong intermediates + expint buffer
   mumode_gpu::DevBuf pad_in, pad_out, lpad;  // odd-leading-extent chains run on an even-padded copy
@@ -110,6 +111,10 @@ struct mumode_handle_s {
 };
 
 namespace mumode_gpu {
+
+// CTAs of a persistent kernel: one per SM, minus the SMs reserved so NCCL's
+// kernels can run beside the compute during an overlapped exchange.
+static int persistent_sms(const mumode_handle_s* h) { return std::max(1, h->num_sms - h->sm_reserve); }
 
 // Launch with programmatic stream serialization (PDL): the kernel may start
 // while its predecessor in the stream drains; it calls griddepcontrol.wait
@@ -510,7 +515,7 @@ static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
   p.mt = int((p.mfrags + Cfg::BM / 8 - 1) / (Cfg::BM / 8));
   p.nt = (p.N + Cfg::BN - 1) / Cfg::BN;
   p.tiles = int64_t(p.mt) * p.nt;
-  const int grid = static_cast<int>(p.tiles < h->num_sms ? p.tiles : h->num_sms);
+  const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
   p.scat = j.scat;
   if (j.scat) {
     if constexpr (Cfg::E == 1) {
@@ -691,7 +696,7 @@ static int launch_fused(mumode_handle_s* h, const double* T, double* S, const do
     MM_TRY(get_map(h, T, 4, d, st, b, &mp));
     p.tiles = (A / RA) * C;
   }
-  const int grid = static_cast<int>(p.tiles < h->num_sms ? p.tiles : h->num_sms);
+  const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
   auto k = fused_pair_kernel<MU, FIRST, RA>;
   MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
   MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, p));
@@ -713,7 +718,7 @@ static int launch_tail(mumode_handle_s* h, const double* T, double* S, const dou
   MM_TRY(get_map(h, T, 5, d, st, bx, &mx, true));
   MM_TRY(get_map(h, S, 5, d, st, bs, &ms, true));
   TailParams p{L1, L2, A / 32, (A / 32) * C};
-  const int grid = static_cast<int>(p.tiles < h->num_sms ? p.tiles : h->num_sms);
+  const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
   auto k = tail_pair_kernel<MU>;
   MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
   MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mx, *ms, p));

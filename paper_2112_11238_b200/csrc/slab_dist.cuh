@@ -222,6 +222,7 @@ struct mumode_comm_s {
   // exchange 1 (peer stores): double-buffered Z and epoch flags, mapped into
   // every peer with CUDA IPC; the scatter table for the epilogue
   int exchange = 0;
+  int overlap_sms = 16;                    // SMs left to NCCL while sub-slabs overlap the exchange
   int64_t epoch = 0;
   mumode_gpu::DevBuf pz[2], flags, handles, scat;
   size_t mapped_bytes = 0;                 // Z size the peer mappings were made for
@@ -403,6 +404,13 @@ static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64
   PackOffsets off{};
   for (int q = 0; q <= P; ++q) off.a[q] = pl.a_off[q] * el;
   size_t op = 0;
+  // overlapped exchange: leave SMs to NCCL's kernels while the sub-slabs run
+  struct Reserve {
+    mumode_handle_s* h;
+    int prev;
+    ~Reserve() { h->sm_reserve = prev; }
+  } reserve{h, h->sm_reserve};
+  if (P > 1 && nch > 1) h->sm_reserve = std::min(cm->overlap_sms, h->num_sms - 1);
   for (int j = 0; j < nch; ++j) {
     const DistChunk& c = pl.ch[j];
     if (c.w > 0) {
@@ -436,6 +444,7 @@ static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64
       MM_NCCL(api.group_end());
     }
   }
+  h->sm_reserve = reserve.prev;  // the last mode runs after the exchange: all SMs
   MM_CUDA(cudaEventRecord(cm->events[nch + 1], cm->stream));
   MM_CUDA(cudaStreamWaitEvent(h->stream, cm->events[nch + 1], 0));
   if (A_r == 0) return MUMODE_OK;
@@ -588,6 +597,14 @@ int mumode_comm_destroy(mumode_comm_t c) {
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->owned && c->comm) mumode_gpu::nccl_api().comm_destroy(c->comm);
   delete c;
+  return MUMODE_OK;
+}
+
+int mumode_comm_set_overlap_sms(mumode_comm_t c, int sms) {
+  using namespace mumode_gpu;
+  if (!c) return fail(MUMODE_ERR_ARGUMENT, "null comm");
+  if (sms < 0 || sms > 128) return fail(MUMODE_ERR_ARGUMENT, "overlap SMs: 0..128");
+  c->overlap_sms = sms;
   return MUMODE_OK;
 }
 

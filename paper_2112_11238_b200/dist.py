@@ -284,6 +284,12 @@ class Comm:
         from .api import _check
         _check(_lib.lib().mumode_comm_set_exchange(self.c, {"nccl": 0, "p2p": 1}[mode]))
 
+    def set_overlap_sms(self, sms: int) -> None:
+        """SMs left to NCCL while sub-slabs overlap the exchange (default 16)."""
+        from . import _lib
+        from .api import _check
+        _check(_lib.lib().mumode_comm_set_overlap_sms(self.c, int(sms)))
+
     def close(self) -> None:
         if getattr(self, "c", None):
             from . import _lib
