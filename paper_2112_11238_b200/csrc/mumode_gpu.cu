@@ -354,6 +354,8 @@ struct ModeJob {
   bool conj;
   bool accumulate = false;  // S += T x_mu op(L)
   const ScatterParams* scat = nullptr;  // device table: scatter the (rows x C) result to ranks (S unused)
+  const double* div_front = nullptr;    // last mode: S(a, n) /= (div_front[a] + div_last[n])
+  const double* div_last = nullptr;
 };
 
 // Compiled tile configurations (BM, BN, BK, stages, warps along M, along N).
@@ -517,7 +519,18 @@ static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
   p.tiles = int64_t(p.mt) * p.nt;
   const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
   p.scat = j.scat;
-  if (j.scat) {
+  p.div_front = j.div_front;
+  p.div_last = j.div_last;
+  if (j.div_front) {
+    if constexpr (Cfg::E == 1) {
+      if (mode1 || j.C != 1) return fail(MUMODE_ERR_ARGUMENT, "divide epilogue: last mode of order >= 2 only");
+      auto k = modeprod_tma_kernel<Cfg, false, 3>;
+      MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
+      MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, *mq, p));
+    } else {
+      return fail(MUMODE_ERR_ARGUMENT, "divide epilogue is real-only");
+    }
+  } else if (j.scat) {
     if constexpr (Cfg::E == 1) {
       auto k = mode1 ? modeprod_tma_kernel<Cfg, true, 2> : modeprod_tma_kernel<Cfg, false, 2>;
       MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
@@ -648,6 +661,22 @@ static int run_job(mumode_handle_s* h, const ModeJob& j0) {
       j = jp;
     }
   }
+  if (j.div_front) {
+    // the direct solver's division in the last mode's epilogue, else a pass
+    if (!j.cplx && !j.accumulate && j.A > 1 && j.C == 1 && tma_ok(j) && h->policy != 1 && h->policy != 8 &&
+        (h->policy >= 2 || tma_worthwhile(j)))
+      return launch_tma_auto(h, j);
+    ModeJob jt = j;
+    jt.div_front = jt.div_last = nullptr;
+    MM_TRY(run_job(h, jt));
+    const int64_t A = j.A, N = j.N;
+    const int gx = static_cast<int>(std::min<int64_t>((A + 255) / 256, 64));
+    const int gy = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(N, int64_t(h->num_sms) * 16 / gx)));
+    eigsum_divide_kernel<<<dim3(gx, gy), 256, 0, h->stream>>>(j.S, j.div_front, j.div_last, A, N);
+    MM_CUDA(cudaGetLastError());
+    h->launches++;
+    return MUMODE_OK;
+  }
   if (j.scat) {
     // fused exchange: the TMA kernel's epilogue scatters to the ranks; any
     // other path computes the (rows x C) result and scatter-copies it
@@ -772,10 +801,13 @@ static int fused_extent(int d, const int64_t* m, const int64_t* n, bool cplx, bo
 static int mode_product_dev(mumode_handle_s* h, int d, const int64_t* m, int mu, int64_t n_mu,
                             const double* T, const double* L, int64_t sLi, int64_t sLk,
                             bool cplx, bool conj, double* S, bool accumulate = false,
-                            const ScatterParams* scat = nullptr) {
+                            const ScatterParams* scat = nullptr, const double* div_front = nullptr,
+                            const double* div_last = nullptr) {
   ModeJob j;
   j.accumulate = accumulate;
   j.scat = scat;
+  j.div_front = div_front;
+  j.div_last = div_last;
   j.T = T;
   j.L = L;
   j.S = S;
@@ -797,7 +829,8 @@ static int mode_product_dev(mumode_handle_s* h, int d, const int64_t* m, int mu,
 // access, or a materialised op(L) when the TMA path applies.
 static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t* n,
                       const double* T, const double* const* L, double* S, bool adjoint,
-                      bool cplx, int mu_lo = 1, int mu_hi = 0, const ScatterParams* scat = nullptr) {
+                      bool cplx, int mu_lo = 1, int mu_hi = 0, const ScatterParams* scat = nullptr,
+                      const double* div_front = nullptr, const double* div_last = nullptr) {
   if (mu_hi == 0) mu_hi = d;
   const int el = cplx ? 2 : 1;
   const int nmodes = mu_hi - mu_lo + 1;
@@ -823,7 +856,7 @@ static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t
   // mode-1 factor by a zero column / row): zero k-terms leave the FMA chains
   // unchanged, the pad row of the output is dropped. Two copy passes buy the
   // TMA/DMMA kernels for every mode.
-  if (!cplx && !adjoint && mu_lo == 1 && mu_hi == d && d >= 2 && h->policy == 0 && ((m[0] | n[0]) & 1) &&
+  if (!cplx && !adjoint && !div_front && mu_lo == 1 && mu_hi == d && d >= 2 && h->policy == 0 && ((m[0] | n[0]) & 1) &&
       aligned16_ptr(T) && aligned16_ptr(S)) {
     // measured (tools/odd_sweep.py): the padded chain wins from ~223^3 up
     // (255^3: 26.5 -> 28.7 TF/s); below ~208 the LDG-staged kernel's smaller
@@ -916,14 +949,25 @@ static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t
       MM_TRY(rc);
       src = dst;
     }
-    if (mu == mu_hi)
-      MM_TRY(mode_product_dev(h, d, ext.data(), mu, n[mu - 1], src, L[mu - 1], 1, n[mu - 1], false, false, S));
+    if (mu == mu_hi) {
+      MM_TRY(mode_product_dev(h, d, ext.data(), mu, n[mu - 1], src, L[mu - 1], 1, n[mu - 1], false, false, S,
+                              false, nullptr, div_front, div_last));
+    } else if (div_front) {  // the last pass was a fused pair: divide in a pass of its own
+      const int64_t A = prod(n, 0, d - 1), N = n[d - 1];
+      const int gx = static_cast<int>(std::min<int64_t>((A + 255) / 256, 64));
+      const int gy = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(N, int64_t(h->num_sms) * 16 / gx)));
+      eigsum_divide_kernel<<<dim3(gx, gy), 256, 0, h->stream>>>(S, div_front, div_last, A, N);
+      MM_CUDA(cudaGetLastError());
+      h->launches++;
+    }
     return MUMODE_OK;
   }
   for (int mu = mu_lo; mu <= mu_hi; ++mu) {
     double* dst = (mu == mu_hi) ? S : static_cast<double*>(h->ws[(mu - mu_lo) % 2].p);
+    const bool last = (mu == mu_hi);
     MM_TRY(mode_product_dev(h, d, ext.data(), mu, n[mu - 1], src, Lop[mu - 1], 1, n[mu - 1],
-                            cplx, false, dst));
+                            cplx, false, dst, false, nullptr, last ? div_front : nullptr,
+                            last ? div_last : nullptr));
     ext[mu - 1] = n[mu - 1];
     src = dst;
   }
@@ -1162,41 +1206,34 @@ int mumode_kronsum_solve_f64(mumode_handle_t h, int d, const int64_t* m, const d
   MM_CUDA(cudaSetDevice(h->device));
   const int64_t numel = prod(m, 0, d);
   const int64_t A = prod(m, 0, d - 1), N = m[d - 1];
-  // eigenvalue sums over modes 1..d-1 (the reference adds mode by mode from 0)
+  // eigenvalue sums over modes 1..d-1, built mode by mode: esum(a) =
+  // ((0 + ev_1) + ev_2) + ... in the reference's summation order (imex.cpp:73-75)
   std::vector<double> esum(static_cast<size_t>(A + N));
-  std::vector<int64_t> j(static_cast<size_t>(d), 0);
-  for (int64_t a = 0; a < A; ++a) {
-    double s = 0.0;
-    for (int k = 0; k < d - 1; ++k) s += evals[k][j[k]];
-    esum[static_cast<size_t>(a)] = s;
-    for (int k = 0; k < d - 1; ++k) {
-      if (++j[k] < m[k]) break;
-      j[k] = 0;
-    }
+  esum[0] = 0.0;
+  int64_t len = 1;
+  for (int k = 0; k < d - 1; ++k) {
+    for (int64_t jk = m[k] - 1; jk >= 0; --jk)  // in place, high blocks first
+      for (int64_t a = 0; a < len; ++a) esum[static_cast<size_t>(a + len * jk)] = esum[static_cast<size_t>(a)] + evals[k][jk];
+    len *= m[k];
   }
-  for (int64_t n = 0; n < N; ++n) {
-    esum[static_cast<size_t>(A + n)] = evals[d - 1][n];
-    for (int64_t a = 0; a < A; ++a)
-      if (esum[static_cast<size_t>(a)] + evals[d - 1][n] == 0.0)
-        return fail(MUMODE_ERR_NUMERICAL, "imex direct backend: singular implicit operator");
-  }
+  // a zero denominator esum[a] + ev_last[n] (the reference throws on it,
+  // imex.cpp:76-77) exists iff ev_last[n] == -esum[a] exactly (IEEE: x + y
+  // rounds to 0 only when y == -x): binary search in the sorted ev_last
+  std::vector<double> last(evals[d - 1], evals[d - 1] + N);
+  std::sort(last.begin(), last.end());
+  for (int64_t a = 0; a < A; ++a)
+    if (std::binary_search(last.begin(), last.end(), -esum[static_cast<size_t>(a)]))
+      return fail(MUMODE_ERR_NUMERICAL, "imex direct backend: singular implicit operator");
+  for (int64_t n = 0; n < N; ++n) esum[static_cast<size_t>(A + n)] = evals[d - 1][n];
   MM_TRY(h->ws[2].ensure(size_t(numel) * sizeof(double)));
   MM_TRY(h->lbuf.ensure(esum.size() * sizeof(double)));
   double* w = static_cast<double*>(h->ws[2].p);
   double* dsum = static_cast<double*>(h->lbuf.p);
+  // pageable source: the call returns once esum is staged, so it may go
   MM_CUDA(cudaMemcpyAsync(dsum, esum.data(), esum.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-  MM_TRY(tucker_dev(h, d, m, m, b, Qt, w, false, false));
-  {
-    const int gx = static_cast<int>(std::min<int64_t>((A + 255) / 256, 64));
-    const int gy = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(N, int64_t(h->num_sms) * 16 / gx)));
-    eigsum_divide_kernel<<<dim3(gx, gy), 256, 0, h->stream>>>(w, dsum, dsum + A, A, N);
-  }
-  MM_CUDA(cudaGetLastError());
-  h->launches++;
-  MM_TRY(tucker_dev(h, d, m, m, w, Q, x, false, false));
-  // the host staging of esum must outlive the async copy
-  MM_CUDA(cudaStreamSynchronize(h->stream));
-  return MUMODE_OK;
+  // w = b x {Q^T}, divided by the eigenvalue sums in the last mode's epilogue
+  MM_TRY(tucker_dev(h, d, m, m, b, Qt, w, false, false, 1, d, nullptr, dsum, dsum + A));
+  return tucker_dev(h, d, m, m, w, Q, x, false, false);
 }
 
 int mumode_tucker_promote(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,

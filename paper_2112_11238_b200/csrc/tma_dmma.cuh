@@ -69,6 +69,8 @@ __device__ __forceinline__ void scatter_store(const ScatterParams* sp, int64_t r
 
 struct TmaParams {
   const ScatterParams* scat;  // EPI 2 only (device memory)
+  const double* div_front;    // EPI 3: D(a, n) /= (div_front[a] + div_last[n])
+  const double* div_last;
   double* D;
   int64_t ldD;      // stride of D between consecutive n (elements)
   int64_t bstride;  // stride of D between batches c (elements)
@@ -145,8 +147,10 @@ struct TmaCfg {
 // QK == true  (mu == 1): P = L (XK), Q = T (KX)
 // QK == false (mu  > 1): P = T (XK, fragment list over (a-block, c)), Q = L (XK)
 // EPI: 0 = store; 1 = D += result (kronsumv term accumulation,
-// tucker.hpp:222-231); 2 = scatter to the owning ranks (real only). A
-// compile-time switch -- a runtime branch in the epilogue costs ~2 % on C2.
+// tucker.hpp:222-231); 2 = scatter to the owning ranks (real only); 3 =
+// divide by the eigenvalue Kronecker sum (the direct solver's pointwise step,
+// imex.cpp:70-80; last mode, real). A compile-time switch -- a runtime branch
+// in the epilogue costs ~2 % on C2.
 template <class Cfg, bool QK, int EPI = 0>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
     modeprod_tma_kernel(const __grid_constant__ CUtensorMap mapP,
@@ -155,7 +159,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   constexpr int FM = Cfg::FM, FN = Cfg::FN, E = Cfg::E, ROW = Cfg::ROW;
   constexpr bool CPLX = (E == 2);
   constexpr bool ACC = (EPI == 1);
-  static_assert(EPI != 2 || !CPLX, "scatter epilogue is real-only");
+  static_assert(EPI < 2 || !CPLX, "scatter / divide epilogues are real-only");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment by pointer arithmetic so the compiler keeps the shared
   // address space (LDS, not generic LD).
@@ -396,6 +400,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             continue;
           }
           double* dst = base + static_cast<int64_t>(n) * p.ldD;
+          if constexpr (EPI == 3) {
+            // the last mode: rows m, m+1 index the modes before it (batch 0)
+            const double2 fr = *reinterpret_cast<const double2*>(p.div_front + m);
+            const double ln = __ldg(p.div_last + n);
+            stg_f64x2(dst, acc[fm][fn][0] / (fr.x + ln), acc[fm][fn][1] / (fr.y + ln));
+            continue;
+          }
           if constexpr (ACC) {
             const double2 o = *reinterpret_cast<const double2*>(dst);
             stg_f64x2(dst, o.x + acc[fm][fn][0], o.y + acc[fm][fn][1]);

@@ -420,6 +420,26 @@ def test_kronsum_direct_solve():
             dev(np.ones((2, 2))))
 
 
+def test_kronsum_solve_epilogue_division_bitwise():
+    # the division fused into the last mode's epilogue (TMA path) equals the
+    # separate division pass (policy 8: LDG-staged kernels + divide kernel)
+    rng = np.random.default_rng(7)
+    m = (64, 48, 40)
+    Ms = [np.eye(e) / 3 - 1e-2 * O.port_advection_diffusion(e, 0.3) for e in m]
+    Ms = [0.5 * (M + M.T) for M in Ms]
+    solver = mm.KronSumSolver(Ms=Ms)
+    b = dev(rnd(rng, m))
+    h = mm.get_handle(0)
+    out = {}
+    for pol in (0, 8):
+        h.set_kernel_policy(pol)
+        try:
+            out[pol] = host(solver.solve(b))
+        finally:
+            h.set_kernel_policy(0)
+    np.testing.assert_array_equal(out[0], out[8])
+
+
 def test_concurrent_threads_get_independent_workspaces():
     # the reference's operators are safe for concurrent callers; each thread
     # gets its own handle (workspaces), results match the single-thread ones

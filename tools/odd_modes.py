@@ -23,19 +23,20 @@ def timeit(fn, reps=10):
     return sorted(a.elapsed_time(b) for a, b in evs)[reps // 2]
 
 
-h = mm.get_handle(0)
-for shape in [(256, 255, 255), (202, 201, 201), (256, 256, 256), (200, 200, 200)]:
-    T = mm.colmajor_empty(shape, torch.float64, "cuda").normal_()
-    for mu in (1, 2, 3):
-        e = shape[mu - 1]
-        L = mm.to_colmajor(torch.randn(e, e, dtype=torch.float64, device="cuda"))
-        row = {"shape": shape, "mu": mu}
-        for pol in (0, 8, 3, 4, 5, 6):
-            h.set_kernel_policy(pol)
-            try:
-                ms = timeit(lambda: mm.mode_product(T, L, mu))
-                row[f"p{pol}"] = round(2 * e * T.numel() / ms / 1e9, 1)
-            except Exception as ex:  # noqa: BLE001
-                row[f"p{pol}"] = str(ex)[:30]
-        h.set_kernel_policy(0)
-        print(json.dumps(row))
+if __name__ == "__main__":
+    h = mm.get_handle(0)
+    for shape in [(256, 255, 255), (202, 201, 201), (256, 256, 256), (200, 200, 200)]:
+        T = mm.colmajor_empty(shape, torch.float64, "cuda").normal_()
+        for mu in (1, 2, 3):
+            e = shape[mu - 1]
+            L = mm.to_colmajor(torch.randn(e, e, dtype=torch.float64, device="cuda"))
+            row = {"shape": shape, "mu": mu}
+            for pol in (0, 8, 3, 4, 5, 6):
+                h.set_kernel_policy(pol)
+                try:
+                    ms = timeit(lambda: mm.mode_product(T, L, mu))
+                    row[f"p{pol}"] = round(2 * e * T.numel() / ms / 1e9, 1)
+                except Exception as ex:  # noqa: BLE001
+                    row[f"p{pol}"] = str(ex)[:30]
+            h.set_kernel_policy(0)
+            print(json.dumps(row))
