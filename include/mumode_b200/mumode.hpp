@@ -2,7 +2,9 @@
 //
 // A user of the reference library's hot path (/root/reference/proj/include/
 // mumode: core::mode_product, ops::tucker, ops::cttucker, ops::tucker_sequential,
-// ops::kronsumv) includes this header instead and links libmumode_b200.so. The
+// ops::kronsumv, ops::itucker; plus the host-side callback helpers of the same
+// files: core::matricize / dematricize / mode_action, ops::tuckerfun)
+// includes this header instead and links libmumode_b200.so. The
 // value types (Shape, Tensor<T>, Matrix<T>, ModeIndex), the exception types and
 // their messages follow the reference's contracts (shape.hpp, tensor.hpp,
 // matrix.hpp, errors.hpp, mode_product.hpp:64-83, tucker.hpp:57-232); the
@@ -17,6 +19,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdint>
+#include <functional>
 #include <initializer_list>
 #include <numeric>
 #include <stdexcept>
@@ -229,6 +232,50 @@ double rel_max_dist(const Tensor<T>& a, const Tensor<T>& b) {
   return s == 0 ? 0 : max_abs_diff(a, b) / s;
 }
 
+// mu-matricization (matricize.hpp:22-31): m_mu x (prod of the other extents),
+// columns = the mu-fibres ordered by the remaining indices, earliest fastest.
+// Host-side (it feeds user callbacks, not the engine): element (i, a + A*c)
+// is T[a + A*(i + m_mu*c)], a over the modes before mu, c after.
+template <class T>
+Matrix<T> matricize(const Tensor<T>& t, ModeIndex mu) {
+  t.shape().check_mode(mu);
+  const index_t rows = t.extent(mu), A = t.shape().stride(mu), C = t.numel() / (A * rows);
+  Matrix<T> M(rows, A * C);
+  for (index_t c = 0; c < C; ++c)
+    for (index_t i = 0; i < rows; ++i)
+      for (index_t a = 0; a < A; ++a) M(i, a + A * c) = t[a + A * (i + rows * c)];
+  return M;
+}
+
+// Inverse of matricize (matricize.hpp:35-56): the output shape is s with
+// extent mu replaced by M.rows().
+template <class T>
+Tensor<T> dematricize(const Matrix<T>& M, ModeIndex mu, const Shape& s) {
+  s.check_mode(mu);
+  if (M.cols() != s.numel_except(mu))
+    throw SizeError("dematricize: column count does not match remaining extents");
+  std::vector<index_t> ext = s.extents();
+  ext[static_cast<std::size_t>(mu - 1)] = M.rows();
+  const index_t rows = M.rows(), A = s.stride(mu), C = M.cols() / A;
+  Tensor<T> t{Shape(ext)};
+  for (index_t c = 0; c < C; ++c)
+    for (index_t i = 0; i < rows; ++i)
+      for (index_t a = 0; a < A; ++a) t[a + A * (i + rows * c)] = M(i, a + A * c);
+  return t;
+}
+
+// mu-mode action (mode_product.hpp:88-100): a columnwise host operator on the
+// mu-matricization. The engine's mode_product is the matrix case.
+template <class T>
+Tensor<T> mode_action(const Tensor<T>& t, const std::function<Matrix<T>(const Matrix<T>&)>& op, ModeIndex mu) {
+  t.shape().check_mode(mu);
+  Matrix<T> X = matricize(t, mu);
+  Matrix<T> Y = op(X);
+  if (Y.cols() != X.cols())
+    throw ContractError("mode_action: operator changed the column count on mode " + std::to_string(mu.mu));
+  return dematricize(Y, mu, t.shape());
+}
+
 }  // namespace core
 
 // ------------------------------------------------------------------ engine glue
@@ -431,6 +478,33 @@ inline Tensor<double> itucker(const Tensor<double>& t, const FactorizedStack& F)
     if (F.inverses()[static_cast<std::size_t>(mu - 1)].rows() != t.extent(mu))
       throw core::SizeError("itucker: factor size does not match extent of mode " + std::to_string(mu));
   return tucker(t, F.inverses());
+}
+
+/// Columnwise operator of the operator-action Tucker (tucker.hpp:24-32).
+template <class T>
+struct ColumnOperator {
+  index_t out_rows;
+  std::function<Matrix<T>(const Matrix<T>&)> apply;
+};
+template <class T>
+using OperatorStack = std::vector<ColumnOperator<T>>;
+
+/// Operator-action Tucker (ops::tuckerfun, tucker.hpp:169-185): host
+/// callbacks, applied per mode in order 1..d (arbitrary operators have no
+/// device form; not the accelerated path).
+template <class T>
+Tensor<T> tuckerfun(const Tensor<T>& t, const OperatorStack<T>& ops) {
+  if (static_cast<index_t>(ops.size()) != t.order())
+    throw core::SizeError("tuckerfun: stack length does not match tensor order");
+  Tensor<T> cur = t;
+  for (index_t mu = 1; mu <= t.order(); ++mu) {
+    const auto& op = ops[static_cast<std::size_t>(mu - 1)];
+    cur = core::mode_action(cur, op.apply, mu);
+    if (cur.extent(mu) != op.out_rows)
+      throw core::ContractError("tuckerfun: operator on mode " + std::to_string(mu) + " produced " +
+                                std::to_string(cur.extent(mu)) + " rows, declared " + std::to_string(op.out_rows));
+  }
+  return cur;
 }
 
 }  // namespace ops

@@ -195,6 +195,48 @@ int main() {
     }
     CHECK(num);
   }
+  // matricize / dematricize / mode_action / tuckerfun (matricize.hpp,
+  // mode_product.hpp:88-100, tucker.hpp:169-185): host helpers around user
+  // callbacks; with matrix-multiply operators they equal the engine's results
+  {
+    auto T = rand_tensor<double>(g, Shape({3, 4, 5}));
+    for (index_t mu = 1; mu <= 3; ++mu) {
+      auto M = core::matricize(T, mu);
+      CHECK(M.rows() == T.extent(mu) && M.cols() == T.numel() / T.extent(mu));
+      CHECK(core::max_abs_diff(core::dematricize(M, mu, T.shape()), T) == 0.0);
+      // column j of the mu-matricization holds the fibre with the other
+      // indices in original order, earliest fastest
+      auto j = core::multi_index(T.shape(), 17);
+      index_t col = 0, scale = 1;
+      for (index_t k = 1; k <= 3; ++k) {
+        if (k == mu) continue;
+        col += (j[static_cast<std::size_t>(k - 1)] - 1) * scale;
+        scale *= T.extent(k);
+      }
+      CHECK(M(j[static_cast<std::size_t>(mu - 1)] - 1, col) == T[17]);
+    }
+    ops::MatrixStack<double> Ls = {rand_matrix<double>(g, 2, 3), rand_matrix<double>(g, 6, 4),
+                                   rand_matrix<double>(g, 5, 5)};
+    ops::OperatorStack<double> opsk;
+    for (const auto& L : Ls)
+      opsk.push_back({L.rows(), [L](const Matrix<double>& X) {
+                        Matrix<double> Y(L.rows(), X.cols());
+                        for (index_t c = 0; c < X.cols(); ++c)
+                          for (index_t k = 0; k < X.rows(); ++k)
+                            for (index_t i = 0; i < L.rows(); ++i) Y(i, c) += L(i, k) * X(k, c);
+                        return Y;
+                      }});
+    CHECK(rel(core::mode_action(T, opsk[1].apply, 2), core::mode_product(T, Ls[1], 2)) < 1e-14);
+    CHECK(rel(ops::tuckerfun(T, opsk), ops::tucker(T, Ls)) < 1e-14);
+    bool contract = false;
+    opsk[2].out_rows = 4;  // declared rows disagree with what the operator makes
+    try {
+      ops::tuckerfun(T, opsk);
+    } catch (const ContractError& e) {
+      contract = std::string(e.what()).find("mode 3") != std::string::npos;
+    }
+    CHECK(contract);
+  }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "PASSED", failures);
   return failures ? 1 : 0;
 }
