@@ -16,6 +16,7 @@ from .api import (  # noqa: F401
     SizeError,
     colmajor_empty,
     cttucker,
+    dematricize,
     expint,
     expm,
     get_handle,
@@ -23,10 +24,13 @@ from .api import (  # noqa: F401
     itucker,
     kronsumv,
     launch_count,
+    matricize,
+    mode_action,
     mode_product,
     to_colmajor,
     tucker,
     tucker_sequential,
+    tuckerfun,
 )
 
 __version__ = "0.1.0"

@@ -389,6 +389,61 @@ def expint(u0, Es, steps: int, out=None):
     return res
 
 
+def matricize(T, mu: int):
+    """mu-matricization (core::matricize, matricize.hpp:22-31): the
+    m_mu x (prod of the other extents) matrix of mu-fibres, columns ordered by
+    the remaining indices with the earliest fastest. Host-side helper for
+    user callbacks (numpy in, numpy out)."""
+    T = np.asarray(T.cpu() if _is_torch(T) else T)
+    d = T.ndim
+    if mu < 1 or mu > d:
+        raise ArgumentError(f"mode index {mu} out of range 1..{d}")
+    order = [mu - 1] + [k for k in range(d) if k != mu - 1]
+    return np.asfortranarray(np.transpose(T, order).reshape((T.shape[mu - 1], -1), order="F"))
+
+
+def dematricize(M, mu: int, shape):
+    """Inverse of matricize (matricize.hpp:35-56); the output's extent mu is
+    M's row count."""
+    M = np.asarray(M)
+    shape = [int(e) for e in shape]
+    d = len(shape)
+    if mu < 1 or mu > d:
+        raise ArgumentError(f"mode index {mu} out of range 1..{d}")
+    rest = [shape[k] for k in range(d) if k != mu - 1]
+    if M.shape[1] != int(np.prod(rest)):
+        raise SizeError("dematricize: column count does not match remaining extents")
+    fronted = M.reshape([M.shape[0]] + rest, order="F")
+    inv = np.argsort([mu - 1] + [k for k in range(d) if k != mu - 1])
+    return np.asfortranarray(np.transpose(fronted, inv))
+
+
+def mode_action(T, op, mu: int):
+    """mu-mode action (core::mode_action, mode_product.hpp:88-100): a columnwise
+    host operator on the mu-matricization."""
+    X = matricize(T, mu)
+    Y = np.asarray(op(X))
+    if Y.ndim != 2 or Y.shape[1] != X.shape[1]:
+        raise ContractError(f"mode_action: operator changed the column count on mode {mu}")
+    return dematricize(Y, mu, np.asarray(T.cpu() if _is_torch(T) else T).shape)
+
+
+def tuckerfun(T, ops):
+    """Operator-action Tucker (ops::tuckerfun, tucker.hpp:169-185): ``ops`` is a
+    list of (out_rows, callable) per mode, applied in mode order. Host
+    callbacks, so this runs on the host (not the accelerated path)."""
+    T = np.asarray(T.cpu() if _is_torch(T) else T)
+    if len(ops) != T.ndim:
+        raise SizeError("tuckerfun: stack length does not match tensor order")
+    cur = T
+    for mu, (out_rows, fn) in enumerate(ops, start=1):
+        cur = mode_action(cur, fn, mu)
+        if cur.shape[mu - 1] != out_rows:
+            raise ContractError(f"tuckerfun: operator on mode {mu} produced {cur.shape[mu - 1]} rows, "
+                                f"declared {out_rows}")
+    return cur
+
+
 class FactorizedStack:
     """Per-mode factorizations of square P_1..P_d for the inverse Tucker
     operator (ops::FactorizedStack, tucker.hpp:34-51). Factorizes at

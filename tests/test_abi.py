@@ -167,3 +167,25 @@ def test_empty_tensors_rejected_like_reference():
     from paper_2112_11238_b200.dist import slab_plan_offsets
     with pytest.raises(mm.ArgumentError, match="extents must be positive"):
         slab_plan_offsets(1, (2, 0, 3), (2, 1, 3))
+
+
+def test_matricize_mode_action_tuckerfun_host_helpers():
+    # matricize.hpp / mode_product.hpp:88-100 / tucker.hpp:169-185 semantics
+    rng = np.random.default_rng(11)
+    T = np.asfortranarray(rng.standard_normal((3, 4, 5)))
+    for mu in (1, 2, 3):
+        M = mm.matricize(T, mu)
+        assert M.shape == (T.shape[mu - 1], T.size // T.shape[mu - 1])
+        np.testing.assert_array_equal(mm.dematricize(M, mu, T.shape), T)
+    # column order: remaining indices, earliest fastest (test_tensor_core.cpp)
+    M2 = mm.matricize(T, 2)
+    assert M2[3, 1 + 3 * 4] == T[1, 3, 4]
+    Ls = [rng.standard_normal((2, 3)), rng.standard_normal((6, 4)), rng.standard_normal((5, 5))]
+    ops = [(L.shape[0], (lambda L: (lambda X: L @ X))(L)) for L in Ls]
+    ref = O.port_tucker(T, Ls)
+    assert O.rel_max(mm.tuckerfun(T, ops), ref) < 1e-13
+    assert O.rel_max(mm.mode_action(T, ops[1][1], 2), O.port_mode_product(T, Ls[1], 2)) < 1e-13
+    with pytest.raises(mm.ContractError, match="mode 3"):
+        mm.tuckerfun(T, ops[:2] + [(4, ops[2][1])])
+    with pytest.raises(mm.ContractError):
+        mm.mode_action(T, lambda X: X[:, :-1], 1)
