@@ -1,0 +1,301 @@
+// Tucker chains on device buffers: the fused two-mode passes (fused.cuh,
+// tail.cuh) and tucker_dev, which runs modes mu_lo..mu_hi of a chain
+// (odd-extent padding, fused pairs, per-mode jobs, scatter / divide
+// epilogues of the last mode). Included by mumode_gpu.cu after dispatch.cuh.
+#pragma once
+
+namespace mumode_gpu {
+
+// ------------------------------------------------------------------ fused pairs
+template <int MU, bool FIRST, int RA>
+static int launch_fused(mumode_handle_s* h, const double* T, double* S, const double* L1,
+                        const double* L2, int64_t A, int64_t C) {
+  using Cfg = FusedCfg<MU, FIRST, RA>;
+  const CUtensorMap* mp = nullptr;
+  FusedParams p{S, L1, L2, A, C, 0};
+  if (FIRST) {
+    uint64_t d[3] = {8, uint64_t(MU) * uint64_t(C), uint64_t(MU / 8)}, st[2] = {uint64_t(MU), 8};
+    uint32_t b[3] = {8, 8 * MU, MU / 8};
+    MM_TRY(get_map(h, T, 3, d, st, b, &mp));
+    p.tiles = (C + 7) / 8;
+  } else {
+    uint64_t d[4] = {uint64_t(A), uint64_t(MU), uint64_t(MU), uint64_t(C)};
+    uint64_t st[3] = {uint64_t(A), uint64_t(A) * MU, uint64_t(A) * MU * MU};
+    uint32_t b[4] = {8, MU, MU, 1};
+    MM_TRY(get_map(h, T, 4, d, st, b, &mp));
+    p.tiles = (A / RA) * C;
+  }
+  const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
+  auto k = fused_pair_kernel<MU, FIRST, RA>;
+  MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
+  MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, p));
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return MUMODE_OK;
+}
+
+// Strided-pair pass with 32-wide a tiles (tail.cuh): 256-B rows for loads and
+// stores instead of 64-B ones.
+template <int MU>
+static int launch_tail(mumode_handle_s* h, const double* T, double* S, const double* L1,
+                       const double* L2, int64_t A, int64_t C) {
+  using Cfg = TailCfg<MU>;
+  const CUtensorMap *mx = nullptr, *ms = nullptr;
+  uint64_t d[5] = {16, uint64_t(A / 16), uint64_t(MU), uint64_t(MU), uint64_t(C)};
+  uint64_t st[4] = {16, uint64_t(A), uint64_t(A) * MU, uint64_t(A) * MU * MU};
+  uint32_t bx[5] = {16, 2, MU, Cfg::KB, 1}, bs[5] = {16, 2, 1, MU, 1};
+  MM_TRY(get_map(h, T, 5, d, st, bx, &mx, true));
+  MM_TRY(get_map(h, S, 5, d, st, bs, &ms, true));
+  TailParams p{L1, L2, A / 32, (A / 32) * C};
+  const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
+  auto k = tail_pair_kernel<MU>;
+  MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
+  MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mx, *ms, p));
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return MUMODE_OK;
+}
+
+// The tail kernel pays off once the a-stride makes every tile row a new page
+// (policy 9 forces it wherever the shape allows, 10 disables it).
+static constexpr int64_t kTailMinA = 16384;
+
+template <int MU>
+static int launch_fused_mu(mumode_handle_s* h, bool first, const double* T, double* S,
+                           const double* L1, const double* L2, int64_t A, int64_t C) {
+  if (first) return launch_fused<MU, true, 8>(h, T, S, L1, L2, A, C);
+  if constexpr (MU <= 24) {
+    if (A % 32 == 0 && h->policy != 10 && (h->policy == 9 || A >= kTailMinA))
+      return launch_tail<MU>(h, T, S, L1, L2, A, C);
+  }
+  // 16 a's per tile when shared memory allows it and A tiles evenly
+  constexpr bool wide_fits = FusedCfg<MU, false, 16>::SMEM_BYTES <= 227 * 1024 &&
+                             FusedCfg<MU, false, 16>::NBUF >= 2;
+  if (wide_fits && A % 16 == 0 && A <= 4096) return launch_fused<MU, false, (wide_fits ? 16 : 8)>(h, T, S, L1, L2, A, C);
+  return launch_fused<MU, false, 8>(h, T, S, L1, L2, A, C);
+}
+
+// Fused two-mode passes apply to real, forward chains whose modes are all
+// square with one small extent MU in {8, 16, 24, 32} (e.g. config C5, 24^6):
+// there each single product is HBM-bound and pairing halves the HBM passes.
+static int fused_extent(int d, const int64_t* m, const int64_t* n, bool cplx, bool adjoint,
+                        int policy, int mu_lo, int mu_hi, const double* T, const double* S,
+                        const double* const* L) {
+  if (cplx || adjoint || !(policy == 0 || policy == 7 || policy == 9 || policy == 10) || mu_hi - mu_lo < 1)
+    return 0;
+  const int64_t MU = m[0];
+  if (MU != 8 && MU != 16 && MU != 24 && MU != 32) return 0;
+  for (int k = 0; k < d; ++k)
+    if (m[k] != MU || n[k] != MU) return 0;
+  if (!aligned16_ptr(T) || !aligned16_ptr(S)) return 0;
+  for (int k = mu_lo - 1; k < mu_hi; ++k)
+    if (!aligned16_ptr(L[k])) return 0;
+  int64_t total = 1;
+  for (int k = 0; k < d; ++k) total *= MU;
+  if (total / MU >= (int64_t(1) << 31)) return 0;
+  return static_cast<int>(MU);
+}
+
+// One mode product on device buffers: T with extents m (d modes), op(L)
+// n_mu x m_mu given by (L, sLi, sLk, conj).
+static int mode_product_dev(mumode_handle_s* h, int d, const int64_t* m, int mu, int64_t n_mu,
+                            const double* T, const double* L, int64_t sLi, int64_t sLk,
+                            bool cplx, bool conj, double* S, bool accumulate = false,
+                            const ScatterParams* scat = nullptr, const double* div_front = nullptr,
+                            const double* div_last = nullptr) {
+  ModeJob j;
+  j.accumulate = accumulate;
+  j.scat = scat;
+  j.div_front = div_front;
+  j.div_last = div_last;
+  j.T = T;
+  j.L = L;
+  j.S = S;
+  j.A = prod(m, 0, mu - 1);
+  j.K = m[mu - 1];
+  j.C = prod(m, mu, d);
+  j.N = n_mu;
+  j.sLi = sLi;
+  j.sLk = sLk;
+  j.cplx = cplx;
+  j.conj = conj;
+  return run_job(h, j);
+}
+
+// ------------------------------------------------------------------ tucker chain
+// Modes 1..d in order (tucker.hpp:84-110). Lmat[mu] points at the stored
+// matrix; forward: op(L) = L (n x m, ld n); adjoint: op(L) = L^H (L is m x n).
+// Real adjoint and complex adjoint use the generic kernel's strided/conj
+// access, or a materialised op(L) when the TMA path applies.
+static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t* n,
+                      const double* T, const double* const* L, double* S, bool adjoint,
+                      bool cplx, int mu_lo = 1, int mu_hi = 0, const ScatterParams* scat = nullptr,
+                      const double* div_front = nullptr, const double* div_last = nullptr) {
+  if (mu_hi == 0) mu_hi = d;
+  const int el = cplx ? 2 : 1;
+  const int nmodes = mu_hi - mu_lo + 1;
+  if (scat) {
+    // the range's last mode scatters its (rows x cols) result to the ranks
+    // (fused exchange, csrc/slab_dist.cuh); the modes before it run as usual
+    if (adjoint) return fail(MUMODE_ERR_ARGUMENT, "scatter: forward chains only");
+    std::vector<int64_t> ext(m, m + d);
+    const double* src = T;
+    if (nmodes > 1) {
+      for (int k = mu_lo - 1; k < mu_hi - 1; ++k) ext[k] = n[k];
+      MM_TRY(h->scat_mid.ensure(size_t(prod(ext.data(), 0, d) * el) * sizeof(double)));
+      auto* mid = static_cast<double*>(h->scat_mid.p);
+      MM_TRY(tucker_dev(h, d, m, n, T, L, mid, false, cplx, mu_lo, mu_hi - 1));
+      src = mid;
+    }
+    return mode_product_dev(h, d, ext.data(), mu_hi, n[mu_hi - 1], src, L[mu_hi - 1], 1, n[mu_hi - 1], cplx,
+                            false, nullptr, false, scat);
+  }
+  // An odd real leading extent gives 8-byte strides, which TMA cannot
+  // describe (every stride is a multiple of the mode-1 extent). A whole
+  // chain then runs on a copy whose mode 1 is padded by one zero row (and
+  // mode-1 factor by a zero column / row): zero k-terms leave the FMA chains
+  // unchanged, the pad row of the output is dropped. Two copy passes buy the
+  // TMA/DMMA kernels for every mode.
+  if (!cplx && !adjoint && !div_front && mu_lo == 1 && mu_hi == d && d >= 2 && h->policy == 0 && ((m[0] | n[0]) & 1) &&
+      aligned16_ptr(T) && aligned16_ptr(S)) {
+    // measured (tools/odd_sweep.py): the padded chain wins from ~223^3 up
+    // (255^3: 26.5 -> 28.7 TF/s); below ~208 the LDG-staged kernel's smaller
+    // tiles quantise better
+    bool big = true;
+    for (int k = 0; k < d; ++k) big = big && m[k] >= 208 && n[k] >= 208;
+    const int64_t numel_in = prod(m, 0, d), numel_out = prod(n, 0, d);
+    if (big && std::max(numel_in, numel_out) >= (int64_t(1) << 20)) {
+      std::vector<int64_t> mp(m, m + d), np(n, n + d);
+      mp[0] += m[0] & 1;
+      np[0] += n[0] & 1;
+      const int64_t rest_in = numel_in / m[0], rest_out = numel_out / n[0];
+      const bool ok = (mp[0] == m[0] || h->pad_in.ensure(size_t(mp[0] * rest_in) * sizeof(double)) == MUMODE_OK) &&
+                      h->lpad.ensure(size_t(np[0] * mp[0]) * sizeof(double)) == MUMODE_OK &&
+                      (np[0] == n[0] || h->pad_out.ensure(size_t(np[0] * rest_out) * sizeof(double)) == MUMODE_OK);
+      if (ok) {
+        const double* Tp = T;
+        auto* Lp = static_cast<double*>(h->lpad.p);
+        double* Sp = np[0] == n[0] ? S : static_cast<double*>(h->pad_out.p);
+        if (mp[0] != m[0]) {
+          auto* Tpad = static_cast<double*>(h->pad_in.p);
+          pad2d_kernel<<<pad_grid(mp[0], rest_in, h->num_sms), 256, 0, h->stream>>>(T, m[0], rest_in, Tpad, mp[0],
+                                                                                    rest_in);
+          h->launches++;
+          Tp = Tpad;
+        }
+        pad2d_kernel<<<pad_grid(np[0], mp[0], h->num_sms), 256, 0, h->stream>>>(L[0], n[0], m[0], Lp, np[0], mp[0]);
+        MM_CUDA(cudaGetLastError());
+        h->launches++;
+        std::vector<const double*> Lpad(L, L + d);
+        Lpad[0] = Lp;
+        MM_TRY(tucker_dev(h, d, mp.data(), np.data(), Tp, Lpad.data(), Sp, false, false));
+        if (Sp != S) {
+          pad2d_kernel<<<pad_grid(n[0], rest_out, h->num_sms), 256, 0, h->stream>>>(Sp, np[0], rest_out, S, n[0],
+                                                                                 rest_out);
+          MM_CUDA(cudaGetLastError());
+          h->launches++;
+        }
+        return MUMODE_OK;
+      }
+      g_err.clear();  // not enough memory for the padded copies: run unpadded
+    }
+  }
+  // workspace: largest intermediate
+  std::vector<int64_t> ext(m, m + d);
+  size_t maxel = 0;
+  for (int mu = mu_lo - 1; mu < mu_hi - 1; ++mu) {
+    ext[mu] = n[mu];
+    maxel = std::max(maxel, size_t(prod(ext.data(), 0, d)));
+  }
+  if (nmodes > 1) {
+    MM_TRY(h->ws[0].ensure(maxel * el * sizeof(double)));
+    if (nmodes > 2) MM_TRY(h->ws[1].ensure(maxel * el * sizeof(double)));
+  }
+  // materialise op(L) = L^T / L^H when adjoint (tiny: n x m per mode)
+  std::vector<const double*> Lop(d);
+  if (adjoint) {
+    size_t tot = 0;
+    for (int mu = mu_lo - 1; mu < mu_hi; ++mu) tot += size_t(m[mu] * n[mu]) * el + 2;
+    MM_TRY(h->lbuf.ensure(tot * sizeof(double) + 256));
+    double* dst = static_cast<double*>(h->lbuf.p);
+    for (int mu = mu_lo - 1; mu < mu_hi; ++mu) {
+      const int64_t rows = m[mu], cols = n[mu];  // stored L is m x n
+      transpose_conj_kernel<<<grid_for(rows * cols, h->num_sms), 256, 0, h->stream>>>(
+          L[mu], dst, rows, cols, cplx ? 1 : 0, 1);
+      MM_CUDA(cudaGetLastError());
+      h->launches++;
+      Lop[mu] = dst;
+      dst += ((rows * cols * el + 1) / 2) * 2;  // keep 16-B alignment
+    }
+  } else {
+    for (int mu = 0; mu < d; ++mu) Lop[mu] = L[mu];
+  }
+  ext.assign(m, m + d);
+  const double* src = T;
+  const int MU = fused_extent(d, m, n, cplx, adjoint, h->policy, mu_lo, mu_hi, T, S, L);
+  if (MU) {
+    // pairs (mu, mu+1) as fused passes; an odd last mode runs alone below
+    int pass = 0, mu = mu_lo;
+    for (; mu + 1 <= mu_hi; mu += 2, ++pass) {
+      double* dst = (mu + 1 == mu_hi) ? S : static_cast<double*>(h->ws[pass % 2].p);
+      const int64_t A = prod(ext.data(), 0, mu - 1), C = prod(ext.data(), mu + 1, d);
+      int rc;
+      switch (MU) {
+        case 8: rc = launch_fused_mu<8>(h, mu == 1, src, dst, L[mu - 1], L[mu], A, C); break;
+        case 16: rc = launch_fused_mu<16>(h, mu == 1, src, dst, L[mu - 1], L[mu], A, C); break;
+        case 24: rc = launch_fused_mu<24>(h, mu == 1, src, dst, L[mu - 1], L[mu], A, C); break;
+        default: rc = launch_fused_mu<32>(h, mu == 1, src, dst, L[mu - 1], L[mu], A, C); break;
+      }
+      MM_TRY(rc);
+      src = dst;
+    }
+    if (mu == mu_hi) {
+      MM_TRY(mode_product_dev(h, d, ext.data(), mu, n[mu - 1], src, L[mu - 1], 1, n[mu - 1], false, false, S,
+                              false, nullptr, div_front, div_last));
+    } else if (div_front) {  // the last pass was a fused pair: divide in a pass of its own
+      const int64_t A = prod(n, 0, d - 1), N = n[d - 1];
+      const int gx = static_cast<int>(std::min<int64_t>((A + 255) / 256, 64));
+      const int gy = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(N, int64_t(h->num_sms) * 16 / gx)));
+      eigsum_divide_kernel<<<dim3(gx, gy), 256, 0, h->stream>>>(S, div_front, div_last, A, N);
+      MM_CUDA(cudaGetLastError());
+      h->launches++;
+    }
+    return MUMODE_OK;
+  }
+  for (int mu = mu_lo; mu <= mu_hi; ++mu) {
+    double* dst = (mu == mu_hi) ? S : static_cast<double*>(h->ws[(mu - mu_lo) % 2].p);
+    const bool last = (mu == mu_hi);
+    MM_TRY(mode_product_dev(h, d, ext.data(), mu, n[mu - 1], src, Lop[mu - 1], 1, n[mu - 1],
+                            cplx, false, dst, false, nullptr, last ? div_front : nullptr,
+                            last ? div_last : nullptr));
+    ext[mu - 1] = n[mu - 1];
+    src = dst;
+  }
+  return MUMODE_OK;
+}
+
+// [a, a + na) and [b, b + nb) (doubles) overlap?
+static bool overlaps(const double* a, int64_t na, const double* b, int64_t nb) {
+  return a < b + nb && b < a + na;
+}
+
+static int check_no_alias(const double* T, int64_t nt, const double* S, int64_t ns, const char* who) {
+  if (overlaps(T, nt, S, ns))
+    return fail(MUMODE_ERR_ARGUMENT, std::string(who) + ": output overlaps the input (results are new tensors)");
+  return MUMODE_OK;
+}
+
+static int check_stack(int d, const int64_t* m, const int64_t* n, const double* T,
+                       const double* const* L, const void* S, const char* who) {
+  MM_TRY(check_shape(d, m, who));
+  if (!T || !L || !S || !n) return fail(MUMODE_ERR_ARGUMENT, std::string(who) + ": null pointer");
+  for (int k = 0; k < d; ++k) {
+    if (n[k] < 1) return fail(MUMODE_ERR_ARGUMENT, "matrix dimensions must be positive");
+    if (!L[k])
+      return fail(MUMODE_ERR_ARGUMENT,
+                  std::string(who) + ": null matrix for mode " + std::to_string(k + 1));
+  }
+  return MUMODE_OK;
+}
+
+}  // namespace mumode_gpu

@@ -342,663 +342,11 @@ static int64_t prod(const int64_t* m, int lo, int hi) {
   return p;
 }
 
-// ------------------------------------------------------------------ one product
-// S(a, i, c) = sum_k op(L)(i, k) T(a, k, c); op(L)(i,k) = L[i*sLi + k*sLk].
-struct ModeJob {
-  const double* T;
-  const double* L;
-  double* S;
-  int64_t A, K, N, C;
-  int64_t sLi, sLk;
-  bool cplx;
-  bool conj;
-  bool accumulate = false;  // S += T x_mu op(L)
-  const ScatterParams* scat = nullptr;  // device table: scatter the (rows x C) result to ranks (S unused)
-  const double* div_front = nullptr;    // last mode: S(a, n) /= (div_front[a] + div_last[n])
-  const double* div_last = nullptr;
-};
-
-// Compiled tile configurations (BM, BN, BK, stages, warps along M, along N).
-using CfgBig = TmaCfg<128, 128, 16, 4, 4, 4>;  // 16 MMA warps, 32x32 warp tiles (C2-class shapes)
-using CfgTM = TmaCfg<128, 40, 40, 3, 16, 1>;   // T-side M, small L-side N (n = 40k)
-using CfgLM = TmaCfg<40, 128, 40, 3, 1, 16>;   // small L-side M, T-side N (mode 1, n = 40k)
-using CfgMid = TmaCfg<64, 128, 32, 4, 2, 4>;   // 32x32 warp tiles
-// complex128 (E = 2): 4 real DMMAs per complex MAC, 16-B elements
-using CfgCa = TmaCfg<64, 128, 16, 4, 4, 4, 2>;  // 16 MMA warps, 16x32 complex warp tiles
-using CfgCb = TmaCfg<128, 64, 16, 4, 4, 4, 2>;
-using CfgCc = TmaCfg<96, 32, 16, 4, 4, 4, 2>;   // 24x8 warp tiles, fine-grained
-using CfgCd = TmaCfg<192, 16, 16, 4, 8, 1, 2>;
-
-static bool aligned16(const void* p) { return aligned16_ptr(p); }
-
-// Can the TMA/DMMA kernel describe this job? (16-byte strides and bases,
-// forward layout of L, real, even M, sizes within int32 coordinates.)
-static bool tma_ok(const ModeJob& j) {
-  if (j.conj) return false;
-  if (j.cplx) {  // 16-byte elements: every stride is 16-B aligned
-    if (j.sLi != 1 || !aligned16(j.T) || !aligned16(j.L) || !aligned16(j.S)) return false;
-    const int64_t lim = int64_t(1) << 30;
-    return j.N < lim && j.K < lim && j.C < lim && j.A < lim && (j.A + 7) / 8 * j.C < lim;
-  }
-  if (j.sLi != 1) return false;  // L must be used forward: op(L) = L, ld = N
-  if (!aligned16(j.T) || !aligned16(j.L) || !aligned16(j.S)) return false;
-  if (j.sLk % 2) return false;
-  const int64_t lim = int64_t(1) << 31;
-  if (j.N >= lim || j.K >= lim || j.C >= lim || j.A >= lim) return false;
-  if (j.A == 1) {  // mode 1: M = N_out, Q = T (K x C)
-    if (j.N % 2 || j.K % 2) return false;
-  } else {
-    if (j.A % 2) return false;
-    if ((j.A + 7) / 8 * j.C >= lim) return false;
-  }
-  return true;
-}
-
-static bool tma_worthwhile(const ModeJob& j) {
-  const int64_t M = (j.A == 1) ? j.N : j.A;
-  return M >= 16 && j.K >= 16 && ((j.A == 1) ? j.C : j.N) >= 16;
-}
-
-struct TileChoice {
-  int cfg;  // 0 Big, 1 TM, 2 LM, 3 Mid
-  double cost;
-};
-
-// Wave-quantised padded work: waves * (BM * BN * K_padded) / efficiency.
-template <class Cfg>
-static double tile_cost(int64_t mfrags, int64_t N, int64_t K, int sms, double eff) {
-  const int64_t mt = (mfrags + Cfg::BM / 8 - 1) / (Cfg::BM / 8);
-  const int64_t nt = (N + Cfg::BN - 1) / Cfg::BN;
-  const int64_t tiles = mt * nt;
-  const int64_t waves = (tiles + sms - 1) / sms;
-  const int64_t kp = (K + Cfg::BK - 1) / Cfg::BK * Cfg::BK;
-  return double(waves) * double(Cfg::BM) * double(Cfg::BN) * double(kp) / eff;
-}
-
-static int choose_cfg(const ModeJob& j, int sms) {
-  const bool mode1 = (j.A == 1);
-  const int64_t mfrags = mode1 ? (j.N + 7) / 8 : (j.A + 7) / 8 * j.C;
-  const int64_t N = mode1 ? j.C : j.N;
-  if (j.cplx) {
-    const double c[4] = {tile_cost<CfgCa>(mfrags, N, j.K, sms, 1.00),
-                         tile_cost<CfgCb>(mfrags, N, j.K, sms, 1.00),
-                         tile_cost<CfgCc>(mfrags, N, j.K, sms, 0.97),
-                         tile_cost<CfgCd>(mfrags, N, j.K, sms, 0.96)};
-    int best = 0;
-    for (int i = 1; i < 4; ++i)
-      if (c[i] < c[best]) best = i;
-    return 4 + best;
-  }
-  const double c0 = tile_cost<CfgBig>(mfrags, N, j.K, sms, 1.00);
-  const double c1 = tile_cost<CfgTM>(mfrags, N, j.K, sms, 0.96);
-  const double c2 = tile_cost<CfgLM>(mfrags, N, j.K, sms, 0.96);
-  const double c3 = tile_cost<CfgMid>(mfrags, N, j.K, sms, 0.97);
-  int best = 0;
-  double bc = c0;
-  if (c1 < bc) best = 1, bc = c1;
-  if (c2 < bc) best = 2, bc = c2;
-  if (c3 < bc) best = 3, bc = c3;
-  return best;
-}
-
-template <class Cfg>
-static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
-  const CUtensorMap* mp = nullptr;
-  const CUtensorMap* mq = nullptr;
-  TmaParams p{};
-  p.D = j.S;
-  const bool mode1 = (j.A == 1);
-  constexpr uint32_t BM8 = Cfg::BM / 8, BN8 = Cfg::BN / 8, BK8 = Cfg::BK / 8;
-  // all map dims/strides in doubles: e doubles per element, 8e per box row
-  constexpr uint64_t e = Cfg::E;
-  constexpr uint32_t box0 = 8 * Cfg::E;
-  constexpr bool sw = (Cfg::E == 2);
-  if (mode1) {
-    // P = L (n_out x K, ld = sLk), Q = T (K x C, K contiguous)
-    p.p_blocked = (j.N % 8 == 0);
-    if (p.p_blocked) {
-      uint64_t d[3] = {box0, uint64_t(j.K), uint64_t(j.N / 8)}, st[2] = {e * uint64_t(j.sLk), 8 * e};
-      uint32_t b[3] = {box0, Cfg::BK, BM8};
-      MM_TRY(get_map(h, j.L, 3, d, st, b, &mp, sw));
-    } else {
-      uint64_t d[2] = {e * uint64_t(j.N), uint64_t(j.K)}, st[1] = {e * uint64_t(j.sLk)};
-      uint32_t b[2] = {box0, Cfg::BK};
-      MM_TRY(get_map(h, j.L, 2, d, st, b, &mp, sw));
-    }
-    p.q_blocked = (j.K % 8 == 0);
-    if (p.q_blocked) {
-      uint64_t d[3] = {box0, uint64_t(j.C), uint64_t(j.K / 8)}, st[2] = {e * uint64_t(j.K), 8 * e};
-      uint32_t b[3] = {box0, Cfg::BN, BK8};
-      MM_TRY(get_map(h, j.T, 3, d, st, b, &mq, sw));
-    } else {
-      uint64_t d[2] = {e * uint64_t(j.K), uint64_t(j.C)}, st[1] = {e * uint64_t(j.K)};
-      uint32_t b[2] = {box0, Cfg::BN};
-      MM_TRY(get_map(h, j.T, 2, d, st, b, &mq, sw));
-    }
-    p.Mlim = int(j.N);
-    p.N = int(j.C);
-    p.ldD = j.N;
-    p.bstride = 0;
-    p.AB = int((j.N + 7) / 8);
-    p.mfrags = p.AB;
-  } else {
-    // P = T (A x K x C, A contiguous), Q = L (n_out x K, ld = sLk)
-    const int64_t AB = (j.A + 7) / 8;
-    p.p_blocked = (j.A % 8 == 0) && (AB % BM8 == 0);
-    if (p.p_blocked) {
-      uint64_t d[4] = {box0, uint64_t(j.K), uint64_t(AB), uint64_t(j.C)};
-      uint64_t st[3] = {e * uint64_t(j.A), 8 * e, e * uint64_t(j.A * j.K)};
-      uint32_t b[4] = {box0, Cfg::BK, BM8, 1};
-      MM_TRY(get_map(h, j.T, 4, d, st, b, &mp, sw));
-    } else {
-      uint64_t d[3] = {e * uint64_t(j.A), uint64_t(j.K), uint64_t(j.C)};
-      uint64_t st[2] = {e * uint64_t(j.A), e * uint64_t(j.A * j.K)};
-      uint32_t b[3] = {box0, Cfg::BK, 1};
-      MM_TRY(get_map(h, j.T, 3, d, st, b, &mp, sw));
-    }
-    p.q_blocked = (j.N % 8 == 0);
-    if (p.q_blocked) {
-      uint64_t d[3] = {box0, uint64_t(j.K), uint64_t(j.N / 8)}, st[2] = {e * uint64_t(j.sLk), 8 * e};
-      uint32_t b[3] = {box0, Cfg::BK, BN8};
-      MM_TRY(get_map(h, j.L, 3, d, st, b, &mq, sw));
-    } else {
-      uint64_t d[2] = {e * uint64_t(j.N), uint64_t(j.K)}, st[1] = {e * uint64_t(j.sLk)};
-      uint32_t b[2] = {box0, Cfg::BK};
-      MM_TRY(get_map(h, j.L, 2, d, st, b, &mq, sw));
-    }
-    p.Mlim = int(j.A);
-    p.N = int(j.N);
-    p.ldD = j.A;
-    p.bstride = j.A * j.N;
-    p.AB = int(AB);
-    p.mfrags = AB * j.C;
-  }
-  p.K = int(j.K);
-  p.mt = int((p.mfrags + Cfg::BM / 8 - 1) / (Cfg::BM / 8));
-  p.nt = (p.N + Cfg::BN - 1) / Cfg::BN;
-  p.tiles = int64_t(p.mt) * p.nt;
-  const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
-  p.scat = j.scat;
-  p.div_front = j.div_front;
-  p.div_last = j.div_last;
-  if (j.div_front) {
-    if constexpr (Cfg::E == 1) {
-      if (mode1 || j.C != 1) return fail(MUMODE_ERR_ARGUMENT, "divide epilogue: last mode of order >= 2 only");
-      auto k = modeprod_tma_kernel<Cfg, false, 3>;
-      MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
-      MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, *mq, p));
-    } else {
-      return fail(MUMODE_ERR_ARGUMENT, "divide epilogue is real-only");
-    }
-  } else if (j.scat) {
-    if constexpr (Cfg::E == 1) {
-      auto k = mode1 ? modeprod_tma_kernel<Cfg, true, 2> : modeprod_tma_kernel<Cfg, false, 2>;
-      MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
-      MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, *mq, p));
-    } else {
-      return fail(MUMODE_ERR_ARGUMENT, "scatter epilogue is real-only");
-    }
-  } else if (mode1) {
-    auto k = modeprod_tma_kernel<Cfg, true>;
-    MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
-    MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, *mq, p));
-  } else if (j.accumulate) {
-    if constexpr (Cfg::E == 1) {
-      auto k = modeprod_tma_kernel<Cfg, false, 1>;
-      MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
-      MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, *mq, p));
-    } else {
-      return fail(MUMODE_ERR_ARGUMENT, "accumulating complex mode product is not compiled");
-    }
-  } else {
-    auto k = modeprod_tma_kernel<Cfg, false>;
-    MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
-    MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, *mq, p));
-  }
-  MM_CUDA(cudaGetLastError());
-  h->launches++;
-  return MUMODE_OK;
-}
-
-static int launch_tma_auto(mumode_handle_s* h, const ModeJob& j) {
-  const int forced = (h->policy >= 3 && h->policy <= 6) ? h->policy - 3 : -1;
-  int cfg = choose_cfg(j, h->num_sms);
-  if (forced >= 0) cfg = j.cplx ? 4 + forced : forced;
-  switch (cfg) {
-    case 1: return launch_tma<CfgTM>(h, j);
-    case 2: return launch_tma<CfgLM>(h, j);
-    case 3: return launch_tma<CfgMid>(h, j);
-    case 4: return launch_tma<CfgCa>(h, j);
-    case 5: return launch_tma<CfgCb>(h, j);
-    case 6: return launch_tma<CfgCc>(h, j);
-    case 7: return launch_tma<CfgCd>(h, j);
-    default: return launch_tma<CfgBig>(h, j);
-  }
-}
-
-static int launch_generic(mumode_handle_s* h, const ModeJob& j) {
-  GenericArgs g{j.T, j.L, j.S, j.A, j.K, j.N, j.C, j.sLi, j.sLk, j.conj ? 1 : 0, j.accumulate ? 1 : 0};
-  const int64_t nfib = j.A * j.C;
-  dim3 grid(static_cast<unsigned>((nfib + kGenFibers - 1) / kGenFibers),
-            static_cast<unsigned>((j.N + kGenRows - 1) / kGenRows));
-  if (grid.y > 65535) return fail(MUMODE_ERR_SIZE, "mode product output extent too large");
-  if (j.cplx)
-    modeprod_generic_kernel<true><<<grid, kGenThreads, 0, h->stream>>>(g);
-  else
-    modeprod_generic_kernel<false><<<grid, kGenThreads, 0, h->stream>>>(g);
-  MM_CUDA(cudaGetLastError());
-  h->launches++;
-  return MUMODE_OK;
-}
-
-// LDG-staged DMMA kernel for real shapes the TMA path cannot describe.
-constexpr int kLdgBM = 64, kLdgBN = 64, kLdgBK = 16, kLdgWM = 2, kLdgWN = 2;
-
-static int launch_ldg(mumode_handle_s* h, const ModeJob& j) {
-  LdgArgs g{};
-  g.T = j.T;
-  g.L = j.L;
-  g.S = j.S;
-  g.A = j.A;
-  g.K = j.K;
-  g.N = j.N;
-  g.C = j.C;
-  g.sLi = j.sLi;
-  g.sLk = j.sLk;
-  g.accumulate = j.accumulate ? 1 : 0;
-  const bool mode1 = (j.A == 1);
-  if (mode1) {
-    g.Mlim = j.N;
-    g.ntot = j.C;
-    g.AB = int((j.N + 7) / 8);
-    g.mfrags = g.AB;
-  } else {
-    g.Mlim = j.A;
-    g.ntot = j.N;
-    g.AB = int((j.A + 7) / 8);
-    g.mfrags = int64_t(g.AB) * j.C;
-  }
-  g.mt = int((g.mfrags + kLdgBM / 8 - 1) / (kLdgBM / 8));
-  g.nt = int((g.ntot + kLdgBN - 1) / kLdgBN);
-  const int64_t tiles = int64_t(g.mt) * g.nt;
-  if (tiles >= (int64_t(1) << 31)) return fail(MUMODE_ERR_SIZE, "mode product too large for one launch");
-  constexpr int smem = 2 * (kLdgBM + kLdgBN) * kLdgBK * 8 + 1024;
-  if (mode1) {
-    auto k = modeprod_ldg_kernel<true, kLdgBM, kLdgBN, kLdgBK, kLdgWM, kLdgWN>;
-    MM_TRY(smem_opt_in(k, smem));
-    k<<<static_cast<unsigned>(tiles), kLdgWM * kLdgWN * 32, smem, h->stream>>>(g);
-  } else {
-    auto k = modeprod_ldg_kernel<false, kLdgBM, kLdgBN, kLdgBK, kLdgWM, kLdgWN>;
-    MM_TRY(smem_opt_in(k, smem));
-    k<<<static_cast<unsigned>(tiles), kLdgWM * kLdgWN * 32, smem, h->stream>>>(g);
-  }
-  MM_CUDA(cudaGetLastError());
-  h->launches++;
-  return MUMODE_OK;
-}
-
-static bool ldg_worthwhile(const ModeJob& j) {
-  const int64_t M = (j.A == 1) ? j.N : j.A;
-  return M >= 16 && j.K >= 8 && ((j.A == 1) ? j.C : j.N) >= 16;
-}
-
-static int run_job(mumode_handle_s* h, const ModeJob& j0) {
-  ModeJob j = j0;
-  // A real mu > 1 product whose factor has an odd leading dimension (odd n_mu)
-  // is TMA-describable once the factor is re-laid with ld = n_mu + 1 (a tiny
-  // copy; the tensor strides are what they are).
-  if (!j.cplx && !j.conj && j.A != 1 && j.sLi == 1 && (j.sLk & 1) && h->policy != 1 && h->policy != 8) {
-    ModeJob jp = j;
-    jp.sLk = j.sLk + 1;
-    jp.L = reinterpret_cast<const double*>(uintptr_t(256));  // the staged copy is 256-B aligned
-    if (tma_ok(jp) && tma_worthwhile(jp)) {
-      MM_TRY(h->lstage.ensure(size_t(jp.sLk * j.K) * sizeof(double)));
-      auto* Lp = static_cast<double*>(h->lstage.p);
-      pad2d_kernel<<<pad_grid(jp.sLk, j.K, h->num_sms), 256, 0, h->stream>>>(j.L, j.sLk, j.K, Lp, jp.sLk, j.K);
-      MM_CUDA(cudaGetLastError());
-      h->launches++;
-      jp.L = Lp;
-      j = jp;
-    }
-  }
-  if (j.div_front) {
-    // the direct solver's division in the last mode's epilogue, else a pass
-    if (!j.cplx && !j.accumulate && j.A > 1 && j.C == 1 && tma_ok(j) && h->policy != 1 && h->policy != 8 &&
-        (h->policy >= 2 || tma_worthwhile(j)))
-      return launch_tma_auto(h, j);
-    ModeJob jt = j;
-    jt.div_front = jt.div_last = nullptr;
-    MM_TRY(run_job(h, jt));
-    const int64_t A = j.A, N = j.N;
-    const int gx = static_cast<int>(std::min<int64_t>((A + 255) / 256, 64));
-    const int gy = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(N, int64_t(h->num_sms) * 16 / gx)));
-    eigsum_divide_kernel<<<dim3(gx, gy), 256, 0, h->stream>>>(j.S, j.div_front, j.div_last, A, N);
-    MM_CUDA(cudaGetLastError());
-    h->launches++;
-    return MUMODE_OK;
-  }
-  if (j.scat) {
-    // fused exchange: the TMA kernel's epilogue scatters to the ranks; any
-    // other path computes the (rows x C) result and scatter-copies it
-    if (!j.cplx && !j.accumulate && tma_ok(j) && h->policy != 1 && h->policy != 8 &&
-        (h->policy >= 2 || tma_worthwhile(j)))
-      return launch_tma_auto(h, j);
-    ModeJob jt = j;
-    jt.scat = nullptr;
-    const int64_t rows = (j.A == 1) ? j.N : j.A * j.N, cols = (j.A == 1) ? j.C : j.C;
-    MM_TRY(h->scat_tmp.ensure(size_t(rows * cols * (j.cplx ? 2 : 1)) * sizeof(double)));
-    jt.S = static_cast<double*>(h->scat_tmp.p);
-    MM_TRY(run_job(h, jt));
-    if (j.cplx) return fail(MUMODE_ERR_ARGUMENT, "scatter of complex products is not supported");
-    const unsigned gy = static_cast<unsigned>(std::min<int64_t>(8, (rows + 255) / 256));
-    scatter_copy_kernel<<<dim3(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cols * 64, int64_t(h->num_sms) * 8))), gy),
-                          256, 0, h->stream>>>(static_cast<const double*>(h->scat_tmp.p), rows, cols, j.scat);
-    MM_CUDA(cudaGetLastError());
-    h->launches++;
-    return MUMODE_OK;
-  }
-  // accumulating products: real mu > 1 have a TMA instantiation; others generic
-  const bool can_tma = tma_ok(j) && !(j.accumulate && (j.A == 1 || j.cplx));
-  if (h->policy == 8 && !j.cplx) return launch_ldg(h, j);
-  if (h->policy == 1) return launch_generic(h, j);
-  if (!can_tma) return (!j.cplx && ldg_worthwhile(j)) ? launch_ldg(h, j) : launch_generic(h, j);
-  if ((h->policy >= 2 && h->policy <= 6) || tma_worthwhile(j)) return launch_tma_auto(h, j);
-  return launch_generic(h, j);
-}
-
-// ------------------------------------------------------------------ fused pairs
-template <int MU, bool FIRST, int RA>
-static int launch_fused(mumode_handle_s* h, const double* T, double* S, const double* L1,
-                        const double* L2, int64_t A, int64_t C) {
-  using Cfg = FusedCfg<MU, FIRST, RA>;
-  const CUtensorMap* mp = nullptr;
-  FusedParams p{S, L1, L2, A, C, 0};
-  if (FIRST) {
-    uint64_t d[3] = {8, uint64_t(MU) * uint64_t(C), uint64_t(MU / 8)}, st[2] = {uint64_t(MU), 8};
-    uint32_t b[3] = {8, 8 * MU, MU / 8};
-    MM_TRY(get_map(h, T, 3, d, st, b, &mp));
-    p.tiles = (C + 7) / 8;
-  } else {
-    uint64_t d[4] = {uint64_t(A), uint64_t(MU), uint64_t(MU), uint64_t(C)};
-    uint64_t st[3] = {uint64_t(A), uint64_t(A) * MU, uint64_t(A) * MU * MU};
-    uint32_t b[4] = {8, MU, MU, 1};
-    MM_TRY(get_map(h, T, 4, d, st, b, &mp));
-    p.tiles = (A / RA) * C;
-  }
-  const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
-  auto k = fused_pair_kernel<MU, FIRST, RA>;
-  MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
-  MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, p));
-  MM_CUDA(cudaGetLastError());
-  h->launches++;
-  return MUMODE_OK;
-}
-
-// Strided-pair pass with 32-wide a tiles (tail.cuh): 256-B rows for loads and
-// stores instead of 64-B ones.
-template <int MU>
-static int launch_tail(mumode_handle_s* h, const double* T, double* S, const double* L1,
-                       const double* L2, int64_t A, int64_t C) {
-  using Cfg = TailCfg<MU>;
-  const CUtensorMap *mx = nullptr, *ms = nullptr;
-  uint64_t d[5] = {16, uint64_t(A / 16), uint64_t(MU), uint64_t(MU), uint64_t(C)};
-  uint64_t st[4] = {16, uint64_t(A), uint64_t(A) * MU, uint64_t(A) * MU * MU};
-  uint32_t bx[5] = {16, 2, MU, Cfg::KB, 1}, bs[5] = {16, 2, 1, MU, 1};
-  MM_TRY(get_map(h, T, 5, d, st, bx, &mx, true));
-  MM_TRY(get_map(h, S, 5, d, st, bs, &ms, true));
-  TailParams p{L1, L2, A / 32, (A / 32) * C};
-  const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
-  auto k = tail_pair_kernel<MU>;
-  MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
-  MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mx, *ms, p));
-  MM_CUDA(cudaGetLastError());
-  h->launches++;
-  return MUMODE_OK;
-}
-
-// The tail kernel pays off once the a-stride makes every tile row a new page
-// (policy 9 forces it wherever the shape allows, 10 disables it).
-static constexpr int64_t kTailMinA = 16384;
-
-template <int MU>
-static int launch_fused_mu(mumode_handle_s* h, bool first, const double* T, double* S,
-                           const double* L1, const double* L2, int64_t A, int64_t C) {
-  if (first) return launch_fused<MU, true, 8>(h, T, S, L1, L2, A, C);
-  if constexpr (MU <= 24) {
-    if (A % 32 == 0 && h->policy != 10 && (h->policy == 9 || A >= kTailMinA))
-      return launch_tail<MU>(h, T, S, L1, L2, A, C);
-  }
-  // 16 a's per tile when shared memory allows it and A tiles evenly
-  constexpr bool wide_fits = FusedCfg<MU, false, 16>::SMEM_BYTES <= 227 * 1024 &&
-                             FusedCfg<MU, false, 16>::NBUF >= 2;
-  if (wide_fits && A % 16 == 0 && A <= 4096) return launch_fused<MU, false, (wide_fits ? 16 : 8)>(h, T, S, L1, L2, A, C);
-  return launch_fused<MU, false, 8>(h, T, S, L1, L2, A, C);
-}
-
-// Fused two-mode passes apply to real, forward chains whose modes are all
-// square with one small extent MU in {8, 16, 24, 32} (e.g. config C5, 24^6):
-// there each single product is HBM-bound and pairing halves the HBM passes.
-static int fused_extent(int d, const int64_t* m, const int64_t* n, bool cplx, bool adjoint,
-                        int policy, int mu_lo, int mu_hi, const double* T, const double* S,
-                        const double* const* L) {
-  if (cplx || adjoint || !(policy == 0 || policy == 7 || policy == 9 || policy == 10) || mu_hi - mu_lo < 1)
-    return 0;
-  const int64_t MU = m[0];
-  if (MU != 8 && MU != 16 && MU != 24 && MU != 32) return 0;
-  for (int k = 0; k < d; ++k)
-    if (m[k] != MU || n[k] != MU) return 0;
-  if (!aligned16_ptr(T) || !aligned16_ptr(S)) return 0;
-  for (int k = mu_lo - 1; k < mu_hi; ++k)
-    if (!aligned16_ptr(L[k])) return 0;
-  int64_t total = 1;
-  for (int k = 0; k < d; ++k) total *= MU;
-  if (total / MU >= (int64_t(1) << 31)) return 0;
-  return static_cast<int>(MU);
-}
-
-// One mode product on device buffers: T with extents m (d modes), op(L)
-// n_mu x m_mu given by (L, sLi, sLk, conj).
-static int mode_product_dev(mumode_handle_s* h, int d, const int64_t* m, int mu, int64_t n_mu,
-                            const double* T, const double* L, int64_t sLi, int64_t sLk,
-                            bool cplx, bool conj, double* S, bool accumulate = false,
-                            const ScatterParams* scat = nullptr, const double* div_front = nullptr,
-                            const double* div_last = nullptr) {
-  ModeJob j;
-  j.accumulate = accumulate;
-  j.scat = scat;
-  j.div_front = div_front;
-  j.div_last = div_last;
-  j.T = T;
-  j.L = L;
-  j.S = S;
-  j.A = prod(m, 0, mu - 1);
-  j.K = m[mu - 1];
-  j.C = prod(m, mu, d);
-  j.N = n_mu;
-  j.sLi = sLi;
-  j.sLk = sLk;
-  j.cplx = cplx;
-  j.conj = conj;
-  return run_job(h, j);
-}
-
-// ------------------------------------------------------------------ tucker chain
-// Modes 1..d in order (tucker.hpp:84-110). Lmat[mu] points at the stored
-// matrix; forward: op(L) = L (n x m, ld n); adjoint: op(L) = L^H (L is m x n).
-// Real adjoint and complex adjoint use the generic kernel's strided/conj
-// access, or a materialised op(L) when the TMA path applies.
-static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t* n,
-                      const double* T, const double* const* L, double* S, bool adjoint,
-                      bool cplx, int mu_lo = 1, int mu_hi = 0, const ScatterParams* scat = nullptr,
-                      const double* div_front = nullptr, const double* div_last = nullptr) {
-  if (mu_hi == 0) mu_hi = d;
-  const int el = cplx ? 2 : 1;
-  const int nmodes = mu_hi - mu_lo + 1;
-  if (scat) {
-    // the range's last mode scatters its (rows x cols) result to the ranks
-    // (fused exchange, csrc/slab_dist.cuh); the modes before it run as usual
-    if (adjoint) return fail(MUMODE_ERR_ARGUMENT, "scatter: forward chains only");
-    std::vector<int64_t> ext(m, m + d);
-    const double* src = T;
-    if (nmodes > 1) {
-      for (int k = mu_lo - 1; k < mu_hi - 1; ++k) ext[k] = n[k];
-      MM_TRY(h->scat_mid.ensure(size_t(prod(ext.data(), 0, d) * el) * sizeof(double)));
-      auto* mid = static_cast<double*>(h->scat_mid.p);
-      MM_TRY(tucker_dev(h, d, m, n, T, L, mid, false, cplx, mu_lo, mu_hi - 1));
-      src = mid;
-    }
-    return mode_product_dev(h, d, ext.data(), mu_hi, n[mu_hi - 1], src, L[mu_hi - 1], 1, n[mu_hi - 1], cplx,
-                            false, nullptr, false, scat);
-  }
-  // An odd real leading extent gives 8-byte strides, which TMA cannot
-  // describe (every stride is a multiple of the mode-1 extent). A whole
-  // chain then runs on a copy whose mode 1 is padded by one zero row (and
-  // mode-1 factor by a zero column / row): zero k-terms leave the FMA chains
-  // unchanged, the pad row of the output is dropped. Two copy passes buy the
-  // TMA/DMMA kernels for every mode.
-  if (!cplx && !adjoint && !div_front && mu_lo == 1 && mu_hi == d && d >= 2 && h->policy == 0 && ((m[0] | n[0]) & 1) &&
-      aligned16_ptr(T) && aligned16_ptr(S)) {
-    // measured (tools/odd_sweep.py): the padded chain wins from ~223^3 up
-    // (255^3: 26.5 -> 28.7 TF/s); below ~208 the LDG-staged kernel's smaller
-    // tiles quantise better
-    bool big = true;
-    for (int k = 0; k < d; ++k) big = big && m[k] >= 208 && n[k] >= 208;
-    const int64_t numel_in = prod(m, 0, d), numel_out = prod(n, 0, d);
-    if (big && std::max(numel_in, numel_out) >= (int64_t(1) << 20)) {
-      std::vector<int64_t> mp(m, m + d), np(n, n + d);
-      mp[0] += m[0] & 1;
-      np[0] += n[0] & 1;
-      const int64_t rest_in = numel_in / m[0], rest_out = numel_out / n[0];
-      const bool ok = (mp[0] == m[0] || h->pad_in.ensure(size_t(mp[0] * rest_in) * sizeof(double)) == MUMODE_OK) &&
-                      h->lpad.ensure(size_t(np[0] * mp[0]) * sizeof(double)) == MUMODE_OK &&
-                      (np[0] == n[0] || h->pad_out.ensure(size_t(np[0] * rest_out) * sizeof(double)) == MUMODE_OK);
-      if (ok) {
-        const double* Tp = T;
-        auto* Lp = static_cast<double*>(h->lpad.p);
-        double* Sp = np[0] == n[0] ? S : static_cast<double*>(h->pad_out.p);
-        if (mp[0] != m[0]) {
-          auto* Tpad = static_cast<double*>(h->pad_in.p);
-          pad2d_kernel<<<pad_grid(mp[0], rest_in, h->num_sms), 256, 0, h->stream>>>(T, m[0], rest_in, Tpad, mp[0],
-                                                                                    rest_in);
-          h->launches++;
-          Tp = Tpad;
-        }
-        pad2d_kernel<<<pad_grid(np[0], mp[0], h->num_sms), 256, 0, h->stream>>>(L[0], n[0], m[0], Lp, np[0], mp[0]);
-        MM_CUDA(cudaGetLastError());
-        h->launches++;
-        std::vector<const double*> Lpad(L, L + d);
-        Lpad[0] = Lp;
-        MM_TRY(tucker_dev(h, d, mp.data(), np.data(), Tp, Lpad.data(), Sp, false, false));
-        if (Sp != S) {
-          pad2d_kernel<<<pad_grid(n[0], rest_out, h->num_sms), 256, 0, h->stream>>>(Sp, np[0], rest_out, S, n[0],
-                                                                                 rest_out);
-          MM_CUDA(cudaGetLastError());
-          h->launches++;
-        }
-        return MUMODE_OK;
-      }
-      g_err.clear();  // not enough memory for the padded copies: run unpadded
-    }
-  }
-  // workspace: largest intermediate
-  std::vector<int64_t> ext(m, m + d);
-  size_t maxel = 0;
-  for (int mu = mu_lo - 1; mu < mu_hi - 1; ++mu) {
-    ext[mu] = n[mu];
-    maxel = std::max(maxel, size_t(prod(ext.data(), 0, d)));
-  }
-  if (nmodes > 1) {
-    MM_TRY(h->ws[0].ensure(maxel * el * sizeof(double)));
-    if (nmodes > 2) MM_TRY(h->ws[1].ensure(maxel * el * sizeof(double)));
-  }
-  // materialise op(L) = L^T / L^H when adjoint (tiny: n x m per mode)
-  std::vector<const double*> Lop(d);
-  if (adjoint) {
-    size_t tot = 0;
-    for (int mu = mu_lo - 1; mu < mu_hi; ++mu) tot += size_t(m[mu] * n[mu]) * el + 2;
-    MM_TRY(h->lbuf.ensure(tot * sizeof(double) + 256));
-    double* dst = static_cast<double*>(h->lbuf.p);
-    for (int mu = mu_lo - 1; mu < mu_hi; ++mu) {
-      const int64_t rows = m[mu], cols = n[mu];  // stored L is m x n
-      transpose_conj_kernel<<<grid_for(rows * cols, h->num_sms), 256, 0, h->stream>>>(
-          L[mu], dst, rows, cols, cplx ? 1 : 0, 1);
-      MM_CUDA(cudaGetLastError());
-      h->launches++;
-      Lop[mu] = dst;
-      dst += ((rows * cols * el + 1) / 2) * 2;  // keep 16-B alignment
-    }
-  } else {
-    for (int mu = 0; mu < d; ++mu) Lop[mu] = L[mu];
-  }
-  ext.assign(m, m + d);
-  const double* src = T;
-  const int MU = fused_extent(d, m, n, cplx, adjoint, h->policy, mu_lo, mu_hi, T, S, L);
-  if (MU) {
-    // pairs (mu, mu+1) as fused passes; an odd last mode runs alone below
-    int pass = 0, mu = mu_lo;
-    for (; mu + 1 <= mu_hi; mu += 2, ++pass) {
-      double* dst = (mu + 1 == mu_hi) ? S : static_cast<double*>(h->ws[pass % 2].p);
-      const int64_t A = prod(ext.data(), 0, mu - 1), C = prod(ext.data(), mu + 1, d);
-      int rc;
-      switch (MU) {
-        case 8: rc = launch_fused_mu<8>(h, mu == 1, src, dst, L[mu - 1], L[mu], A, C); break;
-        case 16: rc = launch_fused_mu<16>(h, mu == 1, src, dst, L[mu - 1], L[mu], A, C); break;
-        case 24: rc = launch_fused_mu<24>(h, mu == 1, src, dst, L[mu - 1], L[mu], A, C); break;
-        default: rc = launch_fused_mu<32>(h, mu == 1, src, dst, L[mu - 1], L[mu], A, C); break;
-      }
-      MM_TRY(rc);
-      src = dst;
-    }
-    if (mu == mu_hi) {
-      MM_TRY(mode_product_dev(h, d, ext.data(), mu, n[mu - 1], src, L[mu - 1], 1, n[mu - 1], false, false, S,
-                              false, nullptr, div_front, div_last));
-    } else if (div_front) {  // the last pass was a fused pair: divide in a pass of its own
-      const int64_t A = prod(n, 0, d - 1), N = n[d - 1];
-      const int gx = static_cast<int>(std::min<int64_t>((A + 255) / 256, 64));
-      const int gy = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(N, int64_t(h->num_sms) * 16 / gx)));
-      eigsum_divide_kernel<<<dim3(gx, gy), 256, 0, h->stream>>>(S, div_front, div_last, A, N);
-      MM_CUDA(cudaGetLastError());
-      h->launches++;
-    }
-    return MUMODE_OK;
-  }
-  for (int mu = mu_lo; mu <= mu_hi; ++mu) {
-    double* dst = (mu == mu_hi) ? S : static_cast<double*>(h->ws[(mu - mu_lo) % 2].p);
-    const bool last = (mu == mu_hi);
-    MM_TRY(mode_product_dev(h, d, ext.data(), mu, n[mu - 1], src, Lop[mu - 1], 1, n[mu - 1],
-                            cplx, false, dst, false, nullptr, last ? div_front : nullptr,
-                            last ? div_last : nullptr));
-    ext[mu - 1] = n[mu - 1];
-    src = dst;
-  }
-  return MUMODE_OK;
-}
-
-// [a, a + na) and [b, b + nb) (doubles) overlap?
-static bool overlaps(const double* a, int64_t na, const double* b, int64_t nb) {
-  return a < b + nb && b < a + na;
-}
-
-static int check_no_alias(const double* T, int64_t nt, const double* S, int64_t ns, const char* who) {
-  if (overlaps(T, nt, S, ns))
-    return fail(MUMODE_ERR_ARGUMENT, std::string(who) + ": output overlaps the input (results are new tensors)");
-  return MUMODE_OK;
-}
-
-static int check_stack(int d, const int64_t* m, const int64_t* n, const double* T,
-                       const double* const* L, const void* S, const char* who) {
-  MM_TRY(check_shape(d, m, who));
-  if (!T || !L || !S || !n) return fail(MUMODE_ERR_ARGUMENT, std::string(who) + ": null pointer");
-  for (int k = 0; k < d; ++k) {
-    if (n[k] < 1) return fail(MUMODE_ERR_ARGUMENT, "matrix dimensions must be positive");
-    if (!L[k])
-      return fail(MUMODE_ERR_ARGUMENT,
-                  std::string(who) + ": null matrix for mode " + std::to_string(k + 1));
-  }
-  return MUMODE_OK;
-}
-
 }  // namespace mumode_gpu
+
+#include "dispatch.cuh"
+#include "chain.cuh"
+
 
 using namespace mumode_gpu;
 
