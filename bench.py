@@ -454,6 +454,9 @@ def run_distributed(args, world, rank, local):
     t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_value = plan.flops() * args.steps / float(t[0]) / 1e9
+    extras = {}
+    if not args.py_dist and not args.no_extras:
+        extras["C5_6d_24_slab"] = dist_c5(args, world, rank, dev, comm, stream, flush)
     if not args.py_dist:
         comm.close()
     if rank != 0:
@@ -480,7 +483,47 @@ def run_distributed(args, world, rank, local):
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }
+    if extras:
+        line["extras"] = extras
     print(json.dumps(line), flush=True)
+
+
+def dist_c5(args, world, rank, dev, comm, stream, flush):
+    """BASELINE configs[4]: the 6-D 24^6 Tucker slab-partitioned over the last
+    mode across the ranks (24/P columns each), through the same C-ABI path
+    (fused local passes, exchange, last mode). Device-generated synthetic
+    slab (no parity check here; tests cover the path)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2112_11238_b200 as mm
+    from paper_2112_11238_b200.dist import SlabPlan, dist_tucker
+    m = (24,) * 6
+    plan = SlabPlan(m, m, world)
+    gen = torch.Generator(device=dev).manual_seed(SEED + rank)
+    T_r = torch.empty((24,) * 5 + (plan.c_sizes[rank],), dtype=torch.float64, device=dev)
+    T_r = mm.to_colmajor(torch.randn(T_r.shape, dtype=torch.float64, device=dev, generator=gen))
+    g = torch.Generator(device=dev).manual_seed(SEED)
+    Ls = [mm.to_colmajor(torch.randn(24, 24, dtype=torch.float64, device=dev, generator=g)) for _ in range(6)]
+    out = torch.empty(plan.a_sizes[rank] * 24, dtype=torch.float64, device=dev)
+    steps = max(3, min(args.steps, 10))
+    for _ in range(3):
+        dist_tucker(comm, T_r, Ls, m, chunks=args.chunks, out=out)
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
+    dist.barrier()
+    for e0, e1 in ev:
+        flush.fill_(1.0)
+        e0.record(stream)
+        dist_tucker(comm, T_r, Ls, m, chunks=args.chunks, out=out)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    ms = sum(e0.elapsed_time(e1) for e0, e1 in ev) / steps
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    return {"ms": round(ms, 4), "gflops": round(plan.flops() / (ms * 1e-3) / 1e9, 2),
+            "exchange_bytes_per_rank": plan.exchange_bytes(rank), "steps": steps,
+            "scaling": "strong (the full 24^6 application split over the ranks)"}
 
 
 def ctypes_peak(lib, h) -> float:
