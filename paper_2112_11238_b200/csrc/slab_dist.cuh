@@ -377,15 +377,14 @@ static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64
   const int el = cplx ? 2 : 1;
   DistPlan pl;
   MM_TRY(dist_plan(P, r, d, m, n, chunks, el, pl));
-  const int64_t A = pl.A, A_r = pl.A_r, m_d = pl.m_d, n_d = pl.n_d;
   if (cm->exchange == 1 && !cplx) return dist_tucker_p2p(h, cm, d, m, n, T, L, S, pl);
   if (P == 1 && chunks <= 1) {
     // one rank: no exchange, and its output rows (A x n_d) ARE the whole
     // result: the plain chain (fused passes included). Explicit chunks > 1
     // still take the general path (exercised by the tests).
-    (void)A, (void)m_d, (void)n_d, (void)A_r;
     return tucker_dev(h, d, m, n, T, L, S, false, cplx);
   }
+  const int64_t A = pl.A, A_r = pl.A_r, m_d = pl.m_d, n_d = pl.n_d;
   const int nch = static_cast<int>(pl.ch.size());
   MM_TRY(cm->y.ensure(size_t(std::max<int64_t>(A * pl.wmax * el, 1)) * sizeof(double)));
   MM_TRY(cm->send.ensure(size_t(std::max<int64_t>(pl.send_elems, 1)) * sizeof(double)));
