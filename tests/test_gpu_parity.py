@@ -499,3 +499,31 @@ def test_odd_leading_extent_padded_chain_bitwise(m, n):
             h.set_kernel_policy(0)
     np.testing.assert_array_equal(got[0], got[8])
     assert O.rel_fro(got[0], O.port_tucker(T, Ls)) < 1e-14
+
+
+def test_user_cuda_graph_capture_of_tucker_and_kronsumv():
+    # after one warm-up call (workspace, TMA descriptors), the device path
+    # neither allocates nor synchronises, so a caller can capture it into a
+    # CUDA graph on its own stream and replay it
+    rng = np.random.default_rng(3)
+    m, n = (64, 48, 40), (56, 48, 72)
+    T = dev(rnd(rng, m))
+    Ls = [dev(rnd(rng, (n[k], m[k]))) for k in range(3)]
+    As = [dev(rnd(rng, (e, e))) for e in m]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ref_S = mm.tucker(T, Ls)
+        ref_W = mm.kronsumv(T, As)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        S = mm.tucker(T, Ls)
+        W = mm.kronsumv(T, As)
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(S, ref_S) and torch.equal(W, ref_W)
+    T.mul_(2.0)  # a replay reads the captured input buffer afresh
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(S, 2.0 * ref_S)
