@@ -24,7 +24,7 @@ struct ModeJob {
 };
 
 // Compiled tile configurations (BM, BN, BK, stages, warps along M, along N).
-using CfgBig = TmaCfg<128, 128, 16, 4, 4, 4>;  // 16 MMA warps, 32x32 warp tiles (C2-class shapes)
+using CfgBig = TmaCfg<128, 128, 16, 6, 4, 4>;  // 16 MMA warps, 32x32 warp tiles, 6-stage ring (C2-class shapes)
 using CfgTM = TmaCfg<128, 40, 40, 3, 16, 1>;   // T-side M, small L-side N (n = 40k)
 using CfgLM = TmaCfg<40, 128, 40, 3, 1, 16>;   // small L-side M, T-side N (mode 1, n = 40k)
 using CfgMid = TmaCfg<64, 128, 32, 4, 2, 4>;   // 32x32 warp tiles
