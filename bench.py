@@ -59,6 +59,10 @@ def tucker_flops(m, n):
 
 
 # ----------------------------------------------------------------- clocks
+# throttle reasons that invalidate a timed run (sw_power_cap is kept and noted)
+THROTTLE_REJECT = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "hw_power_brake_slowdown"}
+
+
 class ClockSampler:
     """nvidia-smi clocks line via NVML, sampled every 10 ms during the run."""
 
@@ -231,22 +235,33 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    # ---- timed region: exactly K steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    l0 = h.launches
-    for a, b in ev:
-        flush.fill_(1.0)  # evict L2 between steps (outside the events)
-        a.record(stream)
-        step()
-        b.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    launches = h.launches - l0
-    step_ms = [a.elapsed_time(b) for a, b in ev]
+    # ---- timed region: exactly K steps; a run that saw thermal / hardware
+    # slowdown is measured once more (the recipe's rejection rule)
+    def timed_region():
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = h.launches
+        for a, b in ev:
+            flush.fill_(1.0)  # evict L2 between steps (outside the events)
+            a.record(stream)
+            step()
+            b.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        return [a.elapsed_time(b) for a, b in ev], h.launches - l0
+
+    step_ms, launches = timed_region()
+    remeasured = False
+    if set(clocks.summary().get("reasons", [])) & THROTTLE_REJECT:
+        clocks.stop()
+        clocks = ClockSampler(local)
+        clocks.start()
+        step_ms, launches = timed_region()
+        remeasured = True
     total_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
@@ -339,7 +354,7 @@ def main():
                 "d2h_bytes_per_step": int(d2h),
                 "path": "mumode_host_tucker_f64 (host drop-in C-ABI), pinned host buffers"},
         "gpu_launches": int(launches),
-        "clocks": clocks.summary(),
+        "clocks": dict(clocks.summary(), remeasured=remeasured),
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(T_host, L_host, flops)
