@@ -1,9 +1,12 @@
 // Persistent, warp-specialised mu-mode product kernel for sm_100a:
 // TMA (cp.async.bulk.tensor) stages operand slabs into a multi-stage
-// shared-memory ring guarded by mbarriers; eight consumer warps run fp64
+// shared-memory ring guarded by mbarriers (one elected lane of a 4-warp
+// producer group issues the boxes); the MMA warps (Cfg::MMA_WARPS, 16 for the
+// main configurations; registers rebalanced with setmaxnreg) run fp64
 // tensor-core MMAs (mma.sync m8n8k4 -> SASS DMMA.8x8x4: the only fp64
 // tensor-core path on sm_100a, tcgen05 has no f64 kind) and store straight
-// from registers. Real fp64 and complex128 share the pipeline.
+// from registers (or scatter / accumulate / divide, see EPI). Real fp64 and
+// complex128 share the pipeline. Launched with programmatic dependent launch.
 //
 // Every mu-mode product is cast as D(M x N) [+ batch] = P(M x K) * Q(K x N)
 // with D and P contiguous along M (column-major):
