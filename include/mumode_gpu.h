@@ -109,10 +109,14 @@ int mumode_tucker_range_f64(mumode_handle_t h, int d, const int64_t* m, const in
  * dst[q], a column-major (a_off[q+1]-a_off[q]) x (col0 + cols ...) matrix,
  * at column col0 + c. The TMA kernel's epilogue stores straight to dst[q]
  * (the fused exchange of mumode_dist_tucker_* with peer pointers); other
- * paths compute then copy. Real, forward. */
+ * paths compute then copy. Forward chains. */
 int mumode_tucker_range_scatter_f64(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
                                     const double* T, const double* const* L, int mu_lo, int mu_hi,
                                     int P, const int64_t* a_off, int64_t col0, double* const* dst);
+/* complex128: offsets and rows count complex elements; dst interleaved. */
+int mumode_tucker_range_scatter_c128(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                                     const double* T, const double* const* L, int mu_lo, int mu_hi,
+                                     int P, const int64_t* a_off, int64_t col0, double* const* dst);
 /* Slab-transpose pack for the all-to-all: Y is A x C column-major; for each
  * destination rank q the row block Y[a_off[q]:a_off[q+1], :] is written as a
  * contiguous column-major block, blocks in rank order (a_off has P+1
@@ -140,7 +144,7 @@ int mumode_comm_destroy(mumode_comm_t c);
  * (default), 1 = peer stores: the last local mode's epilogue writes every row
  * straight into the owning rank's matrix through CUDA-IPC peer pointers
  * (NVLink), then a system-scope flag handshake (csrc/slab_dist.cuh). The
- * first call per shape maps the peers (collective). Complex stays on NCCL. */
+ * first call per shape maps the peers (collective). */
 int mumode_comm_set_exchange(mumode_comm_t c, int mode);
 /* SMs the persistent compute kernels leave free while sub-slabs overlap the
  * NCCL exchange (default 16; NCCL's kernels need SMs to run beside them). */

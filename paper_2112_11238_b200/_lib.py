@@ -37,6 +37,8 @@ SIGNATURES = {
     "mumode_tucker_range_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int, ctypes.c_int]),
     "mumode_tucker_range_scatter_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), ctypes.c_int,
                                                        ctypes.c_int, ctypes.c_int, I64P, I64, ctypes.POINTER(VP)]),
+    "mumode_tucker_range_scatter_c128": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), ctypes.c_int,
+                                                        ctypes.c_int, ctypes.c_int, I64P, I64, ctypes.POINTER(VP)]),
     "mumode_slab_pack_f64": (ctypes.c_int, [H, I64, I64, ctypes.c_int, I64P, VP, VP]),
     "mumode_slab_unpack_f64": (ctypes.c_int, [H, I64, I64, ctypes.c_int, I64P, VP, VP]),
     "mumode_comm_unique_id": (ctypes.c_int, [VP]),

@@ -196,13 +196,9 @@ static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
       return fail(MUMODE_ERR_ARGUMENT, "divide epilogue is real-only");
     }
   } else if (j.scat) {
-    if constexpr (Cfg::E == 1) {
-      auto k = mode1 ? modeprod_tma_kernel<Cfg, true, 2> : modeprod_tma_kernel<Cfg, false, 2>;
-      MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
-      MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, *mq, p));
-    } else {
-      return fail(MUMODE_ERR_ARGUMENT, "scatter epilogue is real-only");
-    }
+    auto k = mode1 ? modeprod_tma_kernel<Cfg, true, 2> : modeprod_tma_kernel<Cfg, false, 2>;
+    MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
+    MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, *mq, p));
   } else if (mode1) {
     auto k = modeprod_tma_kernel<Cfg, true>;
     MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
@@ -345,19 +341,18 @@ static int run_job(mumode_handle_s* h, const ModeJob& j0) {
   if (j.scat) {
     // fused exchange: the TMA kernel's epilogue scatters to the ranks; any
     // other path computes the (rows x C) result and scatter-copies it
-    if (!j.cplx && !j.accumulate && tma_ok(j) && h->policy != 1 && h->policy != 8 &&
-        (h->policy >= 2 || tma_worthwhile(j)))
+    if (!j.accumulate && tma_ok(j) && h->policy != 1 && h->policy != 8 && (h->policy >= 2 || tma_worthwhile(j)))
       return launch_tma_auto(h, j);
     ModeJob jt = j;
     jt.scat = nullptr;
-    const int64_t rows = (j.A == 1) ? j.N : j.A * j.N, cols = (j.A == 1) ? j.C : j.C;
-    MM_TRY(h->scat_tmp.ensure(size_t(rows * cols * (j.cplx ? 2 : 1)) * sizeof(double)));
+    const int el = j.cplx ? 2 : 1;
+    const int64_t rows = (j.A == 1) ? j.N : j.A * j.N, cols = j.C;
+    MM_TRY(h->scat_tmp.ensure(size_t(rows * cols * el) * sizeof(double)));
     jt.S = static_cast<double*>(h->scat_tmp.p);
     MM_TRY(run_job(h, jt));
-    if (j.cplx) return fail(MUMODE_ERR_ARGUMENT, "scatter of complex products is not supported");
-    const unsigned gy = static_cast<unsigned>(std::min<int64_t>(8, (rows + 255) / 256));
+    const unsigned gy = static_cast<unsigned>(std::min<int64_t>(8, (rows * el + 255) / 256));
     scatter_copy_kernel<<<dim3(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cols * 64, int64_t(h->num_sms) * 8))), gy),
-                          256, 0, h->stream>>>(static_cast<const double*>(h->scat_tmp.p), rows, cols, j.scat);
+                          256, 0, h->stream>>>(static_cast<const double*>(h->scat_tmp.p), rows, cols, el, j.scat);
     MM_CUDA(cudaGetLastError());
     h->launches++;
     return MUMODE_OK;

@@ -268,16 +268,17 @@ __global__ void __launch_bounds__(256) slab_pack_kernel(const double* __restrict
   }
 }
 
-// Fallback of the scatter epilogue: Y (A x C) -> dst[q] rows (A_q x ...) at
-// column col0 + c, one contiguous run per (column, rank).
-__global__ void __launch_bounds__(256) scatter_copy_kernel(const double* __restrict__ Y, int64_t A, int64_t C,
+// Fallback of the scatter epilogue: Y (A x C, el doubles per element) ->
+// dst[q] rows (A_q x ...) at column col0 + c, one contiguous run per
+// (column, rank).
+__global__ void __launch_bounds__(256) scatter_copy_kernel(const double* __restrict__ Y, int64_t A, int64_t C, int el,
                                                            const ScatterParams* __restrict__ sp) {
   const int P = sp->P;
   for (int64_t pr = blockIdx.x; pr < C * P; pr += gridDim.x) {
     const int64_t c = pr / P;
     const int q = static_cast<int>(pr - c * P);
-    const int64_t lo = sp->a_off[q], rows = sp->a_off[q + 1] - lo;
-    const double* src = Y + c * A + lo;
+    const int64_t lo = sp->a_off[q] * el, rows = (sp->a_off[q + 1] - sp->a_off[q]) * el;
+    const double* src = Y + c * A * el + lo;
     double* dst = sp->dst[q] + rows * (sp->col0 + c);
     for (int64_t i = blockIdx.y * int64_t(blockDim.x) + threadIdx.x; i < rows; i += int64_t(gridDim.y) * blockDim.x)
       dst[i] = src[i];
@@ -480,9 +481,9 @@ int mumode_tucker_range_f64(mumode_handle_t h, int d, const int64_t* m, const in
   return tucker_dev(h, d, m, n, T, L, S, false, false, mu_lo, mu_hi);
 }
 
-int mumode_tucker_range_scatter_f64(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
-                                    const double* T, const double* const* L, int mu_lo, int mu_hi, int P,
-                                    const int64_t* a_off, int64_t col0, double* const* dst) {
+static int tucker_range_scatter(mumode_handle_t h, int d, const int64_t* m, const int64_t* n, const double* T,
+                                const double* const* L, int mu_lo, int mu_hi, int P, const int64_t* a_off,
+                                int64_t col0, double* const* dst, bool cplx) {
   if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
   MM_TRY(check_shape(d, m, "tucker_range_scatter"));
   if (mu_lo < 1 || mu_hi > d || mu_lo > mu_hi)
@@ -511,7 +512,19 @@ int mumode_tucker_range_scatter_f64(mumode_handle_t h, int d, const int64_t* m, 
   MM_TRY(h->scat_params.ensure(sizeof(ScatterParams)));
   auto* dsp = static_cast<ScatterParams*>(h->scat_params.p);
   MM_CUDA(cudaMemcpyAsync(dsp, &sp, sizeof(sp), cudaMemcpyHostToDevice, h->stream));
-  return tucker_dev(h, d, m, n, T, L, nullptr, false, false, mu_lo, mu_hi, dsp);
+  return tucker_dev(h, d, m, n, T, L, nullptr, false, cplx, mu_lo, mu_hi, dsp);
+}
+
+int mumode_tucker_range_scatter_f64(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                                    const double* T, const double* const* L, int mu_lo, int mu_hi, int P,
+                                    const int64_t* a_off, int64_t col0, double* const* dst) {
+  return tucker_range_scatter(h, d, m, n, T, L, mu_lo, mu_hi, P, a_off, col0, dst, false);
+}
+
+int mumode_tucker_range_scatter_c128(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                                     const double* T, const double* const* L, int mu_lo, int mu_hi, int P,
+                                     const int64_t* a_off, int64_t col0, double* const* dst) {
+  return tucker_range_scatter(h, d, m, n, T, L, mu_lo, mu_hi, P, a_off, col0, dst, true);
 }
 
 int mumode_slab_pack_f64(mumode_handle_t h, int64_t A, int64_t C, int P, const int64_t* a_off,

@@ -330,12 +330,13 @@ static int p2p_map(mumode_comm_s* cm, size_t zbytes) {
 // epilogue: the TMA kernel stores every row pair straight into the owning
 // rank's Z (peer pointers), then signal / wait, then mode d on the local Z.
 static int dist_tucker_p2p(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64_t* m, const int64_t* n,
-                           const double* T, const double* const* L, double* S, const DistPlan& pl) {
+                           const double* T, const double* const* L, double* S, const DistPlan& pl, bool cplx) {
   const int P = cm->nranks, r = cm->rank;
+  const int el = cplx ? 2 : 1;
   // all ranks see the same shapes, so they remap in the same call
   size_t want = 0;
   for (int q = 0; q < P; ++q)
-    want = std::max(want, size_t((pl.a_off[q + 1] - pl.a_off[q]) * pl.m_d) * sizeof(double));
+    want = std::max(want, size_t((pl.a_off[q + 1] - pl.a_off[q]) * pl.m_d * el) * sizeof(double));
   want = std::max(want, size_t(8));
   if (P > 1 && want > cm->mapped_bytes) MM_TRY(p2p_map(cm, want));
   if (P == 1) {
@@ -355,7 +356,7 @@ static int dist_tucker_p2p(mumode_handle_s* h, mumode_comm_s* cm, int d, const i
   MM_CUDA(cudaMemcpyAsync(dsp, &sp, sizeof(sp), cudaMemcpyHostToDevice, h->stream));
   if (P > 1)
     MM_CUDA(cudaMemcpyAsync(dflags, cm->peer_flags.data(), sizeof(int64_t*) * P, cudaMemcpyHostToDevice, h->stream));
-  MM_TRY(tucker_dev(h, d, m, n, T, L, nullptr, false, false, 1, d - 1, dsp));
+  MM_TRY(tucker_dev(h, d, m, n, T, L, nullptr, false, cplx, 1, d - 1, dsp));
   if (P > 1) {
     p2p_signal_kernel<<<1, 64, 0, h->stream>>>(dflags, P, r, cm->epoch);
     p2p_wait_kernel<<<1, 64, 0, h->stream>>>(static_cast<const int64_t*>(cm->flags.p), P, cm->epoch);
@@ -364,7 +365,7 @@ static int dist_tucker_p2p(mumode_handle_s* h, mumode_comm_s* cm, int d, const i
   }
   if (pl.A_r == 0) return MUMODE_OK;
   const int64_t zext[2] = {pl.A_r, pl.m_d};
-  return mode_product_dev(h, 2, zext, 2, pl.n_d, cm->peer_z[par][r], L[d - 1], 1, pl.n_d, false, false, S);
+  return mode_product_dev(h, 2, zext, 2, pl.n_d, cm->peer_z[par][r], L[d - 1], 1, pl.n_d, cplx, false, S);
 }
 
 static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64_t* m, const int64_t* n,
@@ -377,7 +378,7 @@ static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64
   const int el = cplx ? 2 : 1;
   DistPlan pl;
   MM_TRY(dist_plan(P, r, d, m, n, chunks, el, pl));
-  if (cm->exchange == 1 && !cplx) return dist_tucker_p2p(h, cm, d, m, n, T, L, S, pl);
+  if (cm->exchange == 1) return dist_tucker_p2p(h, cm, d, m, n, T, L, S, pl, cplx);
   if (P == 1 && chunks <= 1) {
     // one rank: no exchange, and its output rows (A x n_d) ARE the whole
     // result: the plain chain (fused passes included). Explicit chunks > 1

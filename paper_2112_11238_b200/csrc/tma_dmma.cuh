@@ -70,6 +70,15 @@ __device__ __forceinline__ void scatter_store(const ScatterParams* sp, int64_t r
   }
 }
 
+// complex element (re, im) of row rho, column col (rows and offsets count
+// complex elements; dst points at interleaved doubles)
+__device__ __forceinline__ void scatter_store_c(const ScatterParams* sp, int64_t rho, int64_t col, double re,
+                                                double im) {
+  const int q = scatter_owner(sp, rho);
+  const int64_t lo = __ldg(&sp->a_off[q]), hi = __ldg(&sp->a_off[q + 1]);
+  stg_f64x2(sp->dst[q] + 2 * ((rho - lo) + (hi - lo) * (sp->col0 + col)), re, im);
+}
+
 struct TmaParams {
   const ScatterParams* scat;  // EPI 2 only (device memory)
   const double* div_front;    // EPI 3: D(a, n) /= (div_front[a] + div_last[n])
@@ -162,7 +171,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   constexpr int FM = Cfg::FM, FN = Cfg::FN, E = Cfg::E, ROW = Cfg::ROW;
   constexpr bool CPLX = (E == 2);
   constexpr bool ACC = (EPI == 1);
-  static_assert(EPI < 2 || !CPLX, "scatter / divide epilogues are real-only");
+  static_assert(EPI != 3 || !CPLX, "the divide epilogue is real-only");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment by pointer arithmetic so the compiler keeps the shared
   // address space (LDS, not generic LD).
@@ -427,6 +436,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           if (n >= p.N) continue;
           double* col = base + 2 * static_cast<int64_t>(n) * p.ldD;
           double r0 = acc[fm][fn][0], i0 = acc[fm][fn][2], r1 = acc[fm][fn][1], i1 = acc[fm][fn][3];
+          if constexpr (EPI == 2) {
+            // one complex element per 16-byte store: rows m and m + 4
+            const int64_t rho0 = QK ? m : m + static_cast<int64_t>(n) * p.ldD;
+            const int64_t colx = QK ? n : static_cast<int64_t>(c);
+            if (m < p.Mlim) scatter_store_c(p.scat, rho0, colx, r0, i0);
+            if (m + 4 < p.Mlim) scatter_store_c(p.scat, rho0 + 4, colx, r1, i1);
+            continue;
+          }
           if constexpr (ACC) {
             if (m < p.Mlim) {
               const double2 o = *reinterpret_cast<const double2*>(col);

@@ -534,11 +534,16 @@ def test_scatter_epilogue_to_rank_buffers(policy):
     h.bind_torch_stream()
     h.set_kernel_policy(policy)
     try:
-        for m, n, lo, hi in [((48, 40, 32), (40, 56, 24), 1, 2), ((64, 48, 20), (56, 48, 20), 1, 2),
-                             ((40, 30), (64, 30), 1, 1), ((16, 16, 16, 16), (16, 16, 16, 16), 1, 3)]:
+        for m, n, lo, hi, cplx in [((48, 40, 32), (40, 56, 24), 1, 2, False), ((64, 48, 20), (56, 48, 20), 1, 2, False),
+                                   ((40, 30), (64, 30), 1, 1, False), ((16, 16, 16, 16), (16, 16, 16, 16), 1, 3, False),
+                                   ((24, 16, 20), (32, 24, 16), 1, 2, True), ((40, 12), (48, 12), 1, 1, True)]:
             rng = np.random.default_rng(sum(m))
-            T = np.asfortranarray(rng.standard_normal(m))
-            Ls = [np.asfortranarray(rng.standard_normal((n[k], m[k]))) for k in range(len(m))]
+
+            def rnd(shape):
+                x = rng.standard_normal(shape)
+                return np.asfortranarray(x + 1j * rng.standard_normal(shape) if cplx else x)
+            T = rnd(m)
+            Ls = [rnd((n[k], m[k])) for k in range(len(m))]
             Y = T
             for mu in range(lo, hi + 1):
                 Y = O.port_mode_product(Y, Ls[mu - 1], mu)
@@ -549,18 +554,20 @@ def test_scatter_epilogue_to_rank_buffers(policy):
             a_off = [0, 37, 37] + [c for c in cuts if c > 37]  # rank 1 empty
             P = len(a_off) - 1
             col0 = 3
-            bufs = [torch.full(((a_off[q + 1] - a_off[q]) * (col0 + cols + 2),), float("nan"), dtype=torch.float64,
+            dt = torch.complex128 if cplx else torch.float64
+            bufs = [torch.full(((a_off[q + 1] - a_off[q]) * (col0 + cols + 2),), float("nan"), dtype=dt,
                                device="cuda") for q in range(P)]
             Td = torch.from_numpy(T).cuda()
             Lds = [torch.from_numpy(L).cuda() for L in Ls]
-            rc = lib.mumode_tucker_range_scatter_f64(
+            fn = lib.mumode_tucker_range_scatter_c128 if cplx else lib.mumode_tucker_range_scatter_f64
+            rc = fn(
                 h.h, len(m), _lib.i64_array(m), _lib.i64_array(n), Td.data_ptr(), _lib.ptr_array([L.data_ptr() for L in Lds]),
                 lo, hi, P, _lib.i64_array(a_off), col0, _lib.ptr_array([b.data_ptr() if b.numel() else 0 for b in bufs]))
             assert rc == 0, lib.mumode_last_error()
             for q in range(P):
                 r = a_off[q + 1] - a_off[q]
                 got = bufs[q].cpu().numpy().reshape((r, col0 + cols + 2), order="F")
-                assert np.isnan(got[:, :col0]).all() and np.isnan(got[:, col0 + cols:]).all()
+                assert np.isnan(got[:, :col0].real).all() and np.isnan(got[:, col0 + cols:].real).all()
                 ref = Y2[a_off[q]:a_off[q + 1], :]
                 if r:
                     assert O.rel_max(got[:, col0:col0 + cols], ref) < 1e-13, (m, q)
@@ -577,9 +584,10 @@ def test_dist_tucker_peer_store_exchange_single_rank():
     try:
         comm.set_exchange("p2p")
         g = mm.Rng(5)
-        for m, n in [((96, 64, 48), (64, 96, 40)), ((24, 24, 24, 24, 24), (24, 24, 24, 24, 24)), ((60, 40), (30, 50))]:
-            T = torch.from_numpy(g.normal(m)).cuda()
-            Ls = [torch.from_numpy(g.normal((n[k], m[k]))).cuda() for k in range(len(m))]
+        for m, n, cplx in [((96, 64, 48), (64, 96, 40), False), ((24, 24, 24, 24, 24), (24, 24, 24, 24, 24), False),
+                           ((60, 40), (30, 50), False), ((32, 24, 16), (40, 24, 24), True)]:
+            T = torch.from_numpy(g.normal(m, cplx)).cuda()
+            Ls = [torch.from_numpy(g.normal((n[k], m[k]), cplx)).cuda() for k in range(len(m))]
             ref = mm.tucker(T, Ls).cpu().numpy().reshape(-1, order="F")
             for _ in range(3):  # both Z parities
                 S_r = dist_tucker(comm, T, Ls, m, n)
