@@ -158,32 +158,289 @@ struct TmaCfg {
 
 // QK == true  (mu == 1): P = L (XK), Q = T (KX)
 // QK == false (mu  > 1): P = T (XK, fragment list over (a-block, c)), Q = L (XK)
+// One output tile of the mode product, producer side: the elected lane
+// issues the tile's K-stages into the ring (stage / phase persist across
+// tiles and, in the chain kernel, across modes).
+template <class Cfg, bool QK>
+__device__ __forceinline__ void tma_produce_tile(const CUtensorMap* mapP, const CUtensorMap* mapQ, const TmaParams& p,
+                                                 int mtile, int ntile, uint8_t* smem, uint64_t* full_bar,
+                                                 uint64_t* empty_bar, int& stage, uint32_t& phase) {
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES, E = Cfg::E, ROW = Cfg::ROW;
+  const int KT = (p.K + BK - 1) / BK;
+  const int n0 = ntile * BN;
+  // first M fragment of the tile -> (batch c0, a-block ab0); later
+  // fragments advance incrementally (no per-stage divisions)
+  const uint32_t q0 = static_cast<uint32_t>(mtile) * (BM / 8);
+  const uint32_t qlast = static_cast<uint32_t>(p.mfrags - 1);
+  uint32_t c0 = 0, ab0 = q0;
+  if constexpr (!QK) {
+    c0 = q0 / static_cast<uint32_t>(p.AB);
+    ab0 = q0 - c0 * static_cast<uint32_t>(p.AB);
+  }
+  for (int kb = 0; kb < KT; ++kb) {
+    mbar_wait(&empty_bar[stage], phase ^ 1);
+    uint8_t* sP = smem + stage * Cfg::STAGE_BYTES;
+    uint8_t* sQ = sP + Cfg::P_BYTES;
+    mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+    const int k0 = kb * BK;
+    if (p.p_blocked) {
+      if constexpr (QK)
+        tma_load_3d(sP, mapP, &full_bar[stage], 0, k0, static_cast<int32_t>(q0));
+      else
+        tma_load_4d(sP, mapP, &full_bar[stage], 0, k0, static_cast<int32_t>(ab0),
+                    static_cast<int32_t>(c0));
+    } else {
+      uint32_t c = c0, ab = ab0;
+#pragma unroll 1
+      for (int f = 0; f < BM / 8; ++f) {
+        // fragments past the end re-load the last valid one (masked later)
+        if constexpr (QK) {
+          const uint32_t q = (q0 + f <= qlast) ? (q0 + f) : qlast;
+          tma_load_2d(sP + f * BK * ROW, mapP, &full_bar[stage], static_cast<int32_t>(8 * E * q), k0);
+        } else {
+          if (q0 + f > qlast) {
+            c = qlast / static_cast<uint32_t>(p.AB);
+            ab = qlast - c * static_cast<uint32_t>(p.AB);
+          }
+          tma_load_3d(sP + f * BK * ROW, mapP, &full_bar[stage], static_cast<int32_t>(8 * E * ab), k0,
+                      static_cast<int32_t>(c));
+          if (++ab == static_cast<uint32_t>(p.AB)) {
+            ab = 0;
+            ++c;
+          }
+        }
+      }
+    }
+    if (p.q_blocked) {
+      if constexpr (QK)
+        tma_load_3d(sQ, mapQ, &full_bar[stage], 0, n0, k0 / 8);
+      else
+        tma_load_3d(sQ, mapQ, &full_bar[stage], 0, k0, n0 / 8);
+    } else if constexpr (QK) {
+#pragma unroll 1
+      for (int b = 0; b < BK / 8; ++b)
+        tma_load_2d(sQ + b * BN * ROW, mapQ, &full_bar[stage], E * (k0 + 8 * b), n0);
+    } else {
+#pragma unroll 1
+      for (int b = 0; b < BN / 8; ++b)
+        tma_load_2d(sQ + b * BK * ROW, mapQ, &full_bar[stage], E * (n0 + 8 * b), k0);
+    }
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+}
+
+// Thread-constant parts of the fragment addresses (see the maps above).
+struct FragOffsets {
+  int g, t, mw, nw;
+  uint32_t J0, xk_off, kx_off;
+};
+
+template <class Cfg>
+__device__ __forceinline__ FragOffsets tma_frag_offsets(int warp, int lane) {
+  FragOffsets o;
+  o.g = lane >> 2;
+  o.t = lane & 3;
+  o.mw = (warp % Cfg::WM) * Cfg::WTM;
+  o.nw = (warp / Cfg::WM) * Cfg::WTN;
+  if constexpr (Cfg::E == 2) {
+    o.J0 = static_cast<uint32_t>(xmapc(o.g) ^ o.t) << 4;
+    o.xk_off = static_cast<uint32_t>(o.t * 128);
+    o.kx_off = static_cast<uint32_t>(xmapc(o.g) * 128);
+  } else {
+    const int jg = 2 * ((o.g >> 1) & 1) + (o.g >> 2);
+    o.J0 = static_cast<uint32_t>(jg ^ (o.t >> 1)) << 4;
+    o.xk_off = static_cast<uint32_t>(o.t * 64 + (o.g & 1) * 8);
+    o.kx_off = static_cast<uint32_t>(xmap8(o.g) * 64 + (o.t & 1) * 8);
+  }
+  return o;
+}
+
+// One output tile, MMA-warp side: consume the tile's K-stages from the ring
+// (DMMA), then the epilogue (EPI) straight from registers.
+template <class Cfg, bool QK, int EPI>
+__device__ __forceinline__ void tma_consume_tile(const TmaParams& p, int mtile, int ntile, const uint8_t* smem,
+                                                 uint64_t* full_bar, uint64_t* empty_bar, int& stage,
+                                                 uint32_t& phase, const FragOffsets& fo, int lane) {
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
+  constexpr int FM = Cfg::FM, FN = Cfg::FN, E = Cfg::E, ROW = Cfg::ROW;
+  constexpr bool CPLX = (E == 2);
+  constexpr bool ACC = (EPI == 1);
+  constexpr uint32_t JFLIP = CPLX ? 64u : 32u;  // XOR applied on odd k-steps
+  const int KT = (p.K + BK - 1) / BK;
+  const int g = fo.g, t = fo.t, mw = fo.mw, nw = fo.nw;
+  const uint32_t J0 = fo.J0, xk_off = fo.xk_off, kx_off = fo.kx_off;
+  // real: acc[fm][fn][0..1]; complex: re in [0..1], im in [2..3]
+  double acc[FM][FN][2 * E];
+#pragma unroll
+  for (int fm = 0; fm < FM; ++fm)
+#pragma unroll
+    for (int fn = 0; fn < FN; ++fn)
+#pragma unroll
+      for (int r = 0; r < 2 * E; ++r) acc[fm][fn][r] = 0.0;
+
+  for (int kb = 0; kb < KT; ++kb) {
+    mbar_wait(&full_bar[stage], phase);
+    const uint8_t* sP = smem + stage * Cfg::STAGE_BYTES;
+    const uint8_t* sQ = sP + Cfg::P_BYTES;
+#pragma unroll
+    for (int s = 0; s < BK / 4; ++s) {
+      const uint32_t Js = J0 ^ (JFLIP * static_cast<uint32_t>(s & 1));
+      if constexpr (!CPLX) {
+        double pf[FM], qf[FN];
+#pragma unroll
+        for (int fm = 0; fm < FM; ++fm)
+          pf[fm] = *reinterpret_cast<const double*>(sP + ((mw >> 3) + fm) * (BK * ROW) + (4 * s) * ROW +
+                                                    xk_off + Js);
+#pragma unroll
+        for (int fn = 0; fn < FN; ++fn) {
+          if constexpr (QK)
+            qf[fn] = *reinterpret_cast<const double*>(sQ + (s >> 1) * (BN * ROW) + (nw + 8 * fn) * ROW +
+                                                      kx_off + Js);
+          else
+            qf[fn] = *reinterpret_cast<const double*>(sQ + ((nw >> 3) + fn) * (BK * ROW) + (4 * s) * ROW +
+                                                      xk_off + Js);
+        }
+#pragma unroll
+        for (int fm = 0; fm < FM; ++fm)
+#pragma unroll
+          for (int fn = 0; fn < FN; ++fn) dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], qf[fn], pf[fm]);
+      } else {
+        double2 pf[FM], qf[FN];
+#pragma unroll
+        for (int fm = 0; fm < FM; ++fm)
+          pf[fm] = *reinterpret_cast<const double2*>(sP + ((mw >> 3) + fm) * (BK * ROW) + (4 * s) * ROW +
+                                                     xk_off + Js);
+#pragma unroll
+        for (int fn = 0; fn < FN; ++fn) {
+          if constexpr (QK)
+            qf[fn] = *reinterpret_cast<const double2*>(sQ + (s >> 1) * (BN * ROW) + (nw + 8 * fn) * ROW +
+                                                       kx_off + Js);
+          else
+            qf[fn] = *reinterpret_cast<const double2*>(sQ + ((nw >> 3) + fn) * (BK * ROW) + (4 * s) * ROW +
+                                                       xk_off + Js);
+        }
+        // complex MAC as four real DMMAs: re += qr*pr - qi*pi, im += qr*pi + qi*pr
+#pragma unroll
+        for (int fn = 0; fn < FN; ++fn) {
+          const double qneg = -qf[fn].y;
+#pragma unroll
+          for (int fm = 0; fm < FM; ++fm) {
+            dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], qf[fn].x, pf[fm].x);
+            dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], qneg, pf[fm].y);
+            dmma_8x8x4(acc[fm][fn][2], acc[fm][fn][3], qf[fn].x, pf[fm].y);
+            dmma_8x8x4(acc[fm][fn][2], acc[fm][fn][3], qf[fn].y, pf[fm].x);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[stage]);
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+
+  // epilogue straight from registers
+#pragma unroll
+  for (int fm = 0; fm < FM; ++fm) {
+    const uint32_t q = static_cast<uint32_t>(mtile) * (BM / 8) + (mw >> 3) + fm;
+    if (q >= static_cast<uint32_t>(p.mfrags)) continue;
+    uint32_t c = 0, ab = q;
+    if constexpr (!QK) {
+      c = q / static_cast<uint32_t>(p.AB);
+      ab = q - c * static_cast<uint32_t>(p.AB);
+    }
+    if constexpr (!CPLX) {
+      // D(m, m+1 ; n): one 16-byte store along M
+      const int m = 8 * static_cast<int>(ab) + xmap8(2 * t);
+      if (m >= p.Mlim) continue;
+      double* base = p.D + static_cast<int64_t>(c) * p.bstride + m;
+#pragma unroll
+      for (int fn = 0; fn < FN; ++fn) {
+        const int n = ntile * BN + nw + 8 * fn + xmap8(g);
+        if (n >= p.N) continue;
+        if constexpr (EPI == 2) {
+          // row of the (rows x w) matrix and its column (m even, Mlim even)
+          if constexpr (QK)
+            scatter_store(p.scat, m, n, acc[fm][fn][0], acc[fm][fn][1]);
+          else
+            scatter_store(p.scat, m + static_cast<int64_t>(n) * p.ldD, c, acc[fm][fn][0], acc[fm][fn][1]);
+          continue;
+        }
+        double* dst = base + static_cast<int64_t>(n) * p.ldD;
+        if constexpr (EPI == 3) {
+          // the last mode: rows m, m+1 index the modes before it (batch 0)
+          const double2 fr = *reinterpret_cast<const double2*>(p.div_front + m);
+          const double ln = __ldg(p.div_last + n);
+          stg_f64x2(dst, acc[fm][fn][0] / (fr.x + ln), acc[fm][fn][1] / (fr.y + ln));
+          continue;
+        }
+        if constexpr (ACC) {
+          const double2 o = *reinterpret_cast<const double2*>(dst);
+          stg_f64x2(dst, o.x + acc[fm][fn][0], o.y + acc[fm][fn][1]);
+        } else {
+          stg_f64x2(dst, acc[fm][fn][0], acc[fm][fn][1]);
+        }
+      }
+    } else {
+      // D(m) and D(m+4) (xmapc(2t) = t, xmapc(2t+1) = t+4): two 16-byte stores
+      const int m = 8 * static_cast<int>(ab) + t;
+      double* base = p.D + 2 * (static_cast<int64_t>(c) * p.bstride + m);
+#pragma unroll
+      for (int fn = 0; fn < FN; ++fn) {
+        const int n = ntile * BN + nw + 8 * fn + xmapc(g);
+        if (n >= p.N) continue;
+        double* col = base + 2 * static_cast<int64_t>(n) * p.ldD;
+        double r0 = acc[fm][fn][0], i0 = acc[fm][fn][2], r1 = acc[fm][fn][1], i1 = acc[fm][fn][3];
+        if constexpr (EPI == 2) {
+          // one complex element per 16-byte store: rows m and m + 4
+          const int64_t rho0 = QK ? m : m + static_cast<int64_t>(n) * p.ldD;
+          const int64_t colx = QK ? n : static_cast<int64_t>(c);
+          if (m < p.Mlim) scatter_store_c(p.scat, rho0, colx, r0, i0);
+          if (m + 4 < p.Mlim) scatter_store_c(p.scat, rho0 + 4, colx, r1, i1);
+          continue;
+        }
+        if constexpr (ACC) {
+          if (m < p.Mlim) {
+            const double2 o = *reinterpret_cast<const double2*>(col);
+            r0 += o.x, i0 += o.y;
+          }
+          if (m + 4 < p.Mlim) {
+            const double2 o = *reinterpret_cast<const double2*>(col + 8);
+            r1 += o.x, i1 += o.y;
+          }
+        }
+        if (m < p.Mlim) stg_f64x2(col, r0, i0);
+        if (m + 4 < p.Mlim) stg_f64x2(col + 8, r1, i1);
+      }
+    }
+  }
+}
+
 // EPI: 0 = store; 1 = D += result (kronsumv term accumulation,
-// tucker.hpp:222-231); 2 = scatter to the owning ranks (real only); 3 =
-// divide by the eigenvalue Kronecker sum (the direct solver's pointwise step,
+// tucker.hpp:222-231); 2 = scatter to the owning ranks; 3 = divide by the
+// eigenvalue Kronecker sum (the direct solver's pointwise step,
 // imex.cpp:70-80; last mode, real). A compile-time switch -- a runtime branch
 // in the epilogue costs ~2 % on C2.
 template <class Cfg, bool QK, int EPI = 0>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
     modeprod_tma_kernel(const __grid_constant__ CUtensorMap mapP,
                         const __grid_constant__ CUtensorMap mapQ, const TmaParams p) {
-  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
-  constexpr int FM = Cfg::FM, FN = Cfg::FN, E = Cfg::E, ROW = Cfg::ROW;
-  constexpr bool CPLX = (E == 2);
-  constexpr bool ACC = (EPI == 1);
-  static_assert(EPI != 3 || !CPLX, "the divide epilogue is real-only");
+  static_assert(EPI != 3 || Cfg::E == 1, "the divide epilogue is real-only");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment by pointer arithmetic so the compiler keeps the shared
   // address space (LDS, not generic LD).
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
-  uint64_t* empty_bar = full_bar + STAGES;
-
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + Cfg::STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int KT = (p.K + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], Cfg::MMA_WARPS);
     }
@@ -207,258 +464,27 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       mt = static_cast<int>(tile / p.nt);
     }
   };
-
+  int stage = 0;
+  uint32_t phase = 0;
   if (warp >= Cfg::MMA_WARPS) {
-    // ------------------------------------------------------------ producer
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Cfg::PRODUCER_REGS) : "memory");
     if (warp == Cfg::MMA_WARPS && lane == 0) {
       tma_prefetch_desc(&mapP);
       tma_prefetch_desc(&mapQ);
-      int stage = 0;
-      uint32_t phase = 0;
       for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
         int mtile, ntile;
         decode(tile, mtile, ntile);
-        const int n0 = ntile * BN;
-        // first M fragment of the tile -> (batch c0, a-block ab0); later
-        // fragments advance incrementally (no per-stage divisions)
-        const uint32_t q0 = static_cast<uint32_t>(mtile) * (BM / 8);
-        const uint32_t qlast = static_cast<uint32_t>(p.mfrags - 1);
-        uint32_t c0 = 0, ab0 = q0;
-        if constexpr (!QK) {
-          c0 = q0 / static_cast<uint32_t>(p.AB);
-          ab0 = q0 - c0 * static_cast<uint32_t>(p.AB);
-        }
-        for (int kb = 0; kb < KT; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sP = smem + stage * Cfg::STAGE_BYTES;
-          uint8_t* sQ = sP + Cfg::P_BYTES;
-          mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
-          const int k0 = kb * BK;
-          if (p.p_blocked) {
-            if constexpr (QK)
-              tma_load_3d(sP, &mapP, &full_bar[stage], 0, k0, static_cast<int32_t>(q0));
-            else
-              tma_load_4d(sP, &mapP, &full_bar[stage], 0, k0, static_cast<int32_t>(ab0),
-                          static_cast<int32_t>(c0));
-          } else {
-            uint32_t c = c0, ab = ab0;
-#pragma unroll 1
-            for (int f = 0; f < BM / 8; ++f) {
-              // fragments past the end re-load the last valid one (masked later)
-              if constexpr (QK) {
-                const uint32_t q = (q0 + f <= qlast) ? (q0 + f) : qlast;
-                tma_load_2d(sP + f * BK * ROW, &mapP, &full_bar[stage], static_cast<int32_t>(8 * E * q), k0);
-              } else {
-                if (q0 + f > qlast) {
-                  c = qlast / static_cast<uint32_t>(p.AB);
-                  ab = qlast - c * static_cast<uint32_t>(p.AB);
-                }
-                tma_load_3d(sP + f * BK * ROW, &mapP, &full_bar[stage], static_cast<int32_t>(8 * E * ab), k0,
-                            static_cast<int32_t>(c));
-                if (++ab == static_cast<uint32_t>(p.AB)) {
-                  ab = 0;
-                  ++c;
-                }
-              }
-            }
-          }
-          if (p.q_blocked) {
-            if constexpr (QK)
-              tma_load_3d(sQ, &mapQ, &full_bar[stage], 0, n0, k0 / 8);
-            else
-              tma_load_3d(sQ, &mapQ, &full_bar[stage], 0, k0, n0 / 8);
-          } else if constexpr (QK) {
-#pragma unroll 1
-            for (int b = 0; b < BK / 8; ++b)
-              tma_load_2d(sQ + b * BN * ROW, &mapQ, &full_bar[stage], E * (k0 + 8 * b), n0);
-          } else {
-#pragma unroll 1
-            for (int b = 0; b < BN / 8; ++b)
-              tma_load_2d(sQ + b * BK * ROW, &mapQ, &full_bar[stage], E * (n0 + 8 * b), k0);
-          }
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
+        tma_produce_tile<Cfg, QK>(&mapP, &mapQ, p, mtile, ntile, smem, full_bar, empty_bar, stage, phase);
       }
     }
     return;
   }
-
-  // -------------------------------------------------------------- consumers
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Cfg::CONSUMER_REGS) : "memory");
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = warp % Cfg::WM, wn = warp / Cfg::WM;
-  const int mw = wm * Cfg::WTM, nw = wn * Cfg::WTN;
-  // thread-constant parts of the fragment addresses (see the maps above)
-  uint32_t J0, xk_off, kx_off;
-  if constexpr (CPLX) {
-    J0 = static_cast<uint32_t>(xmapc(g) ^ t) << 4;
-    xk_off = static_cast<uint32_t>(t * 128);
-    kx_off = static_cast<uint32_t>(xmapc(g) * 128);
-  } else {
-    const int jg = 2 * ((g >> 1) & 1) + (g >> 2);
-    J0 = static_cast<uint32_t>(jg ^ (t >> 1)) << 4;
-    xk_off = static_cast<uint32_t>(t * 64 + (g & 1) * 8);
-    kx_off = static_cast<uint32_t>(xmap8(g) * 64 + (t & 1) * 8);
-  }
-  constexpr uint32_t JFLIP = CPLX ? 64u : 32u;  // XOR applied on odd k-steps
-
-  int stage = 0;
-  uint32_t phase = 0;
+  const FragOffsets fo = tma_frag_offsets<Cfg>(warp, lane);
   for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
     int mtile, ntile;
     decode(tile, mtile, ntile);
-
-    // real: acc[fm][fn][0..1]; complex: re in [0..1], im in [2..3]
-    double acc[FM][FN][2 * E];
-#pragma unroll
-    for (int fm = 0; fm < FM; ++fm)
-#pragma unroll
-      for (int fn = 0; fn < FN; ++fn)
-#pragma unroll
-        for (int r = 0; r < 2 * E; ++r) acc[fm][fn][r] = 0.0;
-
-    for (int kb = 0; kb < KT; ++kb) {
-      mbar_wait(&full_bar[stage], phase);
-      const uint8_t* sP = smem + stage * Cfg::STAGE_BYTES;
-      const uint8_t* sQ = sP + Cfg::P_BYTES;
-#pragma unroll
-      for (int s = 0; s < BK / 4; ++s) {
-        const uint32_t Js = J0 ^ (JFLIP * static_cast<uint32_t>(s & 1));
-        if constexpr (!CPLX) {
-          double pf[FM], qf[FN];
-#pragma unroll
-          for (int fm = 0; fm < FM; ++fm)
-            pf[fm] = *reinterpret_cast<const double*>(sP + ((mw >> 3) + fm) * (BK * ROW) + (4 * s) * ROW +
-                                                      xk_off + Js);
-#pragma unroll
-          for (int fn = 0; fn < FN; ++fn) {
-            if constexpr (QK)
-              qf[fn] = *reinterpret_cast<const double*>(sQ + (s >> 1) * (BN * ROW) + (nw + 8 * fn) * ROW +
-                                                        kx_off + Js);
-            else
-              qf[fn] = *reinterpret_cast<const double*>(sQ + ((nw >> 3) + fn) * (BK * ROW) + (4 * s) * ROW +
-                                                        xk_off + Js);
-          }
-#pragma unroll
-          for (int fm = 0; fm < FM; ++fm)
-#pragma unroll
-            for (int fn = 0; fn < FN; ++fn) dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], qf[fn], pf[fm]);
-        } else {
-          double2 pf[FM], qf[FN];
-#pragma unroll
-          for (int fm = 0; fm < FM; ++fm)
-            pf[fm] = *reinterpret_cast<const double2*>(sP + ((mw >> 3) + fm) * (BK * ROW) + (4 * s) * ROW +
-                                                       xk_off + Js);
-#pragma unroll
-          for (int fn = 0; fn < FN; ++fn) {
-            if constexpr (QK)
-              qf[fn] = *reinterpret_cast<const double2*>(sQ + (s >> 1) * (BN * ROW) + (nw + 8 * fn) * ROW +
-                                                         kx_off + Js);
-            else
-              qf[fn] = *reinterpret_cast<const double2*>(sQ + ((nw >> 3) + fn) * (BK * ROW) + (4 * s) * ROW +
-                                                         xk_off + Js);
-          }
-          // complex MAC as four real DMMAs: re += qr*pr - qi*pi, im += qr*pi + qi*pr
-#pragma unroll
-          for (int fn = 0; fn < FN; ++fn) {
-            const double qneg = -qf[fn].y;
-#pragma unroll
-            for (int fm = 0; fm < FM; ++fm) {
-              dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], qf[fn].x, pf[fm].x);
-              dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], qneg, pf[fm].y);
-              dmma_8x8x4(acc[fm][fn][2], acc[fm][fn][3], qf[fn].x, pf[fm].y);
-              dmma_8x8x4(acc[fm][fn][2], acc[fm][fn][3], qf[fn].y, pf[fm].x);
-            }
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[stage]);
-      if (++stage == STAGES) {
-        stage = 0;
-        phase ^= 1;
-      }
-    }
-
-    // epilogue straight from registers
-#pragma unroll
-    for (int fm = 0; fm < FM; ++fm) {
-      const uint32_t q = static_cast<uint32_t>(mtile) * (BM / 8) + (mw >> 3) + fm;
-      if (q >= static_cast<uint32_t>(p.mfrags)) continue;
-      uint32_t c = 0, ab = q;
-      if constexpr (!QK) {
-        c = q / static_cast<uint32_t>(p.AB);
-        ab = q - c * static_cast<uint32_t>(p.AB);
-      }
-      if constexpr (!CPLX) {
-        // D(m, m+1 ; n): one 16-byte store along M
-        const int m = 8 * static_cast<int>(ab) + xmap8(2 * t);
-        if (m >= p.Mlim) continue;
-        double* base = p.D + static_cast<int64_t>(c) * p.bstride + m;
-#pragma unroll
-        for (int fn = 0; fn < FN; ++fn) {
-          const int n = ntile * BN + nw + 8 * fn + xmap8(g);
-          if (n >= p.N) continue;
-          if constexpr (EPI == 2) {
-            // row of the (rows x w) matrix and its column (m even, Mlim even)
-            if constexpr (QK)
-              scatter_store(p.scat, m, n, acc[fm][fn][0], acc[fm][fn][1]);
-            else
-              scatter_store(p.scat, m + static_cast<int64_t>(n) * p.ldD, c, acc[fm][fn][0], acc[fm][fn][1]);
-            continue;
-          }
-          double* dst = base + static_cast<int64_t>(n) * p.ldD;
-          if constexpr (EPI == 3) {
-            // the last mode: rows m, m+1 index the modes before it (batch 0)
-            const double2 fr = *reinterpret_cast<const double2*>(p.div_front + m);
-            const double ln = __ldg(p.div_last + n);
-            stg_f64x2(dst, acc[fm][fn][0] / (fr.x + ln), acc[fm][fn][1] / (fr.y + ln));
-            continue;
-          }
-          if constexpr (ACC) {
-            const double2 o = *reinterpret_cast<const double2*>(dst);
-            stg_f64x2(dst, o.x + acc[fm][fn][0], o.y + acc[fm][fn][1]);
-          } else {
-            stg_f64x2(dst, acc[fm][fn][0], acc[fm][fn][1]);
-          }
-        }
-      } else {
-        // D(m) and D(m+4) (xmapc(2t) = t, xmapc(2t+1) = t+4): two 16-byte stores
-        const int m = 8 * static_cast<int>(ab) + t;
-        double* base = p.D + 2 * (static_cast<int64_t>(c) * p.bstride + m);
-#pragma unroll
-        for (int fn = 0; fn < FN; ++fn) {
-          const int n = ntile * BN + nw + 8 * fn + xmapc(g);
-          if (n >= p.N) continue;
-          double* col = base + 2 * static_cast<int64_t>(n) * p.ldD;
-          double r0 = acc[fm][fn][0], i0 = acc[fm][fn][2], r1 = acc[fm][fn][1], i1 = acc[fm][fn][3];
-          if constexpr (EPI == 2) {
-            // one complex element per 16-byte store: rows m and m + 4
-            const int64_t rho0 = QK ? m : m + static_cast<int64_t>(n) * p.ldD;
-            const int64_t colx = QK ? n : static_cast<int64_t>(c);
-            if (m < p.Mlim) scatter_store_c(p.scat, rho0, colx, r0, i0);
-            if (m + 4 < p.Mlim) scatter_store_c(p.scat, rho0 + 4, colx, r1, i1);
-            continue;
-          }
-          if constexpr (ACC) {
-            if (m < p.Mlim) {
-              const double2 o = *reinterpret_cast<const double2*>(col);
-              r0 += o.x, i0 += o.y;
-            }
-            if (m + 4 < p.Mlim) {
-              const double2 o = *reinterpret_cast<const double2*>(col + 8);
-              r1 += o.x, i1 += o.y;
-            }
-          }
-          if (m < p.Mlim) stg_f64x2(col, r0, i0);
-          if (m + 4 < p.Mlim) stg_f64x2(col + 8, r1, i1);
-        }
-      }
-    }
+    tma_consume_tile<Cfg, QK, EPI>(p, mtile, ntile, smem, full_bar, empty_bar, stage, phase, fo, lane);
   }
 }
 
