@@ -122,6 +122,177 @@ static int mode_product_dev(mumode_handle_s* h, int d, const int64_t* m, int mu,
   return run_job(h, j);
 }
 
+// ------------------------------------------------------------------ chain kernel
+// middle modes run N-tile slowest (their consumers' inputs complete
+// progressively: measured better than n-fastest, 2.1 % on C2, 4.3 % at 200^3)
+#define CHAIN_N_MAJOR 1
+// Tile decode shared by the host tables and the kernel (tma_chain.cuh):
+// mode 1 m-fastest; middle modes N-tile slowest (their consumers' inputs then
+// complete progressively); the last mode n-fastest.
+static void chain_decode(const TmaParams& p, int k, int nmodes, int64_t tile, int& mt, int& nt) {
+  if (k == 0 || (CHAIN_N_MAJOR && k + 1 < nmodes)) {
+    mt = static_cast<int>(tile % p.mt);
+    nt = static_cast<int>(tile / p.mt);
+  } else {
+    nt = static_cast<int>(tile % p.nt);
+    mt = static_cast<int>(tile / p.nt);
+  }
+}
+
+// For every producer tile of mode k, the consumer (mode k+1) M-tiles whose
+// input rows it writes; targets = how many producer tiles each consumer
+// M-tile waits for.
+static void chain_boundary(const ModeJob& jp, const TmaParams& pp, int bm_p, int bn_p, const ModeJob& jc,
+                           const TmaParams& pc, int bm_c, int k, int nmodes, std::vector<int>& target,
+                           std::vector<int>& sig_off, std::vector<int>& sig_idx) {
+  const int64_t A_c = jp.A * jp.N, K_c = jc.K, AB_c = (A_c + 7) / 8, FB_c = bm_c / 8;
+  target.assign(static_cast<size_t>(pc.mt), 0);
+  sig_off.assign(1, 0);
+  sig_idx.clear();
+  std::vector<int> cur;
+  for (int64_t t = 0; t < pp.tiles; ++t) {
+    int mt, nt;
+    chain_decode(pp, k, nmodes, t, mt, nt);
+    cur.clear();
+    if (k == 0) {  // QK: rows i (= consumer a), columns = (k_c + K_c * c)
+      const int64_t i0 = int64_t(mt) * bm_p, i1 = std::min<int64_t>(i0 + bm_p, pp.Mlim);
+      const int64_t c0 = int64_t(nt) * bn_p, c1 = std::min<int64_t>(c0 + bn_p, pp.N);
+      for (int64_t c = c0 / K_c; c <= (c1 - 1) / K_c; ++c) {
+        const int64_t qlo = i0 / 8 + AB_c * c, qhi = (i1 - 1) / 8 + AB_c * c;
+        for (int64_t m = qlo / FB_c; m <= qhi / FB_c; ++m) cur.push_back(static_cast<int>(m));
+      }
+    } else {  // fragments (alpha, c') x outputs i: consumer a = a' + A_p i, c = c' / K_c
+      const int64_t A_p = jp.A, AB_p = (A_p + 7) / 8;
+      const int64_t q0 = int64_t(mt) * (bm_p / 8), q1 = std::min<int64_t>(q0 + bm_p / 8, pp.mfrags);
+      const int64_t i0 = int64_t(nt) * bn_p, i1 = std::min<int64_t>(i0 + bn_p, pp.N);
+      int last = -1;
+      for (int64_t q = q0; q < q1; ++q) {
+        const int64_t alpha = q % AB_p, cp_ = q / AB_p, c = cp_ / K_c;
+        const int64_t alo = 8 * alpha, ahi = std::min<int64_t>(8 * alpha + 8, A_p) - 1;
+        for (int64_t i = i0; i < i1; ++i) {
+          const int64_t blo = (alo + A_p * i) / 8, bhi = (ahi + A_p * i) / 8;
+          for (int64_t b = blo; b <= bhi; ++b) {
+            const int m = static_cast<int>((b + AB_c * c) / FB_c);
+            if (m != last) cur.push_back(m), last = m;
+          }
+        }
+      }
+    }
+    std::sort(cur.begin(), cur.end());
+    cur.erase(std::unique(cur.begin(), cur.end()), cur.end());
+    for (int m : cur) {
+      sig_idx.push_back(m);
+      ++target[static_cast<size_t>(m)];
+    }
+    sig_off.push_back(static_cast<int>(sig_idx.size()));
+  }
+}
+
+template <class CfgA, class CfgB>
+static int launch_chain(mumode_handle_s* h, const std::vector<ModeJob>& jobs, int cfg_a, int cfg_b) {
+  const int d = static_cast<int>(jobs.size());
+  ChainMaps maps;
+  ChainParams cp{};
+  cp.nphases = d;
+  std::vector<TmaParams> ps(static_cast<size_t>(d));
+  for (int k = 0; k < d; ++k) {
+    const CUtensorMap *mp = nullptr, *mq = nullptr;
+    if (k == 0)
+      MM_TRY(tma_setup<CfgA>(h, jobs[0], &mp, &mq, ps[0]));
+    else
+      MM_TRY(tma_setup<CfgB>(h, jobs[static_cast<size_t>(k)], &mp, &mq, ps[static_cast<size_t>(k)]));
+    maps.P[k] = *mp;
+    maps.Q[k] = *mq;
+  }
+  // dependency tables: built once per shape and config pair
+  std::vector<int64_t> key{d, jobs[0].cplx ? 1 : 0, cfg_a, cfg_b};
+  for (const auto& j : jobs) key.insert(key.end(), {j.A, j.K, j.N, j.C});
+  auto it = h->chains.find(key);
+  if (it == h->chains.end()) {
+    auto plan = std::make_unique<ChainPlan>();
+    std::vector<int> all;
+    size_t ctr = 0;
+    plan->target_off.assign(d, -1);
+    plan->sigoff_off.assign(d, -1);
+    plan->sigidx_off.assign(d, -1);
+    plan->ctr_off.assign(d, -1);
+    for (int k = 0; k + 1 < d; ++k) {
+      std::vector<int> target, sig_off, sig_idx;
+      chain_boundary(jobs[k], ps[k], k == 0 ? CfgA::BM : CfgB::BM, k == 0 ? CfgA::BN : CfgB::BN, jobs[k + 1],
+                     ps[k + 1], CfgB::BM, k, d, target, sig_off, sig_idx);
+      plan->target_off[k + 1] = static_cast<int64_t>(all.size());
+      all.insert(all.end(), target.begin(), target.end());
+      plan->sigoff_off[k] = static_cast<int64_t>(all.size());
+      all.insert(all.end(), sig_off.begin(), sig_off.end());
+      plan->sigidx_off[k] = static_cast<int64_t>(all.size());
+      all.insert(all.end(), sig_idx.begin(), sig_idx.end());
+      plan->ctr_off[k + 1] = static_cast<int64_t>(ctr);
+      ctr += target.size();
+    }
+    MM_TRY(plan->tables.ensure(std::max<size_t>(all.size(), 1) * sizeof(int)));
+    MM_CUDA(cudaMemcpy(plan->tables.p, all.data(), all.size() * sizeof(int), cudaMemcpyHostToDevice));
+    MM_TRY(plan->counters.ensure(std::max<size_t>(ctr, 1) * sizeof(int)));
+    plan->counter_ints = ctr;
+    it = h->chains.emplace(key, std::move(plan)).first;
+  }
+  const ChainPlan& pl = *it->second;
+  auto* tab = static_cast<const int*>(pl.tables.p);
+  auto* ctr = static_cast<int*>(pl.counters.p);
+  int64_t base = 0;
+  for (int k = 0; k < d; ++k) {
+    ChainPhase& P = cp.ph[k];
+    P.p = ps[static_cast<size_t>(k)];
+    P.base = base;
+    P.n_major = (CHAIN_N_MAJOR && k > 0 && k + 1 < d) ? 1 : 0;
+    base += P.p.tiles;
+    if (k > 0) {
+      P.wait_ctr = ctr + pl.ctr_off[k];
+      P.wait_target = tab + pl.target_off[k];
+    }
+    if (k + 1 < d) {
+      P.sig_off = tab + pl.sigoff_off[k];
+      P.sig_idx = tab + pl.sigidx_off[k];
+      P.sig_ctr = ctr + pl.ctr_off[k + 1];
+    }
+  }
+  cp.total = base;
+  if (pl.counter_ints) MM_CUDA(cudaMemsetAsync(pl.counters.p, 0, pl.counter_ints * sizeof(int), h->stream));
+  const int grid = static_cast<int>(std::min<int64_t>(cp.total, persistent_sms(h)));
+  auto kern = tucker_chain_kernel<CfgA, CfgB>;
+  MM_TRY(smem_opt_in(kern, CfgB::SMEM_BYTES));
+  MM_TRY(launch_pdl(kern, grid, CfgB::THREADS, CfgB::SMEM_BYTES, h->stream, maps, cp));
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return MUMODE_OK;
+}
+
+// The whole chain as one persistent launch when every mode is a plain TMA
+// product (no fused pairs / epilogue variants) and the per-mode tile configs
+// form an instantiated pair. Sets `done` when it ran.
+static int try_chain(mumode_handle_s* h, const std::vector<ModeJob>& jobs, bool& done) {
+  done = false;
+  const int d = static_cast<int>(jobs.size());
+  if (d < 2 || d > kChainMaxModes) return MUMODE_OK;
+  for (const auto& j : jobs)
+    if (j.accumulate || j.scat || j.div_front || !tma_ok(j) || !tma_worthwhile(j)) return MUMODE_OK;
+  const int a = choose_cfg(jobs[0], h->num_sms);
+  int b = -1;
+  for (int k = 1; k < d; ++k) {
+    const int c = choose_cfg(jobs[static_cast<size_t>(k)], h->num_sms);
+    if (b >= 0 && c != b) return MUMODE_OK;
+    b = c;
+  }
+  // instantiated pairs (same CTA shape and ring): 0 Big, 1 TM, 2 LM (real)
+  int rc = -1;
+  if (a == 0 && b == 0) rc = launch_chain<CfgBig, CfgBig>(h, jobs, a, b);
+  else if (a == 2 && b == 1) rc = launch_chain<CfgLM, CfgTM>(h, jobs, a, b);
+  else if (a == 1 && b == 1) rc = launch_chain<CfgTM, CfgTM>(h, jobs, a, b);
+  if (rc < 0) return MUMODE_OK;
+  MM_TRY(rc);
+  done = true;
+  return MUMODE_OK;
+}
+
 // ------------------------------------------------------------------ tucker chain
 // Modes 1..d in order (tucker.hpp:84-110). Lmat[mu] points at the stored
 // matrix; forward: op(L) = L (n x m, ld n); adjoint: op(L) = L^H (L is m x n).
@@ -261,6 +432,35 @@ static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t
       h->launches++;
     }
     return MUMODE_OK;
+  }
+  if (h->policy == 11 && !div_front && nmodes >= 2) {
+    // one persistent launch for the whole chain (tma_chain.cuh)
+    std::vector<ModeJob> jobs;
+    std::vector<int64_t> e2(ext);
+    const double* src2 = src;
+    for (int mu = mu_lo; mu <= mu_hi; ++mu) {
+      ModeJob j;
+      j.T = src2;
+      j.L = Lop[mu - 1];
+      j.S = (mu == mu_hi) ? S : static_cast<double*>(h->ws[(mu - mu_lo) % 2].p);
+      j.A = prod(e2.data(), 0, mu - 1);
+      j.K = e2[mu - 1];
+      j.C = prod(e2.data(), mu, d);
+      j.N = n[mu - 1];
+      j.sLi = 1;
+      j.sLk = n[mu - 1];
+      j.cplx = cplx;
+      j.conj = false;
+      jobs.push_back(j);
+      e2[mu - 1] = n[mu - 1];
+      src2 = j.S;
+    }
+    // the chain kernel's first mode must be a QK (mode 1) product
+    if (mu_lo == 1) {
+      bool done = false;
+      MM_TRY(try_chain(h, jobs, done));
+      if (done) return MUMODE_OK;
+    }
   }
   for (int mu = mu_lo; mu <= mu_hi; ++mu) {
     double* dst = (mu == mu_hi) ? S : static_cast<double*>(h->ws[(mu - mu_lo) % 2].p);

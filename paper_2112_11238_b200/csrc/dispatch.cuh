@@ -106,11 +106,14 @@ static int choose_cfg(const ModeJob& j, int sms) {
   return best;
 }
 
+// Tensor maps and kernel parameters of one mode product for tile config Cfg
+// (shared by the single-mode launch and the chain kernel).
 template <class Cfg>
-static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
+static int tma_setup(mumode_handle_s* h, const ModeJob& j, const CUtensorMap** mpo, const CUtensorMap** mqo,
+                     TmaParams& p) {
   const CUtensorMap* mp = nullptr;
   const CUtensorMap* mq = nullptr;
-  TmaParams p{};
+  p = TmaParams{};
   p.D = j.S;
   const bool mode1 = (j.A == 1);
   constexpr uint32_t BM8 = Cfg::BM / 8, BN8 = Cfg::BN / 8, BK8 = Cfg::BK / 8;
@@ -182,10 +185,22 @@ static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
   p.mt = int((p.mfrags + Cfg::BM / 8 - 1) / (Cfg::BM / 8));
   p.nt = (p.N + Cfg::BN - 1) / Cfg::BN;
   p.tiles = int64_t(p.mt) * p.nt;
-  const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
   p.scat = j.scat;
   p.div_front = j.div_front;
   p.div_last = j.div_last;
+  *mpo = mp;
+  *mqo = mq;
+  return MUMODE_OK;
+}
+
+template <class Cfg>
+static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
+  const CUtensorMap* mp = nullptr;
+  const CUtensorMap* mq = nullptr;
+  TmaParams p;
+  MM_TRY(tma_setup<Cfg>(h, j, &mp, &mq, p));
+  const bool mode1 = (j.A == 1);
+  const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
   if (j.div_front) {
     if constexpr (Cfg::E == 1) {
       if (mode1 || j.C != 1) return fail(MUMODE_ERR_ARGUMENT, "divide epilogue: last mode of order >= 2 only");

@@ -25,6 +25,7 @@
 #include "tma_dmma.cuh"
 #include "fused.cuh"
 #include "tail.cuh"
+#include "tma_chain.cuh"
 #include "ldg_dmma.cuh"
 
 namespace mumode_gpu {
@@ -83,6 +84,16 @@ struct MapKeyHash {
   }
 };
 
+// Dependency tables of the chain kernel for one shape and config pair
+// (tma_chain.cuh): per mode boundary, the consumer M-tile counters' targets
+// and the CSR list of counters each producer tile increments.
+struct ChainPlan {
+  DevBuf tables;    // int32 targets / sig_off / sig_idx of every boundary
+  DevBuf counters;  // int32, zeroed per launch
+  size_t counter_ints = 0;
+  std::vector<int64_t> target_off, sigoff_off, sigidx_off, ctr_off;  // per mode, in ints
+};
+
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
   int64_t nodes = 0;
@@ -108,6 +119,7 @@ struct mumode_handle_s {
   std::vector<cudaEvent_t> events;                            // pipeline events (reused)
   std::unordered_map<mumode_gpu::MapKey, CUtensorMap, mumode_gpu::MapKeyHash> maps;
   std::map<std::vector<uint64_t>, mumode_gpu::GraphEntry> graphs;
+  std::map<std::vector<int64_t>, std::unique_ptr<mumode_gpu::ChainPlan>> chains;  // per shape + configs
 };
 
 namespace mumode_gpu {
@@ -411,7 +423,7 @@ void* mumode_get_stream(mumode_handle_t h) { return h ? static_cast<void*>(h->st
 int64_t mumode_launch_count(mumode_handle_t h) { return h ? h->launches : -1; }
 
 int mumode_set_kernel_policy(mumode_handle_t h, int policy) {
-  if (!h || policy < 0 || policy > 10) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
+  if (!h || policy < 0 || policy > 11) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
   // 3..6 force real tile configuration 0..3 / complex configuration 0..3
   h->policy = policy;
   return MUMODE_OK;

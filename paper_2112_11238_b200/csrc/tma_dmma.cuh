@@ -260,10 +260,17 @@ __device__ __forceinline__ FragOffsets tma_frag_offsets(int warp, int lane) {
 
 // One output tile, MMA-warp side: consume the tile's K-stages from the ring
 // (DMMA), then the epilogue (EPI) straight from registers.
-template <class Cfg, bool QK, int EPI>
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// (before_epilogue runs between the main loop and the epilogue: the chain
+// kernel publishes the previous tile there)
+template <class Cfg, bool QK, int EPI, class Hook = NoHook>
 __device__ __forceinline__ void tma_consume_tile(const TmaParams& p, int mtile, int ntile, const uint8_t* smem,
                                                  uint64_t* full_bar, uint64_t* empty_bar, int& stage,
-                                                 uint32_t& phase, const FragOffsets& fo, int lane) {
+                                                 uint32_t& phase, const FragOffsets& fo, int lane,
+                                                 const Hook& before_epilogue = Hook()) {
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
   constexpr int FM = Cfg::FM, FN = Cfg::FN, E = Cfg::E, ROW = Cfg::ROW;
   constexpr bool CPLX = (E == 2);
@@ -344,6 +351,7 @@ __device__ __forceinline__ void tma_consume_tile(const TmaParams& p, int mtile, 
     }
   }
 
+  before_epilogue();
   // epilogue straight from registers
 #pragma unroll
   for (int fm = 0; fm < FM; ++fm) {
