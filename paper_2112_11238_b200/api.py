@@ -101,7 +101,10 @@ class Handle:
         return int(_lib.lib().mumode_launch_count(self.h))
 
     def set_kernel_policy(self, policy: int) -> None:
-        """0 auto, 1 generic SIMT kernel only, 2 prefer the TMA/DMMA kernel."""
+        """Kernel path selection for tests / benchmarks (include/mumode_gpu.h):
+        0 auto, 1 SIMT kernel, 2 TMA/DMMA where legal, 3..6 one TMA tile
+        config forced, 7 auto incl. fused pairs, 8 LDG-staged DMMA, 9 / 10 tail
+        pass forced / disabled, 11 whole chains as one persistent launch."""
         _check(_lib.lib().mumode_set_kernel_policy(self.h, int(policy)))
 
     def close(self) -> None:
