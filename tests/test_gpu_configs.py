@@ -111,6 +111,27 @@ def test_c4_complex_rectangular():
 
 
 @needs_ref
+def test_c4_size_adjoint_promotion_kronsumv_against_reference():
+    # the section 8(f) operators at BASELINE scale against the reference
+    # library itself: cttucker (the HLF analysis direction, Psi^H), the
+    # real-tensor x complex-stack promotion, and kronsumv (the RK4/CG driver)
+    g = mm.Rng(77)
+    Tc = g.normal((192, 192, 192), True)
+    Psis = [g.normal((192, 128), True) for _ in range(3)]  # stored m x n: applies Psi^H
+    S = host(mm.cttucker(dev(Tc), [dev(P) for P in Psis]))
+    assert S.shape == (128, 128, 128)
+    assert O.rel_fro(S, O.ref_tucker(Tc, Psis, "cttucker")) < TOL
+    Tr = g.normal((128, 128, 128))
+    Ls = [g.normal((192, 128), True) for _ in range(3)]
+    S = host(mm.tucker(dev(Tr), [dev(L) for L in Ls]))
+    assert O.rel_fro(S, O.ref_tucker(Tr, Ls)) < TOL
+    V = g.normal((200, 200, 200))
+    As = [g.normal((200, 200)) for _ in range(3)]
+    W = host(mm.kronsumv(dev(V), [dev(A) for A in As]))
+    assert O.rel_fro(W, O.ref_tucker(V, As, "kronsumv")) < TOL
+
+
+@needs_ref
 def test_c5_6d_tucker():
     g = mm.Rng(1234)
     T = g.normal((24,) * 6)
