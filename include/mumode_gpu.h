@@ -220,6 +220,16 @@ int mumode_host_mode_product_c128(mumode_handle_t h, int d, const int64_t* m, in
                                   int64_t n_mu, const double* T, const double* L, double* S);
 int mumode_host_tucker_f64(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
                            const double* T, const double* const* L, double* S, int adjoint);
+/* Enqueue-only variant of mumode_host_tucker_f64 (forward, real): returns
+ * after queuing the upload, the chain and the download. Consecutive calls
+ * alternate two device staging slots, so one call's download overlaps the
+ * next call's upload (PCIe full duplex). T, L and S must stay valid (and S
+ * unread) until mumode_host_wait; T and S in pinned memory make it fully
+ * asynchronous (pageable buffers still work, with host-blocking copies). */
+int mumode_host_tucker_f64_async(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                                 const double* T, const double* const* L, double* S);
+/* Wait for every queued host-buffer call on the handle. */
+int mumode_host_wait(mumode_handle_t h);
 int mumode_host_tucker_c128(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
                             const double* T, const double* const* L, double* S, int adjoint);
 int mumode_host_tucker_promote(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,

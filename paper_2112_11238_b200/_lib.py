@@ -62,6 +62,8 @@ SIGNATURES = {
     "mumode_host_mode_product_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, ctypes.c_int, I64, VP, VP, VP]),
     "mumode_host_mode_product_c128": (ctypes.c_int, [H, ctypes.c_int, I64P, ctypes.c_int, I64, VP, VP, VP]),
     "mumode_host_tucker_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
+    "mumode_host_tucker_f64_async": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP]),
+    "mumode_host_wait": (ctypes.c_int, [H]),
     "mumode_host_tucker_c128": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
     "mumode_host_tucker_promote": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
     "mumode_host_kronsumv_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, VP, ctypes.POINTER(VP), VP]),

@@ -115,6 +115,8 @@ struct mumode_handle_s {
   mumode_gpu::DevBuf scat_params, scat_tmp, scat_mid;  // scatter table; fallback output; chain intermediate
   mumode_gpu::DevBuf lbuf;      // materialised op(L) for adjoint / promotion
   mumode_gpu::DevBuf host_in, host_out, host_mats, host_mid;  // host drop-in staging
+  mumode_gpu::DevBuf slot_in[2], slot_out[2], slot_mats[2];   // pipelined host calls, double-buffered
+  int64_t host_calls = 0;
   cudaStream_t copy_in = nullptr, copy_out = nullptr;         // host drop-in copy engines
   std::vector<cudaEvent_t> events;                            // pipeline events (reused)
   std::unordered_map<mumode_gpu::MapKey, CUtensorMap, mumode_gpu::MapKeyHash> maps;
@@ -757,33 +759,56 @@ static int ensure_pipeline(mumode_handle_t h, size_t nev) {
   return MUMODE_OK;
 }
 
-static int host_tucker_pipelined(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
-                                 const double* T, const double* const* L, double* S) {
-  constexpr int kChunks = 8;
-  MM_TRY(ensure_pipeline(h, 2 * kChunks + 2));
-  cudaEvent_t* ev = h->events.data();
+// One pipelined host-buffer application, enqueued only: the slot's staging
+// buffers (input, factors, output) alternate between consecutive calls, so
+// call k+1's upload (copy_in) runs while call k's download (copy_out) drains
+// -- PCIe is full duplex. The intermediate is one buffer: the compute stream
+// serialises the calls. Per-slot events guard slot reuse on the device; the
+// host never waits here.
+constexpr int kHostChunks = 8;
+constexpr int kSlotEvents = 2 * kHostChunks + 2;  // slabs, blocks, compute end, download end
+
+static int host_tucker_enqueue(mumode_handle_t h, int d, const int64_t* m, const int64_t* n, const double* T,
+                               const double* const* L, double* S) {
+  constexpr int kChunks = kHostChunks;
+  const int slot = static_cast<int>(h->host_calls & 1);
+  const bool reuse = h->host_calls >= 2;  // the slot's previous call must be done with it
+  ++h->host_calls;
+  MM_TRY(ensure_pipeline(h, 2 * kSlotEvents));
+  cudaEvent_t* ev = h->events.data() + slot * kSlotEvents;
+  cudaEvent_t ev_compute_end = ev[2 * kChunks], ev_d2h_end = ev[2 * kChunks + 1];
   const int64_t md = m[d - 1], nd = n[d - 1];
   const int64_t in_slab = prod(m, 0, d - 1);   // elements per unit of the last input mode
   const int64_t A = prod(n, 0, d - 1);         // rows of the (A x m_d) intermediate
-  // factors: one contiguous upload
   size_t mat_bytes = 0;
   for (int k = 0; k < d; ++k) mat_bytes += ((size_t(m[k] * n[k]) * sizeof(double) + 255) / 256) * 256;
-  MM_TRY(h->host_mats.ensure(mat_bytes + 256));
-  MM_TRY(h->host_in.ensure(size_t(in_slab * md) * sizeof(double)));
-  MM_TRY(h->host_mid.ensure(size_t(A * md) * sizeof(double)));
-  MM_TRY(h->host_out.ensure(size_t(A * nd) * sizeof(double)));
+  // growing a staging buffer frees memory that queued calls may still use
+  const size_t in_bytes = size_t(in_slab * md) * sizeof(double), mid_bytes = size_t(A * md) * sizeof(double),
+               out_bytes = size_t(A * nd) * sizeof(double);
+  if (h->slot_mats[slot].bytes < mat_bytes + 256 || h->slot_in[slot].bytes < in_bytes ||
+      h->host_mid.bytes < mid_bytes || h->slot_out[slot].bytes < out_bytes) {
+    if (h->copy_in) MM_CUDA(cudaStreamSynchronize(h->copy_in));
+    MM_CUDA(cudaStreamSynchronize(h->stream));
+    if (h->copy_out) MM_CUDA(cudaStreamSynchronize(h->copy_out));
+  }
+  MM_TRY(h->slot_mats[slot].ensure(mat_bytes + 256));
+  MM_TRY(h->slot_in[slot].ensure(in_bytes));
+  MM_TRY(h->host_mid.ensure(mid_bytes));
+  MM_TRY(h->slot_out[slot].ensure(out_bytes));
+  // the slot's input and factors are free once its previous call's compute ended
+  if (reuse) MM_CUDA(cudaStreamWaitEvent(h->copy_in, ev_compute_end, 0));
   std::vector<const double*> dL(d);
   size_t off = 0;
   for (int k = 0; k < d; ++k) {
     const size_t b = size_t(m[k] * n[k]) * sizeof(double);
-    MM_CUDA(cudaMemcpyAsync(static_cast<char*>(h->host_mats.p) + off, L[k], b, cudaMemcpyHostToDevice,
+    MM_CUDA(cudaMemcpyAsync(static_cast<char*>(h->slot_mats[slot].p) + off, L[k], b, cudaMemcpyHostToDevice,
                             h->copy_in));
-    dL[k] = reinterpret_cast<const double*>(static_cast<char*>(h->host_mats.p) + off);
+    dL[k] = reinterpret_cast<const double*>(static_cast<char*>(h->slot_mats[slot].p) + off);
     off += ((b + 255) / 256) * 256;
   }
-  double* dT = static_cast<double*>(h->host_in.p);
+  double* dT = static_cast<double*>(h->slot_in[slot].p);
   double* dY = static_cast<double*>(h->host_mid.p);
-  double* dS = static_cast<double*>(h->host_out.p);
+  double* dS = static_cast<double*>(h->slot_out[slot].p);
   // input slabs of the last mode (8-aligned boundaries keep TMA bases 16-B aligned)
   auto bounds = [](int64_t total, int parts, int64_t q, int64_t align) {
     int64_t step = (total + parts - 1) / parts;
@@ -807,6 +832,8 @@ static int host_tucker_pipelined(mumode_handle_t h, int d, const int64_t* m, con
     MM_TRY(tucker_dev(h, d, ms.data(), ns.data(), dT + c0 * in_slab, dL.data(), dY + c0 * A, false, false, 1,
                       d - 1));
   }
+  // the slot's output is free once its previous call's download ended
+  if (reuse) MM_CUDA(cudaStreamWaitEvent(cs, ev_d2h_end, 0));
   // last mode in row blocks of L_d -> contiguous slabs of S, streamed back
   const int64_t ym[2] = {A, md};
   for (int q = 0; q < kChunks; ++q) {
@@ -818,9 +845,21 @@ static int host_tucker_pipelined(mumode_handle_t h, int d, const int64_t* m, con
     MM_CUDA(cudaMemcpyAsync(S + i0 * A, dS + i0 * A, size_t((i1 - i0) * A) * sizeof(double), cudaMemcpyDeviceToHost,
                             h->copy_out));
   }
-  MM_CUDA(cudaStreamSynchronize(h->copy_out));
-  MM_CUDA(cudaStreamSynchronize(cs));
+  MM_CUDA(cudaEventRecord(ev_compute_end, cs));
+  MM_CUDA(cudaEventRecord(ev_d2h_end, h->copy_out));
   return MUMODE_OK;
+}
+
+static int host_wait(mumode_handle_t h) {
+  if (h->copy_in) MM_CUDA(cudaStreamSynchronize(h->copy_in));
+  MM_CUDA(cudaStreamSynchronize(h->stream));
+  if (h->copy_out) MM_CUDA(cudaStreamSynchronize(h->copy_out));
+  return MUMODE_OK;
+}
+
+static bool host_pipelinable(int d, const int64_t* m, const int64_t* n, int adjoint, int t_el, int l_el) {
+  return d >= 2 && !adjoint && t_el == 1 && l_el == 1 && m[d - 1] >= 16 && n[d - 1] >= 16 &&
+         prod(m, 0, d) >= (int64_t(1) << 20);
 }
 
 static int host_tucker_impl(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
@@ -829,9 +868,10 @@ static int host_tucker_impl(mumode_handle_t h, int d, const int64_t* m, const in
   if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
   MM_TRY(check_stack(d, m, n, T, L, S, adjoint ? "cttucker" : "tucker"));
   MM_CUDA(cudaSetDevice(h->device));
-  if (d >= 2 && !adjoint && t_el == 1 && l_el == 1 && m[d - 1] >= 16 && n[d - 1] >= 16 &&
-      prod(m, 0, d) >= (int64_t(1) << 20))
-    return host_tucker_pipelined(h, d, m, n, T, L, S);
+  if (host_pipelinable(d, m, n, adjoint, t_el, l_el)) {
+    MM_TRY(host_tucker_enqueue(h, d, m, n, T, L, S));
+    return host_wait(h);
+  }
   std::vector<int64_t> lsz(d);
   for (int k = 0; k < d; ++k) lsz[k] = m[k] * n[k] * l_el;
   const double* dT;
@@ -851,6 +891,21 @@ int mumode_host_tucker_f64(mumode_handle_t h, int d, const int64_t* m, const int
                            const double* T, const double* const* L, double* S, int adjoint) {
   return host_tucker_impl(h, d, m, n, T, L, S, adjoint, 1, 1);
 }
+int mumode_host_tucker_f64_async(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
+                                 const double* T, const double* const* L, double* S) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  MM_TRY(check_stack(d, m, n, T, L, S, "tucker"));
+  MM_CUDA(cudaSetDevice(h->device));
+  if (!host_pipelinable(d, m, n, 0, 1, 1)) return host_tucker_impl(h, d, m, n, T, L, S, 0, 1, 1);
+  return host_tucker_enqueue(h, d, m, n, T, L, S);
+}
+
+int mumode_host_wait(mumode_handle_t h) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  MM_CUDA(cudaSetDevice(h->device));
+  return host_wait(h);
+}
+
 int mumode_host_tucker_c128(mumode_handle_t h, int d, const int64_t* m, const int64_t* n,
                             const double* T, const double* const* L, double* S, int adjoint) {
   return host_tucker_impl(h, d, m, n, T, L, S, adjoint, 2, 2);

@@ -373,6 +373,43 @@ def test_pipelined_host_path_bitwise_equals_device_path(m, n):
         assert O.rel_fro(Sh, O.port_tucker(T, Ls)) < 1e-14
 
 
+def test_async_host_calls_bitwise_equal_sync():
+    # mumode_host_tucker_f64_async: K calls queued back to back on two
+    # alternating staging slots (call k+1 uploads while call k downloads),
+    # then one mumode_host_wait; every result equals the synchronous call's
+    from paper_2112_11238_b200 import _lib
+
+    lib = _lib.lib()
+    h = mm.get_handle(0)
+    rng = np.random.default_rng(77)
+    m, n = (96, 88, 136), (88, 104, 120)
+    Ls = [rnd(rng, (n[k], m[k])) for k in range(3)]
+    Lp = _lib.ptr_array([L.ctypes.data for L in Ls])
+    Ts = [torch.from_numpy(rnd(rng, m).ravel(order="F")).pin_memory() for _ in range(5)]
+    Ss = [torch.full((int(np.prod(n)),), np.nan, dtype=torch.float64).pin_memory() for _ in range(5)]
+    mi, ni = _lib.i64_array(m), _lib.i64_array(n)
+    for T, S in zip(Ts, Ss):
+        assert lib.mumode_host_tucker_f64_async(h.h, 3, mi, ni, T.data_ptr(), Lp, S.data_ptr()) == 0
+    assert lib.mumode_host_wait(h.h) == 0
+    for T, S in zip(Ts, Ss):
+        ref = np.empty(n, order="F")
+        assert lib.mumode_host_tucker_f64(h.h, 3, mi, ni, T.data_ptr(), Lp, ref.ctypes.data, 0) == 0
+        np.testing.assert_array_equal(S.numpy(), ref.ravel(order="F"))
+    # a shape change between queued calls (staging buffers grow) stays correct
+    m2, n2 = (128, 128, 128), (128, 128, 128)
+    L2 = [rnd(rng, (128, 128)) for _ in range(3)]
+    T2 = rnd(rng, m2)
+    S2 = np.empty(n2, order="F")
+    S1 = np.empty(n, order="F")
+    T1 = np.asfortranarray(Ts[0].numpy().reshape(m, order="F"))
+    assert lib.mumode_host_tucker_f64_async(h.h, 3, mi, ni, T1.ctypes.data, Lp, S1.ctypes.data) == 0
+    assert lib.mumode_host_tucker_f64_async(h.h, 3, _lib.i64_array(m2), _lib.i64_array(n2), T2.ctypes.data,
+                                            _lib.ptr_array([L.ctypes.data for L in L2]), S2.ctypes.data) == 0
+    assert lib.mumode_host_wait(h.h) == 0
+    np.testing.assert_array_equal(S1.ravel(order="F"), Ss[0].numpy())
+    assert O.rel_fro(S2, O.port_tucker(T2, L2)) < 1e-14
+
+
 def test_host_and_device_paths_agree_bitwise():
     rng = np.random.default_rng(7)
     T = rnd(rng, (64, 64, 64))
