@@ -29,8 +29,9 @@ using CfgTM = TmaCfg<128, 40, 40, 3, 16, 1>;   // T-side M, small L-side N (n = 
 using CfgLM = TmaCfg<40, 128, 40, 3, 1, 16>;   // small L-side M, T-side N (mode 1, n = 40k)
 using CfgMid = TmaCfg<64, 128, 32, 4, 2, 4>;   // 32x32 warp tiles
 // complex128 (E = 2): 4 real DMMAs per complex MAC, 16-B elements
-using CfgCa = TmaCfg<64, 128, 16, 4, 4, 4, 2>;  // 16 MMA warps, 16x32 complex warp tiles
-using CfgCb = TmaCfg<128, 64, 16, 4, 4, 4, 2>;
+// (four accumulator chains per complex output: warp tiles hold 32 outputs)
+using CfgCa = TmaCfg<64, 64, 16, 6, 2, 4, 2>;  // 8 MMA warps, 32x16 complex warp tiles
+using CfgCb = TmaCfg<128, 32, 16, 5, 4, 2, 2>;  // 8 MMA warps, 32x16
 using CfgCc = TmaCfg<96, 32, 16, 4, 4, 4, 2>;   // 24x8 warp tiles, fine-grained
 using CfgCd = TmaCfg<192, 16, 16, 4, 8, 1, 2>;
 

@@ -45,11 +45,13 @@ __global__ void __launch_bounds__(kGenThreads)
   const V* L = reinterpret_cast<const V*>(g.L);
   V* S = reinterpret_cast<V*>(g.S);
 
-  V acc[kGenRows / 4];
+  // complex: four real chains (rr, ii, ri, ir) combined at the end, as
+  // OpenBLAS's zgemm kernels do (re = rr - ii, im = ri + ir)
+  V acc[kGenRows / 4], acc2[kGenRows / 4];
 #pragma unroll
   for (int j = 0; j < kGenRows / 4; ++j) {
-    if constexpr (CPLX) acc[j] = make_double2(0.0, 0.0);
-    else acc[j] = 0.0;
+    if constexpr (CPLX) acc[j] = acc2[j] = make_double2(0.0, 0.0);
+    else acc[j] = acc2[j] = 0.0;
   }
 
   for (int64_t k0 = 0; k0 < g.K; k0 += kGenK) {
@@ -88,10 +90,10 @@ __global__ void __launch_bounds__(kGenThreads)
       for (int j = 0; j < kGenRows / 4; ++j) {
         const V l = Ls[kk][ig + 4 * j];
         if constexpr (CPLX) {
-          acc[j].x = fma(l.x, t.x, acc[j].x);
-          acc[j].x = fma(-l.y, t.y, acc[j].x);
-          acc[j].y = fma(l.x, t.y, acc[j].y);
-          acc[j].y = fma(l.y, t.x, acc[j].y);
+          acc[j].x = fma(l.x, t.x, acc[j].x);    // rr
+          acc2[j].x = fma(l.y, t.y, acc2[j].x);  // ii
+          acc[j].y = fma(l.x, t.y, acc[j].y);    // ri
+          acc2[j].y = fma(l.y, t.x, acc2[j].y);  // ir
         } else {
           acc[j] = fma(l, t, acc[j]);
         }
@@ -100,6 +102,10 @@ __global__ void __launch_bounds__(kGenThreads)
     __syncthreads();
   }
 
+  if constexpr (CPLX) {
+#pragma unroll
+    for (int j = 0; j < kGenRows / 4; ++j) acc[j] = make_double2(acc[j].x - acc2[j].x, acc[j].y + acc2[j].y);
+  }
   const int64_t f = f0 + fl;
   if (f < nfib) {
     const int64_t a = f % g.A, c = f / g.A;

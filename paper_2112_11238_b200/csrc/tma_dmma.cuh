@@ -279,14 +279,18 @@ __device__ __forceinline__ void tma_consume_tile(const TmaParams& p, int mtile, 
   const int KT = (p.K + BK - 1) / BK;
   const int g = fo.g, t = fo.t, mw = fo.mw, nw = fo.nw;
   const uint32_t J0 = fo.J0, xk_off = fo.xk_off, kx_off = fo.kx_off;
-  // real: acc[fm][fn][0..1]; complex: re in [0..1], im in [2..3]
-  double acc[FM][FN][2 * E];
+  // real: acc[fm][fn][0..1]. complex: four real chains, as OpenBLAS's zgemm
+  // kernels keep them -- [0..1] sum qr*pr, [2..3] sum qi*pi, [4..5] sum qr*pi,
+  // [6..7] sum qi*pr -- combined once in the epilogue (re = rr - ii,
+  // im = ri + ir), so complex results round like the reference's cblas_zgemm
+  constexpr int NACC = CPLX ? 8 : 2;
+  double acc[FM][FN][NACC];
 #pragma unroll
   for (int fm = 0; fm < FM; ++fm)
 #pragma unroll
     for (int fn = 0; fn < FN; ++fn)
 #pragma unroll
-      for (int r = 0; r < 2 * E; ++r) acc[fm][fn][r] = 0.0;
+      for (int r = 0; r < NACC; ++r) acc[fm][fn][r] = 0.0;
 
   for (int kb = 0; kb < KT; ++kb) {
     mbar_wait(&full_bar[stage], phase);
@@ -329,18 +333,16 @@ __device__ __forceinline__ void tma_consume_tile(const TmaParams& p, int mtile, 
             qf[fn] = *reinterpret_cast<const double2*>(sQ + ((nw >> 3) + fn) * (BK * ROW) + (4 * s) * ROW +
                                                        xk_off + Js);
         }
-        // complex MAC as four real DMMAs: re += qr*pr - qi*pi, im += qr*pi + qi*pr
+        // complex MAC as four real DMMAs into four separate chains
 #pragma unroll
-        for (int fn = 0; fn < FN; ++fn) {
-          const double qneg = -qf[fn].y;
+        for (int fn = 0; fn < FN; ++fn)
 #pragma unroll
           for (int fm = 0; fm < FM; ++fm) {
             dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], qf[fn].x, pf[fm].x);
-            dmma_8x8x4(acc[fm][fn][0], acc[fm][fn][1], qneg, pf[fm].y);
-            dmma_8x8x4(acc[fm][fn][2], acc[fm][fn][3], qf[fn].x, pf[fm].y);
-            dmma_8x8x4(acc[fm][fn][2], acc[fm][fn][3], qf[fn].y, pf[fm].x);
+            dmma_8x8x4(acc[fm][fn][2], acc[fm][fn][3], qf[fn].y, pf[fm].y);
+            dmma_8x8x4(acc[fm][fn][4], acc[fm][fn][5], qf[fn].x, pf[fm].y);
+            dmma_8x8x4(acc[fm][fn][6], acc[fm][fn][7], qf[fn].y, pf[fm].x);
           }
-        }
       }
     }
     __syncwarp();
@@ -403,7 +405,8 @@ __device__ __forceinline__ void tma_consume_tile(const TmaParams& p, int mtile, 
         const int n = ntile * BN + nw + 8 * fn + xmapc(g);
         if (n >= p.N) continue;
         double* col = base + 2 * static_cast<int64_t>(n) * p.ldD;
-        double r0 = acc[fm][fn][0], i0 = acc[fm][fn][2], r1 = acc[fm][fn][1], i1 = acc[fm][fn][3];
+        double r0 = acc[fm][fn][0] - acc[fm][fn][2], r1 = acc[fm][fn][1] - acc[fm][fn][3];
+        double i0 = acc[fm][fn][4] + acc[fm][fn][6], i1 = acc[fm][fn][5] + acc[fm][fn][7];
         if constexpr (EPI == 2) {
           // one complex element per 16-byte store: rows m and m + 4
           const int64_t rho0 = QK ? m : m + static_cast<int64_t>(n) * p.ldD;

@@ -305,6 +305,30 @@ def test_complex_medium_shapes_all_modes(policy):
         assert O.rel_fro(host(mm.cttucker(dev(T), [dev(P) for P in Ps])), O.port_tucker(T, Ps, adjoint=True)) < 1e-14
 
 
+def test_complex_against_reference(policy):
+    # every complex kernel keeps four real chains per output (rr, ii, ri, ir)
+    # combined once, like OpenBLAS's main zgemm kernels; mode products, Tucker
+    # chains, cttucker (conjugate-transpose factors) and real->complex
+    # promotion against the reference library. Exact equality holds where
+    # OpenBLAS's main kernel computes the element (its M/N edge kernels and
+    # thread partitions group differently), so the bound is 1 ulp-level.
+    if not O.ref_available():
+        pytest.skip("reference library not built")
+    rng = np.random.default_rng(18)
+    for m, n in [((32, 24, 40), (48, 36, 56)), ((33, 17, 20), (20, 31, 9)), ((64, 64, 64), (96, 96, 96))]:
+        T = rnd(rng, m, True)
+        Ls = [rnd(rng, (n[k], m[k]), True) for k in range(3)]
+        for mu in (1, 2, 3):
+            S = host(mm.mode_product(dev(T), dev(Ls[mu - 1]), mu))
+            assert O.rel_max(S, O.ref_mode_product(T, Ls[mu - 1], mu)) < 1e-14, (m, mu)
+        assert O.rel_fro(host(mm.tucker(dev(T), [dev(L) for L in Ls])), O.ref_tucker(T, Ls)) < 1e-15
+        Ps = [rnd(rng, (m[k], n[k]), True) for k in range(3)]
+        assert O.rel_fro(host(mm.cttucker(dev(T), [dev(P) for P in Ps])),
+                         O.ref_tucker(T, Ps, variant="cttucker")) < 1e-15
+        Tr = rnd(rng, m)
+        assert O.rel_fro(host(mm.tucker(dev(Tr), [dev(L) for L in Ls])), O.ref_tucker(Tr, Ls)) < 1e-15
+
+
 @pytest.mark.parametrize("shape", [(8,) * 6, (16,) * 4, (24,) * 4, (24,) * 5, (24,) * 3, (32,) * 3, (16, 16),
                                    (8,) * 4, (16,) * 5, (8,) * 8])
 def test_fused_small_square_modes(policy, shape):
