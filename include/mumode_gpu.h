@@ -70,7 +70,9 @@ int64_t mumode_launch_count(mumode_handle_t h);
  * 8 = force the LDG-staged DMMA kernel for real products, 9 = auto with the
  * 32-wide strided-pair (tail) pass forced wherever the shape allows it,
  * 10 = auto with the tail pass disabled, 11 = auto with whole Tucker chains
- * run as one persistent launch where the tile configs allow (tma_chain.cuh).
+ * run as one persistent launch where the tile configs allow (tma_chain.cuh),
+ * 12 = auto with the fused passes' non-warp-specialised kernels
+ * (fused_pair_kernel / tail_pair_kernel instead of fused_ws / tail_ws).
  * Not a fallback switch: all are CUDA kernels. */
 int mumode_set_kernel_policy(mumode_handle_t h, int policy);
 

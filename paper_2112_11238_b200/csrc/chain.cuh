@@ -34,6 +34,25 @@ static int launch_fused(mumode_handle_s* h, const double* T, double* S, const do
   return MUMODE_OK;
 }
 
+// Warp-specialised first pass (fused_ws.cuh): modes 1 and 2.
+template <int MU>
+static int launch_fused_ws(mumode_handle_s* h, const double* T, double* S, const double* L1,
+                           const double* L2, int64_t C) {
+  using Cfg = FusedWsCfg<MU>;
+  const CUtensorMap* mp = nullptr;
+  FusedParams p{S, L1, L2, 1, C, (C + 7) / 8};
+  uint64_t d[3] = {8, uint64_t(MU) * uint64_t(C), uint64_t(MU / 8)}, st[2] = {uint64_t(MU), 8};
+  uint32_t b[3] = {8, 8 * MU, MU / 8};
+  MM_TRY(get_map(h, T, 3, d, st, b, &mp));
+  const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
+  auto k = fused_ws_kernel<MU, 2>;
+  MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
+  MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, p));
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return MUMODE_OK;
+}
+
 // Strided-pair pass with 32-wide a tiles (tail.cuh): 256-B rows for loads and
 // stores instead of 64-B ones.
 template <int MU>
@@ -56,17 +75,44 @@ static int launch_tail(mumode_handle_s* h, const double* T, double* S, const dou
   return MUMODE_OK;
 }
 
-// The tail kernel pays off once the a-stride makes every tile row a new page
-// (policy 9 forces it wherever the shape allows, 10 disables it).
+template <int MU>
+static int launch_tail_ws(mumode_handle_s* h, const double* T, double* S, const double* L1,
+                          const double* L2, int64_t A, int64_t C) {
+  using Cfg = TailWsCfg<MU>;
+  const CUtensorMap *mx = nullptr, *ms = nullptr;
+  uint64_t d[5] = {16, uint64_t(A / 16), uint64_t(MU), uint64_t(MU), uint64_t(C)};
+  uint64_t st[4] = {16, uint64_t(A), uint64_t(A) * MU, uint64_t(A) * MU * MU};
+  uint32_t bx[5] = {16, 2, MU, Cfg::KB, 1}, bs[5] = {16, 2, 1, MU, 1};
+  MM_TRY(get_map(h, T, 5, d, st, bx, &mx, true));
+  MM_TRY(get_map(h, S, 5, d, st, bs, &ms, true));
+  TailParams p{L1, L2, A / 32, (A / 32) * C};
+  const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
+  auto k = tail_ws_kernel<MU>;
+  MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
+  MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mx, *ms, p));
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return MUMODE_OK;
+}
+
+// The tail kernels pay off once the a-stride makes every tile row a new page
+// (and for MU = 8 at any A: 8^8 middle passes 60-80 -> 51 us). Policy 9
+// forces the tail path wherever the shape allows, 10 disables it, 12 runs the
+// kernels without warp specialisation (fused_pair_kernel for the first pass,
+// tail_pair_kernel for the tail).
 static constexpr int64_t kTailMinA = 16384;
 
 template <int MU>
 static int launch_fused_mu(mumode_handle_s* h, bool first, const double* T, double* S,
                            const double* L1, const double* L2, int64_t A, int64_t C) {
+  const bool legacy = h->policy == 12;
+  if constexpr (MU <= 24) {
+    if (first && !legacy) return launch_fused_ws<MU>(h, T, S, L1, L2, C);
+  }
   if (first) return launch_fused<MU, true, 8>(h, T, S, L1, L2, A, C);
   if constexpr (MU <= 24) {
-    if (A % 32 == 0 && h->policy != 10 && (h->policy == 9 || A >= kTailMinA))
-      return launch_tail<MU>(h, T, S, L1, L2, A, C);
+    if (A % 32 == 0 && h->policy != 10 && (h->policy == 9 || A >= kTailMinA || (MU == 8 && !legacy)))
+      return legacy ? launch_tail<MU>(h, T, S, L1, L2, A, C) : launch_tail_ws<MU>(h, T, S, L1, L2, A, C);
   }
   // 16 a's per tile when shared memory allows it and A tiles evenly
   constexpr bool wide_fits = FusedCfg<MU, false, 16>::SMEM_BYTES <= 227 * 1024 &&
@@ -81,7 +127,7 @@ static int launch_fused_mu(mumode_handle_s* h, bool first, const double* T, doub
 static int fused_extent(int d, const int64_t* m, const int64_t* n, bool cplx, bool adjoint,
                         int policy, int mu_lo, int mu_hi, const double* T, const double* S,
                         const double* const* L) {
-  if (cplx || adjoint || !(policy == 0 || policy == 7 || policy == 9 || policy == 10) || mu_hi - mu_lo < 1)
+  if (cplx || adjoint || !(policy == 0 || policy == 7 || policy == 9 || policy == 10 || policy == 12) || mu_hi - mu_lo < 1)
     return 0;
   const int64_t MU = m[0];
   if (MU != 8 && MU != 16 && MU != 24 && MU != 32) return 0;

@@ -40,9 +40,9 @@ def _require_gpu():
         pytest.fail("GPU test run without a GPU")
 
 
-@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11],
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12],
                 ids=["auto", "generic", "tma", "tma_big", "tma_tm", "tma_lm", "tma_mid", "fused", "ldg", "tail",
-                     "no_tail", "chain"])
+                     "no_tail", "chain", "no_ws"])
 def policy(request):
     h = mm.get_handle(0)
     h.set_kernel_policy(request.param)
@@ -341,6 +341,24 @@ def test_fused_small_square_modes(policy, shape):
     assert O.rel_fro(S, O.port_tucker(T, Ls)) < 1e-14
     I = [dev(np.eye(e)) for e in shape]
     np.testing.assert_array_equal(host(mm.tucker(dev(T), I)), T)
+
+
+@pytest.mark.parametrize("shape", [(24,) * 6, (8,) * 8, (16,) * 6, (24,) * 5, (8,) * 3])
+def test_warp_specialised_passes_equal_legacy_kernels(shape):
+    # fused_ws (first pass) and tail_ws (strided tail pass) keep every output's
+    # DMMA k-order, so they are bitwise equal to fused_pair / tail_pair
+    # (policy 12); (24,)*6 is config C5 at full size
+    torch.manual_seed(len(shape) * 31 + shape[0])
+    T = mm.colmajor_empty(shape, torch.float64, "cuda").normal_()
+    Ls = [mm.to_colmajor(torch.randn(e, e, dtype=torch.float64, device="cuda")) for e in shape]
+    h = mm.get_handle(0)
+    try:
+        ws = mm.tucker(T, Ls)
+        h.set_kernel_policy(12)
+        legacy = mm.tucker(T, Ls)
+    finally:
+        h.set_kernel_policy(0)
+    assert torch.equal(ws, legacy)
 
 
 def test_kronsumv_fused_epilogue_vs_reference(policy):
