@@ -113,6 +113,10 @@ static int launch_fused_mu(mumode_handle_s* h, bool first, const double* T, doub
   if constexpr (MU <= 24) {
     if (A % 32 == 0 && h->policy != 10 && (h->policy == 9 || A >= kTailMinA || (MU == 8 && !legacy)))
       return legacy ? launch_tail<MU>(h, T, S, L1, L2, A, C) : launch_tail_ws<MU>(h, T, S, L1, L2, A, C);
+    // the streamed tail kernel also wins at smaller A once there are enough
+    // 32-a tiles to fill the SMs (C5 pass 2, A = 576: 614 -> 604 us)
+    if (A % 32 == 0 && h->policy != 10 && !legacy && (A / 32) * C >= 8 * persistent_sms(h))
+      return launch_tail_ws<MU>(h, T, S, L1, L2, A, C);
   }
   // 16 a's per tile when shared memory allows it and A tiles evenly
   constexpr bool wide_fits = FusedCfg<MU, false, 16>::SMEM_BYTES <= 227 * 1024 &&

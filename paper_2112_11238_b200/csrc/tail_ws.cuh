@@ -7,11 +7,11 @@
 // the two modes by CTA-wide barriers (ncu on C5 pass 3: DMMA pipe 76 %
 // active; stage-data waits ~10 % and phase barriers ~9 % of stall samples).
 // Here mode mu+1 accumulates in registers as the b2 stages arrive, so only
-// one stage of the intermediate exists at a time (double-buffered), and the
+// a few stages of the intermediate exist at a time (NYS buffers), and the
 // two modes run on separate warp groups:
 //
 //   producer warpgroup : TMA ring of stages {16 a, 2, MU b1, 4 b2, 1} (as tail)
-//   group A (1 wg)     : mode mu on stage z: X -> Ys[z & 1] (tail's maps)
+//   group A (1 wg)     : mode mu on stage z: X -> Ys[z % NYS] (tail's maps)
 //   group B (2 wgs)    : mode mu+1: acc(i, j, a) += L2(j, b2) Ys(i, b2, a)
 //                        over the tile's MU/4 stages; each warp owns MU/8
 //                        i's (MU/8 x 4 x NF accumulator fragments); at the
@@ -19,7 +19,7 @@
 //                        256 B, TMA-box layout) and TMA-stores it.
 //
 // Ys handoffs are named barriers (ids 2 + yb "stage full": A arrives, B
-// syncs; 4 + yb "stage free": B arrives, A syncs; the first two / last two
+// syncs; 2 + NYS + yb "stage free": B arrives, A syncs; the first / last NYS
 // stages of a CTA skip the free handshake). The k-order of every output's
 // DMMA chain (b1 for mode mu, b2 = stage by stage for mode mu+1) is the
 // tail kernel's, so results are bitwise equal to it. Stage buffer rows and
@@ -46,7 +46,10 @@ struct TailWsCfg {
   static constexpr int X_BYTES = 32 * MU * KB * 8;
   static constexpr int YS_BYTES = MU * 1024;   // MU slots of 4 b2 rows x 256 B
   static constexpr int STG_BYTES = MU * 256;   // one i: MU j-rows x 256 B
-  static constexpr int FIXED = 2 * YS_BYTES + WB * STG_BYTES + 1024 + 256;
+  // stage buffers between the groups: C5 pass 3 643 (2) / 614 (3) / 607 (4)
+  // / 653 us (5: the load ring drops to 2 stages)
+  static constexpr int NYS = 4;
+  static constexpr int FIXED = NYS * YS_BYTES + WB * STG_BYTES + 1024 + 256;
   static constexpr int NBUF_RAW = (227 * 1024 - FIXED) / X_BYTES;
   static constexpr int NBUF = NBUF_RAW > 6 ? 6 : NBUF_RAW;
   static constexpr int SMEM_BYTES = NBUF * X_BYTES + FIXED;
@@ -72,6 +75,7 @@ __global__ void __launch_bounds__(TailWsCfg<MU>::THREADS, 1)
     tail_ws_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapS,
                    const TailParams p) {
   using Cfg = TailWsCfg<MU>;
+  constexpr int NYS = Cfg::NYS;
   constexpr int NF = Cfg::NF, KS = Cfg::KS, NST = Cfg::NST, NBUF = Cfg::NBUF;
   constexpr int WA = Cfg::WA, WB = Cfg::WB, GA = Cfg::GA;
   constexpr int PAIR = (WA + WB) * 32;
@@ -79,7 +83,7 @@ __global__ void __launch_bounds__(TailWsCfg<MU>::THREADS, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* Xs = smem;
   uint8_t* Ys = Xs + NBUF * Cfg::X_BYTES;
-  uint8_t* Stg = Ys + 2 * Cfg::YS_BYTES;
+  uint8_t* Stg = Ys + NYS * Cfg::YS_BYTES;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(Stg + WB * Cfg::STG_BYTES);
   uint64_t* empty_bar = full_bar + NBUF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -137,9 +141,9 @@ __global__ void __launch_bounds__(TailWsCfg<MU>::THREADS, 1)
     int buf = 0;
     uint32_t phase = 0;
     for (int64_t z = 0; z < nst; ++z) {
-      const int yb = static_cast<int>(z & 1);
+      const int yb = static_cast<int>(z % NYS);
       mbar_wait(&full_bar[buf], phase);
-      if (z >= 2) named_barrier_sync(4 + yb, PAIR);  // Ys[yb] consumed by group B
+      if (z >= NYS) named_barrier_sync(2 + NYS + yb, PAIR);  // Ys[yb] consumed by group B
       const uint8_t* X = Xs + buf * Cfg::X_BYTES;
       uint8_t* Y = Ys + yb * Cfg::YS_BYTES;
 #pragma unroll
@@ -202,7 +206,7 @@ __global__ void __launch_bounds__(TailWsCfg<MU>::THREADS, 1)
       double l2f[NF];
 #pragma unroll
       for (int nf = 0; nf < NF; ++nf) l2f[nf] = __ldg(l2col + 8 * nf + 4 * st * MU);
-      const int yb = static_cast<int>(z & 1);
+      const int yb = static_cast<int>(z % NYS);
       named_barrier_sync(2 + yb, PAIR);  // Ys[yb] complete
       const uint8_t* Y = Ys + yb * Cfg::YS_BYTES;
 #pragma unroll
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(TailWsCfg<MU>::THREADS, 1)
         }
       }
       // every Ys value of this stage has been consumed by a DMMA
-      if (z + 2 < nst) named_barrier_arrive(4 + yb, PAIR);
+      if (z + NYS < nst) named_barrier_arrive(2 + NYS + yb, PAIR);
     }
     // epilogue: one i at a time through this warp's staging slot (TMA-box
     // layout {16 a, 2 h, 1, MU j}: row 2j + h), then one TMA store

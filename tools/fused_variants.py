@@ -14,6 +14,7 @@ from paper_2112_11238_b200 import _lib  # noqa: E402
 lib = _lib.lib()
 h = mm.get_handle(0)
 h.bind_torch_stream()
+h.set_kernel_policy(int(os.environ.get("POLICY", "0")))
 # variant "F:T" = MUMODE_FUSED_VARIANT F, MUMODE_TAIL_VARIANT T
 variants = sys.argv[1].split(",") if len(sys.argv) > 1 else ["0:0", "2:0", "2:1", "2:3"]
 shapes = [tuple(int(x) for x in s.split("x")) for s in sys.argv[2].split(",")] if len(sys.argv) > 2 else \
