@@ -35,17 +35,17 @@ static int launch_fused(mumode_handle_s* h, const double* T, double* S, const do
 }
 
 // Warp-specialised first pass (fused_ws.cuh): modes 1 and 2.
-template <int MU>
+template <int MU, int NY = 2>
 static int launch_fused_ws(mumode_handle_s* h, const double* T, double* S, const double* L1,
                            const double* L2, int64_t C) {
-  using Cfg = FusedWsCfg<MU>;
+  using Cfg = FusedWsCfg<MU, NY>;
   const CUtensorMap* mp = nullptr;
   FusedParams p{S, L1, L2, 1, C, (C + 7) / 8};
   uint64_t d[3] = {8, uint64_t(MU) * uint64_t(C), uint64_t(MU / 8)}, st[2] = {uint64_t(MU), 8};
   uint32_t b[3] = {8, 8 * MU, MU / 8};
   MM_TRY(get_map(h, T, 3, d, st, b, &mp));
   const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
-  auto k = fused_ws_kernel<MU, 2>;
+  auto k = fused_ws_kernel<MU, 2, NY>;
   MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
   MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, p));
   MM_CUDA(cudaGetLastError());

@@ -26,7 +26,7 @@
 
 namespace mumode_gpu {
 
-template <int MU>
+template <int MU, int NY_ = 2>
 struct FusedWsCfg {
   using Base = FusedCfg<MU, true, 8>;
   static constexpr int NF = MU / 8;
@@ -37,26 +37,29 @@ struct FusedWsCfg {
   static constexpr int THREADS = (2 * GW + 1) * 32;
   static constexpr int X_BYTES = Base::X_BYTES;
   static constexpr int Y_BYTES = Base::Y_BYTES;
-  static constexpr int NBUF = (4 * X_BYTES + 2 * Y_BYTES + 2048 <= 227 * 1024) ? 4
-                              : (3 * X_BYTES + 2 * Y_BYTES + 2048 <= 227 * 1024) ? 3 : 2;
-  static constexpr int SMEM_BYTES = NBUF * X_BYTES + 2 * Y_BYTES + 1024 + 128;
+  // Y buffers between the groups (C5 pass 1: 2 -> 556 us with a 4-deep ring,
+  // 3 -> 567 us with a 3-deep ring)
+  static constexpr int NY = NY_;
+  static constexpr int NBUF = (4 * X_BYTES + NY * Y_BYTES + 2048 <= 227 * 1024) ? 4
+                              : (3 * X_BYTES + NY * Y_BYTES + 2048 <= 227 * 1024) ? 3 : 2;
+  static constexpr int SMEM_BYTES = NBUF * X_BYTES + NY * Y_BYTES + 1024 + 128;
   static_assert(MU == 8 || MU == 16 || MU == 24, "square modes of 8, 16, 24");
   static_assert(UNITS % GW == 0, "units split evenly over a group");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 };
 
 // GA = mode-1 units a warp advances together (independent accumulator chains)
-template <int MU, int GA>
-__global__ void __launch_bounds__(FusedWsCfg<MU>::THREADS, 1)
+template <int MU, int GA, int NY>
+__global__ void __launch_bounds__(FusedWsCfg<MU, NY>::THREADS, 1)
     fused_ws_kernel(const __grid_constant__ CUtensorMap mapX, const FusedParams p) {
-  using Cfg = FusedWsCfg<MU>;
+  using Cfg = FusedWsCfg<MU, NY>;
   constexpr int NF = Cfg::NF, KS = Cfg::KS, GW = Cfg::GW, UPW = Cfg::UPW, NBUF = Cfg::NBUF;
   constexpr int PAIR = 2 * GW * 32;  // threads of both groups
   static_assert(UPW % GA == 0, "group-0 unit batches");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* Ybase = smem + NBUF * Cfg::X_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(Ybase + 2 * Cfg::Y_BYTES);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(Ybase + NY * Cfg::Y_BYTES);
   uint64_t* empty_bar = full_bar + NBUF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -108,10 +111,10 @@ __global__ void __launch_bounds__(FusedWsCfg<MU>::THREADS, 1)
     int buf = 0;
     uint32_t phase = 0;
     for (int64_t k = 0; k < ntiles; ++k) {
-      const int yb = static_cast<int>(k & 1);
+      const int yb = static_cast<int>(k % NY);
       uint8_t* Y = Ybase + yb * Cfg::Y_BYTES;
       mbar_wait(&full_bar[buf], phase);
-      if (k >= 2) named_barrier_sync(4 + yb, PAIR);  // Y[yb] read by group 1
+      if (k >= NY) named_barrier_sync(2 + NY + yb, PAIR);  // Y[yb] read by group 1
       const uint8_t* X = smem + buf * Cfg::X_BYTES;
 #pragma unroll
       for (int bt = 0; bt < UPW / GA; ++bt) {
@@ -165,7 +168,7 @@ __global__ void __launch_bounds__(FusedWsCfg<MU>::THREADS, 1)
   const int x = xmap8(2 * t);  // output pair along the contiguous index
   for (int64_t k = 0; k < ntiles; ++k) {
     const int64_t c_base = (blockIdx.x + k * gridDim.x) * 8;
-    const int yb = static_cast<int>(k & 1);
+    const int yb = static_cast<int>(k % NY);
     const uint8_t* Y = Ybase + yb * Cfg::Y_BYTES;
     named_barrier_sync(2 + yb, PAIR);  // Y[yb] complete
 #pragma unroll
@@ -181,7 +184,7 @@ __global__ void __launch_bounds__(FusedWsCfg<MU>::THREADS, 1)
         for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[nf][0], acc[nf][1], l2[nf][s], yf);
       }
       // every Y value of this tile has been consumed by a DMMA: free Y[yb]
-      if (q == UPW - 1 && k + 2 < ntiles) named_barrier_arrive(4 + yb, PAIR);
+      if (q == UPW - 1 && k + NY < ntiles) named_barrier_arrive(2 + NY + yb, PAIR);
       const int cl = u / NF, ib = u % NF;
       const int64_t c = c_base + cl;
       if (c < p.C) {
