@@ -772,7 +772,7 @@ constexpr int kSlotEvents = 2 * kHostChunks + 2;  // slabs, blocks, compute end,
 
 static int host_tucker_enqueue(mumode_handle_t h, int d, const int64_t* m, const int64_t* n, const double* T,
                                const double* const* L, double* S) {
-  constexpr int kChunks = kHostChunks;
+  constexpr int kChunks = kHostChunks;  // 8: 2.94 ms per queued C2 call; 1, 2, 3, 4: 2.99 ms
   const int slot = static_cast<int>(h->host_calls & 1);
   const bool reuse = h->host_calls >= 2;  // the slot's previous call must be done with it
   ++h->host_calls;
