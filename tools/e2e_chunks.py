@@ -1,6 +1,6 @@
-"""Host-buffer C2 Tucker through mumode_host_tucker_f64_async, K queued calls,
-for several pipeline chunk counts (MUMODE_ASYNC_CHUNKS): ms per application."""
-import os
+"""Host-buffer C2 Tucker through mumode_host_tucker_f64_async, K queued calls:
+ms per application (best of 3). Used with kHostChunks (csrc/mumode_gpu.cu)
+rebuilt at 1, 2, 3, 4, 8 for the chunk sweep quoted in DESIGN.md."""
 import sys
 import time
 from pathlib import Path
@@ -21,8 +21,7 @@ Lpin = [torch.randn(256 * 256, dtype=torch.float64).pin_memory() for _ in range(
 Spins = [torch.empty_like(Tpin).pin_memory() for _ in range(2)]
 Lp = _lib.ptr_array([L.data_ptr() for L in Lpin])
 K = 30
-for ch in [int(c) for c in (sys.argv[1] if len(sys.argv) > 1 else "8,4,2,1,8").split(",")]:
-    os.environ["MUMODE_ASYNC_CHUNKS"] = str(ch)
+for _ in range(2):
     res = []
     for rep in range(3):
         for k in range(2):
@@ -33,4 +32,4 @@ for ch in [int(c) for c in (sys.argv[1] if len(sys.argv) > 1 else "8,4,2,1,8").s
             assert lib.mumode_host_tucker_f64_async(h.h, 3, m, m, Tpin.data_ptr(), Lp, Spins[k % 2].data_ptr()) == 0
         assert lib.mumode_host_wait(h.h) == 0
         res.append((time.perf_counter() - t0) / K * 1e3)
-    print(f"chunks {ch}: {min(res):.3f} ms per application ({2.5769e10 / (min(res) * 1e-3) / 1e12:.2f} TF/s)", flush=True)
+    print(f"{min(res):.3f} ms per application ({2.5769e10 / (min(res) * 1e-3) / 1e12:.2f} TF/s)", flush=True)
