@@ -28,6 +28,7 @@ using CfgBig = TmaCfg<128, 128, 16, 6, 4, 4>;  // 16 MMA warps, 32x32 warp tiles
 using CfgTM = TmaCfg<128, 40, 40, 3, 16, 1>;   // T-side M, small L-side N (n = 40k)
 using CfgLM = TmaCfg<40, 128, 40, 3, 1, 16>;   // small L-side M, T-side N (mode 1, n = 40k)
 using CfgMid = TmaCfg<64, 128, 32, 4, 2, 4>;   // 32x32 warp tiles
+using CfgSmall = TmaCfg<32, 32, 32, 2, 2, 4>;  // 16x8 warp tiles: spreads small products over SMs
 // complex128 (E = 2): 4 real DMMAs per complex MAC, 16-B elements
 // (four accumulator chains per complex output: warp tiles hold 32 outputs)
 using CfgCa = TmaCfg<64, 64, 16, 6, 2, 4, 2>;  // 8 MMA warps, 32x16 complex warp tiles
@@ -99,11 +100,19 @@ static int choose_cfg(const ModeJob& j, int sms) {
   const double c1 = tile_cost<CfgTM>(mfrags, N, j.K, sms, 0.96);
   const double c2 = tile_cost<CfgLM>(mfrags, N, j.K, sms, 0.96);
   const double c3 = tile_cost<CfgMid>(mfrags, N, j.K, sms, 0.97);
+  // small tiles reuse operands poorly; they win only when they save waves
+  // (products of a few tiles: C1's 100 x 100 modes take 16 CTAs, not 3).
+  // tools/small_sweep.py, GPU time per Tucker without / with it: 100^2
+  // 15.8 -> 8.0 us, 256^2 27.6 -> 8.8, 512^2 47.6 -> 26.4, 48^3 18.8 -> 8.3,
+  // 64^3 19.4 -> 11.1, >= 80^3 unchanged (efficiency 0.4-0.6 choose alike,
+  // 0.25 gives up 512^2 and 64^3)
+  const double c8 = tile_cost<CfgSmall>(mfrags, N, j.K, sms, 0.5);
   int best = 0;
   double bc = c0;
   if (c1 < bc) best = 1, bc = c1;
   if (c2 < bc) best = 2, bc = c2;
   if (c3 < bc) best = 3, bc = c3;
+  if (c8 < bc) best = 8, bc = c8;
   return best;
 }
 
@@ -249,6 +258,7 @@ static int launch_tma_auto(mumode_handle_s* h, const ModeJob& j) {
     case 5: return launch_tma<CfgCb>(h, j);
     case 6: return launch_tma<CfgCc>(h, j);
     case 7: return launch_tma<CfgCd>(h, j);
+    case 8: return launch_tma<CfgSmall>(h, j);
     default: return launch_tma<CfgBig>(h, j);
   }
 }
