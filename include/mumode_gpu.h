@@ -72,7 +72,8 @@ int64_t mumode_launch_count(mumode_handle_t h);
  * 10 = auto with the tail pass disabled, 11 = auto with whole Tucker chains
  * run as one persistent launch where the tile configs allow (tma_chain.cuh),
  * 12 = auto with the fused passes' non-warp-specialised kernels
- * (fused_pair_kernel / tail_pair_kernel instead of fused_ws / tail_ws).
+ * (fused_pair_kernel / tail_pair_kernel instead of fused_ws / tail_ws),
+ * 13 = auto without the small-extent (skinny) mode-product kernel.
  * Not a fallback switch: all are CUDA kernels. */
 int mumode_set_kernel_policy(mumode_handle_t h, int policy);
 

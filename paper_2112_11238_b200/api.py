@@ -105,7 +105,8 @@ class Handle:
         0 auto, 1 SIMT kernel, 2 TMA/DMMA where legal, 3..6 one TMA tile
         config forced, 7 auto incl. fused pairs, 8 LDG-staged DMMA, 9 / 10 tail
         pass forced / disabled, 11 whole chains as one persistent launch, 12
-        fused passes without warp specialisation."""
+        fused passes without warp specialisation, 13 no skinny small-extent
+        kernel."""
         _check(_lib.lib().mumode_set_kernel_policy(self.h, int(policy)))
 
     def close(self) -> None:

@@ -131,7 +131,7 @@ static int launch_fused_mu(mumode_handle_s* h, bool first, const double* T, doub
 static int fused_extent(int d, const int64_t* m, const int64_t* n, bool cplx, bool adjoint,
                         int policy, int mu_lo, int mu_hi, const double* T, const double* S,
                         const double* const* L) {
-  if (cplx || adjoint || !(policy == 0 || policy == 7 || policy == 9 || policy == 10 || policy == 12) || mu_hi - mu_lo < 1)
+  if (cplx || adjoint || !(policy == 0 || policy == 7 || policy == 9 || policy == 10 || policy == 12 || policy == 13) || mu_hi - mu_lo < 1)
     return 0;
   const int64_t MU = m[0];
   if (MU != 8 && MU != 16 && MU != 24 && MU != 32) return 0;

@@ -329,6 +329,80 @@ static bool ldg_worthwhile(const ModeJob& j) {
   return M >= 16 && j.K >= 8 && ((j.A == 1) ? j.C : j.N) >= 16;
 }
 
+// ------------------------------------------------------------ skinny products
+// Small-extent real products (skinny.cuh): HBM-bound, 32-wide tiles with
+// 256-B rows. Policy 13 disables the path (auto otherwise).
+static bool skinny_ok(const mumode_handle_s* h, const ModeJob& j) {
+  if (j.cplx || j.conj || j.accumulate || j.scat || j.div_front) return false;
+  if (!(h->policy == 0 || h->policy == 7 || h->policy == 9 || h->policy == 10 || h->policy == 12)) return false;
+  if (j.K > 32 || j.N > 32 || !aligned16(j.T) || !aligned16(j.S)) return false;
+  if (j.A == 1) {
+    if ((j.K & 1) || (j.N & 1) || (j.C + 31) / 32 >= (int64_t(1) << 31)) return false;
+    return j.C >= int64_t(64) * 148;  // enough 32-fibre tiles to fill the SMs
+  }
+  if (j.A % 2 != 0 || j.A >= (int64_t(1) << 31) || j.C >= (int64_t(1) << 31)) return false;
+  // 16-a tiles (A not a multiple of 16) pay off from A ~ 64 (18^6 modes 3/4,
+  // A = 324 / 5832: 300 -> 193 us); for A = 12..24 they waste up to a third
+  // of every box and lose to the tile kernels
+  if (j.A % 16 != 0 && j.A < 64) return false;
+  return ((j.A + 31) / 32) * j.C >= int64_t(2) * 148;
+}
+
+template <int P, int TA>
+static int launch_skinny_p(mumode_handle_s* h, const ModeJob& j) {
+  using Cfg = SkinnyCfg<P, TA>;
+  const CUtensorMap *mx = nullptr, *ms = nullptr;
+  SkinnyParams p{j.L, j.sLi, j.sLk, int(j.K), int(j.N), 0, 0};
+  const bool mode1 = (j.A == 1);
+  if (TA == 16) {
+    // A even, not a multiple of 16: 3-D view {A, K, C}, 16-a boxes
+    uint64_t dx[3] = {uint64_t(j.A), uint64_t(j.K), uint64_t(j.C)}, sx[2] = {uint64_t(j.A), uint64_t(j.A * j.K)};
+    uint64_t ds[3] = {uint64_t(j.A), uint64_t(j.N), uint64_t(j.C)}, ss[2] = {uint64_t(j.A), uint64_t(j.A * j.N)};
+    uint32_t b[3] = {16, P, 1};
+    MM_TRY(get_map(h, j.T, 3, dx, sx, b, &mx, 1));
+    MM_TRY(get_map(h, j.S, 3, ds, ss, b, &ms, 1));
+    p.ablks = (j.A + 15) / 16;
+    p.tiles = p.ablks * j.C;
+  } else if (mode1) {
+    uint64_t dx[2] = {uint64_t(j.K), uint64_t(j.C)}, sx[1] = {uint64_t(j.K)};
+    uint64_t ds[2] = {uint64_t(j.N), uint64_t(j.C)}, ss[1] = {uint64_t(j.N)};
+    uint32_t b[2] = {P, 32};
+    MM_TRY(get_map(h, j.T, 2, dx, sx, b, &mx, 2));
+    MM_TRY(get_map(h, j.S, 2, ds, ss, b, &ms, 2));
+    p.tiles = (j.C + 31) / 32;
+  } else {
+    uint64_t dx[4] = {16, uint64_t(j.A / 16), uint64_t(j.K), uint64_t(j.C)};
+    uint64_t sx[3] = {16, uint64_t(j.A), uint64_t(j.A * j.K)};
+    uint64_t ds[4] = {16, uint64_t(j.A / 16), uint64_t(j.N), uint64_t(j.C)};
+    uint64_t ss[3] = {16, uint64_t(j.A), uint64_t(j.A * j.N)};
+    uint32_t b[4] = {16, 2, P, 1};
+    MM_TRY(get_map(h, j.T, 4, dx, sx, b, &mx, 1));
+    MM_TRY(get_map(h, j.S, 4, ds, ss, b, &ms, 1));
+    p.ablks = (j.A + 31) / 32;
+    p.tiles = p.ablks * j.C;
+  }
+  const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
+  auto k = TA == 16 ? skinny_kernel<P, false, 16> : (mode1 ? skinny_kernel<P, true> : skinny_kernel<P, false>);
+  MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
+  MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mx, *ms, p));
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return MUMODE_OK;
+}
+
+template <int TA>
+static int launch_skinny_ta(mumode_handle_s* h, const ModeJob& j) {
+  const int64_t e = std::max(j.K, j.N);
+  if (e <= 8) return launch_skinny_p<8, TA>(h, j);
+  if (e <= 16) return launch_skinny_p<16, TA>(h, j);
+  if (e <= 24) return launch_skinny_p<24, TA>(h, j);
+  return launch_skinny_p<32, TA>(h, j);
+}
+
+static int launch_skinny(mumode_handle_s* h, const ModeJob& j) {
+  return (j.A != 1 && j.A % 16 != 0) ? launch_skinny_ta<16>(h, j) : launch_skinny_ta<32>(h, j);
+}
+
 static int run_job(mumode_handle_s* h, const ModeJob& j0) {
   ModeJob j = j0;
   // A real mu > 1 product whose factor has an odd leading dimension (odd n_mu)
@@ -383,6 +457,7 @@ static int run_job(mumode_handle_s* h, const ModeJob& j0) {
     h->launches++;
     return MUMODE_OK;
   }
+  if (skinny_ok(h, j)) return launch_skinny(h, j);
   // accumulating products: real mu > 1 have a TMA instantiation; others generic
   const bool can_tma = tma_ok(j) && !(j.accumulate && (j.A == 1 || j.cplx));
   if (h->policy == 8 && !j.cplx) return launch_ldg(h, j);

@@ -27,6 +27,7 @@
 #include "fused_ws.cuh"
 #include "tail.cuh"
 #include "tail_ws.cuh"
+#include "skinny.cuh"
 #include "tma_chain.cuh"
 #include "ldg_dmma.cuh"
 
@@ -186,8 +187,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // boxes (real), 128B swizzle for 16-double boxes (8 complex). dims/strides in elements (dim0 contiguous).
 static int get_map(mumode_handle_s* h, const void* base, int rank, const uint64_t* dims,
                    const uint64_t* strides_el, const uint32_t* box, const CUtensorMap** out,
-                   bool swz128 = false) {
-  MapKey key{reinterpret_cast<uint64_t>(base), uint64_t(rank), uint64_t(swz128)};
+                   int swz = 0) {  // 0: 64B swizzle, 1 (true): 128B, 2: none
+  MapKey key{reinterpret_cast<uint64_t>(base), uint64_t(rank), uint64_t(swz)};
   for (int r = 0; r < rank; ++r) key.push_back(dims[r]);
   for (int r = 0; r + 1 < rank; ++r) key.push_back(strides_el[r]);
   for (int r = 0; r < rank; ++r) key.push_back(box[r]);
@@ -210,7 +211,8 @@ static int get_map(mumode_handle_s* h, const void* base, int rank, const uint64_
   for (int r = 0; r + 1 < rank; ++r) gstride[r] = strides_el[r] * sizeof(double);
   CUresult res = fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), gdim,
                     gstride, bdim, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                    swz == 1 ? CU_TENSOR_MAP_SWIZZLE_128B
+                             : (swz == 2 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_64B),
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (res != CUDA_SUCCESS)
@@ -427,7 +429,7 @@ void* mumode_get_stream(mumode_handle_t h) { return h ? static_cast<void*>(h->st
 int64_t mumode_launch_count(mumode_handle_t h) { return h ? h->launches : -1; }
 
 int mumode_set_kernel_policy(mumode_handle_t h, int policy) {
-  if (!h || policy < 0 || policy > 12) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
+  if (!h || policy < 0 || policy > 13) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
   // 3..6 force real tile configuration 0..3 / complex configuration 0..3
   h->policy = policy;
   return MUMODE_OK;

@@ -40,9 +40,9 @@ def _require_gpu():
         pytest.fail("GPU test run without a GPU")
 
 
-@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12],
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13],
                 ids=["auto", "generic", "tma", "tma_big", "tma_tm", "tma_lm", "tma_mid", "fused", "ldg", "tail",
-                     "no_tail", "chain", "no_ws"])
+                     "no_tail", "chain", "no_ws", "no_skinny"])
 def policy(request):
     h = mm.get_handle(0)
     h.set_kernel_policy(request.param)
@@ -359,6 +359,34 @@ def test_warp_specialised_passes_equal_legacy_kernels(shape):
     finally:
         h.set_kernel_policy(0)
     assert torch.equal(ws, legacy)
+
+
+@pytest.mark.parametrize("shape", [(20,) * 6, (12,) * 6, (18, 14, 16, 10, 12, 22), (32, 8, 30, 26, 16, 6),
+                                   (24,) * 5])
+def test_skinny_mode_products(shape):
+    # small-extent products take the 32-wide-tile skinny kernel (skinny.cuh):
+    # every mode, square and rectangular factors (odd n_mu included), equal
+    # to the tile kernels (policy 13) bit for bit and to the oracle
+    rng = np.random.default_rng(sum(shape))
+    T = rnd(rng, shape)
+    Td = dev(T)
+    h = mm.get_handle(0)
+    for mu in range(1, len(shape) + 1):
+        for n_out in sorted({shape[mu - 1], 7 + mu % 2, 32 - 2 * (mu % 3)}):
+            L = rnd(rng, (n_out, shape[mu - 1]))
+            launches = h.launches
+            S = mm.mode_product(Td, dev(L), mu)
+            assert h.launches == launches + 1
+            try:
+                h.set_kernel_policy(13)
+                S13 = mm.mode_product(Td, dev(L), mu)
+            finally:
+                h.set_kernel_policy(0)
+            assert torch.equal(S, S13), (mu, n_out)
+            if mu in (1, len(shape)) and n_out == shape[mu - 1]:
+                assert O.rel_max(host(S), O.port_mode_product(T, L, mu)) < 1e-13
+    Ls = [rnd(rng, (e, e)) for e in shape]
+    assert O.rel_fro(host(mm.tucker(Td, [dev(L) for L in Ls])), O.port_tucker(T, Ls)) < 1e-13
 
 
 def test_kronsumv_fused_epilogue_vs_reference(policy):

@@ -12,6 +12,8 @@ from paper_2112_11238_b200 import _lib  # noqa: E402
 
 lib = _lib.lib()
 h = mm.get_handle(0)
+import os  # noqa: E402
+h.set_kernel_policy(int(os.environ.get("POLICY", "0")))
 shapes = [tuple(int(x) for x in s.split("x")) for s in sys.argv[1].split(",")] if len(sys.argv) > 1 else \
     [(100, 100), (256, 256), (512, 512), (16,) * 3, (32,) * 3, (48,) * 3, (64,) * 3, (80,) * 3, (96,) * 3,
      (128,) * 3, (160,) * 3]
