@@ -343,46 +343,85 @@ static bool skinny_ok(const mumode_handle_s* h, const ModeJob& j) {
   if (j.A % 2 != 0 || j.A >= (int64_t(1) << 31) || j.C >= (int64_t(1) << 31)) return false;
   // 16-a tiles (A not a multiple of 16) pay off from A ~ 64 (18^6 modes 3/4,
   // A = 324 / 5832: 300 -> 193 us); for A = 12..24 they waste up to a third
-  // of every box and lose to the tile kernels
-  if (j.A % 16 != 0 && j.A < 64) return false;
+  // of every box, so A <= 32 takes whole c-slabs (skinny_slab_kernel)
+  if (j.A % 16 != 0 && j.A < 64) {
+    if (j.A > 32) return false;
+    const int P = int((std::max(j.K, j.N) + 7) / 8 * 8);
+    const int64_t tc = std::max<int64_t>(1, std::min<int64_t>(256, (32 * P) / (P * j.A)));
+    return (j.C + tc - 1) / tc >= int64_t(2) * 148;
+  }
   return ((j.A + 31) / 32) * j.C >= int64_t(2) * 148;
 }
 
 template <int P, int TA>
 static int launch_skinny_p(mumode_handle_s* h, const ModeJob& j) {
   using Cfg = SkinnyCfg<P, TA>;
+  constexpr uint32_t TC = Cfg::TC;
   const CUtensorMap *mx = nullptr, *ms = nullptr;
-  SkinnyParams p{j.L, j.sLi, j.sLk, int(j.K), int(j.N), 0, 0};
+  SkinnyParams p{j.L, j.sLi, j.sLk, int(j.K), int(j.N), 0, 0, int(j.A), int(TC), 0};
   const bool mode1 = (j.A == 1);
   if (TA == 16) {
-    // A even, not a multiple of 16: 3-D view {A, K, C}, 16-a boxes
+    // A even, not a multiple of 16: 3-D view {A, K, C}, boxes {16 a, P, TC c}
     uint64_t dx[3] = {uint64_t(j.A), uint64_t(j.K), uint64_t(j.C)}, sx[2] = {uint64_t(j.A), uint64_t(j.A * j.K)};
     uint64_t ds[3] = {uint64_t(j.A), uint64_t(j.N), uint64_t(j.C)}, ss[2] = {uint64_t(j.A), uint64_t(j.A * j.N)};
-    uint32_t b[3] = {16, P, 1};
+    uint32_t b[3] = {16, P, TC};
     MM_TRY(get_map(h, j.T, 3, dx, sx, b, &mx, 1));
     MM_TRY(get_map(h, j.S, 3, ds, ss, b, &ms, 1));
     p.ablks = (j.A + 15) / 16;
-    p.tiles = p.ablks * j.C;
+    p.tiles = p.ablks * ((j.C + TC - 1) / TC);
   } else if (mode1) {
+    // boxes {P k, 32 TC fibres}
     uint64_t dx[2] = {uint64_t(j.K), uint64_t(j.C)}, sx[1] = {uint64_t(j.K)};
     uint64_t ds[2] = {uint64_t(j.N), uint64_t(j.C)}, ss[1] = {uint64_t(j.N)};
-    uint32_t b[2] = {P, 32};
+    uint32_t b[2] = {P, 32 * TC};
     MM_TRY(get_map(h, j.T, 2, dx, sx, b, &mx, 2));
     MM_TRY(get_map(h, j.S, 2, ds, ss, b, &ms, 2));
-    p.tiles = (j.C + 31) / 32;
+    p.tiles = (j.C + 32 * TC - 1) / (32 * TC);
   } else {
-    uint64_t dx[4] = {16, uint64_t(j.A / 16), uint64_t(j.K), uint64_t(j.C)};
-    uint64_t sx[3] = {16, uint64_t(j.A), uint64_t(j.A * j.K)};
-    uint64_t ds[4] = {16, uint64_t(j.A / 16), uint64_t(j.N), uint64_t(j.C)};
-    uint64_t ss[3] = {16, uint64_t(j.A), uint64_t(j.A * j.N)};
-    uint32_t b[4] = {16, 2, P, 1};
-    MM_TRY(get_map(h, j.T, 4, dx, sx, b, &mx, 1));
-    MM_TRY(get_map(h, j.S, 4, ds, ss, b, &ms, 1));
-    p.ablks = (j.A + 31) / 32;
-    p.tiles = p.ablks * j.C;
+    // 5-D view {16, 2, K, A/32, C} (a-block as its own dimension): a tile's TC
+    // boxes run along c, or along the a-blocks when C < TC (e.g. the last
+    // mode, C = 1)
+    const int64_t nab = j.A / 32;
+    p.a_major = (j.C < int64_t(TC)) ? 1 : 0;
+    uint64_t dx[5] = {16, 2, uint64_t(j.K), uint64_t(nab), uint64_t(j.C)};
+    uint64_t sx[4] = {16, uint64_t(j.A), 32, uint64_t(j.A * j.K)};
+    uint64_t ds[5] = {16, 2, uint64_t(j.N), uint64_t(nab), uint64_t(j.C)};
+    uint64_t ss[4] = {16, uint64_t(j.A), 32, uint64_t(j.A * j.N)};
+    uint32_t b[5] = {16, 2, P, p.a_major ? TC : 1u, p.a_major ? 1u : TC};
+    MM_TRY(get_map(h, j.T, 5, dx, sx, b, &mx, 1));
+    MM_TRY(get_map(h, j.S, 5, ds, ss, b, &ms, 1));
+    if (p.a_major) {
+      p.ablks = (nab + TC - 1) / TC;
+      p.tiles = p.ablks * j.C;
+    } else {
+      p.ablks = nab;
+      p.tiles = nab * ((j.C + TC - 1) / TC);
+    }
   }
   const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
   auto k = TA == 16 ? skinny_kernel<P, false, 16> : (mode1 ? skinny_kernel<P, true> : skinny_kernel<P, false>);
+  MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
+  MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mx, *ms, p));
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return MUMODE_OK;
+}
+
+template <int P>
+static int launch_skinny_slab_p(mumode_handle_s* h, const ModeJob& j) {
+  using Cfg = SkinnyCfg<P>;
+  const CUtensorMap *mx = nullptr, *ms = nullptr;
+  SkinnyParams p{j.L, j.sLi, j.sLk, int(j.K), int(j.N), 0, 0, int(j.A), 0, 0};
+  // c-slabs per tile: as many as fit one stage (32 P doubles)
+  p.TC = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(256, (32 * P) / (P * j.A))));
+  uint64_t dx[3] = {uint64_t(j.A), uint64_t(j.K), uint64_t(j.C)}, sx[2] = {uint64_t(j.A), uint64_t(j.A * j.K)};
+  uint64_t ds[3] = {uint64_t(j.A), uint64_t(j.N), uint64_t(j.C)}, ss[2] = {uint64_t(j.A), uint64_t(j.A * j.N)};
+  uint32_t b[3] = {uint32_t(j.A), P, uint32_t(p.TC)};
+  MM_TRY(get_map(h, j.T, 3, dx, sx, b, &mx, 2));
+  MM_TRY(get_map(h, j.S, 3, ds, ss, b, &ms, 2));
+  p.tiles = (j.C + p.TC - 1) / p.TC;
+  const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
+  auto k = skinny_slab_kernel<P>;
   MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
   MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mx, *ms, p));
   MM_CUDA(cudaGetLastError());
@@ -400,7 +439,14 @@ static int launch_skinny_ta(mumode_handle_s* h, const ModeJob& j) {
 }
 
 static int launch_skinny(mumode_handle_s* h, const ModeJob& j) {
-  return (j.A != 1 && j.A % 16 != 0) ? launch_skinny_ta<16>(h, j) : launch_skinny_ta<32>(h, j);
+  if (j.A != 1 && j.A % 16 != 0 && j.A <= 32) {
+    const int64_t e = std::max(j.K, j.N);
+    if (e <= 8) return launch_skinny_slab_p<8>(h, j);
+    if (e <= 16) return launch_skinny_slab_p<16>(h, j);
+    if (e <= 24) return launch_skinny_slab_p<24>(h, j);
+    return launch_skinny_slab_p<32>(h, j);
+  }
+  return (j.A != 1 && j.A % 32 != 0) ? launch_skinny_ta<16>(h, j) : launch_skinny_ta<32>(h, j);
 }
 
 static int run_job(mumode_handle_s* h, const ModeJob& j0) {
