@@ -197,7 +197,7 @@ static void chain_decode(const TmaParams& p, int k, int nmodes, int64_t tile, in
 // For every producer tile of mode k, the consumer (mode k+1) M-tiles whose
 // input rows it writes; targets = how many producer tiles each consumer
 // M-tile waits for.
-static void chain_boundary(const ModeJob& jp, const TmaParams& pp, int bm_p, int bn_p, const ModeJob& jc,
+static bool chain_boundary(const ModeJob& jp, const TmaParams& pp, int bm_p, int bn_p, const ModeJob& jc,
                            const TmaParams& pc, int bm_c, int k, int nmodes, std::vector<int>& target,
                            std::vector<int>& sig_off, std::vector<int>& sig_idx) {
   const int64_t A_c = jp.A * jp.N, K_c = jc.K, AB_c = (A_c + 7) / 8, FB_c = bm_c / 8;
@@ -236,11 +236,18 @@ static void chain_boundary(const ModeJob& jp, const TmaParams& pp, int bm_p, int
     std::sort(cur.begin(), cur.end());
     cur.erase(std::unique(cur.begin(), cur.end()), cur.end());
     for (int m : cur) {
+      if (m < 0 || m >= pc.mt) {
+        if (getenv("MUMODE_DEBUG_CHAIN"))
+          fprintf(stderr, "chain_boundary: phase %d tile %lld -> consumer M-tile %d of %d\n", k, (long long)t, m,
+                  pc.mt);
+        return false;
+      }
       sig_idx.push_back(m);
       ++target[static_cast<size_t>(m)];
     }
     sig_off.push_back(static_cast<int>(sig_idx.size()));
   }
+  return true;
 }
 
 template <class CfgA, class CfgB>
@@ -273,8 +280,9 @@ static int launch_chain(mumode_handle_s* h, const std::vector<ModeJob>& jobs, in
     plan->ctr_off.assign(d, -1);
     for (int k = 0; k + 1 < d; ++k) {
       std::vector<int> target, sig_off, sig_idx;
-      chain_boundary(jobs[k], ps[k], k == 0 ? CfgA::BM : CfgB::BM, k == 0 ? CfgA::BN : CfgB::BN, jobs[k + 1],
-                     ps[k + 1], CfgB::BM, k, d, target, sig_off, sig_idx);
+      if (!chain_boundary(jobs[k], ps[k], k == 0 ? CfgA::BM : CfgB::BM, k == 0 ? CfgA::BN : CfgB::BN,
+                          jobs[k + 1], ps[k + 1], CfgB::BM, k, d, target, sig_off, sig_idx))
+        return -1;  // a producer tile maps outside the consumer's M-tiles: run per mode
       plan->target_off[k + 1] = static_cast<int64_t>(all.size());
       all.insert(all.end(), target.begin(), target.end());
       plan->sigoff_off[k] = static_cast<int64_t>(all.size());
@@ -315,7 +323,17 @@ static int launch_chain(mumode_handle_s* h, const std::vector<ModeJob>& jobs, in
   const int grid = static_cast<int>(std::min<int64_t>(cp.total, persistent_sms(h)));
   auto kern = tucker_chain_kernel<CfgA, CfgB>;
   MM_TRY(smem_opt_in(kern, CfgB::SMEM_BYTES));
-  MM_TRY(launch_pdl(kern, grid, CfgB::THREADS, CfgB::SMEM_BYTES, h->stream, maps, cp));
+  static const bool dbg = getenv("MUMODE_DEBUG_CHAIN") != nullptr;  // TEMP diagnostics
+  if (dbg) {
+    const cudaError_t e0 = cudaStreamSynchronize(h->stream);
+    fprintf(stderr, "chain: before launch d=%d total=%lld grid=%d ctr=%zu err=%s\n", d, (long long)cp.total, grid,
+            pl.counter_ints, cudaGetErrorString(e0));
+  }
+  kern<<<grid, CfgB::THREADS, CfgB::SMEM_BYTES, h->stream>>>(maps, cp);  // no PDL (tma_chain.cuh)
+  if (dbg) {
+    const cudaError_t e1 = cudaStreamSynchronize(h->stream);
+    fprintf(stderr, "chain: after launch err=%s\n", cudaGetErrorString(e1));
+  }
   MM_CUDA(cudaGetLastError());
   h->launches++;
   return MUMODE_OK;

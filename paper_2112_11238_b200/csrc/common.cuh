@@ -168,8 +168,13 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
-// Non-blocking arrival on a named barrier (producer side of a bar.sync).
+// Non-blocking arrival on a named barrier (producer side of a bar.sync). The
+// fence first: the arriving warp's shared-memory reads (and writes) must be
+// complete before the waiting side reuses the buffer -- ptxas otherwise sinks
+// DMMAs that consume in-flight LDS results past the arrive (see
+// tma_consume_tile).
 __device__ __forceinline__ void named_barrier_arrive(int id, int count) {
+  asm volatile("fence.acq_rel.cta;\n" ::: "memory");
   asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
 

@@ -149,6 +149,19 @@ static int launch_pdl(K kernel, int grid, int threads, int smem, cudaStream_t st
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   MM_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
+  static const bool debug_sync = getenv("MUMODE_DEBUG_SYNC") != nullptr;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (debug_sync) cudaStreamIsCapturing(stream, &cap);
+  if (debug_sync && cap == cudaStreamCaptureStatusNone) {  // diagnostics: name the launch that faults
+    const cudaError_t e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) {
+      const char* name = nullptr;
+      cudaFuncGetName(&name, reinterpret_cast<const void*>(kernel));
+      fprintf(stderr, "mumode: kernel %s (grid %d, block %d, smem %d) failed: %s\n", name ? name : "?", grid,
+              threads, smem, cudaGetErrorString(e));
+      return fail(MUMODE_ERR_CUDA, std::string("kernel failed: ") + (name ? name : "?"));
+    }
+  }
   return MUMODE_OK;
 }
 

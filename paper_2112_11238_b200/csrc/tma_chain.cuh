@@ -95,8 +95,12 @@ __global__ void __launch_bounds__(CfgB::THREADS, 1)
     fence_barrier_init();
   }
   __syncthreads();
-  pdl_launch_dependents();
-  pdl_wait();
+  // No programmatic dependent launch here: the CTAs wait on each other's
+  // tiles, so all of them must become resident. An early-launched successor
+  // grid could take the SMs of CTAs not yet scheduled and spin in its own
+  // griddepcontrol.wait until this grid ends -- a deadlock (seen as the
+  // watchdog trap in a long test session). Launched as a plain kernel, it
+  // starts after its predecessor and releases its successor only at exit.
 
   // item -> (mode, tile, M-tile, N-tile); items only increase per CTA
   auto locate = [&](int64_t item, int& ph, int& mt, int& nt) {

@@ -345,6 +345,13 @@ __device__ __forceinline__ void tma_consume_tile(const TmaParams& p, int mtile, 
           }
       }
     }
+    // The stage's shared-memory reads must be complete before it is released:
+    // ptxas sinks the last k-step's DMMAs past the arrive and leaves their
+    // LDS in flight, and the producer's next TMA write then races them (seen
+    // as an intermittently wrong 8x8 output fragment of the complex 96x32
+    // config, ~1 run in 5). fence.acq_rel.cta waits for the warp's
+    // outstanding shared loads.
+    asm volatile("fence.acq_rel.cta;\n" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[stage]);
     if (++stage == STAGES) {

@@ -389,6 +389,33 @@ def test_skinny_mode_products(shape):
     assert O.rel_fro(host(mm.tucker(Td, [dev(L) for L in Ls])), O.port_tucker(T, Ls)) < 1e-13
 
 
+@pytest.mark.parametrize("policy_id", [0, 3, 4, 5, 6])
+def test_repeated_products_are_bitwise_identical(policy_id):
+    # regression guard for stage-release races (a consumer warp releasing a
+    # pipeline stage while its shared-memory loads were still in flight gave
+    # an intermittently wrong 8x8 fragment in ~1 of 5 complex mode-1 runs):
+    # repeated launches on the same data must agree bit for bit, for every
+    # complex tile config (policies 3..6) and the real / fused / skinny paths
+    torch.manual_seed(5)
+    h = mm.get_handle(0)
+    Tc = mm.colmajor_empty((128, 128, 64), torch.complex128, "cuda").normal_()
+    Lc = mm.to_colmajor(torch.randn(192, 128, dtype=torch.complex128, device="cuda"))
+    Tr = mm.colmajor_empty((24,) * 5, torch.float64, "cuda").normal_()
+    Lr = [mm.to_colmajor(torch.randn(24, 24, dtype=torch.float64, device="cuda")) for _ in range(5)]
+    Ts = mm.colmajor_empty((20,) * 5, torch.float64, "cuda").normal_()
+    Ls = [mm.to_colmajor(torch.randn(20, 20, dtype=torch.float64, device="cuda")) for _ in range(5)]
+    try:
+        h.set_kernel_policy(policy_id)
+        runs = {"c_mode1": lambda: mm.mode_product(Tc, Lc, 1), "fused": lambda: mm.tucker(Tr, Lr),
+                "skinny": lambda: mm.tucker(Ts, Ls)}
+        for name, fn in runs.items():
+            first = fn().clone()
+            for _ in range(12):
+                assert torch.equal(fn(), first), name
+    finally:
+        h.set_kernel_policy(0)
+
+
 def test_kronsumv_fused_epilogue_vs_reference(policy):
     # W = sum_mu V x_mu A_mu with the terms accumulated in the epilogues, at
     # TMA-sized shapes, against the reference library's ops::kronsumv
