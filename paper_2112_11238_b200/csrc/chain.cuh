@@ -236,12 +236,7 @@ static bool chain_boundary(const ModeJob& jp, const TmaParams& pp, int bm_p, int
     std::sort(cur.begin(), cur.end());
     cur.erase(std::unique(cur.begin(), cur.end()), cur.end());
     for (int m : cur) {
-      if (m < 0 || m >= pc.mt) {
-        if (getenv("MUMODE_DEBUG_CHAIN"))
-          fprintf(stderr, "chain_boundary: phase %d tile %lld -> consumer M-tile %d of %d\n", k, (long long)t, m,
-                  pc.mt);
-        return false;
-      }
+      if (m < 0 || m >= pc.mt) return false;  // never expected; the caller runs the modes one by one
       sig_idx.push_back(m);
       ++target[static_cast<size_t>(m)];
     }
@@ -322,18 +317,8 @@ static int launch_chain(mumode_handle_s* h, const std::vector<ModeJob>& jobs, in
   if (pl.counter_ints) MM_CUDA(cudaMemsetAsync(pl.counters.p, 0, pl.counter_ints * sizeof(int), h->stream));
   const int grid = static_cast<int>(std::min<int64_t>(cp.total, persistent_sms(h)));
   auto kern = tucker_chain_kernel<CfgA, CfgB>;
-  MM_TRY(smem_opt_in(kern, CfgB::SMEM_BYTES));
-  static const bool dbg = getenv("MUMODE_DEBUG_CHAIN") != nullptr;  // TEMP diagnostics
-  if (dbg) {
-    const cudaError_t e0 = cudaStreamSynchronize(h->stream);
-    fprintf(stderr, "chain: before launch d=%d total=%lld grid=%d ctr=%zu err=%s\n", d, (long long)cp.total, grid,
-            pl.counter_ints, cudaGetErrorString(e0));
-  }
-  kern<<<grid, CfgB::THREADS, CfgB::SMEM_BYTES, h->stream>>>(maps, cp);  // no PDL (tma_chain.cuh)
-  if (dbg) {
-    const cudaError_t e1 = cudaStreamSynchronize(h->stream);
-    fprintf(stderr, "chain: after launch err=%s\n", cudaGetErrorString(e1));
-  }
+  MM_TRY(smem_opt_in(kern, CfgB::SMEM_BYTES + kChainExtraSmem));
+  kern<<<grid, CfgB::THREADS, CfgB::SMEM_BYTES + kChainExtraSmem, h->stream>>>(maps, cp);  // no PDL (tma_chain.cuh)
   MM_CUDA(cudaGetLastError());
   h->launches++;
   return MUMODE_OK;

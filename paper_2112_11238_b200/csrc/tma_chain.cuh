@@ -27,6 +27,8 @@
 namespace mumode_gpu {
 
 constexpr int kChainMaxModes = 8;
+constexpr int kChainPubSlots = 4;  // publisher hand-off ring depth
+constexpr int kChainExtraSmem = 2 * kChainPubSlots * 8;
 
 struct ChainMaps {
   CUtensorMap P[kChainMaxModes];
@@ -86,11 +88,23 @@ __global__ void __launch_bounds__(CfgB::THREADS, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty_bar = full_bar + Cfg::STAGES;
+  // publisher hand-off ring: the MMA warps report a finished producer tile in
+  // slot j % NB (pub_full), the publisher frees the slot after signalling
+  // (pub_empty). Flow-controlled: with named barriers the MMA warps could
+  // lap the publisher on short tiles (K = 24..32) and corrupt the barrier
+  // count -- a deadlock that ended in the watchdog trap (32^5, policy 11).
+  constexpr int NB = kChainPubSlots;
+  uint64_t* pub_full = empty_bar + Cfg::STAGES;
+  uint64_t* pub_empty = pub_full + NB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], Cfg::MMA_WARPS);
+    }
+    for (int s = 0; s < NB; ++s) {
+      mbar_init(&pub_full[s], Cfg::MMA_WARPS);
+      mbar_init(&pub_empty[s], 1);
     }
     fence_barrier_init();
   }
@@ -120,25 +134,26 @@ __global__ void __launch_bounds__(CfgB::THREADS, 1)
   };
   int stage = 0;
   uint32_t phase = 0;
-  constexpr int NB = 4;                          // rotating named barriers 1..NB
-  constexpr int NPUB = Cfg::MMA_WARPS * 32 + 32;  // MMA threads + the publisher warp
   if (warp >= Cfg::MMA_WARPS) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PREGS) : "memory");
     if (warp == Cfg::MMA_WARPS + 1) {
       // publisher: after the MMA warps' arrival for a producer tile (its
       // epilogue stores issued), fence and increment the listed counters;
       // the MMA warps never wait for this
-      int ph = 0, par = 0;
-      for (int64_t item = blockIdx.x; item < cp.total; item += gridDim.x) {
+      int ph = 0;
+      int64_t j = 0;
+      for (int64_t item = blockIdx.x; item < cp.total; item += gridDim.x, ++j) {
         while (ph + 1 < cp.nphases && item >= cp.ph[ph + 1].base) ++ph;
         if (ph + 1 == cp.nphases) break;
         const ChainPhase& P = cp.ph[ph];
-        named_barrier_sync(1 + par, NPUB);
-        par = (par + 1) % NB;
+        const int slot = static_cast<int>(j % NB);
+        mbar_wait(&pub_full[slot], static_cast<uint32_t>((j / NB) & 1));
         __threadfence();
         asm volatile("fence.proxy.async.global;\n" ::: "memory");
         const int64_t tile = item - P.base;
         for (int k = P.sig_off[tile] + lane; k < P.sig_off[tile + 1]; k += 32) chain_signal(P.sig_ctr + P.sig_idx[k]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pub_empty[slot]);
       }
     }
     if (warp == Cfg::MMA_WARPS && lane == 0) {
@@ -162,8 +177,9 @@ __global__ void __launch_bounds__(CfgB::THREADS, 1)
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CREGS) : "memory");
   const FragOffsets foA = tma_frag_offsets<CfgA>(warp, lane);
   const FragOffsets foB = tma_frag_offsets<CfgB>(warp, lane);
-  int ph = 0, par = 0;
-  for (int64_t item = blockIdx.x; item < cp.total; item += gridDim.x) {
+  int ph = 0;
+  int64_t j = 0;
+  for (int64_t item = blockIdx.x; item < cp.total; item += gridDim.x, ++j) {
     int mt, nt;
     locate(item, ph, mt, nt);
     const ChainPhase& P = cp.ph[ph];
@@ -172,8 +188,11 @@ __global__ void __launch_bounds__(CfgB::THREADS, 1)
     else
       tma_consume_tile<CfgB, false, 0>(P.p, mt, nt, smem, full_bar, empty_bar, stage, phase, foB, lane);
     if (ph + 1 < cp.nphases) {  // the tile's stores are issued: hand it to the publisher
-      named_barrier_arrive(1 + par, NPUB);
-      par = (par + 1) % NB;
+      const int slot = static_cast<int>(j % NB);
+      mbar_wait(&pub_empty[slot], static_cast<uint32_t>((j / NB) & 1) ^ 1);  // the slot's last use is published
+      asm volatile("fence.acq_rel.cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pub_full[slot]);
     }
   }
 }

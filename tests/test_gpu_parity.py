@@ -416,6 +416,26 @@ def test_repeated_products_are_bitwise_identical(policy_id):
         h.set_kernel_policy(0)
 
 
+@pytest.mark.parametrize("shape", [(32,) * 5, (24,) * 5, (16,) * 5, (24,) * 6])
+def test_chain_kernel_short_tiles(shape):
+    # policy 11 (whole chain in one launch) with short tiles (K = 16..32):
+    # the MMA warps outpace the publisher warp; its hand-off ring must flow-
+    # control them (with unthrottled named barriers 32^5 deadlocked into the
+    # watchdog trap). Repeated, bitwise against the per-mode path.
+    torch.manual_seed(11)
+    h = mm.get_handle(0)
+    T = mm.colmajor_empty(shape, torch.float64, "cuda").normal_()
+    Ls = [mm.to_colmajor(torch.randn(e, e, dtype=torch.float64, device="cuda")) for e in shape]
+    try:
+        h.set_kernel_policy(10)
+        ref = mm.tucker(T, Ls)
+        h.set_kernel_policy(11)
+        for _ in range(4):
+            assert torch.equal(mm.tucker(T, Ls), ref)
+    finally:
+        h.set_kernel_policy(0)
+
+
 def test_kronsumv_fused_epilogue_vs_reference(policy):
     # W = sum_mu V x_mu A_mu with the terms accumulated in the epilogues, at
     # TMA-sized shapes, against the reference library's ops::kronsumv
