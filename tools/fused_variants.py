@@ -1,7 +1,8 @@
 """Time the fused two-mode passes of C5 (24^6) and of a few other small-mode
-shapes under each fused-kernel variant (MUMODE_FUSED_VARIANT), and check every
-variant's outputs are bitwise equal to variant 0's."""
-import os
+shapes under several kernel policies (0 = auto: warp-specialised passes,
+12 = the non-warp-specialised kernels, 9 / 10 = tail pass forced / off), and
+check every policy's outputs are bitwise equal to the first one's.
+argv: policies (e.g. 0,12) and shapes (e.g. 24x24x24x24x24x24)."""
 import sys
 from pathlib import Path
 
@@ -14,9 +15,7 @@ from paper_2112_11238_b200 import _lib  # noqa: E402
 lib = _lib.lib()
 h = mm.get_handle(0)
 h.bind_torch_stream()
-h.set_kernel_policy(int(os.environ.get("POLICY", "0")))
-# variant "F:T" = MUMODE_FUSED_VARIANT F, MUMODE_TAIL_VARIANT T
-variants = sys.argv[1].split(",") if len(sys.argv) > 1 else ["0:0", "2:0", "2:1", "2:3"]
+variants = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else [0, 12]
 shapes = [tuple(int(x) for x in s.split("x")) for s in sys.argv[2].split(",")] if len(sys.argv) > 2 else \
     [(24,) * 6, (16,) * 6, (8,) * 8, (24,) * 4, (24, 24, 24, 24, 24)]
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
@@ -50,8 +49,8 @@ for shape in shapes:
     d = len(shape)
     ref = {}
     for v in variants:
-        os.environ["MUMODE_FUSED_VARIANT"], os.environ["MUMODE_TAIL_VARIANT"] = v.split(":")
-        line = [f"{'x'.join(map(str, shape))} v{v}:"]
+        h.set_kernel_policy(v)
+        line = [f"{'x'.join(map(str, shape))} policy {v}:"]
         for lo in range(1, d, 2):
             S = torch.empty_like(T)
             us = timed(lambda: run_range(T, Ls, S, shape, lo, lo + 1))
@@ -68,4 +67,4 @@ for shape in shapes:
         us = timed(lambda: mm.tucker(T, Ls), reps=5)
         line.append(f"tucker {us:.1f} us")
         print("  ".join(line), flush=True)
-os.environ.pop("MUMODE_FUSED_VARIANT", None)
+h.set_kernel_policy(0)
