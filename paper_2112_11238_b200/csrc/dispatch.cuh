@@ -337,10 +337,11 @@ static bool skinny_ok(const mumode_handle_s* h, const ModeJob& j) {
   if (!(h->policy == 0 || h->policy == 7 || h->policy == 9 || h->policy == 10 || h->policy == 12)) return false;
   if (j.K > 32 || j.N > 32 || !aligned16(j.T) || !aligned16(j.S)) return false;
   if (j.A == 1) {
-    if ((j.K & 1) || (j.N & 1) || (j.C + 31) / 32 >= (int64_t(1) << 31)) return false;
-    return j.C >= int64_t(64) * 148;  // enough 32-fibre tiles to fill the SMs
+    // TMA box coordinates are int32: fibre offsets up to C + 32 TC
+    if ((j.K & 1) || (j.N & 1) || j.C >= (int64_t(1) << 31) - 1024) return false;
+    return j.C >= int64_t(64) * h->num_sms;  // enough 32-fibre tiles to fill the SMs
   }
-  if (j.A % 2 != 0 || j.A >= (int64_t(1) << 31) || j.C >= (int64_t(1) << 31)) return false;
+  if (j.A % 2 != 0 || j.A >= (int64_t(1) << 31) - 1024 || j.C >= (int64_t(1) << 31) - 1024) return false;
   // 16-a tiles (A not a multiple of 16) pay off from A ~ 64 (18^6 modes 3/4,
   // A = 324 / 5832: 300 -> 193 us); for A = 12..24 they waste up to a third
   // of every box, so A <= 32 takes whole c-slabs (skinny_slab_kernel)
@@ -348,9 +349,9 @@ static bool skinny_ok(const mumode_handle_s* h, const ModeJob& j) {
     if (j.A > 32) return false;
     const int P = int((std::max(j.K, j.N) + 7) / 8 * 8);
     const int64_t tc = std::max<int64_t>(1, std::min<int64_t>(256, (32 * P) / (P * j.A)));
-    return (j.C + tc - 1) / tc >= int64_t(2) * 148;
+    return (j.C + tc - 1) / tc >= int64_t(2) * h->num_sms;
   }
-  return ((j.A + 31) / 32) * j.C >= int64_t(2) * 148;
+  return ((j.A + 31) / 32) * j.C >= int64_t(2) * h->num_sms;
 }
 
 template <int P, int TA>
