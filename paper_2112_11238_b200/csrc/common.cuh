@@ -168,13 +168,18 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
-// Non-blocking arrival on a named barrier (producer side of a bar.sync). The
-// fence first: the arriving warp's shared-memory reads (and writes) must be
-// complete before the waiting side reuses the buffer -- ptxas otherwise sinks
-// DMMAs that consume in-flight LDS results past the arrive (see
-// tma_consume_tile).
+// Non-blocking arrival on a named barrier (producer side of a bar.sync).
+// bar.arrive orders the arriving threads' prior shared-memory WRITES for the
+// waiting side; it does not make ptxas wait for prior LOADS whose consumers
+// it has sunk past the arrive (see tma_consume_tile). A warp that releases a
+// buffer it only READ uses named_barrier_arrive_after_reads, unless every
+// load result already feeds a store issued before the arrive.
 __device__ __forceinline__ void named_barrier_arrive(int id, int count) {
-  asm volatile("fence.acq_rel.cta;\n" ::: "memory");
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void named_barrier_arrive_after_reads(int id, int count) {
+  asm volatile("fence.acq_rel.cta;\n" ::: "memory");  // the warp's shared loads are complete
   asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
 

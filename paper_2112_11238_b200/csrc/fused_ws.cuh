@@ -12,8 +12,11 @@
 //   group 1 (GW warps): mode 2   Y[k & 1] -> HBM        (waits: Y full)
 //
 // Y handoffs are named barriers (bar.arrive by the writer group, bar.sync by
-// the reader group; ids 2 + yb "Y full", 4 + yb "Y free"), which order the
-// shared-memory accesses between the two groups. Group 0 skips the "Y free"
+// the reader group; ids 2 + yb "Y full", 2 + NY + yb "Y free"). bar.arrive
+// orders prior shared WRITES only, so group 1 frees Y[yb] after a shared
+// store that depends on every value it loaded from it (loads complete,
+// DMMAs may follow); freeing it only after the global stores cost 545 ->
+// 590 us on C5 pass 1, a fence 557 -> 586 us. Group 0 skips the "Y free"
 // wait for its first two tiles and group 1 skips the "Y free" arrival for its
 // last two, so every barrier instance completes. Each group holds only its
 // own factor's fragments. Measured on C5 (24^6) pass 1: 581 -> 564 us, DMMA
@@ -37,12 +40,12 @@ struct FusedWsCfg {
   static constexpr int THREADS = (2 * GW + 1) * 32;
   static constexpr int X_BYTES = Base::X_BYTES;
   static constexpr int Y_BYTES = Base::Y_BYTES;
-  // Y buffers between the groups (C5 pass 1: 2 -> 556 us with a 4-deep ring,
-  // 3 -> 567 us with a 3-deep ring)
+  // Y buffers between the groups (C5 pass 1: 2 -> 545 us with a 4-deep ring,
+  // 3 -> 551 us with a 3-deep ring)
   static constexpr int NY = NY_;
-  static constexpr int NBUF = (4 * X_BYTES + NY * Y_BYTES + 2048 <= 227 * 1024) ? 4
-                              : (3 * X_BYTES + NY * Y_BYTES + 2048 <= 227 * 1024) ? 3 : 2;
-  static constexpr int SMEM_BYTES = NBUF * X_BYTES + NY * Y_BYTES + 1024 + 128;
+  static constexpr int NBUF = (4 * X_BYTES + NY * Y_BYTES + 2048 + GW * 256 <= 227 * 1024) ? 4
+                              : (3 * X_BYTES + NY * Y_BYTES + 2048 + GW * 256 <= 227 * 1024) ? 3 : 2;
+  static constexpr int SMEM_BYTES = NBUF * X_BYTES + NY * Y_BYTES + 1024 + 128 + GW * 32 * 8;
   static_assert(MU == 8 || MU == 16 || MU == 24, "square modes of 8, 16, 24");
   static_assert(UNITS % GW == 0, "units split evenly over a group");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
@@ -62,6 +65,8 @@ __global__ void __launch_bounds__(FusedWsCfg<MU, NY>::THREADS, 1)
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(Ybase + NY * Cfg::Y_BYTES);
   uint64_t* empty_bar = full_bar + NBUF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // per group-1 warp: 32 words the "Y free" dependency stores go to
+  uint64_t* scratch = empty_bar + NBUF + 32 * (warp % Cfg::GW);
 
   if (threadIdx.x == 0) {
     for (int b = 0; b < NBUF; ++b) {
@@ -174,17 +179,27 @@ __global__ void __launch_bounds__(FusedWsCfg<MU, NY>::THREADS, 1)
 #pragma unroll
     for (int q = 0; q < UPW; ++q) {
       const int u = w + GW * q;  // (cl, ib) = (u / NF, u % NF)
+      double yf[KS];
+#pragma unroll
+      for (int s = 0; s < KS; ++s)
+        yf[s] = *reinterpret_cast<const double*>(Y + y_off(u * (MU + 1) + 4 * s + t, xmap8(g)));
+      if (q == UPW - 1 && k + NY < ntiles) {
+        // free Y[yb] as soon as the last unit's loads are complete: a shared
+        // store that depends on every loaded value (bar.arrive keeps it
+        // before the arrive; ptxas cannot sink it like a DMMA)
+        uint64_t dep = 0;
+#pragma unroll
+        for (int s = 0; s < KS; ++s) dep ^= static_cast<uint64_t>(__double_as_longlong(yf[s]));
+        *reinterpret_cast<volatile uint64_t*>(scratch + lane) = dep;
+        named_barrier_arrive(2 + NY + yb, PAIR);
+      }
       double acc[NF][2];
 #pragma unroll
       for (int nf = 0; nf < NF; ++nf) acc[nf][0] = acc[nf][1] = 0.0;
 #pragma unroll
-      for (int s = 0; s < KS; ++s) {
-        const double yf = *reinterpret_cast<const double*>(Y + y_off(u * (MU + 1) + 4 * s + t, xmap8(g)));
+      for (int s = 0; s < KS; ++s)
 #pragma unroll
-        for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[nf][0], acc[nf][1], l2[nf][s], yf);
-      }
-      // every Y value of this tile has been consumed by a DMMA: free Y[yb]
-      if (q == UPW - 1 && k + NY < ntiles) named_barrier_arrive(2 + NY + yb, PAIR);
+        for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[nf][0], acc[nf][1], l2[nf][s], yf[s]);
       const int cl = u / NF, ib = u % NF;
       const int64_t c = c_base + cl;
       if (c < p.C) {

@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(TailWsCfg<MU>::THREADS, 1)
         }
       }
       // every Ys value of this stage has been consumed by a DMMA
-      if (z + NYS < nst) named_barrier_arrive(2 + NYS + yb, PAIR);
+      if (z + NYS < nst) named_barrier_arrive_after_reads(2 + NYS + yb, PAIR);
     }
     // epilogue: one i at a time through this warp's staging slot (TMA-box
     // layout {16 a, 2 h, 1, MU j}: row 2j + h), then one TMA store
