@@ -123,24 +123,19 @@ class ClockSampler:
 
 # ----------------------------------------------------------------- reference arm
 def run_reference(args, rank: int) -> None:
+    """The driver's reference arm: the reference library itself (oracle/_ref,
+    compiled from /root/reference/proj/src) on all host cores. One call into
+    it draws the C2 inputs with the reference's generator and times each
+    ops::tucker application in C++ (oracle/ref_shim.cpp ref_bench_tucker_f64),
+    so neither this package nor any copy of the operands is on the path."""
     if rank != 0:
         return
     import oracle as O
-    from paper_2112_11238_b200 import Rng
     cores = os.cpu_count() or 1
     O.ref_lib(threads=cores)
-    g = Rng(SEED)
-    T = g.normal(C2)
-    Ls = [g.normal((256, 256)) for _ in range(3)]
     flops = tucker_flops(C2, [256, 256, 256])
-    for _ in range(args.warmup):
-        O.ref_tucker(T, Ls)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        O.ref_tucker(T, Ls)
-        times.append(time.perf_counter() - t0)
-    total = sum(times)
+    times, checksum = O.ref_bench_tucker(SEED, C2, (256, 256, 256), args.warmup, args.steps)
+    total = float(sum(times))
     value = flops * args.steps / total / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
@@ -152,8 +147,10 @@ def run_reference(args, rank: int) -> None:
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": f"ops::tucker 256^3 x {args.steps} steps (full C2 workload per step), "
                                    f"reference library compiled from /root/reference/proj/src "
-                                   f"(oracle/_ref), OpenBLAS {O.ref_blas_kernel_name()}"},
+                                   f"(oracle/_ref), inputs drawn and each step timed inside it; "
+                                   f"OpenBLAS {O.ref_blas_kernel_name()}"},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "result_checksum": checksum,
     }
     print(json.dumps(line), flush=True)
 
@@ -382,7 +379,7 @@ def main():
         "clocks": dict(clocks.summary(), remeasured=remeasured),
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(T_host, L_host, flops)
+        line["cpu_baseline"] = cpu_baseline(flops)
     if world == 1 and not args.no_extras:
         line["extras"] = extras(mm, lib, h, dev, stream, peak, flush)
     print(json.dumps(line), flush=True)
@@ -592,14 +589,18 @@ def ctypes_peak(lib, h) -> float:
     return float(v.value)
 
 
-def cpu_baseline(T_host, L_host, flops):
-    """The reference library (oracle/_ref) on this box's host cores, same bytes."""
+def cpu_baseline(flops):
+    """The reference library (oracle/_ref) on this box's host cores: the same
+    C2 workload, inputs drawn inside it with the same generator and seed, each
+    ops::tucker timed in C++ (the --impl reference arm's measurement, bounded
+    to 1 warm-up + 5 steps)."""
     try:
         import oracle as O
         cores = os.cpu_count() or 1
         O.ref_lib(threads=cores)
         reps = 5
-        med, _ = O.ref_time_tucker(T_host, L_host, steps=1, reps=reps)
+        times, _ = O.ref_bench_tucker(SEED, C2, (256, 256, 256), 1, reps)
+        med = statistics.median(times)
         return {"value": round(flops / med / 1e9, 3), "unit": UNIT, "cores": cores, "kind": "reference",
                 "sample": f"ops::tucker on the full C2 workload (256^3), 1 warm-up + median of {reps}; "
                           f"OMP/OpenBLAS threads = {cores}; OpenBLAS core {O.ref_blas_kernel_name()}",

@@ -451,33 +451,61 @@ inline Tensor<double> kronsumv(const Tensor<double>& v, const MatrixStack<double
 }
 
 /// Per-mode factorizations for the inverse Tucker operator
-/// (ops::FactorizedStack, tucker.hpp:34-51), real. Factorizes (LU with partial
-/// pivoting) at construction and throws NumericalError on a singular pivot
-/// (lu.hpp:33); keeps P_mu^-1 for the GPU.
+/// (ops::FactorizedStack<T>, tucker.hpp:34-51): la::lu_factor (lu.hpp:23-47)
+/// at construction, on the host through mumode_lu_factor_* (bitwise the
+/// reference's factors), throwing NumericalError on a singular pivot
+/// (lu.hpp:33). T is double or cplx.
+template <class T>
 class FactorizedStack {
+  static_assert(std::is_same_v<T, double> || std::is_same_v<T, cplx>, "FactorizedStack<double> or <cplx>");
+
  public:
-  explicit FactorizedStack(const MatrixStack<double>& Ps) {
+  struct Factors {
+    Matrix<T> lu;
+    std::vector<index_t> piv;
+  };
+  explicit FactorizedStack(const MatrixStack<T>& Ps) {
     for (const auto& P : Ps) {
       if (P.rows() != P.cols()) throw core::SizeError("lu_factor: matrix must be square");
-      Matrix<double> inv(P.rows(), P.cols());
-      engine::check(mumode_inverse_f64(P.rows(), P.data(), inv.data()));
-      inv_.push_back(std::move(inv));
+      Factors f{Matrix<T>(P.rows(), P.cols()), std::vector<index_t>(static_cast<std::size_t>(P.rows()))};
+      if constexpr (std::is_same_v<T, double>)
+        engine::check(mumode_lu_factor_f64(P.rows(), P.data(), f.lu.data(), f.piv.data()));
+      else
+        engine::check(mumode_lu_factor_c128(P.rows(), engine::raw(P.data()), engine::raw(f.lu.data()), f.piv.data()));
+      factors_.push_back(std::move(f));
     }
   }
-  index_t size() const { return static_cast<index_t>(inv_.size()); }
-  const MatrixStack<double>& inverses() const { return inv_; }
+  index_t size() const { return static_cast<index_t>(factors_.size()); }
+  const Factors& factor(index_t mu) const { return factors_.at(static_cast<std::size_t>(mu - 1)); }
 
  private:
-  MatrixStack<double> inv_;
+  std::vector<Factors> factors_;
 };
 
-/// Inverse Tucker S = T x_1 P_1^-1 ... x_d P_d^-1 (ops::itucker, tucker.hpp:187-204).
-inline Tensor<double> itucker(const Tensor<double>& t, const FactorizedStack& F) {
+/// Inverse Tucker S = T x_1 P_1^-1 ... x_d P_d^-1 (ops::itucker,
+/// tucker.hpp:187-204): per-mode triangular solves with the stored factors on
+/// the GPU (mumode_host_itucker_*); no inverse is formed.
+template <class T>
+Tensor<T> itucker(const Tensor<T>& t, const FactorizedStack<T>& F) {
   if (F.size() != t.order()) throw core::SizeError("itucker: stack length does not match tensor order");
-  for (index_t mu = 1; mu <= t.order(); ++mu)
-    if (F.inverses()[static_cast<std::size_t>(mu - 1)].rows() != t.extent(mu))
+  std::vector<const double*> lus;
+  std::vector<const int64_t*> pivs;
+  for (index_t mu = 1; mu <= t.order(); ++mu) {
+    const auto& f = F.factor(mu);
+    if (f.lu.rows() != t.extent(mu))
       throw core::SizeError("itucker: factor size does not match extent of mode " + std::to_string(mu));
-  return tucker(t, F.inverses());
+    lus.push_back(engine::raw(f.lu.data()));
+    pivs.push_back(f.piv.data());
+  }
+  Tensor<T> S{t.shape()};
+  const int dd = static_cast<int>(t.order());
+  if constexpr (std::is_same_v<T, double>)
+    engine::check(mumode_host_itucker_f64(engine::handle(), dd, t.shape().extents().data(), t.data(), lus.data(),
+                                          pivs.data(), S.data()));
+  else
+    engine::check(mumode_host_itucker_c128(engine::handle(), dd, t.shape().extents().data(), engine::raw(t.data()),
+                                           lus.data(), pivs.data(), engine::raw(S.data())));
+  return S;
 }
 
 /// Columnwise operator of the operator-action Tucker (tucker.hpp:24-32).

@@ -253,11 +253,44 @@ int mumode_probe_fp64_peak(mumode_handle_t h, double* tflops);
  * (proj/src/expm.cpp:97-151) for the exponential integrator's E_mu. */
 int mumode_expm_f64(int64_t n, const double* A, double* E);
 
-/* Inverse of a square matrix (LU with partial pivoting, host fp64); the
- * per-mode factor of the inverse Tucker operator ops::itucker
- * (tucker.hpp:187-204): itucker(T, P) = tucker(T, {P_mu^-1}). Returns
- * MUMODE_ERR_NUMERICAL on a zero pivot, like FactorizedStack (lu.hpp:33). */
+/* Inverse of a square matrix (LU with partial pivoting, host fp64). Kept for
+ * callers that want P^-1 itself; ops::itucker runs on mumode_lu_factor_* +
+ * mumode_itucker_* (per-mode solves, no inverse formed). Returns
+ * MUMODE_ERR_NUMERICAL on a zero pivot (lu.hpp:33). */
 int mumode_inverse_f64(int64_t n, const double* P, double* Pinv);
+
+/* la::lu_factor (proj/include/mumode/lu.hpp:23-47), host: P = perm * L * U
+ * with partial pivoting; lu (n x n, column-major) holds the unit-lower L
+ * below the diagonal and U on/above it, piv[k] = the row swapped into row k
+ * at step k. Bitwise the reference's factors (the FactorizedStack role,
+ * tucker.hpp:34-51). MUMODE_ERR_NUMERICAL "lu_factor: singular pivot". */
+int mumode_lu_factor_f64(int64_t n, const double* P, double* lu, int64_t* piv);
+int mumode_lu_factor_c128(int64_t n, const double* P, double* lu, int64_t* piv);
+
+/* Replaces ops::itucker (tucker.hpp:187-204): S = T x_1 P_1^-1 ... x_d P_d^-1
+ * by per-mode triangular solves with DEVICE factors LU[k] (m_k x m_k, as
+ * mumode_lu_factor_*) and DEVICE pivots piv[k] (m_k int64); lu_solve's
+ * arithmetic (lu.hpp:52-69 on OpenBLAS's trsm kernels). S may alias T. */
+int mumode_itucker_f64(mumode_handle_t h, int d, const int64_t* m, const double* T, const double* const* LU,
+                       const int64_t* const* piv, double* S);
+int mumode_itucker_c128(mumode_handle_t h, int d, const int64_t* m, const double* T, const double* const* LU,
+                        const int64_t* const* piv, double* S);
+/* The same with HOST buffers (copies included). */
+int mumode_host_itucker_f64(mumode_handle_t h, int d, const int64_t* m, const double* T, const double* const* LU,
+                            const int64_t* const* piv, double* S);
+int mumode_host_itucker_c128(mumode_handle_t h, int d, const int64_t* m, const double* T, const double* const* LU,
+                             const int64_t* const* piv, double* S);
+
+/* The IMEX direct backend's factor preprocessing (apps DirectSolver,
+ * src/imex.cpp:56-65), host: extract_tridiag (src/imex.cpp:28-48) returns the
+ * symmetric tridiagonal part of M (n x n) or MUMODE_ERR_ARGUMENT with the
+ * reference's "factor is not tridiagonal" / "not symmetric" text;
+ * symtridiag_eig (src/tridiag.cpp:12-90, EigMode::FullVectors) returns the
+ * ascending eigenvalues and the m x m eigenvector matrix (columns), bitwise
+ * the reference's implicit-shift QL. */
+int mumode_extract_tridiag_f64(int64_t n, const double* M, double* diag, double* offdiag);
+int mumode_symtridiag_eig_f64(int64_t m, const double* diag, const double* offdiag, double* values,
+                              double* vectors);
 
 /* Seeded input generator reproducing the reference's draws bit-for-bit:
  * std::mt19937_64(seed) and a FRESH std::normal_distribution<double> per

@@ -230,12 +230,54 @@ def ref_mode_product(T: np.ndarray, L: np.ndarray, mu: int, loops: bool = False)
 
 
 def ref_itucker(T: np.ndarray, Ps) -> np.ndarray:
+    """ops::itucker with ops::FactorizedStack<T> (tucker.hpp:34-51, 187-204)."""
     lib = ref_lib()
-    T = _f(T, False)
-    Ps = [_f(P, False) for P in Ps]
-    S = np.empty(T.shape, order="F")
-    _check(lib.ref_itucker_f64(ctypes.c_int(T.ndim), _i64(T.shape), _ptr(T), _ptrs(Ps), _ptr(S)))
+    cplx = np.iscomplexobj(T) or any(np.iscomplexobj(P) for P in Ps)
+    T = _f(T, cplx)
+    Ps = [_f(P, cplx) for P in Ps]
+    S = np.empty(T.shape, dtype=T.dtype, order="F")
+    fn = lib.ref_itucker_c128 if cplx else lib.ref_itucker_f64
+    _check(fn(ctypes.c_int(T.ndim), _i64(T.shape), _ptr(T), _ptrs(Ps), _ptr(S)))
     return S
+
+
+def ref_lu_factor(P: np.ndarray):
+    """la::lu_factor (lu.hpp:23-47): (lu, piv)."""
+    lib = ref_lib()
+    cplx = np.iscomplexobj(P)
+    P = _f(P, cplx)
+    n = P.shape[0]
+    lu = np.empty(P.shape, dtype=P.dtype, order="F")
+    piv = np.empty(n, dtype=np.int64)
+    fn = lib.ref_lu_factor_c128 if cplx else lib.ref_lu_factor_f64
+    _check(fn(ctypes.c_int64(n), _ptr(P), _ptr(lu), piv.ctypes.data_as(I64P)))
+    return lu, piv
+
+
+def ref_symtridiag_eig(diag: np.ndarray, offdiag: np.ndarray):
+    """la::symtridiag_eig, EigMode::FullVectors (src/tridiag.cpp:12-90)."""
+    lib = ref_lib()
+    d = np.ascontiguousarray(diag, dtype=np.float64)
+    e = np.ascontiguousarray(offdiag, dtype=np.float64)
+    m = d.shape[0]
+    w = np.empty(m)
+    V = np.empty((m, m), order="F")
+    ep = e if m > 1 else np.zeros(1)
+    _check(lib.ref_symtridiag_eig_f64(ctypes.c_int64(m), _ptr(d), _ptr(ep), _ptr(w), _ptr(V)))
+    return w, V
+
+
+def ref_imex_direct(u0: np.ndarray, As, tau: float, steps: int = 1) -> np.ndarray:
+    """apps::imex_evolve with ImexBackend::Direct and no nonlinearity
+    (src/imex.cpp:88-200): `steps` DirectSolver solves (:53-86) with
+    M_mu = (1/d) I - tau A_mu."""
+    lib = ref_lib()
+    u0 = _f(u0, False)
+    As = [_f(A, False) for A in As]
+    u = np.empty(u0.shape, order="F")
+    _check(lib.ref_imex_direct_f64(ctypes.c_int(u0.ndim), _i64(u0.shape), _ptrs(As), _ptr(u0),
+                                   ctypes.c_double(tau), ctypes.c_int(steps), _ptr(u)))
+    return u
 
 
 def ref_expm(A: np.ndarray) -> np.ndarray:
@@ -276,6 +318,19 @@ def ref_time_tucker(T: np.ndarray, Ls, steps: int = 1, reps: int = 3):
                                        ctypes.c_int(steps), ctypes.c_int(reps), _ptr(S),
                                        ctypes.byref(med), None))
     return med.value, S
+
+
+def ref_bench_tucker(seed: int, m, n, warmup: int, reps: int):
+    """bench.py's reference arm in one call into the reference library: inputs
+    drawn there with the reference's generator, `warmup` untimed then `reps`
+    individually timed ops::tucker applications. Returns (per-rep seconds,
+    checksum of the last result)."""
+    lib = ref_lib()
+    times = np.zeros(max(reps, 1))
+    chk = ctypes.c_double()
+    _check(lib.ref_bench_tucker_f64(ctypes.c_uint64(seed), ctypes.c_int(len(m)), _i64(m), _i64(n),
+                                    ctypes.c_int(warmup), ctypes.c_int(reps), _ptr(times), ctypes.byref(chk)))
+    return times[:reps], chk.value
 
 
 def ref_blas_kernel_name() -> str:

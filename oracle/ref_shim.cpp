@@ -10,6 +10,9 @@
 //   kronref::kron_apply_oracle      (proj/include/mumode/kron.hpp:73-99)
 //   reference::mode_product_loops   (proj/include/mumode/reference.hpp:62-80)
 //   la::expm                        (proj/src/expm.cpp:97-151)
+//   la::lu_factor                   (proj/include/mumode/lu.hpp:23-47)
+//   la::symtridiag_eig              (proj/src/tridiag.cpp:12-90)
+//   apps::imex_evolve, Direct       (proj/src/imex.cpp:88-200; DirectSolver :53-86)
 //   basis::laplacian_stencil        (proj/src/stencils.cpp:34-50)
 // Buffers are column-major; complex is interleaved (re, im) doubles, which is
 // the std::complex<double> layout. Return codes: 0 ok, 1 SizeError,
@@ -20,11 +23,15 @@
 #include <complex>
 #include <cstdint>
 #include <cstring>
+#include <random>
 #include <string>
 #include <vector>
 
 #include "mumode/expm.hpp"
 #include "mumode/gemm.hpp"
+#include "mumode/imex.hpp"
+#include "mumode/lu.hpp"
+#include "mumode/tridiag.hpp"
 #include "mumode/kron.hpp"
 #include "mumode/mode_product.hpp"
 #include "mumode/reference.hpp"
@@ -186,6 +193,67 @@ int ref_itucker_f64(int d, const int64_t* m, const double* T, const double* cons
   });
 }
 
+int ref_itucker_c128(int d, const int64_t* m, const double* T, const double* const* Ps, double* S) {
+  return guarded([&] {
+    Tensor<cplx> t = make_tensor<cplx>(d, m, T);
+    auto st = make_stack<cplx>(d, m, m, Ps);
+    ops::FactorizedStack<cplx> F(st);
+    store(ops::itucker(t, F), S, nullptr);
+  });
+}
+
+// la::lu_factor (lu.hpp:23-47): lu (n x n) and piv (n).
+int ref_lu_factor_f64(int64_t n, const double* P, double* lu, int64_t* piv) {
+  return guarded([&] {
+    auto f = la::lu_factor(make_matrix<double>(n, n, P));
+    std::memcpy(lu, f.lu.data(), sizeof(double) * static_cast<std::size_t>(n * n));
+    for (int64_t k = 0; k < n; ++k) piv[k] = f.piv[static_cast<std::size_t>(k)];
+  });
+}
+int ref_lu_factor_c128(int64_t n, const double* P, double* lu, int64_t* piv) {
+  return guarded([&] {
+    auto f = la::lu_factor(make_matrix<cplx>(n, n, P));
+    std::memcpy(lu, f.lu.data(), sizeof(cplx) * static_cast<std::size_t>(n * n));
+    for (int64_t k = 0; k < n; ++k) piv[k] = f.piv[static_cast<std::size_t>(k)];
+  });
+}
+
+// la::symtridiag_eig, EigMode::FullVectors (tridiag.cpp:12-90).
+int ref_symtridiag_eig_f64(int64_t m, const double* diag, const double* offdiag, double* values,
+                           double* vectors) {
+  return guarded([&] {
+    la::TridiagSym T;
+    T.diag.assign(diag, diag + m);
+    T.offdiag.assign(offdiag, offdiag + (m - 1));
+    auto r = la::symtridiag_eig(T, la::EigMode::FullVectors);
+    std::memcpy(values, r.values.data(), sizeof(double) * static_cast<std::size_t>(m));
+    std::memcpy(vectors, r.vectors.data(), sizeof(double) * static_cast<std::size_t>(m * m));
+  });
+}
+
+// One step of apps::imex_evolve with the Direct backend and no nonlinearity
+// (src/imex.cpp:88-200): builds DirectSolver from M_mu = (1/d) I - tau A_mu
+// (extract_tridiag + symtridiag_eig, :28-65) and returns u1 = solve(u0)
+// (:67-86) -- the reference's own DirectSolver, reached through its public
+// driver. A_mu: m_mu x m_mu stencil matrices.
+int ref_imex_direct_f64(int d, const int64_t* m, const double* const* As, const double* u0, double tau,
+                        int steps, double* u) {
+  return guarded([&] {
+    apps::EvolutionProblem prob;
+    for (int k = 0; k < d; ++k) {
+      basis::StencilMatrix st;
+      st.A = make_matrix<double>(m[k], m[k], As[k]);
+      prob.stencils.push_back(std::move(st));
+    }
+    prob.u0 = make_tensor<double>(d, m, u0);
+    prob.tau = tau;
+    prob.t_final = tau * steps;
+    prob.nonlinearity = apps::NonlinearTerm::None;
+    auto res = apps::imex_evolve(prob, apps::ImexBackend::Direct);
+    store(res.first, u, nullptr);
+  });
+}
+
 int ref_expm_f64(int64_t n, const double* A, double* E) {
   return guarded([&] {
     Matrix<double> Am = make_matrix<double>(n, n, A);
@@ -227,6 +295,45 @@ int ref_time_tucker_f64(int d, const int64_t* m, const int64_t* Lrows, const int
     std::sort(sorted.begin(), sorted.end());
     *median_s = sorted[sorted.size() / 2];
     if (S) store(u, S, nullptr);
+  });
+}
+
+// The reference arm of bench.py, entirely inside the reference library: draws
+// T (m_1 x ... x m_d) then L_1..L_d (n_mu x m_mu) with the reference's
+// generator (std::mt19937_64(seed), a FRESH std::normal_distribution<double>
+// per object, column-major fill; tools/mumode_cli.cpp:92-121, :237-240), runs
+// `warmup` untimed ops::tucker applications, then times `reps` of them one by
+// one (times[r], seconds). No input or output crosses this boundary, so the
+// timed region is ops::tucker alone (its own output allocation included, as
+// in the reference's bench-tucker, tools/mumode_cli.cpp:219-255).
+int ref_bench_tucker_f64(uint64_t seed, int d, const int64_t* m, const int64_t* n, int warmup, int reps,
+                         double* times, double* checksum) {
+  return guarded([&] {
+    std::mt19937_64 g(seed);
+    auto fill = [&g](double* p, index_t count) {
+      std::normal_distribution<double> dist;
+      for (index_t k = 0; k < count; ++k) p[k] = dist(g);
+    };
+    Tensor<double> t{Shape(std::vector<index_t>(m, m + d))};
+    fill(t.data(), t.numel());
+    ops::MatrixStack<double> st;
+    for (int k = 0; k < d; ++k) {
+      Matrix<double> L(n[k], m[k]);
+      fill(L.data(), n[k] * m[k]);
+      st.push_back(std::move(L));
+    }
+    Tensor<double> s;
+    for (int w = 0; w < warmup; ++w) s = ops::tucker(t, st);
+    for (int r = 0; r < reps; ++r) {
+      const double a = now_s();
+      s = ops::tucker(t, st);
+      times[r] = now_s() - a;
+    }
+    if (checksum) {
+      double c = 0.0;
+      for (index_t k = 0; k < s.numel(); ++k) c += s[k];
+      *checksum = c;
+    }
   });
 }
 

@@ -19,6 +19,7 @@ from .api import (  # noqa: F401
     dematricize,
     expint,
     expm,
+    extract_tridiag,
     get_handle,
     is_colmajor,
     itucker,
@@ -29,6 +30,7 @@ from .api import (  # noqa: F401
     mode_product,
     to_colmajor,
     tucker,
+    symtridiag_eig,
     tucker_sequential,
     tuckerfun,
 )

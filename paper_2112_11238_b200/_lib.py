@@ -71,6 +71,14 @@ SIGNATURES = {
     "mumode_probe_fp64_peak": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_double)]),
     "mumode_expm_f64": (ctypes.c_int, [I64, VP, VP]),
     "mumode_inverse_f64": (ctypes.c_int, [I64, VP, VP]),
+    "mumode_lu_factor_f64": (ctypes.c_int, [I64, VP, VP, VP]),
+    "mumode_lu_factor_c128": (ctypes.c_int, [I64, VP, VP, VP]),
+    "mumode_itucker_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, VP, ctypes.POINTER(VP), ctypes.POINTER(VP), VP]),
+    "mumode_itucker_c128": (ctypes.c_int, [H, ctypes.c_int, I64P, VP, ctypes.POINTER(VP), ctypes.POINTER(VP), VP]),
+    "mumode_host_itucker_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, VP, ctypes.POINTER(VP), ctypes.POINTER(VP), VP]),
+    "mumode_host_itucker_c128": (ctypes.c_int, [H, ctypes.c_int, I64P, VP, ctypes.POINTER(VP), ctypes.POINTER(VP), VP]),
+    "mumode_extract_tridiag_f64": (ctypes.c_int, [I64, VP, VP, VP]),
+    "mumode_symtridiag_eig_f64": (ctypes.c_int, [I64, VP, VP, VP, VP]),
     "mumode_rng_create": (ctypes.c_int, [ctypes.POINTER(VP), ctypes.c_uint64]),
     "mumode_rng_destroy": (ctypes.c_int, [VP]),
     "mumode_rng_normal": (ctypes.c_int, [VP, VP, I64, ctypes.c_int]),

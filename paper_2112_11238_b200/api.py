@@ -14,6 +14,9 @@ this module            reference
 ``expint``             repeated ``apps::linear_evolution_exact`` step
                        (src/evolution.cpp:70-82) with precomputed factors
 ``expm``               ``la::expm`` role (src/expm.cpp:97-151), host
+``FactorizedStack``    ``ops::FactorizedStack<T>`` (tucker.hpp:34-51)
+``itucker``            ``ops::itucker`` (tucker.hpp:187-204)
+``KronSumSolver``      IMEX ``DirectSolver`` (src/imex.cpp:53-86)
 ``SizeError`` ...      ``mumode::SizeError`` ... (errors.hpp:8-26)
 =====================  ==================================================
 
@@ -450,56 +453,132 @@ def tuckerfun(T, ops):
 
 
 class FactorizedStack:
-    """Per-mode factorizations of square P_1..P_d for the inverse Tucker
-    operator (ops::FactorizedStack, tucker.hpp:34-51). Factorizes at
-    construction, raising NumericalError on a singular pivot (lu.hpp:33); what
-    is kept is each P_mu^-1, applied on the GPU as a Tucker operator."""
+    """Per-mode LU factorizations of square P_1..P_d for the inverse Tucker
+    operator (ops::FactorizedStack<T>, tucker.hpp:34-51). Factorizes at
+    construction exactly as la::lu_factor (lu.hpp:23-47; host,
+    mumode_lu_factor_*), raising NumericalError on a singular pivot (lu.hpp:33)
+    and SizeError for a non-square factor. The stack is complex if any P_mu
+    is. ``factor(mu)`` returns (lu, piv) like the reference's ``factor``."""
 
     def __init__(self, Ps):
-        self.inverses = []
-        for mu, P in enumerate(Ps, 1):
-            Pn = _np_f(np.asarray(P.cpu() if _is_torch(P) else P), False)
+        Ps = [np.asarray(P.cpu() if _is_torch(P) else P) for P in Ps]
+        self.cplx = any(np.iscomplexobj(P) for P in Ps)
+        self.lu, self.piv = [], []
+        fn = _lib.lib().mumode_lu_factor_c128 if self.cplx else _lib.lib().mumode_lu_factor_f64
+        for P in Ps:
+            Pn = _np_f(P, self.cplx)
             if Pn.ndim != 2 or Pn.shape[0] != Pn.shape[1]:
                 raise SizeError("lu_factor: matrix must be square")
-            inv = np.empty(Pn.shape, order="F")
-            _check(_lib.lib().mumode_inverse_f64(int(Pn.shape[0]), Pn.ctypes.data, inv.ctypes.data))
-            self.inverses.append(inv)
+            lu = np.empty(Pn.shape, dtype=Pn.dtype, order="F")
+            piv = np.empty(Pn.shape[0], dtype=np.int64)
+            _check(fn(int(Pn.shape[0]), Pn.ctypes.data, lu.ctypes.data, piv.ctypes.data))
+            self.lu.append(lu)
+            self.piv.append(piv)
+        self._dev = {}
 
     def size(self) -> int:
-        return len(self.inverses)
+        return len(self.lu)
+
+    def factor(self, mu: int):
+        return self.lu[mu - 1], self.piv[mu - 1]
+
+    def _device(self, device, cplx: bool):
+        key = (str(device), cplx)
+        if key not in self._dev:
+            dt = torch.complex128 if cplx else torch.float64
+            self._dev[key] = ([torch.from_numpy(lu).to(device=device, dtype=dt) for lu in self.lu],
+                              [torch.from_numpy(p).to(device) for p in self.piv])
+        return self._dev[key]
 
 
 def itucker(T, F: FactorizedStack):
-    """S = T x_1 P_1^-1 ... x_d P_d^-1 (ops::itucker, tucker.hpp:187-204)."""
+    """S = T x_1 P_1^-1 ... x_d P_d^-1 (ops::itucker, tucker.hpp:187-204):
+    per-mode triangular solves with the stored factors on the GPU (no inverse
+    is formed). A real tensor with a complex stack promotes to complex."""
     _validate_tensor(T)
     if F.size() != T.ndim:
         raise SizeError("itucker: stack length does not match tensor order")
-    for mu, inv in enumerate(F.inverses, 1):
-        if inv.shape[0] != int(T.shape[mu - 1]):
+    for mu, lu in enumerate(F.lu, 1):
+        if lu.shape[0] != int(T.shape[mu - 1]):
             raise SizeError(f"itucker: factor size does not match extent of mode {mu}")
+    cplx = F.cplx or _is_cplx(T)
+    m = _extents(T)
+    lib = _lib.lib()
     if _is_torch(T):
-        return tucker(T, [torch.from_numpy(inv).to(T.device) for inv in F.inverses])
-    return tucker(T, F.inverses)
+        h = get_handle(T.device.index)
+        h.bind_torch_stream()
+        Td = to_colmajor(T.to(torch.complex128) if cplx and not T.is_complex() else T)
+        lus, pivs = F._device(T.device, cplx)
+        S = colmajor_empty(m, Td.dtype, T.device)
+        fn = lib.mumode_itucker_c128 if cplx else lib.mumode_itucker_f64
+        _check(fn(h.h, T.ndim, _lib.i64_array(m), _dev_ptr(Td), _lib.ptr_array([_dev_ptr(x) for x in lus]),
+                  _lib.ptr_array([_dev_ptr(p) for p in pivs]), _dev_ptr(S)))
+        return S
+    h = get_handle()
+    Tn = _np_f(T, cplx)
+    lus = [_np_f(lu, cplx) for lu in F.lu]
+    S = np.empty(m, dtype=Tn.dtype, order="F")
+    fn = lib.mumode_host_itucker_c128 if cplx else lib.mumode_host_itucker_f64
+    _check(fn(h.h, T.ndim, _lib.i64_array(m), Tn.ctypes.data, _lib.ptr_array([x.ctypes.data for x in lus]),
+              _lib.ptr_array([p.ctypes.data for p in F.piv]), S.ctypes.data))
+    return S
+
+
+def extract_tridiag(M):
+    """Symmetric tridiagonal part (diag, offdiag) of a factor M -- the IMEX
+    direct backend's extract_tridiag (src/imex.cpp:28-48), with its
+    ArgumentError for entries off the three diagonals or an asymmetric pair."""
+    Mn = _np_f(np.asarray(M.cpu() if _is_torch(M) else M), False)
+    if Mn.ndim != 2 or Mn.shape[0] != Mn.shape[1]:
+        raise SizeError("extract_tridiag: matrix must be square")
+    n = int(Mn.shape[0])
+    diag = np.empty(n)
+    off = np.empty(max(n - 1, 1))
+    _check(_lib.lib().mumode_extract_tridiag_f64(n, Mn.ctypes.data, diag.ctypes.data, off.ctypes.data))
+    return diag, off[:n - 1]
+
+
+def symtridiag_eig(diag, offdiag):
+    """Ascending eigenvalues and eigenvector columns of a symmetric
+    tridiagonal matrix (la::symtridiag_eig with EigMode::FullVectors,
+    src/tridiag.cpp:12-90: implicit-shift QL, bitwise the reference's)."""
+    d = np.ascontiguousarray(diag, dtype=np.float64)
+    e = np.ascontiguousarray(offdiag, dtype=np.float64)
+    m = int(d.shape[0])
+    if m < 1:
+        raise ArgumentError("symtridiag_eig: empty matrix")
+    if int(e.shape[0]) != m - 1:
+        raise ArgumentError("symtridiag_eig: offdiag must have one entry fewer than diag")
+    w = np.empty(m)
+    V = np.empty((m, m), order="F")
+    ep = e if m > 1 else np.zeros(1)
+    _check(_lib.lib().mumode_symtridiag_eig_f64(m, d.ctypes.data, ep.ctypes.data, w.ctypes.data, V.ctypes.data))
+    return w, V
 
 
 class KronSumSolver:
-    """Direct solver for (sum_mu I x ... x M_mu x ... x I) x = b with symmetric
-    M_mu = Q_mu diag(evals_mu) Q_mu^T -- the IMEX direct backend
-    (DirectSolver, src/imex.cpp:53-86): two Tucker applications around a
-    pointwise division by the eigenvalue Kronecker sum, on the GPU. The
-    eigendecompositions are host preprocessing (given, or numpy.linalg.eigh
-    here when built from the M_mu)."""
+    """Direct solver for (sum_mu I x ... x M_mu x ... x I) x = b -- the IMEX
+    direct backend (DirectSolver, src/imex.cpp:53-86). Built from the factors
+    M_mu exactly as the reference builds it: extract_tridiag (ArgumentError
+    unless M_mu is symmetric tridiagonal), symtridiag_eig (implicit-shift QL)
+    and Q_mu^T; or from given eigenpairs (Qs, evals). Each solve is two Tucker
+    applications around a pointwise division by the eigenvalue Kronecker sum,
+    on the GPU (mumode_kronsum_solve_f64)."""
 
     def __init__(self, Ms=None, Qs=None, evals=None, device=None):
         if Ms is not None:
             Qs, evals = [], []
             for M in Ms:
-                Mn = np.asarray(M.cpu() if _is_torch(M) else M, dtype=np.float64)
-                w, V = np.linalg.eigh(0.5 * (Mn + Mn.T))
-                Qs.append(np.asfortranarray(V))
-                evals.append(np.ascontiguousarray(w))
+                w, V = symtridiag_eig(*extract_tridiag(M))
+                Qs.append(V)
+                evals.append(w)
+        if Qs is None or evals is None or len(Qs) != len(evals):
+            raise ArgumentError("kronsum_solve: need the factors Ms, or eigenvectors and eigenvalues per mode")
         self.evals = [np.ascontiguousarray(np.asarray(e, dtype=np.float64)) for e in evals]
         self.Q = [np.asfortranarray(np.asarray(Q, dtype=np.float64)) for Q in Qs]
+        for mu, (Q, e) in enumerate(zip(self.Q, self.evals), 1):
+            if Q.ndim != 2 or Q.shape[0] != Q.shape[1] or e.shape != (Q.shape[0],):
+                raise SizeError(f"kronsum_solve: eigenpairs of mode {mu} do not match")
         self.Qt = [np.asfortranarray(Q.T) for Q in self.Q]
         self._dev = {}
 

@@ -407,19 +407,19 @@ static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t
         double* Sp = np[0] == n[0] ? S : static_cast<double*>(h->pad_out.p);
         if (mp[0] != m[0]) {
           auto* Tpad = static_cast<double*>(h->pad_in.p);
-          pad2d_kernel<<<pad_grid(mp[0], rest_in, h->num_sms), 256, 0, h->stream>>>(T, m[0], rest_in, Tpad, mp[0],
+          pad2d_kernel<<<pad_grid(mp[0], rest_in, h->num_sms), 256, 0, h->stream>>>(T, m[0], rest_in, m[0], Tpad, mp[0],
                                                                                     rest_in);
           h->launches++;
           Tp = Tpad;
         }
-        pad2d_kernel<<<pad_grid(np[0], mp[0], h->num_sms), 256, 0, h->stream>>>(L[0], n[0], m[0], Lp, np[0], mp[0]);
+        pad2d_kernel<<<pad_grid(np[0], mp[0], h->num_sms), 256, 0, h->stream>>>(L[0], n[0], m[0], n[0], Lp, np[0], mp[0]);
         MM_CUDA(cudaGetLastError());
         h->launches++;
         std::vector<const double*> Lpad(L, L + d);
         Lpad[0] = Lp;
         MM_TRY(tucker_dev(h, d, mp.data(), np.data(), Tp, Lpad.data(), Sp, false, false));
         if (Sp != S) {
-          pad2d_kernel<<<pad_grid(n[0], rest_out, h->num_sms), 256, 0, h->stream>>>(Sp, np[0], rest_out, S, n[0],
+          pad2d_kernel<<<pad_grid(n[0], rest_out, h->num_sms), 256, 0, h->stream>>>(Sp, np[0], rest_out, np[0], S, n[0],
                                                                                  rest_out);
           MM_CUDA(cudaGetLastError());
           h->launches++;

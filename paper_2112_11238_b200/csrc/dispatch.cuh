@@ -453,16 +453,18 @@ static int launch_skinny(mumode_handle_s* h, const ModeJob& j) {
 static int run_job(mumode_handle_s* h, const ModeJob& j0) {
   ModeJob j = j0;
   // A real mu > 1 product whose factor has an odd leading dimension (odd n_mu)
-  // is TMA-describable once the factor is re-laid with ld = n_mu + 1 (a tiny
-  // copy; the tensor strides are what they are).
+  // is TMA-describable once the factor's N used rows are re-laid with an even
+  // ld >= N (a tiny copy; the tensor strides are what they are). Only those
+  // rows are read: j.L may be a row block of a larger factor.
   if (!j.cplx && !j.conj && j.A != 1 && j.sLi == 1 && (j.sLk & 1) && h->policy != 1 && h->policy != 8) {
     ModeJob jp = j;
-    jp.sLk = j.sLk + 1;
+    jp.sLk = (j.N + 1) & ~int64_t(1);
     jp.L = reinterpret_cast<const double*>(uintptr_t(256));  // the staged copy is 256-B aligned
     if (tma_ok(jp) && tma_worthwhile(jp)) {
       MM_TRY(h->lstage.ensure(size_t(jp.sLk * j.K) * sizeof(double)));
       auto* Lp = static_cast<double*>(h->lstage.p);
-      pad2d_kernel<<<pad_grid(jp.sLk, j.K, h->num_sms), 256, 0, h->stream>>>(j.L, j.sLk, j.K, Lp, jp.sLk, j.K);
+      pad2d_kernel<<<pad_grid(jp.sLk, j.K, h->num_sms), 256, 0, h->stream>>>(j.L, j.N, j.K, j.sLk, Lp, jp.sLk,
+                                                                              j.K);
       MM_CUDA(cudaGetLastError());
       h->launches++;
       jp.L = Lp;

@@ -3,6 +3,9 @@
 // Neither is on the timed hot path.
 #include <algorithm>
 #include <cmath>
+#include <complex>
+#include <limits>
+#include <numeric>
 #include <cstdint>
 #include <cstring>
 #include <new>
@@ -288,5 +291,162 @@ extern "C" int mumode_inverse_f64(int64_t n, const double* P, double* Pinv) {
     return MUMODE_ERR_NUMERICAL;
   }
   std::memcpy(Pinv, X.data(), sizeof(double) * nn);
+  return MUMODE_OK;
+}
+
+// ------------------------------------------------------------------ LU factors
+// la::lu_factor (lu.hpp:23-47) restated on the same types: partial pivoting on
+// |M(i,k)| (std::abs, complex modulus for complex), a reciprocal pivot
+// T{1}/M(k,k), multipliers M(i,k)*inv_pivot and plain multiply-subtract
+// updates (this file is compiled without FMA contraction, like the reference),
+// so lu and piv are bitwise the reference's FactorizedStack factors.
+namespace {
+template <class T>
+int lu_factor_impl(int64_t n, const T* A, T* lu, int64_t* piv) {
+  if (n < 1 || !A || !lu || !piv) {
+    mumode_gpu::set_error("lu_factor: matrix must be non-empty");
+    return MUMODE_ERR_ARGUMENT;
+  }
+  std::copy(A, A + n * n, lu);
+  auto M = [&](int64_t i, int64_t j) -> T& { return lu[i + j * n]; };
+  for (int64_t k = 0; k < n; ++k) {
+    int64_t p = k;
+    double best = std::abs(M(k, k));
+    for (int64_t i = k + 1; i < n; ++i)
+      if (std::abs(M(i, k)) > best) {
+        best = std::abs(M(i, k));
+        p = i;
+      }
+    if (best == 0.0) {
+      mumode_gpu::set_error("lu_factor: singular pivot");
+      return MUMODE_ERR_NUMERICAL;
+    }
+    piv[k] = p;
+    if (p != k)
+      for (int64_t j = 0; j < n; ++j) std::swap(M(k, j), M(p, j));
+    const T inv_pivot = T{1} / M(k, k);
+    for (int64_t i = k + 1; i < n; ++i) {
+      const T m = M(i, k) * inv_pivot;
+      M(i, k) = m;
+      for (int64_t j = k + 1; j < n; ++j) M(i, j) -= m * M(k, j);
+    }
+  }
+  return MUMODE_OK;
+}
+}  // namespace
+
+extern "C" int mumode_lu_factor_f64(int64_t n, const double* P, double* lu, int64_t* piv) {
+  return lu_factor_impl<double>(n, P, lu, piv);
+}
+
+extern "C" int mumode_lu_factor_c128(int64_t n, const double* P, double* lu, int64_t* piv) {
+  using C = std::complex<double>;
+  return lu_factor_impl<C>(n, reinterpret_cast<const C*>(P), reinterpret_cast<C*>(lu), piv);
+}
+
+// ------------------------------------------------------------------ IMEX direct solver factors
+// extract_tridiag (src/imex.cpp:28-48): the symmetric tridiagonal part of a
+// factor M, rejecting entries off the three diagonals and asymmetric
+// off-diagonals with the reference's ArgumentError texts.
+extern "C" int mumode_extract_tridiag_f64(int64_t n, const double* M, double* diag, double* offdiag) {
+  if (n < 1 || !M || !diag || (n > 1 && !offdiag)) {
+    mumode_gpu::set_error("symtridiag_eig: empty matrix");
+    return MUMODE_ERR_ARGUMENT;
+  }
+  double scale = 0.0;
+  for (int64_t k = 0; k < n * n; ++k) scale = std::max(scale, std::abs(M[k]));
+  for (int64_t i = 0; i < n; ++i) {
+    diag[i] = M[i + i * n];
+    for (int64_t j = 0; j < n; ++j)
+      if (std::abs(i - j) > 1 && M[i + j * n] != 0.0) {
+        mumode_gpu::set_error("imex direct backend: factor is not tridiagonal");
+        return MUMODE_ERR_ARGUMENT;
+      }
+    if (i + 1 < n) {
+      const double up = M[i + (i + 1) * n], lo = M[(i + 1) + i * n];
+      if (std::abs(up - lo) > 1e-12 * scale) {
+        mumode_gpu::set_error("imex direct backend: factor is not symmetric");
+        return MUMODE_ERR_ARGUMENT;
+      }
+      offdiag[i] = 0.5 * (up + lo);
+    }
+  }
+  return MUMODE_OK;
+}
+
+// la::symtridiag_eig with EigMode::FullVectors (src/tridiag.cpp:12-90):
+// implicit-shift QL with Wilkinson shifts (cap 50 iterations per eigenvalue),
+// rotations accumulated into the identity, eigenpairs sorted ascending.
+// Same operations in the same order on the same types, so values and vectors
+// are bitwise the reference's. vectors: m x m column-major, eigenvector j in
+// column j.
+extern "C" int mumode_symtridiag_eig_f64(int64_t m, const double* diag, const double* offdiag, double* values,
+                                         double* vectors) {
+  if (m < 1 || !diag || !values || !vectors || (m > 1 && !offdiag)) {
+    mumode_gpu::set_error("symtridiag_eig: empty matrix");
+    return MUMODE_ERR_ARGUMENT;
+  }
+  std::vector<double> d(diag, diag + m);
+  std::vector<double> e(offdiag ? offdiag : diag, offdiag ? offdiag + (m - 1) : diag);
+  e.push_back(0.0);
+  std::vector<double> zs(static_cast<size_t>(m * m), 0.0);
+  auto z = [&](int64_t i, int64_t j) -> double& { return zs[static_cast<size_t>(i + j * m)]; };
+  for (int64_t i = 0; i < m; ++i) z(i, i) = 1.0;
+  const double eps = std::numeric_limits<double>::epsilon();
+  for (int64_t l = 0; l < m; ++l) {
+    int iter = 0;
+    int64_t mm;
+    do {
+      for (mm = l; mm < m - 1; ++mm) {
+        const double dd = std::abs(d[mm]) + std::abs(d[mm + 1]);
+        if (std::abs(e[mm]) <= eps * dd) break;
+      }
+      if (mm != l) {
+        if (iter++ == 50) {
+          mumode_gpu::set_error("symtridiag_eig: QL iteration did not converge");
+          return MUMODE_ERR_NUMERICAL;
+        }
+        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+        double r = std::hypot(g, 1.0);
+        g = d[mm] - d[l] + e[l] / (g + std::copysign(r, g));
+        double s = 1.0, c = 1.0, p = 0.0;
+        int64_t i;
+        for (i = mm; i-- > l;) {
+          double f = s * e[i];
+          const double b = c * e[i];
+          r = std::hypot(f, g);
+          e[i + 1] = r;
+          if (r == 0.0) {
+            d[i + 1] -= p;
+            e[mm] = 0.0;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = d[i + 1] - p;
+          r = (d[i] - g) * s + 2.0 * c * b;
+          p = s * r;
+          d[i + 1] = g + p;
+          g = c * r - b;
+          for (int64_t k = 0; k < m; ++k) {
+            f = z(k, i + 1);
+            z(k, i + 1) = s * z(k, i) + c * f;
+            z(k, i) = c * z(k, i) - s * f;
+          }
+        }
+        if (r == 0.0 && i + 1 > l) continue;
+        d[l] -= p;
+        e[l] = g;
+        e[mm] = 0.0;
+      }
+    } while (mm != l);
+  }
+  std::vector<int64_t> order(static_cast<size_t>(m));
+  std::iota(order.begin(), order.end(), int64_t{0});
+  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return d[a] < d[b]; });
+  for (int64_t j = 0; j < m; ++j) {
+    values[j] = d[static_cast<size_t>(order[static_cast<size_t>(j)])];
+    for (int64_t k = 0; k < m; ++k) vectors[k + j * m] = z(k, order[static_cast<size_t>(j)]);
+  }
   return MUMODE_OK;
 }

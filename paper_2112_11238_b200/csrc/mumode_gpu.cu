@@ -9,6 +9,7 @@
 
 #include <cstdio>
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <type_traits>
 #include <map>
@@ -30,6 +31,7 @@
 #include "skinny.cuh"
 #include "tma_chain.cuh"
 #include "ldg_dmma.cuh"
+#include "lu_solve.cuh"
 
 namespace mumode_gpu {
 
@@ -58,11 +60,17 @@ static int fail(int code, const std::string& msg) {
 }
 
 // ------------------------------------------------------------------ handle
+// Bumped whenever any workspace buffer is (re)allocated: captured CUDA graphs
+// hold raw workspace pointers and by-value TMA descriptors, so a graph
+// captured before a reallocation must not be replayed after it.
+static std::atomic<uint64_t> g_workspace_gen{0};
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   int ensure(size_t want) {
     if (want <= bytes) return MUMODE_OK;
+    g_workspace_gen.fetch_add(1, std::memory_order_relaxed);
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
@@ -100,7 +108,38 @@ struct ChainPlan {
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
   int64_t nodes = 0;
+  uint64_t gen = 0;  // g_workspace_gen at capture
 };
+
+// Make the handle's device current for the scope of one entry point and
+// restore the caller's device on exit (as torch's DeviceGuard does).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      cudaGetLastError();
+      prev = -1;
+    }
+    if (prev != device) err = cudaSetDevice(device);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
+#define MM_DEVICE(dev)                                                                         \
+  ::mumode_gpu::DeviceGuard device_guard_(dev);                                                \
+  do {                                                                                         \
+    if (device_guard_.err != cudaSuccess) {                                                    \
+      cudaGetLastError();                                                                      \
+      return fail(MUMODE_ERR_CUDA, std::string("cudaSetDevice failed: ") +                     \
+                                       cudaGetErrorString(device_guard_.err));                 \
+    }                                                                                          \
+  } while (0)
 
 }  // namespace mumode_gpu
 
@@ -165,14 +204,16 @@ static int launch_pdl(K kernel, int grid, int threads, int smem, cudaStream_t st
   return MUMODE_OK;
 }
 
-// Opt a kernel instance into its dynamic shared memory once per process
-// (keyed by the kernel's address; attributes are per function, not per device
-// for the single-architecture build).
+// Opt a kernel instance into its dynamic shared memory once per (device,
+// kernel): function attributes belong to the device's context, so a second
+// GPU in the same process needs its own opt-in.
 template <class K>
 static int smem_opt_in(K kernel, int bytes) {
   static std::mutex mu;
-  static std::unordered_map<const void*, int> done;
-  const void* key = reinterpret_cast<const void*>(kernel);
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  MM_CUDA(cudaGetDevice(&dev));
+  const std::pair<int, const void*> key{dev, reinterpret_cast<const void*>(kernel)};
   std::lock_guard<std::mutex> lock(mu);
   auto it = done.find(key);
   if (it != done.end() && it->second >= bytes) return MUMODE_OK;
@@ -330,12 +371,14 @@ __global__ void __launch_bounds__(256) eigsum_divide_kernel(double* __restrict__
 }
 
 // (column, destination) pairs on x, 4096-double segments of long runs on y
-// dst (rd x cd) = src (rs x cs) zero-extended / cropped, column-major.
+// dst (rd x cd) = src (rs x cs, leading dimension src_ld >= rs) zero-extended
+// / cropped, column-major.
 __global__ void __launch_bounds__(256) pad2d_kernel(const double* __restrict__ src, int64_t rs, int64_t cs,
-                                                    double* __restrict__ dst, int64_t rd, int64_t cd) {
+                                                    int64_t src_ld, double* __restrict__ dst, int64_t rd,
+                                                    int64_t cd) {
   for (int64_t c = blockIdx.y; c < cd; c += gridDim.y)
     for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < rd; r += int64_t(gridDim.x) * blockDim.x)
-      dst[r + c * rd] = (r < rs && c < cs) ? src[r + c * rs] : 0.0;
+      dst[r + c * rd] = (r < rs && c < cs) ? src[r + c * src_ld] : 0.0;
 }
 
 static dim3 pad_grid(int64_t rows, int64_t cols, int sms) {
@@ -397,7 +440,7 @@ int mumode_handle_create(mumode_handle_t* out, int device) {
     return fail(MUMODE_ERR_CUDA, "no CUDA device available: the mu-mode engine has no CPU path");
   }
   if (device < 0 || device >= ndev) return fail(MUMODE_ERR_ARGUMENT, "bad device index");
-  MM_CUDA(cudaSetDevice(device));
+  MM_DEVICE(device);
   int major = 0;
   MM_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
   if (major != 10)
@@ -417,7 +460,7 @@ int mumode_handle_create(mumode_handle_t* out, int device) {
 
 int mumode_handle_destroy(mumode_handle_t h) {
   if (!h) return MUMODE_OK;
-  cudaSetDevice(h->device);
+  DeviceGuard guard(h->device);
   cudaStreamSynchronize(h->stream);
   for (auto& kv : h->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -463,7 +506,7 @@ static int mode_product_entry(mumode_handle_t h, int d, const int64_t* m, int mu
     out[mu - 1] = n_mu;
     MM_TRY(check_no_alias(T, prod(m, 0, d) * el, S, prod(out.data(), 0, d) * el, "mode_product"));
   }
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   return mode_product_dev(h, d, m, mu, n_mu, T, L, 1, n_mu, cplx, false, S);
 }
 
@@ -485,7 +528,7 @@ static int tucker_entry(mumode_handle_t h, int d, const int64_t* m, const int64_
     const int el = cplx ? 2 : 1;
     MM_TRY(check_no_alias(T, prod(m, 0, d) * el, S, prod(n, 0, d) * el, "tucker"));
   }
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   return tucker_dev(h, d, m, n, T, L, S, adjoint != 0, cplx);
 }
 
@@ -508,7 +551,7 @@ int mumode_tucker_range_f64(mumode_handle_t h, int d, const int64_t* m, const in
   if (!T || !L || !S || !n) return fail(MUMODE_ERR_ARGUMENT, "tucker_range: null pointer");
   for (int k = mu_lo - 1; k < mu_hi; ++k)
     if (!L[k] || n[k] < 1) return fail(MUMODE_ERR_ARGUMENT, "tucker_range: bad matrix for mode " + std::to_string(k + 1));
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   return tucker_dev(h, d, m, n, T, L, S, false, false, mu_lo, mu_hi);
 }
 
@@ -534,7 +577,7 @@ static int tucker_range_scatter(mumode_handle_t h, int d, const int64_t* m, cons
     if (a_off[q + 1] < a_off[q]) return fail(MUMODE_ERR_ARGUMENT, "tucker_range_scatter: offsets must ascend");
     if (!dst[q] && a_off[q + 1] > a_off[q]) return fail(MUMODE_ERR_ARGUMENT, "tucker_range_scatter: null destination");
   }
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   ScatterParams sp{};
   sp.P = P;
   sp.col0 = col0;
@@ -565,7 +608,7 @@ int mumode_slab_pack_f64(mumode_handle_t h, int64_t A, int64_t C, int P, const i
   if (a_off[0] != 0 || a_off[P] != A) return fail(MUMODE_ERR_SIZE, "slab_pack: row offsets must cover 0..A");
   PackOffsets off{};
   for (int q = 0; q <= P; ++q) off.a[q] = a_off[q];
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   slab_pack_kernel<false><<<pack_grid(A, C, P, h->num_sms), 256, 0, h->stream>>>(Y, send, A, C, P, off);
   MM_CUDA(cudaGetLastError());
   h->launches++;
@@ -579,7 +622,7 @@ int mumode_slab_unpack_f64(mumode_handle_t h, int64_t A, int64_t C, int P, const
   if (a_off[0] != 0 || a_off[P] != A) return fail(MUMODE_ERR_SIZE, "slab_unpack: row offsets must cover 0..A");
   PackOffsets off{};
   for (int q = 0; q <= P; ++q) off.a[q] = a_off[q];
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   slab_pack_kernel<true><<<pack_grid(A, C, P, h->num_sms), 256, 0, h->stream>>>(send, Y, A, C, P, off);
   MM_CUDA(cudaGetLastError());
   h->launches++;
@@ -595,7 +638,7 @@ int mumode_kronsum_solve_f64(mumode_handle_t h, int d, const int64_t* m, const d
   for (int k = 0; k < d; ++k)
     if (!Qt[k] || !evals[k])
       return fail(MUMODE_ERR_ARGUMENT, "kronsum_solve: null data for mode " + std::to_string(k + 1));
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   const int64_t numel = prod(m, 0, d);
   const int64_t A = prod(m, 0, d - 1), N = m[d - 1];
   // eigenvalue sums over modes 1..d-1, built mode by mode: esum(a) =
@@ -632,7 +675,7 @@ int mumode_tucker_promote(mumode_handle_t h, int d, const int64_t* m, const int6
                           const double* T, const double* const* L, double* S, int adjoint) {
   if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
   MM_TRY(check_stack(d, m, n, T, L, S, adjoint ? "cttucker" : "tucker"));
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   const int64_t numel = prod(m, 0, d);
   MM_TRY(h->ws[2].ensure(size_t(numel) * 2 * sizeof(double)));
   double* z = static_cast<double*>(h->ws[2].p);
@@ -647,7 +690,7 @@ int mumode_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double
   if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
   MM_TRY(check_stack(d, m, m, V, A, W, "kronsumv"));
   MM_TRY(check_no_alias(V, prod(m, 0, d), W, prod(m, 0, d), "kronsumv"));
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   // W = V x_1 A_1, then W += V x_mu A_mu for mu = 2..d in the products'
   // epilogues (the reference's acc += term order, tucker.hpp:222-231): no
   // term buffer and no separate accumulation pass over W.
@@ -657,12 +700,62 @@ int mumode_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double
   return MUMODE_OK;
 }
 
+// ops::itucker (tucker.hpp:187-204): per mode, every mu-fibre solved with the
+// stored LU factors of P_mu (lu_solve_mode_kernel). Mode 1 reads T, later
+// modes work in place on S (a CTA only touches its own fibres), so T may
+// alias S and no workspace is needed.
+static int itucker_dev(mumode_handle_t h, int d, const int64_t* m, const double* T, const double* const* LU,
+                       const int64_t* const* piv, double* S, bool cplx) {
+  const size_t vb = cplx ? 16 : 8;
+  constexpr size_t kMaxSmem = 227 * 1024;
+  for (int mu = 1; mu <= d; ++mu) {
+    const int64_t n = m[mu - 1], A = prod(m, 0, mu - 1), C = prod(m, mu, d);
+    size_t smem = vb * size_t(n) * (1 + kLuStride);
+    int staged = 1;
+    if (smem > kMaxSmem) {
+      staged = 0;
+      smem = vb * size_t(n);
+      if (smem > kMaxSmem)
+        return fail(MUMODE_ERR_ARGUMENT, "itucker: extent of mode " + std::to_string(mu) + " is too large");
+    }
+    auto kern = cplx ? lu_solve_mode_kernel<true> : lu_solve_mode_kernel<false>;
+    MM_TRY(smem_opt_in(kern, static_cast<int>(smem)));
+    const int64_t tiles = (A * C + kLuFibres - 1) / kLuFibres;
+    const int grid = static_cast<int>(std::min<int64_t>(tiles, int64_t(h->num_sms) * 32));
+    kern<<<grid, kLuFibres, smem, h->stream>>>(mu == 1 ? T : S, S, A, static_cast<int>(n), C, LU[mu - 1],
+                                               piv[mu - 1], staged);
+    MM_CUDA(cudaGetLastError());
+    h->launches++;
+  }
+  return MUMODE_OK;
+}
+
+static int itucker_entry(mumode_handle_t h, int d, const int64_t* m, const double* T, const double* const* LU,
+                         const int64_t* const* piv, double* S, bool cplx) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  MM_TRY(check_shape(d, m, "itucker"));
+  if (!T || !S || !LU || !piv) return fail(MUMODE_ERR_ARGUMENT, "itucker: null pointer");
+  for (int k = 0; k < d; ++k)
+    if (!LU[k] || !piv[k]) return fail(MUMODE_ERR_ARGUMENT, "itucker: null factor for mode " + std::to_string(k + 1));
+  MM_DEVICE(h->device);
+  return itucker_dev(h, d, m, T, LU, piv, S, cplx);
+}
+
+int mumode_itucker_f64(mumode_handle_t h, int d, const int64_t* m, const double* T, const double* const* LU,
+                       const int64_t* const* piv, double* S) {
+  return itucker_entry(h, d, m, T, LU, piv, S, false);
+}
+int mumode_itucker_c128(mumode_handle_t h, int d, const int64_t* m, const double* T, const double* const* LU,
+                        const int64_t* const* piv, double* S) {
+  return itucker_entry(h, d, m, T, LU, piv, S, true);
+}
+
 int mumode_expint_f64(mumode_handle_t h, int d, const int64_t* m, const double* const* E,
                       const double* u0, double* u_out, int steps) {
   if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
   MM_TRY(check_stack(d, m, m, u0, E, u_out, "expint"));
   if (steps < 0) return fail(MUMODE_ERR_ARGUMENT, "expint: steps must be non-negative");
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   const int64_t numel = prod(m, 0, d);
   const size_t bytes = size_t(numel) * sizeof(double);
   if (steps == 0) {
@@ -692,6 +785,12 @@ int mumode_expint_f64(mumode_handle_t h, int d, const int64_t* m, const double* 
     return MUMODE_OK;
   };
   auto it = h->graphs.find(key);
+  if (it != h->graphs.end() && it->second.gen != g_workspace_gen.load(std::memory_order_relaxed)) {
+    // a workspace the graph was captured on has been reallocated since
+    if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
+    h->graphs.erase(it);
+    it = h->graphs.end();
+  }
   if (it == h->graphs.end()) {
     // First call: run eagerly (allocates workspace, encodes TMA maps), then
     // capture the identical launch sequence for later calls.
@@ -715,6 +814,7 @@ int mumode_expint_f64(mumode_handle_t h, int d, const int64_t* m, const double* 
     if (ce != cudaSuccess) return fail(MUMODE_ERR_CUDA, "graph capture failed");
     ge.nodes = h->launches - l0;
     h->launches = l0;  // captured, not executed
+    ge.gen = g_workspace_gen.load(std::memory_order_relaxed);
     MM_CUDA(cudaGraphInstantiate(&ge.exec, graph, 0));
     cudaGraphDestroy(graph);
     h->graphs.emplace(key, ge);
@@ -884,7 +984,7 @@ static int host_tucker_impl(mumode_handle_t h, int d, const int64_t* m, const in
                             int t_el, int l_el) {
   if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
   MM_TRY(check_stack(d, m, n, T, L, S, adjoint ? "cttucker" : "tucker"));
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   if (host_pipelinable(d, m, n, adjoint, t_el, l_el)) {
     MM_TRY(host_tucker_enqueue(h, d, m, n, T, L, S));
     return host_wait(h);
@@ -912,14 +1012,14 @@ int mumode_host_tucker_f64_async(mumode_handle_t h, int d, const int64_t* m, con
                                  const double* T, const double* const* L, double* S) {
   if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
   MM_TRY(check_stack(d, m, n, T, L, S, "tucker"));
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   if (!host_pipelinable(d, m, n, 0, 1, 1)) return host_tucker_impl(h, d, m, n, T, L, S, 0, 1, 1);
   return host_tucker_enqueue(h, d, m, n, T, L, S);
 }
 
 int mumode_host_wait(mumode_handle_t h) {
   if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   return host_wait(h);
 }
 
@@ -941,7 +1041,7 @@ static int host_mode_product_impl(mumode_handle_t h, int d, const int64_t* m, in
     return fail(MUMODE_ERR_ARGUMENT, "mode index " + std::to_string(mu) + " out of range 1.." +
                                          std::to_string(d));
   if (!T || !L || !S) return fail(MUMODE_ERR_ARGUMENT, "mode_product: null pointer");
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   int64_t lsz = n_mu * m[mu - 1] * el;
   const double* dT;
   std::vector<const double*> dL;
@@ -968,7 +1068,7 @@ int mumode_host_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const d
                              const double* const* A, double* W) {
   if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
   MM_TRY(check_stack(d, m, m, V, A, W, "kronsumv"));
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   std::vector<int64_t> lsz(d);
   for (int k = 0; k < d; ++k) lsz[k] = m[k] * m[k];
   const double* dV;
@@ -980,11 +1080,49 @@ int mumode_host_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const d
   return download(h, W, el);
 }
 
+static int host_itucker_impl(mumode_handle_t h, int d, const int64_t* m, const double* T, const double* const* LU,
+                             const int64_t* const* piv, double* S, bool cplx) {
+  if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
+  MM_TRY(check_shape(d, m, "itucker"));
+  if (!T || !S || !LU || !piv) return fail(MUMODE_ERR_ARGUMENT, "itucker: null pointer");
+  for (int k = 0; k < d; ++k)
+    if (!LU[k] || !piv[k]) return fail(MUMODE_ERR_ARGUMENT, "itucker: null factor for mode " + std::to_string(k + 1));
+  MM_DEVICE(h->device);
+  const int el = cplx ? 2 : 1;
+  // factors then pivots (int64 = one double slot each) through the staging upload
+  std::vector<const double*> src(2 * d);
+  std::vector<int64_t> lsz(2 * d);
+  for (int k = 0; k < d; ++k) {
+    src[k] = LU[k];
+    lsz[k] = m[k] * m[k] * el;
+    src[d + k] = reinterpret_cast<const double*>(piv[k]);
+    lsz[d + k] = m[k];
+  }
+  const double* dT;
+  std::vector<const double*> dL;
+  const size_t numel = size_t(prod(m, 0, d)) * el;
+  MM_TRY(upload(h, T, numel, 2 * d, src.data(), lsz.data(), &dT, dL));
+  std::vector<const int64_t*> dpiv(d);
+  for (int k = 0; k < d; ++k) dpiv[k] = reinterpret_cast<const int64_t*>(dL[d + k]);
+  MM_TRY(h->host_out.ensure(numel * sizeof(double)));
+  MM_TRY(itucker_dev(h, d, m, dT, dL.data(), dpiv.data(), static_cast<double*>(h->host_out.p), cplx));
+  return download(h, S, numel);
+}
+
+int mumode_host_itucker_f64(mumode_handle_t h, int d, const int64_t* m, const double* T, const double* const* LU,
+                            const int64_t* const* piv, double* S) {
+  return host_itucker_impl(h, d, m, T, LU, piv, S, false);
+}
+int mumode_host_itucker_c128(mumode_handle_t h, int d, const int64_t* m, const double* T, const double* const* LU,
+                             const int64_t* const* piv, double* S) {
+  return host_itucker_impl(h, d, m, T, LU, piv, S, true);
+}
+
 int mumode_host_expint_f64(mumode_handle_t h, int d, const int64_t* m, const double* const* E,
                            const double* u0, double* u_out, int steps) {
   if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
   MM_TRY(check_stack(d, m, m, u0, E, u_out, "expint"));
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   std::vector<int64_t> lsz(d);
   for (int k = 0; k < d; ++k) lsz[k] = m[k] * m[k];
   const double* du;

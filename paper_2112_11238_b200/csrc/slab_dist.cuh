@@ -547,7 +547,7 @@ int mumode_comm_create(mumode_comm_t* out, int device, const void* id, int nrank
     return fail(MUMODE_ERR_ARGUMENT, "comm_create: bad rank / size");
   auto& api = nccl_api();
   if (!api.ok) return fail(MUMODE_ERR_NCCL, api.why);
-  MM_CUDA(cudaSetDevice(device));
+  MM_DEVICE(device);
   ncclUniqueId uid;
   std::memcpy(&uid, id, sizeof(uid));
   auto* c = new mumode_comm_s();
@@ -570,7 +570,7 @@ int mumode_comm_wrap(mumode_comm_t* out, int device, void* nccl_comm, int nranks
   if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
     return fail(MUMODE_ERR_ARGUMENT, "comm_wrap: bad rank / size");
   if (nranks > 1 && !nccl_api().ok) return fail(MUMODE_ERR_NCCL, nccl_api().why);
-  MM_CUDA(cudaSetDevice(device));
+  MM_DEVICE(device);
   auto* c = new mumode_comm_s();
   c->comm = static_cast<ncclComm_t>(nccl_comm);
   c->nranks = nranks;
@@ -582,7 +582,7 @@ int mumode_comm_wrap(mumode_comm_t* out, int device, void* nccl_comm, int nranks
 
 int mumode_comm_destroy(mumode_comm_t c) {
   if (!c) return MUMODE_OK;
-  cudaSetDevice(c->device);
+  mumode_gpu::DeviceGuard guard(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto e : c->events) cudaEventDestroy(e);
   for (int b = 0; b < 2; ++b)
@@ -667,7 +667,7 @@ int mumode_dist_expint_f64(mumode_handle_t h, mumode_comm_t c, int d, const int6
   using namespace mumode_gpu;
   if (!h || !c) return fail(MUMODE_ERR_ARGUMENT, "dist_expint: null handle / comm");
   if (!m) return fail(MUMODE_ERR_ARGUMENT, "dist_expint: null extents");
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   return dist_expint(h, c, d, m, E, u0, u, steps);
 }
 
@@ -676,7 +676,7 @@ int mumode_dist_tucker_f64(mumode_handle_t h, mumode_comm_t c, int d, const int6
   using namespace mumode_gpu;
   if (!h || !c) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: null handle / comm");
   if (!m || !n) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: null extents");
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   return dist_tucker(h, c, d, m, n, T, L, S, chunks, false);
 }
 
@@ -685,7 +685,7 @@ int mumode_dist_tucker_c128(mumode_handle_t h, mumode_comm_t c, int d, const int
   using namespace mumode_gpu;
   if (!h || !c) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: null handle / comm");
   if (!m || !n) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: null extents");
-  MM_CUDA(cudaSetDevice(h->device));
+  MM_DEVICE(h->device);
   return dist_tucker(h, c, d, m, n, T, L, S, chunks, true);
 }
 

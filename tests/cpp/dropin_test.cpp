@@ -187,9 +187,21 @@ int main() {
     double diff = 0;
     for (index_t k = 0; k < T.numel(); ++k) diff = std::max(diff, std::abs(S[k] - T[k] / 8.0));
     CHECK(diff < 1e-15);
+    // complex stack (FactorizedStack<cplx>, tucker.hpp:36)
+    auto Tc = rand_tensor<cplx>(g, Shape({4, 3, 2}));
+    ops::MatrixStack<cplx> twoIc;
+    for (index_t e : {4, 3, 2}) {
+      Matrix<cplx> P = Matrix<cplx>::identity(e);
+      for (index_t i = 0; i < e; ++i) P(i, i) = cplx(0.0, 2.0);
+      twoIc.push_back(P);
+    }
+    auto Sc = ops::itucker(Tc, ops::FactorizedStack<cplx>(twoIc));
+    double cdiff = 0;
+    for (index_t k = 0; k < Tc.numel(); ++k) cdiff = std::max(cdiff, std::abs(Sc[k] - Tc[k] / cplx(0.0, -8.0)));
+    CHECK(cdiff < 1e-15);
     bool num = false;
     try {
-      ops::FactorizedStack({Matrix<double>(2, 2)});
+      ops::FactorizedStack<double>({Matrix<double>(2, 2)});
     } catch (const NumericalError&) {
       num = true;
     }

@@ -156,10 +156,76 @@ def test_expm_matches_reference_expm():
 
 def test_factorized_stack_refuses_singular_matrices():
     # test_tucker_ops.cpp:285-288 (host factorization, no GPU needed)
-    with pytest.raises(mm.NumericalError):
+    with pytest.raises(mm.NumericalError, match="singular pivot"):
         mm.FactorizedStack([np.zeros((2, 2))])
-    F = mm.FactorizedStack([np.array([[4.0, 1.0], [2.0, 3.0]])])
-    np.testing.assert_allclose(F.inverses[0] @ np.array([[4.0, 1.0], [2.0, 3.0]]), np.eye(2), atol=1e-15)
+    with pytest.raises(mm.SizeError, match="square"):
+        mm.FactorizedStack([np.zeros((2, 3))])
+    P = np.array([[4.0, 1.0], [2.0, 3.0]])
+    F = mm.FactorizedStack([P])
+    lu, piv = F.factor(1)
+    L = np.tril(lu, -1) + np.eye(2)
+    U = np.triu(lu)
+    np.testing.assert_allclose(L @ U, P[[0, 1]], atol=1e-15)
+    assert list(piv) == [0, 1]
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference library not built")
+def test_lu_factor_bitwise_equals_reference():
+    # FactorizedStack<T> holds la::lu_factor's factors (lu.hpp:23-47) bit for bit,
+    # real and complex, including pivoting on ill-conditioned matrices
+    rng = np.random.default_rng(3)
+    for n in [1, 2, 3, 8, 24, 40, 97, 200]:
+        for cplx in (False, True):
+            P = rng.standard_normal((n, n))
+            if cplx:
+                P = P + 1j * rng.standard_normal((n, n))
+            U, _, Vt = np.linalg.svd(P)
+            P = np.asfortranarray((U * np.logspace(0, -9, n)) @ Vt)
+            lu, piv = O.ref_lu_factor(P)
+            F = mm.FactorizedStack([P])
+            np.testing.assert_array_equal(F.lu[0], lu)
+            np.testing.assert_array_equal(F.piv[0], piv)
+            assert F.cplx == cplx
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference library not built")
+def test_symtridiag_eig_bitwise_equals_reference():
+    # la::symtridiag_eig with FullVectors (src/tridiag.cpp:12-90): the direct
+    # solver's eigenpairs are the reference's, bit for bit
+    rng = np.random.default_rng(4)
+    for n in [1, 2, 3, 10, 64, 200, 257]:
+        d, e = rng.standard_normal(n), rng.standard_normal(n - 1)
+        w, V = mm.symtridiag_eig(d, e)
+        wr, Vr = O.ref_symtridiag_eig(d, e)
+        np.testing.assert_array_equal(w, wr)
+        np.testing.assert_array_equal(V, Vr)
+    # the IMEX factor M = I/d - tau A of the Dirichlet Laplacian (imex.cpp:108-112)
+    A = O.ref_laplacian(200)
+    M = np.eye(200) / 3 + (-1e-3) * A
+    w, V = mm.symtridiag_eig(*mm.extract_tridiag(M))
+    wr, Vr = O.ref_symtridiag_eig(np.diag(M).copy(), 0.5 * (np.diag(M, 1) + np.diag(M, -1)))
+    np.testing.assert_array_equal(w, wr)
+    np.testing.assert_array_equal(V, Vr)
+
+
+def test_extract_tridiag_rejects_like_reference():
+    # src/imex.cpp:28-48: entries off the three diagonals, or an asymmetric
+    # off-diagonal pair beyond 1e-12 of the largest entry, are ArgumentErrors
+    A = np.eye(5)
+    A[0, 3] = 1e-300
+    with pytest.raises(mm.ArgumentError, match="not tridiagonal"):
+        mm.extract_tridiag(A)
+    A = np.diag(np.ones(4)) + np.diag(np.ones(3), 1)
+    with pytest.raises(mm.ArgumentError, match="not symmetric"):
+        mm.extract_tridiag(A)
+    with pytest.raises(mm.ArgumentError, match="not symmetric"):
+        mm.KronSumSolver(Ms=[A, A])
+    B = np.diag(np.full(4, 2.0)) + np.diag(np.full(3, 1.0), 1) + np.diag(np.full(3, 1.0 + 1e-14), -1)
+    d, e = mm.extract_tridiag(B)  # within the 1e-12 relative tolerance: averaged
+    np.testing.assert_array_equal(d, np.full(4, 2.0))
+    np.testing.assert_array_equal(e, np.full(3, 0.5 * (1.0 + (1.0 + 1e-14))))
+    with pytest.raises(mm.ArgumentError, match="fewer than diag"):
+        mm.symtridiag_eig(np.ones(3), np.ones(3))
 
 
 def test_empty_tensors_rejected_like_reference():

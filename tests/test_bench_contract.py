@@ -6,6 +6,7 @@ import subprocess
 import sys
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 import oracle as O
@@ -30,6 +31,27 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["unit"] == d["unit"]
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_reference_arm_loads_only_the_reference():
+    # the reference arm runs the reference library alone: this package is
+    # neither imported nor loaded, and the inputs drawn inside the reference
+    # library equal the reference generator's C2 draws (checksum of the result)
+    code = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '1']; "
+            "runpy.run_path('bench.py', run_name='__main__'); "
+            "maps = open('/proc/self/maps').read(); "
+            "print('LOADED', 'libmumode_b200' in maps, any(k.startswith('paper_2112_11238_b200') for k in sys.modules))")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "LOADED False False" in out.stdout, out.stdout
+    d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][0])
+    import paper_2112_11238_b200 as mm
+    g = mm.Rng(1234)
+    T = g.normal((256, 256, 256))
+    Ls = [g.normal((256, 256)) for _ in range(3)]
+    S = O.ref_tucker(T, Ls)
+    assert float(np.cumsum(S.ravel(order="F"))[-1]) == d["result_checksum"]  # sequential sum, as in C++
 
 
 @pytest.mark.gpu

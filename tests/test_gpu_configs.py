@@ -185,3 +185,55 @@ def test_more_than_2_31_elements():
     rhs = R[:, 0, :]
     err = (torch.linalg.vector_norm(lhs - rhs) / torch.linalg.vector_norm(rhs)).item()
     assert err < 1e-13, err
+
+
+@needs_ref
+def test_imex_direct_solver_200cube_against_reference():
+    # §8(f) row 4: the IMEX DirectSolver (src/imex.cpp:53-86) at 200^3 with the
+    # reference's Dirichlet Laplacian (src/stencils.cpp:34-50) and tau = 1e-3:
+    # the factors M_mu = (1/d) I - tau A_mu (shifted(), imex.cpp:19-26) go
+    # through extract_tridiag + symtridiag_eig like the reference's; one and
+    # three Direct steps of apps::imex_evolve against the engine's solver.
+    A = O.ref_laplacian(200)
+    tau, d = 1e-3, 3
+    M = (-tau) * A + np.eye(200) * (1.0 / d)
+    solver = mm.KronSumSolver(Ms=[M, M, M])
+    u0 = mm.Rng(1234).normal((200, 200, 200))
+    x1 = solver.solve(dev(u0))
+    err1 = O.rel_fro(host(x1), O.ref_imex_direct(u0, [A, A, A], tau, 1))
+    x3 = solver.solve(solver.solve(x1))
+    err3 = O.rel_fro(host(x3), O.ref_imex_direct(u0, [A, A, A], tau, 3))
+    assert err1 < TOL and err3 < TOL, (err1, err3)
+
+
+@needs_ref
+def test_expint_graph_survives_workspace_growth():
+    # A captured integrator graph holds workspace pointers; a larger call on
+    # the same handle in between reallocates the workspaces, and the next
+    # replay must not run on freed memory (it is re-captured).
+    g = mm.Rng(99)
+    u0 = g.normal((64, 48, 40))
+    E = [g.normal((e, e)) * 0.1 for e in u0.shape]
+    ref = u0
+    for _ in range(4):
+        ref = O.ref_tucker(ref, E)
+    Ed = [dev(x) for x in E]
+    first = host(mm.expint(dev(u0), Ed, 4))
+    big = dev(g.normal((160, 160, 160)))
+    mm.tucker(big, [dev(np.eye(160))] * 3)  # grows ws[0..1] on the same handle
+    mm.KronSumSolver(Qs=[np.eye(160)] * 3, evals=[np.ones(160)] * 3).solve(big)  # grows ws[2]
+    torch.cuda.synchronize()
+    again = host(mm.expint(dev(u0), Ed, 4))
+    np.testing.assert_array_equal(first, again)
+    assert O.rel_fro(again, ref) < TOL
+
+
+@needs_ref
+def test_host_pipeline_odd_last_extent_row_blocks():
+    # the host pipeline's last mode runs in row blocks of L_d; an odd n_d
+    # re-lays only the block's rows (no read past the factor's end)
+    g = mm.Rng(5)
+    T = g.normal((256, 256, 255))
+    Ls = [g.normal((256, 256)), g.normal((256, 256)), g.normal((255, 255))]
+    S = mm.tucker(T, Ls)
+    assert O.rel_fro(S, O.ref_tucker(T, Ls)) < TOL
