@@ -430,8 +430,9 @@ Tensor<T> tucker_sequential(const Tensor<T>& t, const MatrixStack<T>& Ls) {
   for (index_t mu = 2; mu <= t.order(); ++mu) cur = core::mode_product(cur, Ls[static_cast<std::size_t>(mu - 1)], mu);
   return cur;
 }
-/// Kronecker-sum action sum_mu V x_mu A_mu (tucker.hpp:206-232), real.
-inline Tensor<double> kronsumv(const Tensor<double>& v, const MatrixStack<double>& As) {
+/// Kronecker-sum action sum_mu V x_mu A_mu (tucker.hpp:206-232), T = double or cplx.
+template <class T>
+Tensor<T> kronsumv(const Tensor<T>& v, const MatrixStack<T>& As) {
   const index_t d = v.order();
   if (static_cast<index_t>(As.size()) != d)
     throw core::SizeError("kronsumv: stack length does not match tensor order");
@@ -442,11 +443,15 @@ inline Tensor<double> kronsumv(const Tensor<double>& v, const MatrixStack<double
       throw core::SizeError("kronsumv: matrix for mode " + std::to_string(mu) + " is not square");
     if (A.cols() != v.extent(mu))
       throw core::SizeError("kronsumv: matrix size does not match extent of mode " + std::to_string(mu));
-    ptrs.push_back(A.data());
+    ptrs.push_back(engine::raw(A.data()));
   }
-  Tensor<double> W{v.shape()};
-  engine::check(mumode_host_kronsumv_f64(engine::handle(), static_cast<int>(d), v.shape().extents().data(),
-                                         v.data(), ptrs.data(), W.data()));
+  Tensor<T> W{v.shape()};
+  if constexpr (std::is_same_v<T, double>)
+    engine::check(mumode_host_kronsumv_f64(engine::handle(), static_cast<int>(d), v.shape().extents().data(),
+                                           v.data(), ptrs.data(), W.data()));
+  else
+    engine::check(mumode_host_kronsumv_c128(engine::handle(), static_cast<int>(d), v.shape().extents().data(),
+                                            engine::raw(v.data()), ptrs.data(), engine::raw(W.data())));
   return W;
 }
 

@@ -153,6 +153,24 @@ int mumode_comm_set_exchange(mumode_comm_t c, int mode);
 /* SMs the persistent compute kernels leave free while sub-slabs overlap the
  * NCCL exchange (default 16; NCCL's kernels need SMs to run beside them). */
 int mumode_comm_set_overlap_sms(mumode_comm_t c, int sms);
+/* A communicator WITHOUT NCCL for the peer-store exchange (mode 1 only):
+ * the caller moves the CUDA-IPC handles between ranks itself --
+ * mumode_comm_ipc_export writes this rank's handles for a shape
+ * (mumode_comm_ipc_handle_bytes() bytes: Z[0], Z[1], flags), the caller
+ * all-gathers them (any transport) and passes the P x that many bytes, in rank
+ * order, to mumode_comm_ipc_import. Used to exercise the IPC mappings and the
+ * epoch handshake across processes. */
+int mumode_comm_create_local(mumode_comm_t* c, int device, int nranks, int rank);
+int mumode_comm_ipc_handle_bytes(void);
+int mumode_comm_ipc_export(mumode_comm_t c, int d, const int64_t* m, const int64_t* n, int cplx, void* handles);
+int mumode_comm_ipc_import(mumode_comm_t c, int d, const int64_t* m, const int64_t* n, int cplx,
+                           const void* all_handles);
+/* Wait for the handle's and the comm's queued work with failure detection:
+ * polls both streams and ncclCommGetAsyncError every 50 us; an NCCL error or
+ * timeout_ms without completion (<= 0: no limit) aborts an owned
+ * communicator (ncclCommAbort) and returns MUMODE_ERR_NCCL instead of
+ * hanging on a lost peer. */
+int mumode_comm_poll(mumode_handle_t h, mumode_comm_t c, int64_t timeout_ms);
 /* The partition (host only): c_off[P+1] = last-mode slab offsets (rank r
  * holds T[..., c_off[r]:c_off[r+1]]), a_off[P+1] = output row blocks over
  * A = n_1...n_{d-1} (rank r returns rows a_off[r]:a_off[r+1] of the result
@@ -162,7 +180,9 @@ int mumode_slab_plan(int nranks, int d, const int64_t* m, const int64_t* n, int6
 /* The schedule mumode_dist_tucker_* executes on rank `rank` (host only):
  * chunk_tab rows (col0, width, send_offset) per sub-slab, op_tab rows
  * (chunk, kind, peer, send_offset, z_offset, count) with kind 0 = NCCL send,
- * 1 = NCCL receive, 2 = own block device copy; offsets/counts in doubles.
+ * 1 = NCCL receive, 2 = own block (written in place by the last local
+ * mode's scatter epilogue, like the packed send blocks -- no pack pass);
+ * offsets/counts in doubles.
  * Lets the multi-rank logic be checked without GPUs. Tables too small ->
  * MUMODE_ERR_ARGUMENT with the needed sizes in n_chunks / n_ops. */
 int mumode_dist_plan(int nranks, int rank, int d, const int64_t* m, const int64_t* n, int chunks,
@@ -181,6 +201,17 @@ int mumode_dist_tucker_f64(mumode_handle_t h, mumode_comm_t c, int d, const int6
 int mumode_dist_tucker_c128(mumode_handle_t h, mumode_comm_t c, int d, const int64_t* m,
                             const int64_t* n, const double* T, const double* const* L, double* S,
                             int chunks);
+/* The peer-store application in phases (exchange mode 1, one sub-slab):
+ * phase 0 = the whole application; 1 = local modes + peer stores + signal;
+ * 2 = wait for every rank's signal of this epoch + mode d. Running phase 2
+ * only after all ranks finished phase 1 (a host barrier) means no kernel ever
+ * waits on another process. */
+int mumode_dist_tucker_phase_f64(mumode_handle_t h, mumode_comm_t c, int d, const int64_t* m,
+                                 const int64_t* n, const double* T, const double* const* L, double* S,
+                                 int phase);
+int mumode_dist_tucker_phase_c128(mumode_handle_t h, mumode_comm_t c, int d, const int64_t* m,
+                                  const int64_t* n, const double* T, const double* const* L, double* S,
+                                  int phase);
 /* Return exchange after an application with output extents n (host only):
  * rank r's output rows (A_r x n_d) -> the last-mode slabs of the output for
  * the next application. op_tab rows as in mumode_dist_plan (send_offset into
@@ -195,9 +226,12 @@ int mumode_dist_expint_f64(mumode_handle_t h, mumode_comm_t c, int d, const int6
                            const double* const* E, const double* u0, double* u, int steps);
 
 /* Replaces ops::kronsumv (tucker.hpp:209-232): W = sum_mu V x_mu A_mu with
- * square A_mu of size m[mu]. */
+ * square A_mu of size m[mu], accumulated in the reference's order
+ * (((t_1 + t_2) + t_3) + ...). */
 int mumode_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double* V,
                         const double* const* A, double* W);
+int mumode_kronsumv_c128(mumode_handle_t h, int d, const int64_t* m, const double* V,
+                         const double* const* A, double* W);
 
 /* Direct solve with the Kronecker sum of d symmetric factors
  * M_mu = Q_mu diag(evals_mu) Q_mu^T: x = tucker(tucker(b, Q^T) ./ Lambda, Q),
@@ -239,6 +273,8 @@ int mumode_host_tucker_promote(mumode_handle_t h, int d, const int64_t* m, const
                                const double* T, const double* const* L, double* S, int adjoint);
 int mumode_host_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double* V,
                              const double* const* A, double* W);
+int mumode_host_kronsumv_c128(mumode_handle_t h, int d, const int64_t* m, const double* V,
+                              const double* const* A, double* W);
 int mumode_host_expint_f64(mumode_handle_t h, int d, const int64_t* m, const double* const* E,
                            const double* u0, double* u_out, int steps);
 

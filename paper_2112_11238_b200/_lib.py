@@ -47,6 +47,13 @@ SIGNATURES = {
     "mumode_comm_destroy": (ctypes.c_int, [VP]),
     "mumode_comm_set_exchange": (ctypes.c_int, [VP, ctypes.c_int]),
     "mumode_comm_set_overlap_sms": (ctypes.c_int, [VP, ctypes.c_int]),
+    "mumode_comm_create_local": (ctypes.c_int, [ctypes.POINTER(VP), ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "mumode_comm_ipc_handle_bytes": (ctypes.c_int, []),
+    "mumode_comm_ipc_export": (ctypes.c_int, [VP, ctypes.c_int, I64P, I64P, ctypes.c_int, VP]),
+    "mumode_comm_ipc_import": (ctypes.c_int, [VP, ctypes.c_int, I64P, I64P, ctypes.c_int, VP]),
+    "mumode_comm_poll": (ctypes.c_int, [H, VP, I64]),
+    "mumode_dist_tucker_phase_f64": (ctypes.c_int, [H, VP, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
+    "mumode_dist_tucker_phase_c128": (ctypes.c_int, [H, VP, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
     "mumode_slab_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, I64P, I64P, I64P, I64P]),
     "mumode_dist_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, I64P, I64P, ctypes.c_int, ctypes.c_int,
                                         I64P, ctypes.c_int, ctypes.POINTER(ctypes.c_int), I64P, ctypes.c_int,
@@ -57,6 +64,7 @@ SIGNATURES = {
     "mumode_dist_tucker_f64": (ctypes.c_int, [H, VP, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
     "mumode_dist_tucker_c128": (ctypes.c_int, [H, VP, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
     "mumode_kronsumv_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, VP, ctypes.POINTER(VP), VP]),
+    "mumode_kronsumv_c128": (ctypes.c_int, [H, ctypes.c_int, I64P, VP, ctypes.POINTER(VP), VP]),
     "mumode_expint_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, ctypes.POINTER(VP), VP, VP, ctypes.c_int]),
     "mumode_kronsum_solve_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, ctypes.POINTER(VP), ctypes.POINTER(VP), ctypes.POINTER(VP), VP, VP]),
     "mumode_host_mode_product_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, ctypes.c_int, I64, VP, VP, VP]),
@@ -67,6 +75,7 @@ SIGNATURES = {
     "mumode_host_tucker_c128": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
     "mumode_host_tucker_promote": (ctypes.c_int, [H, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
     "mumode_host_kronsumv_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, VP, ctypes.POINTER(VP), VP]),
+    "mumode_host_kronsumv_c128": (ctypes.c_int, [H, ctypes.c_int, I64P, VP, ctypes.POINTER(VP), VP]),
     "mumode_host_expint_f64": (ctypes.c_int, [H, ctypes.c_int, I64P, ctypes.POINTER(VP), VP, VP, ctypes.c_int]),
     "mumode_probe_fp64_peak": (ctypes.c_int, [H, ctypes.POINTER(ctypes.c_double)]),
     "mumode_expm_f64": (ctypes.c_int, [I64, VP, VP]),

@@ -328,7 +328,8 @@ def tucker_sequential(T, Ls):
 
 
 def kronsumv(V, As):
-    """W = sum_mu V x_mu A_mu (ops::kronsumv, tucker.hpp:209-232)."""
+    """W = sum_mu V x_mu A_mu (ops::kronsumv, tucker.hpp:209-232), real or
+    complex (mixed operands promote to complex)."""
     _validate_tensor(V)
     d = V.ndim
     As = list(As)
@@ -341,25 +342,25 @@ def kronsumv(V, As):
             raise SizeError(f"kronsumv: matrix for mode {mu} is not square")
         if int(A.shape[1]) != int(V.shape[mu - 1]):
             raise SizeError(f"kronsumv: matrix size does not match extent of mode {mu}")
-    if _is_cplx(V) or any(_is_cplx(A) for A in As):
-        raise ArgumentError("kronsumv: complex operands are not supported by this engine yet")
+    cplx = _is_cplx(V) or any(_is_cplx(A) for A in As)
     m = _extents(V)
     lib = _lib.lib()
     if _is_torch(V):
         h = get_handle(V.device.index)
         h.bind_torch_stream()
-        Vd = to_colmajor(V)
-        Ads = [_dev_matrix(A, False, V.device) for A in As]
-        W = colmajor_empty(m, torch.float64, V.device)
-        _check(lib.mumode_kronsumv_f64(h.h, d, _lib.i64_array(m), _dev_ptr(Vd),
-                                       _lib.ptr_array([_dev_ptr(A) for A in Ads]), _dev_ptr(W)))
+        Vd = to_colmajor(V.to(torch.complex128) if cplx and not V.is_complex() else V)
+        Ads = [_dev_matrix(A, cplx, V.device) for A in As]
+        W = colmajor_empty(m, Vd.dtype, V.device)
+        fn = lib.mumode_kronsumv_c128 if cplx else lib.mumode_kronsumv_f64
+        _check(fn(h.h, d, _lib.i64_array(m), _dev_ptr(Vd), _lib.ptr_array([_dev_ptr(A) for A in Ads]), _dev_ptr(W)))
         return W
     h = get_handle()
-    Vn = _np_f(V, False)
-    Ans = [_np_f(A, False) for A in As]
-    W = np.empty(m, order="F")
-    _check(lib.mumode_host_kronsumv_f64(h.h, d, _lib.i64_array(m), Vn.ctypes.data,
-                                        _lib.ptr_array([A.ctypes.data for A in Ans]), W.ctypes.data))
+    Vn = _np_f(V, cplx)
+    Ans = [_np_f(A, cplx) for A in As]
+    W = np.empty(m, dtype=Vn.dtype, order="F")
+    fn = lib.mumode_host_kronsumv_c128 if cplx else lib.mumode_host_kronsumv_f64
+    _check(fn(h.h, d, _lib.i64_array(m), Vn.ctypes.data, _lib.ptr_array([A.ctypes.data for A in Ans]),
+              W.ctypes.data))
     return W
 
 

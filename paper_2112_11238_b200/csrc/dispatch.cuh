@@ -229,13 +229,9 @@ static int launch_tma(mumode_handle_s* h, const ModeJob& j) {
     MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
     MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, *mq, p));
   } else if (j.accumulate) {
-    if constexpr (Cfg::E == 1) {
-      auto k = modeprod_tma_kernel<Cfg, false, 1>;
-      MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
-      MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, *mq, p));
-    } else {
-      return fail(MUMODE_ERR_ARGUMENT, "accumulating complex mode product is not compiled");
-    }
+    auto k = modeprod_tma_kernel<Cfg, false, 1>;
+    MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
+    MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mp, *mq, p));
   } else {
     auto k = modeprod_tma_kernel<Cfg, false>;
     MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
@@ -508,7 +504,7 @@ static int run_job(mumode_handle_s* h, const ModeJob& j0) {
   }
   if (skinny_ok(h, j)) return launch_skinny(h, j);
   // accumulating products: real mu > 1 have a TMA instantiation; others generic
-  const bool can_tma = tma_ok(j) && !(j.accumulate && (j.A == 1 || j.cplx));
+  const bool can_tma = tma_ok(j) && !(j.accumulate && j.A == 1);
   if (h->policy == 8 && !j.cplx) return launch_ldg(h, j);
   if (h->policy == 1) return launch_generic(h, j);
   if (!can_tma) return (!j.cplx && ldg_worthwhile(j)) ? launch_ldg(h, j) : launch_generic(h, j);

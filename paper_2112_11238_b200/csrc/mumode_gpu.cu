@@ -685,19 +685,29 @@ int mumode_tucker_promote(mumode_handle_t h, int d, const int64_t* m, const int6
   return tucker_dev(h, d, m, n, z, L, S, adjoint != 0, true);
 }
 
-int mumode_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double* V,
-                        const double* const* A, double* W) {
+static int kronsumv_entry(mumode_handle_t h, int d, const int64_t* m, const double* V, const double* const* A,
+                          double* W, bool cplx) {
   if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
   MM_TRY(check_stack(d, m, m, V, A, W, "kronsumv"));
-  MM_TRY(check_no_alias(V, prod(m, 0, d), W, prod(m, 0, d), "kronsumv"));
+  const int el = cplx ? 2 : 1;
+  MM_TRY(check_no_alias(V, prod(m, 0, d) * el, W, prod(m, 0, d) * el, "kronsumv"));
   MM_DEVICE(h->device);
   // W = V x_1 A_1, then W += V x_mu A_mu for mu = 2..d in the products'
   // epilogues (the reference's acc += term order, tucker.hpp:222-231): no
   // term buffer and no separate accumulation pass over W.
-  MM_TRY(mode_product_dev(h, d, m, 1, m[0], V, A[0], 1, m[0], false, false, W));
+  MM_TRY(mode_product_dev(h, d, m, 1, m[0], V, A[0], 1, m[0], cplx, false, W));
   for (int mu = 2; mu <= d; ++mu)
-    MM_TRY(mode_product_dev(h, d, m, mu, m[mu - 1], V, A[mu - 1], 1, m[mu - 1], false, false, W, true));
+    MM_TRY(mode_product_dev(h, d, m, mu, m[mu - 1], V, A[mu - 1], 1, m[mu - 1], cplx, false, W, true));
   return MUMODE_OK;
+}
+
+int mumode_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double* V, const double* const* A,
+                        double* W) {
+  return kronsumv_entry(h, d, m, V, A, W, false);
+}
+int mumode_kronsumv_c128(mumode_handle_t h, int d, const int64_t* m, const double* V, const double* const* A,
+                         double* W) {
+  return kronsumv_entry(h, d, m, V, A, W, true);
 }
 
 // ops::itucker (tucker.hpp:187-204): per mode, every mu-fibre solved with the
@@ -1064,20 +1074,30 @@ int mumode_host_mode_product_c128(mumode_handle_t h, int d, const int64_t* m, in
   return host_mode_product_impl(h, d, m, mu, n_mu, T, L, S, 2);
 }
 
-int mumode_host_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double* V,
-                             const double* const* A, double* W) {
+static int host_kronsumv_impl(mumode_handle_t h, int d, const int64_t* m, const double* V, const double* const* A,
+                              double* W, bool cplx) {
   if (!h) return fail(MUMODE_ERR_ARGUMENT, "null handle");
   MM_TRY(check_stack(d, m, m, V, A, W, "kronsumv"));
   MM_DEVICE(h->device);
+  const int el = cplx ? 2 : 1;
   std::vector<int64_t> lsz(d);
-  for (int k = 0; k < d; ++k) lsz[k] = m[k] * m[k];
+  for (int k = 0; k < d; ++k) lsz[k] = m[k] * m[k] * el;
   const double* dV;
   std::vector<const double*> dA;
-  const size_t el = size_t(prod(m, 0, d));
-  MM_TRY(upload(h, V, el, d, A, lsz.data(), &dV, dA));
-  MM_TRY(h->host_out.ensure(el * sizeof(double)));
-  MM_TRY(mumode_kronsumv_f64(h, d, m, dV, dA.data(), static_cast<double*>(h->host_out.p)));
-  return download(h, W, el);
+  const size_t numel = size_t(prod(m, 0, d)) * el;
+  MM_TRY(upload(h, V, numel, d, A, lsz.data(), &dV, dA));
+  MM_TRY(h->host_out.ensure(numel * sizeof(double)));
+  MM_TRY(kronsumv_entry(h, d, m, dV, dA.data(), static_cast<double*>(h->host_out.p), cplx));
+  return download(h, W, numel);
+}
+
+int mumode_host_kronsumv_f64(mumode_handle_t h, int d, const int64_t* m, const double* V, const double* const* A,
+                             double* W) {
+  return host_kronsumv_impl(h, d, m, V, A, W, false);
+}
+int mumode_host_kronsumv_c128(mumode_handle_t h, int d, const int64_t* m, const double* V, const double* const* A,
+                              double* W) {
+  return host_kronsumv_impl(h, d, m, V, A, W, true);
 }
 
 static int host_itucker_impl(mumode_handle_t h, int d, const int64_t* m, const double* T, const double* const* LU,

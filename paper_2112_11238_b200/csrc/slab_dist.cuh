@@ -19,6 +19,8 @@
 // engine has no link-time NCCL dependency. nccl.h supplies the types only.
 #pragma once
 #include <dlfcn.h>
+#include <chrono>
+#include <thread>
 #include <nccl.h>
 
 namespace mumode_gpu {
@@ -36,6 +38,9 @@ struct NcclApi {
   decltype(&ncclGetErrorString) error_string = nullptr;
   decltype(&ncclGetVersion) get_version = nullptr;
   decltype(&ncclAllGather) all_gather = nullptr;
+  // optional (failure detection): present in every NCCL >= 2.4
+  decltype(&ncclCommGetAsyncError) get_async_error = nullptr;
+  decltype(&ncclCommAbort) comm_abort = nullptr;
 };
 
 static NcclApi& nccl_api() {
@@ -64,6 +69,8 @@ static NcclApi& nccl_api() {
     sym(a.get_version, "ncclGetVersion");
     sym(a.all_gather, "ncclAllGather");
     a.ok = all;
+    a.get_async_error = reinterpret_cast<decltype(&ncclCommGetAsyncError)>(dlsym(lib, "ncclCommGetAsyncError"));
+    a.comm_abort = reinterpret_cast<decltype(&ncclCommAbort)>(dlsym(lib, "ncclCommAbort"));
     if (!all) a.why = "NCCL library lacks the point-to-point API";
     return a;
   }();
@@ -213,6 +220,7 @@ static int return_plan(int P, int r, int d, const int64_t* n, std::vector<DistOp
 struct mumode_comm_s {
   ncclComm_t comm = nullptr;
   bool owned = false;
+  bool local = false;  // no NCCL: peer-store exchange with caller-exchanged IPC handles
   int nranks = 1, rank = 0, device = 0;
   cudaStream_t stream = nullptr;          // exchange stream
   std::vector<cudaEvent_t> events;        // per-chunk "packed" + start/done
@@ -225,6 +233,7 @@ struct mumode_comm_s {
   int overlap_sms = 16;                    // SMs left to NCCL while sub-slabs overlap the exchange
   int64_t epoch = 0;
   mumode_gpu::DevBuf pz[2], flags, handles, scat;
+  mumode_gpu::DevBuf scat_tabs;            // NCCL path: per-chunk scatter tables (pack-free send buffer)
   size_t mapped_bytes = 0;                 // Z size the peer mappings were made for
   std::vector<double*> peer_z[2];          // [parity][rank] (own rank: local pointer)
   std::vector<int64_t*> peer_flags;        // [rank] flag array of that rank
@@ -277,34 +286,44 @@ __global__ void p2p_wait_kernel(const int64_t* __restrict__ flags, int P, int64_
   asm volatile("fence.sc.sys;\n" ::: "memory");
 }
 
-// (Re)map the peers' Z buffers and flag arrays: a collective -- every rank
-// calls it with the same byte size in the same dist_tucker call.
-static int p2p_map(mumode_comm_s* cm, size_t zbytes) {
-  const int P = cm->nranks, r = cm->rank;
+// Peer mappings of the double-buffered Z and the epoch flags. export: make
+// sure the local buffers hold `zbytes` and write their three CUDA-IPC handles
+// (Z[0], Z[1], flags); import: open every other rank's handles (P x 3, rank
+// order). p2p_map does both around an NCCL all-gather (a collective: every
+// rank calls it with the same size in the same dist_tucker call); a comm
+// without NCCL (mumode_comm_create_local) gets the handles from its caller.
+constexpr size_t kIpcHandleBytes = sizeof(cudaIpcMemHandle_t);
+
+static void p2p_unmap(mumode_comm_s* cm) {
+  const int r = cm->rank;
   for (int b = 0; b < 2; ++b)
     for (int q = 0; q < static_cast<int>(cm->peer_z[b].size()); ++q)
       if (q != r && cm->peer_z[b][q]) cudaIpcCloseMemHandle(cm->peer_z[b][q]);
   for (int q = 0; q < static_cast<int>(cm->peer_flags.size()); ++q)
     if (q != r && cm->peer_flags[q]) cudaIpcCloseMemHandle(cm->peer_flags[q]);
+  for (int b = 0; b < 2; ++b) cm->peer_z[b].clear();
+  cm->peer_flags.clear();
+  cm->mapped_bytes = 0;
+}
+
+static int p2p_export(mumode_comm_s* cm, size_t zbytes, void* out3) {
+  p2p_unmap(cm);
   MM_TRY(cm->pz[0].ensure(zbytes));
   MM_TRY(cm->pz[1].ensure(zbytes));
   if (!cm->flags.p) {
     MM_TRY(cm->flags.ensure(sizeof(int64_t) * kMaxRanks));
     MM_CUDA(cudaMemset(cm->flags.p, 0, sizeof(int64_t) * kMaxRanks));
   }
-  constexpr size_t HB = sizeof(cudaIpcMemHandle_t);
-  std::vector<cudaIpcMemHandle_t> mine(3);
-  MM_CUDA(cudaIpcGetMemHandle(&mine[0], cm->pz[0].p));
-  MM_CUDA(cudaIpcGetMemHandle(&mine[1], cm->pz[1].p));
-  MM_CUDA(cudaIpcGetMemHandle(&mine[2], cm->flags.p));
-  MM_TRY(cm->handles.ensure(3 * HB * (P + 1)));
-  auto* dh = static_cast<uint8_t*>(cm->handles.p);
-  MM_CUDA(cudaMemcpy(dh, mine.data(), 3 * HB, cudaMemcpyHostToDevice));
-  auto& api = nccl_api();
-  MM_NCCL(api.all_gather(dh, dh + 3 * HB, 3 * HB, ncclUint8, cm->comm, cm->stream));
-  MM_CUDA(cudaStreamSynchronize(cm->stream));
-  std::vector<cudaIpcMemHandle_t> all(3 * P);
-  MM_CUDA(cudaMemcpy(all.data(), dh + 3 * HB, 3 * HB * P, cudaMemcpyDeviceToHost));
+  auto* h3 = static_cast<cudaIpcMemHandle_t*>(out3);
+  MM_CUDA(cudaIpcGetMemHandle(&h3[0], cm->pz[0].p));
+  MM_CUDA(cudaIpcGetMemHandle(&h3[1], cm->pz[1].p));
+  MM_CUDA(cudaIpcGetMemHandle(&h3[2], cm->flags.p));
+  return MUMODE_OK;
+}
+
+static int p2p_import(mumode_comm_s* cm, size_t zbytes, const void* all3P) {
+  const int P = cm->nranks, r = cm->rank;
+  const auto* all = static_cast<const cudaIpcMemHandle_t*>(all3P);
   for (int b = 0; b < 2; ++b) cm->peer_z[b].assign(P, nullptr);
   cm->peer_flags.assign(P, nullptr);
   for (int q = 0; q < P; ++q) {
@@ -326,42 +345,89 @@ static int p2p_map(mumode_comm_s* cm, size_t zbytes) {
   return MUMODE_OK;
 }
 
-// One application with the exchange fused into the last local mode's
-// epilogue: the TMA kernel stores every row pair straight into the owning
-// rank's Z (peer pointers), then signal / wait, then mode d on the local Z.
-static int dist_tucker_p2p(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64_t* m, const int64_t* n,
-                           const double* T, const double* const* L, double* S, const DistPlan& pl, bool cplx) {
-  const int P = cm->nranks, r = cm->rank;
-  const int el = cplx ? 2 : 1;
-  // all ranks see the same shapes, so they remap in the same call
+static int p2p_map(mumode_comm_s* cm, size_t zbytes) {
+  const int P = cm->nranks;
+  constexpr size_t HB = kIpcHandleBytes;
+  std::vector<cudaIpcMemHandle_t> mine(3);
+  MM_TRY(p2p_export(cm, zbytes, mine.data()));
+  MM_TRY(cm->handles.ensure(3 * HB * (P + 1)));
+  auto* dh = static_cast<uint8_t*>(cm->handles.p);
+  MM_CUDA(cudaMemcpy(dh, mine.data(), 3 * HB, cudaMemcpyHostToDevice));
+  auto& api = nccl_api();
+  MM_NCCL(api.all_gather(dh, dh + 3 * HB, 3 * HB, ncclUint8, cm->comm, cm->stream));
+  MM_CUDA(cudaStreamSynchronize(cm->stream));
+  std::vector<cudaIpcMemHandle_t> all(3 * P);
+  MM_CUDA(cudaMemcpy(all.data(), dh + 3 * HB, 3 * HB * P, cudaMemcpyDeviceToHost));
+  return p2p_import(cm, zbytes, all.data());
+}
+
+// Bytes of one Z buffer of the peer-store exchange for this shape (the
+// largest rank's received matrix, so every rank maps equal sizes).
+static size_t p2p_zbytes(const DistPlan& pl, int P, int el) {
   size_t want = 0;
   for (int q = 0; q < P; ++q)
     want = std::max(want, size_t((pl.a_off[q + 1] - pl.a_off[q]) * pl.m_d * el) * sizeof(double));
-  want = std::max(want, size_t(8));
-  if (P > 1 && want > cm->mapped_bytes) MM_TRY(p2p_map(cm, want));
-  if (P == 1) {
-    MM_TRY(cm->pz[0].ensure(want));
-    MM_TRY(cm->pz[1].ensure(want));
-    for (int b = 0; b < 2; ++b) cm->peer_z[b].assign(1, static_cast<double*>(cm->pz[b].p));
+  return std::max(want, size_t(8));
+}
+
+// One application with the exchange fused into the last local mode's
+// epilogue: the TMA kernel stores every row pair straight into the owning
+// rank's Z (peer pointers), then signal / wait, then mode d on the local Z.
+//
+// phase 0: the whole application. phase 1: local modes + peer stores +
+// signal, then return; phase 2: wait for every rank's signal of the current
+// epoch + mode d. A caller that runs phase 2 only after every rank finished
+// phase 1 (host barrier) never has a kernel waiting on another process --
+// the form in which the handshake can be exercised with several processes
+// on ONE GPU (tests/test_dist_ipc.py).
+static int dist_tucker_p2p(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64_t* m, const int64_t* n,
+                           const double* T, const double* const* L, double* S, const DistPlan& pl, bool cplx,
+                           int phase) {
+  const int P = cm->nranks, r = cm->rank;
+  const int el = cplx ? 2 : 1;
+  const size_t want = p2p_zbytes(pl, P, el);
+  if (phase != 2) {
+    // all ranks see the same shapes, so they remap in the same call
+    if (P > 1 && want > cm->mapped_bytes) {
+      if (!cm->comm)
+        return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: peer buffers not mapped for this shape (" +
+                                             std::to_string(want) +
+                                             " bytes): exchange handles with mumode_comm_ipc_export/import");
+      MM_TRY(p2p_map(cm, want));
+    }
+    if (P == 1) {
+      MM_TRY(cm->pz[0].ensure(want));
+      MM_TRY(cm->pz[1].ensure(want));
+      for (int b = 0; b < 2; ++b) cm->peer_z[b].assign(1, static_cast<double*>(cm->pz[b].p));
+    }
+    const int par = static_cast<int>(++cm->epoch & 1);
+    ScatterParams sp{};
+    sp.P = P;
+    sp.col0 = pl.c_off[r];
+    for (int q = 0; q <= P; ++q) sp.a_off[q] = pl.a_off[q];
+    for (int q = 0; q < P; ++q) sp.dst[q] = cm->peer_z[par][q];
+    MM_TRY(cm->scat.ensure(sizeof(ScatterParams) + sizeof(int64_t*) * kMaxRanks));
+    auto* dsp = static_cast<ScatterParams*>(cm->scat.p);
+    auto** dflags = reinterpret_cast<int64_t**>(static_cast<uint8_t*>(cm->scat.p) + sizeof(ScatterParams));
+    MM_CUDA(cudaMemcpyAsync(dsp, &sp, sizeof(sp), cudaMemcpyHostToDevice, h->stream));
+    if (P > 1)
+      MM_CUDA(cudaMemcpyAsync(dflags, cm->peer_flags.data(), sizeof(int64_t*) * P, cudaMemcpyHostToDevice,
+                              h->stream));
+    MM_TRY(tucker_dev(h, d, m, n, T, L, nullptr, false, cplx, 1, d - 1, dsp));
+    if (P > 1) {
+      p2p_signal_kernel<<<1, 64, 0, h->stream>>>(dflags, P, r, cm->epoch);
+      MM_CUDA(cudaGetLastError());
+      h->launches++;
+    }
+    if (phase == 1) return MUMODE_OK;
+  } else if (cm->epoch == 0 || (P > 1 && cm->mapped_bytes < want)) {
+    return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: phase 2 without a phase 1 for this shape");
   }
-  const int par = static_cast<int>(++cm->epoch & 1);
-  ScatterParams sp{};
-  sp.P = P;
-  sp.col0 = pl.c_off[r];
-  for (int q = 0; q <= P; ++q) sp.a_off[q] = pl.a_off[q];
-  for (int q = 0; q < P; ++q) sp.dst[q] = cm->peer_z[par][q];
-  MM_TRY(cm->scat.ensure(sizeof(ScatterParams) + sizeof(int64_t*) * kMaxRanks));
-  auto* dsp = static_cast<ScatterParams*>(cm->scat.p);
-  auto** dflags = reinterpret_cast<int64_t**>(static_cast<uint8_t*>(cm->scat.p) + sizeof(ScatterParams));
-  MM_CUDA(cudaMemcpyAsync(dsp, &sp, sizeof(sp), cudaMemcpyHostToDevice, h->stream));
-  if (P > 1)
-    MM_CUDA(cudaMemcpyAsync(dflags, cm->peer_flags.data(), sizeof(int64_t*) * P, cudaMemcpyHostToDevice, h->stream));
-  MM_TRY(tucker_dev(h, d, m, n, T, L, nullptr, false, cplx, 1, d - 1, dsp));
+  const int par = static_cast<int>(cm->epoch & 1);
   if (P > 1) {
-    p2p_signal_kernel<<<1, 64, 0, h->stream>>>(dflags, P, r, cm->epoch);
     p2p_wait_kernel<<<1, 64, 0, h->stream>>>(static_cast<const int64_t*>(cm->flags.p), P, cm->epoch);
     MM_CUDA(cudaGetLastError());
-    h->launches += 2;
+    h->launches++;
   }
   if (pl.A_r == 0) return MUMODE_OK;
   const int64_t zext[2] = {pl.A_r, pl.m_d};
@@ -369,7 +435,7 @@ static int dist_tucker_p2p(mumode_handle_s* h, mumode_comm_s* cm, int d, const i
 }
 
 static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64_t* m, const int64_t* n,
-                       const double* T, const double* const* L, double* S, int chunks, bool cplx) {
+                       const double* T, const double* const* L, double* S, int chunks, bool cplx, int phase = 0) {
   const int P = cm->nranks, r = cm->rank;
   if (cm->device != h->device) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: handle and comm on different devices");
   if (!T || !L || !S) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: null pointer");
@@ -378,29 +444,51 @@ static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64
   const int el = cplx ? 2 : 1;
   DistPlan pl;
   MM_TRY(dist_plan(P, r, d, m, n, chunks, el, pl));
-  if (cm->exchange == 1) return dist_tucker_p2p(h, cm, d, m, n, T, L, S, pl, cplx);
+  if (phase != 0 && cm->exchange != 1)
+    return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: phases apply to the peer-store exchange only");
+  if (cm->exchange == 1) return dist_tucker_p2p(h, cm, d, m, n, T, L, S, pl, cplx, phase);
   if (P == 1 && chunks <= 1) {
     // one rank: no exchange, and its output rows (A x n_d) ARE the whole
     // result: the plain chain (fused passes included). Explicit chunks > 1
     // still take the general path (exercised by the tests).
     return tucker_dev(h, d, m, n, T, L, S, false, cplx);
   }
-  const int64_t A = pl.A, A_r = pl.A_r, m_d = pl.m_d, n_d = pl.n_d;
+  const int64_t A_r = pl.A_r, m_d = pl.m_d, n_d = pl.n_d;
   const int nch = static_cast<int>(pl.ch.size());
-  MM_TRY(cm->y.ensure(size_t(std::max<int64_t>(A * pl.wmax * el, 1)) * sizeof(double)));
   MM_TRY(cm->send.ensure(size_t(std::max<int64_t>(pl.send_elems, 1)) * sizeof(double)));
   MM_TRY(cm->z.ensure(size_t(std::max<int64_t>(pl.z_elems, 1)) * sizeof(double)));
   MM_TRY(comm_events(cm, size_t(nch) + 2));
-  auto* Y = static_cast<double*>(cm->y.p);
   auto* send = static_cast<double*>(cm->send.p);
   auto* Z = static_cast<double*>(cm->z.p);
+  // No pack pass: each sub-slab's last local mode stores its rows through the
+  // scatter epilogue (EPI 2) straight into the packed send layout -- row
+  // block q of chunk j is the contiguous (A_q x w) matrix at
+  // send_off + a_off[q] * w -- and its own row block straight into its final
+  // columns of Z. One scatter table per chunk, uploaded once per call.
+  std::vector<ScatterParams> tabs(static_cast<size_t>(nch));
+  for (int j = 0; j < nch; ++j) {
+    const DistChunk& c = pl.ch[j];
+    ScatterParams& sp = tabs[static_cast<size_t>(j)];
+    sp = ScatterParams{};
+    sp.P = P;
+    sp.col0 = 0;
+    for (int q = 0; q <= P; ++q) sp.a_off[q] = pl.a_off[q];
+    for (int q = 0; q < P; ++q) {
+      const bool empty = pl.a_off[q + 1] == pl.a_off[q] || c.w == 0;
+      sp.dst[q] = empty ? nullptr
+                        : (q == r ? Z + A_r * (pl.c_off[r] + c.col0) * el
+                                  : send + c.send_off + pl.a_off[q] * c.w * el);
+    }
+  }
+  MM_TRY(cm->scat_tabs.ensure(sizeof(ScatterParams) * std::max<size_t>(tabs.size(), 1)));
+  auto* dtabs = static_cast<ScatterParams*>(cm->scat_tabs.p);
+  MM_CUDA(cudaMemcpyAsync(dtabs, tabs.data(), sizeof(ScatterParams) * tabs.size(), cudaMemcpyHostToDevice,
+                          h->stream));
 
   // Z (and send) may still be read by the previous call's work on h->stream
   MM_CUDA(cudaEventRecord(cm->events[nch], h->stream));
   MM_CUDA(cudaStreamWaitEvent(cm->stream, cm->events[nch], 0));
   std::vector<int64_t> ext(m, m + d);
-  PackOffsets off{};
-  for (int q = 0; q <= P; ++q) off.a[q] = pl.a_off[q] * el;
   size_t op = 0;
   // overlapped exchange: leave SMs to NCCL's kernels while the sub-slabs run
   struct Reserve {
@@ -413,20 +501,14 @@ static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64
     const DistChunk& c = pl.ch[j];
     if (c.w > 0) {
       ext[d - 1] = c.w;
-      MM_TRY(tucker_dev(h, d, ext.data(), n, T + pl.rows_in * c.col0 * el, L, Y, false, cplx, 1, d - 1));
-      slab_pack_kernel<false><<<pack_grid(A * el, c.w, P, h->num_sms), 256, 0, h->stream>>>(Y, send + c.send_off, A * el,
-                                                                                      c.w, P, off);
-      MM_CUDA(cudaGetLastError());
-      h->launches++;
+      MM_TRY(tucker_dev(h, d, ext.data(), n, T + pl.rows_in * c.col0 * el, L, nullptr, false, cplx, 1, d - 1,
+                        dtabs + j));
       MM_CUDA(cudaEventRecord(cm->events[j], h->stream));
       MM_CUDA(cudaStreamWaitEvent(cm->stream, cm->events[j], 0));
     }
     const size_t first = op;
     while (op < pl.ops.size() && pl.ops[op].chunk == j) ++op;
-    for (size_t k = first; k < op; ++k)
-      if (pl.ops[k].kind == 2)
-        MM_CUDA(cudaMemcpyAsync(Z + pl.ops[k].z_off, send + pl.ops[k].buf_off, size_t(pl.ops[k].count) * sizeof(double),
-                                cudaMemcpyDeviceToDevice, cm->stream));
+    // (the plan's own-block copy, kind 2, is done by the scatter epilogue)
     if (P > 1) {
       auto& api = nccl_api();
       MM_NCCL(api.group_start());
@@ -448,6 +530,51 @@ static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64
   if (A_r == 0) return MUMODE_OK;
   const int64_t zext[2] = {A_r, m_d};
   return mode_product_dev(h, 2, zext, 2, n_d, Z, L[d - 1], 1, n_d, cplx, false, S);
+}
+
+// Wait for the handle's and the comm's queued work with failure detection:
+// polls the streams and ncclCommGetAsyncError; an NCCL error, or no progress
+// within timeout_ms, aborts the communicator (ncclCommAbort) and fails with
+// MUMODE_ERR_NCCL instead of hanging on a lost peer.
+static int comm_poll(mumode_handle_s* h, mumode_comm_s* cm, int64_t timeout_ms) {
+  auto& api = nccl_api();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t a = cudaStreamQuery(h->stream);
+    const cudaError_t b = cm->stream ? cudaStreamQuery(cm->stream) : cudaSuccess;
+    if (a != cudaSuccess && a != cudaErrorNotReady) {
+      cudaGetLastError();
+      return fail(MUMODE_ERR_CUDA, std::string("CUDA error while waiting: ") + cudaGetErrorString(a));
+    }
+    if (b != cudaSuccess && b != cudaErrorNotReady) {
+      cudaGetLastError();
+      return fail(MUMODE_ERR_CUDA, std::string("CUDA error while waiting: ") + cudaGetErrorString(b));
+    }
+    if (a == cudaSuccess && b == cudaSuccess) return MUMODE_OK;
+    if (cm->comm && api.get_async_error) {
+      ncclResult_t st = ncclSuccess;
+      api.get_async_error(cm->comm, &st);
+      if (st != ncclSuccess && st != ncclInProgress) {
+        if (api.comm_abort && cm->owned) {
+          api.comm_abort(cm->comm);
+          cm->comm = nullptr;
+        }
+        return fail(MUMODE_ERR_NCCL, std::string("NCCL asynchronous error: ") + api.error_string(st));
+      }
+    }
+    const auto ms =
+        std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+    if (timeout_ms > 0 && ms > timeout_ms) {
+      if (cm->comm && api.comm_abort && cm->owned) {
+        api.comm_abort(cm->comm);
+        cm->comm = nullptr;
+      }
+      return fail(MUMODE_ERR_NCCL, "timed out after " + std::to_string(ms) +
+                                       " ms waiting for the exchange (a peer is lost or stalled); communicator "
+                                       "aborted");
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
 }
 
 // Copies and one NCCL group of a schedule on the exchange stream.
@@ -585,11 +712,7 @@ int mumode_comm_destroy(mumode_comm_t c) {
   mumode_gpu::DeviceGuard guard(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto e : c->events) cudaEventDestroy(e);
-  for (int b = 0; b < 2; ++b)
-    for (int q = 0; q < static_cast<int>(c->peer_z[b].size()); ++q)
-      if (q != c->rank && c->peer_z[b][q]) cudaIpcCloseMemHandle(c->peer_z[b][q]);
-  for (int q = 0; q < static_cast<int>(c->peer_flags.size()); ++q)
-    if (q != c->rank && c->peer_flags[q]) cudaIpcCloseMemHandle(c->peer_flags[q]);
+  mumode_gpu::p2p_unmap(c);
   if (c->ret_in) cudaEventDestroy(c->ret_in);
   if (c->ret_out) cudaEventDestroy(c->ret_out);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -610,8 +733,10 @@ int mumode_comm_set_exchange(mumode_comm_t c, int mode) {
   using namespace mumode_gpu;
   if (!c) return fail(MUMODE_ERR_ARGUMENT, "null comm");
   if (mode != 0 && mode != 1) return fail(MUMODE_ERR_ARGUMENT, "exchange: 0 = NCCL send/recv, 1 = peer stores");
-  if (mode == 1 && c->nranks > 1 && (!c->comm || !nccl_api().ok))
+  if (mode == 1 && c->nranks > 1 && !c->local && (!c->comm || !nccl_api().ok))
     return fail(MUMODE_ERR_NCCL, "peer-store exchange needs an NCCL communicator to map the peers");
+  if (mode == 0 && c->local && c->nranks > 1)
+    return fail(MUMODE_ERR_ARGUMENT, "a comm without NCCL exchanges by peer stores only");
   c->exchange = mode;
   return MUMODE_OK;
 }
@@ -689,4 +814,72 @@ int mumode_dist_tucker_c128(mumode_handle_t h, mumode_comm_t c, int d, const int
   return dist_tucker(h, c, d, m, n, T, L, S, chunks, true);
 }
 
+int mumode_comm_create_local(mumode_comm_t* out, int device, int nranks, int rank) {
+  using namespace mumode_gpu;
+  if (!out) return fail(MUMODE_ERR_ARGUMENT, "comm_create_local: null pointer");
+  *out = nullptr;
+  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
+    return fail(MUMODE_ERR_ARGUMENT, "comm_create_local: bad rank / size");
+  MM_DEVICE(device);
+  auto* c = new mumode_comm_s();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  c->local = true;
+  c->exchange = 1;
+  return comm_finish(c, out);
+}
+
+int mumode_comm_ipc_export(mumode_comm_t c, int d, const int64_t* m, const int64_t* n, int cplx, void* handles) {
+  using namespace mumode_gpu;
+  if (!c || !m || !n || !handles) return fail(MUMODE_ERR_ARGUMENT, "comm_ipc_export: null pointer");
+  MM_DEVICE(c->device);
+  DistPlan pl;
+  MM_TRY(dist_plan(c->nranks, c->rank, d, m, n, 1, cplx ? 2 : 1, pl));
+  return p2p_export(c, p2p_zbytes(pl, c->nranks, cplx ? 2 : 1), handles);
+}
+
+int mumode_comm_ipc_import(mumode_comm_t c, int d, const int64_t* m, const int64_t* n, int cplx,
+                           const void* all_handles) {
+  using namespace mumode_gpu;
+  if (!c || !m || !n || !all_handles) return fail(MUMODE_ERR_ARGUMENT, "comm_ipc_import: null pointer");
+  MM_DEVICE(c->device);
+  DistPlan pl;
+  MM_TRY(dist_plan(c->nranks, c->rank, d, m, n, 1, cplx ? 2 : 1, pl));
+  const size_t zbytes = p2p_zbytes(pl, c->nranks, cplx ? 2 : 1);
+  if (c->pz[0].bytes < zbytes || !c->flags.p)
+    return fail(MUMODE_ERR_ARGUMENT, "comm_ipc_import: export this shape first");
+  return p2p_import(c, zbytes, all_handles);
+}
+
+int mumode_comm_ipc_handle_bytes(void) { return static_cast<int>(3 * mumode_gpu::kIpcHandleBytes); }
+
+int mumode_dist_tucker_phase_f64(mumode_handle_t h, mumode_comm_t c, int d, const int64_t* m, const int64_t* n,
+                                 const double* T, const double* const* L, double* S, int phase) {
+  using namespace mumode_gpu;
+  if (!h || !c) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: null handle / comm");
+  if (!m || !n) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: null extents");
+  if (phase < 0 || phase > 2) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: phase 0, 1 or 2");
+  MM_DEVICE(h->device);
+  return dist_tucker(h, c, d, m, n, T, L, S, 1, false, phase);
+}
+
+int mumode_dist_tucker_phase_c128(mumode_handle_t h, mumode_comm_t c, int d, const int64_t* m, const int64_t* n,
+                                  const double* T, const double* const* L, double* S, int phase) {
+  using namespace mumode_gpu;
+  if (!h || !c) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: null handle / comm");
+  if (!m || !n) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: null extents");
+  if (phase < 0 || phase > 2) return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: phase 0, 1 or 2");
+  MM_DEVICE(h->device);
+  return dist_tucker(h, c, d, m, n, T, L, S, 1, true, phase);
+}
+
+int mumode_comm_poll(mumode_handle_t h, mumode_comm_t c, int64_t timeout_ms) {
+  using namespace mumode_gpu;
+  if (!h || !c) return fail(MUMODE_ERR_ARGUMENT, "comm_poll: null handle / comm");
+  MM_DEVICE(h->device);
+  return comm_poll(h, c, timeout_ms);
+}
+
 }  // extern "C"
+

@@ -277,6 +277,53 @@ class Comm:
         dev = torch.cuda.current_device() if device is None else device
         return cls(world, rank, obj[0], dev)
 
+    @classmethod
+    def local(cls, nranks: int, rank: int, device: int = 0) -> "Comm":
+        """A communicator without NCCL for the peer-store exchange: the caller
+        moves the CUDA-IPC handles between ranks (``ipc_export`` /
+        ``ipc_import``) over any transport (mumode_comm_create_local)."""
+        import ctypes
+
+        from . import _lib
+        from .api import _check
+        self = cls.__new__(cls)
+        self.nranks, self.rank, self.device = int(nranks), int(rank), int(device)
+        c = ctypes.c_void_p()
+        _check(_lib.lib().mumode_comm_create_local(ctypes.byref(c), self.device, self.nranks, self.rank))
+        self.c = c
+        return self
+
+    def ipc_export(self, m: Sequence[int], n: Sequence[int], cplx: bool = False) -> bytes:
+        """This rank's CUDA-IPC handles (Z[0], Z[1], flags) for a shape."""
+        import ctypes
+
+        from . import _lib
+        from .api import _check
+        nb = _lib.lib().mumode_comm_ipc_handle_bytes()
+        buf = ctypes.create_string_buffer(nb)
+        _check(_lib.lib().mumode_comm_ipc_export(self.c, len(m), _lib.i64_array(m), _lib.i64_array(n), int(cplx),
+                                                  buf))
+        return buf.raw
+
+    def ipc_import(self, m: Sequence[int], n: Sequence[int], handles: Sequence[bytes], cplx: bool = False) -> None:
+        """Open every rank's exported handles (rank order)."""
+        import ctypes
+
+        from . import _lib
+        from .api import _check
+        blob = b"".join(handles)
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        _check(_lib.lib().mumode_comm_ipc_import(self.c, len(m), _lib.i64_array(m), _lib.i64_array(n), int(cplx),
+                                                  buf))
+
+    def poll(self, timeout_ms: int = 60000, device: int | None = None) -> None:
+        """Wait for this rank's queued work with NCCL failure detection
+        (mumode_comm_poll): raises instead of hanging on a lost peer."""
+        from . import _lib
+        from .api import _check, get_handle
+        h = get_handle(self.device if device is None else device)
+        _check(_lib.lib().mumode_comm_poll(h.h, self.c, int(timeout_ms)))
+
     def set_exchange(self, mode: str) -> None:
         """'nccl' (grouped send/recv, default) or 'p2p' (the last local mode's
         epilogue stores rows straight into the owning ranks' memory)."""
@@ -339,12 +386,14 @@ def dist_plan(P: int, rank: int, m: Sequence[int], n: Sequence[int], chunks: int
 
 
 def dist_tucker(comm: Comm, T_local, Ls, m: Sequence[int], n: Sequence[int] | None = None, chunks: int = 4,
-                out=None):
+                out=None, phase: int | None = None):
     """One slab-partitioned Tucker application through the C-ABI
     (``mumode_dist_tucker_{f64,c128}``). ``T_local``: this rank's column-major
     last-mode slab on its GPU; ``Ls``: all d factors on the same GPU; ``m``,
     ``n``: GLOBAL extents. Returns this rank's (A_r x n_d) rows of the result as
-    a flat column-major tensor (``gather_rows`` reassembles)."""
+    a flat column-major tensor (``gather_rows`` reassembles). ``phase`` (peer
+    stores only): 1 = local modes + stores + signal, 2 = wait + last mode
+    (``mumode_dist_tucker_phase_*``)."""
     import torch
 
     from . import _lib
@@ -363,9 +412,14 @@ def dist_tucker(comm: Comm, T_local, Ls, m: Sequence[int], n: Sequence[int] | No
     S = out if out is not None else torch.empty(A_r * n[-1], dtype=dt, device=T_local.device)
     h = get_handle(T_local.device.index)
     h.bind_torch_stream()
-    fn = _lib.lib().mumode_dist_tucker_c128 if cplx else _lib.lib().mumode_dist_tucker_f64
-    _check(fn(h.h, comm.c, d, _lib.i64_array(m), _lib.i64_array(n), T_local.data_ptr(),
-              _lib.ptr_array([L.data_ptr() for L in Ls]), S.data_ptr(), int(chunks)))
+    if phase is None:
+        fn = _lib.lib().mumode_dist_tucker_c128 if cplx else _lib.lib().mumode_dist_tucker_f64
+        _check(fn(h.h, comm.c, d, _lib.i64_array(m), _lib.i64_array(n), T_local.data_ptr(),
+                  _lib.ptr_array([L.data_ptr() for L in Ls]), S.data_ptr(), int(chunks)))
+    else:
+        fn = _lib.lib().mumode_dist_tucker_phase_c128 if cplx else _lib.lib().mumode_dist_tucker_phase_f64
+        _check(fn(h.h, comm.c, d, _lib.i64_array(m), _lib.i64_array(n), T_local.data_ptr(),
+                  _lib.ptr_array([L.data_ptr() for L in Ls]), S.data_ptr(), int(phase)))
     return S
 
 

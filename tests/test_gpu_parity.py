@@ -448,6 +448,23 @@ def test_kronsumv_fused_epilogue_vs_reference(policy):
         assert O.rel_max(W, want) < 1e-14, shape
 
 
+@pytest.mark.skipif(not O.ref_available(), reason="reference library not built")
+@pytest.mark.parametrize("shape", [(64, 48, 40), (24, 24, 24, 24), (33, 17, 9), (128, 128, 128), (5, 3)])
+def test_kronsumv_complex_against_reference(shape):
+    # kronsumv<cplx> (tucker.hpp:209-232): complex terms accumulated in the
+    # TMA epilogue (or the SIMT kernel for unaligned shapes), device and host
+    rng = np.random.default_rng(len(shape) * 7 + shape[0])
+    V = rnd(rng, shape) + 1j * rnd(rng, shape)
+    As = [rnd(rng, (e, e)) + 1j * rnd(rng, (e, e)) for e in shape]
+    W = host(mm.kronsumv(dev(V), [dev(A) for A in As]))
+    want = O.ref_tucker(V, As, "kronsumv")
+    assert O.rel_fro(W, want) < 1e-13, shape
+    np.testing.assert_array_equal(mm.kronsumv(V, As), W)
+    # mixed real tensor / complex factors promote
+    Vr = rnd(rng, shape)
+    assert O.rel_fro(host(mm.kronsumv(dev(Vr), [dev(A) for A in As])), O.ref_tucker(Vr.astype(complex), As, "kronsumv")) < 1e-13
+
+
 def test_itucker_restated_reference_cases(policy):
     # test_tucker_ops.cpp:236-288
     rng = np.random.default_rng(113)
