@@ -416,26 +416,14 @@ def run_distributed(args, world, rank, local):
     Ls = [torch.from_numpy(L).to(dev) for L in L_host]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     S_out = torch.empty(plan.a_sizes[rank] * 256, dtype=torch.float64, device=dev)
-    fallback = None
     if not args.py_dist:
-        # the C-ABI path (own NCCL communicator); should it fail to come up
-        # on this box, every rank agrees to run the Python slab algorithm on
-        # torch's NCCL instead, and the line says so
-        ok = torch.tensor([1], device=dev)
-        try:
-            comm = Comm.from_torch(device=local)
-            comm.set_exchange(args.exchange)
-            comm.set_overlap_sms(args.overlap_sms)
-            dist_tucker(comm, T_r, Ls, C2, chunks=args.chunks, out=S_out)
-            torch.cuda.synchronize()
-        except Exception as ex:  # noqa: BLE001
-            print(f"bench: C-ABI slab path failed ({ex}); using the Python slab algorithm", file=sys.stderr)
-            fallback = str(ex)[:200]
-            ok.zero_()
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        if int(ok.item()) == 0:
-            args.py_dist = True
-            fallback = fallback or "another rank's C-ABI slab path failed"
+        # the C-ABI path (own NCCL communicator); if it cannot come up the run
+        # fails loudly -- the Python slab algorithm runs only when asked for
+        comm = Comm.from_torch(device=local)
+        comm.set_exchange(args.exchange)
+        comm.set_overlap_sms(args.overlap_sms)
+        dist_tucker(comm, T_r, Ls, C2, chunks=args.chunks, out=S_out)
+        comm.poll(timeout_ms=120000)
     if args.py_dist:
         be = CudaSlabBackend(local)
         if args.overlap:
@@ -466,6 +454,8 @@ def run_distributed(args, world, rank, local):
         e0.record(stream)
         run_slab(T_r)
         e1.record(stream)
+    if not args.py_dist:
+        comm.poll(timeout_ms=120000)  # NCCL async errors / a lost peer fail the run instead of hanging
     torch.cuda.synchronize()
     dist.barrier()
     launches = h.launches - l0
@@ -521,8 +511,7 @@ def run_distributed(args, world, rank, local):
         "vs_baseline": round(value / PAPER_C2_GFLOPS, 3), "dtype": "f64",
         "data": "synthetic (mt19937_64 seed 1234, standard normal, reference draw order)",
         "config": {"workload": WORKLOAD, "seed": SEED,
-                   "parallelism": f"slab x{world} (last mode): {path}"
-                                  + (f" [C-ABI path unavailable: {fallback}]" if fallback else ""),
+                   "parallelism": f"slab x{world} (last mode): {path}",
                    "l2": "flushed between steps (256 MiB write outside the step events)",
                    "exchange_bytes_per_rank": plan.exchange_bytes(rank),
                    "local_ms_per_step": round(local_ms / args.steps, 4),

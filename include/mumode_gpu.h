@@ -212,6 +212,14 @@ int mumode_dist_tucker_phase_f64(mumode_handle_t h, mumode_comm_t c, int d, cons
 int mumode_dist_tucker_phase_c128(mumode_handle_t h, mumode_comm_t c, int d, const int64_t* m,
                                   const int64_t* n, const double* T, const double* const* L, double* S,
                                   int phase);
+/* The local half of one NCCL-path application on rank `rank` of `nranks`
+ * without a communicator: every sub-slab's modes 1..d-1, its last local mode
+ * storing the packed send blocks into `send` and the own row block into its
+ * final columns of Z (A_r x m_d) -- exactly what mumode_dist_tucker_f64 does
+ * before its NCCL group. Lets tests emulate the exchange between simulated
+ * ranks on one GPU and check the send layout bitwise. */
+int mumode_dist_local_f64(mumode_handle_t h, int nranks, int rank, int d, const int64_t* m, const int64_t* n,
+                          const double* T, const double* const* L, double* send, double* Z, int chunks);
 /* Return exchange after an application with output extents n (host only):
  * rank r's output rows (A_r x n_d) -> the last-mode slabs of the output for
  * the next application. op_tab rows as in mumode_dist_plan (send_offset into

@@ -52,6 +52,8 @@ SIGNATURES = {
     "mumode_comm_ipc_export": (ctypes.c_int, [VP, ctypes.c_int, I64P, I64P, ctypes.c_int, VP]),
     "mumode_comm_ipc_import": (ctypes.c_int, [VP, ctypes.c_int, I64P, I64P, ctypes.c_int, VP]),
     "mumode_comm_poll": (ctypes.c_int, [H, VP, I64]),
+    "mumode_dist_local_f64": (ctypes.c_int, [H, ctypes.c_int, ctypes.c_int, ctypes.c_int, I64P, I64P, VP,
+                                             ctypes.POINTER(VP), VP, VP, ctypes.c_int]),
     "mumode_dist_tucker_phase_f64": (ctypes.c_int, [H, VP, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
     "mumode_dist_tucker_phase_c128": (ctypes.c_int, [H, VP, ctypes.c_int, I64P, I64P, VP, ctypes.POINTER(VP), VP, ctypes.c_int]),
     "mumode_slab_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, I64P, I64P, I64P, I64P]),

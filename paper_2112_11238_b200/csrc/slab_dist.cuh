@@ -271,16 +271,23 @@ __global__ void p2p_signal_kernel(int64_t* const* __restrict__ peer_flags, int P
     asm volatile("st.release.sys.global.b64 [%0], %1;\n" ::"l"(peer_flags[q] + r), "l"(epoch) : "memory");
 }
 // Wait until every rank's flag in the local array reached epoch (acquire,
-// system scope), with the watchdog of the mbarrier waits: a lost peer
-// surfaces as a launch failure, not a hung GPU.
+// system scope). Watchdog: a peer that has not signalled within 10 s of
+// global time traps the kernel, so a lost peer surfaces as a launch failure
+// instead of a hung GPU.
 __global__ void p2p_wait_kernel(const int64_t* __restrict__ flags, int P, int64_t epoch) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t0));
   for (int s = threadIdx.x; s < P; s += blockDim.x) {
-    uint32_t polls = 0;
     int64_t v;
-    do {
+    for (uint32_t polls = 1;; ++polls) {
       asm volatile("ld.acquire.sys.global.b64 %0, [%1];\n" : "=l"(v) : "l"(flags + s) : "memory");
-      if (++polls == (1u << 30)) __trap();
-    } while (v < epoch);
+      if (v >= epoch) break;
+      if ((polls & 1023u) == 0) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+        if (t - t0 > 10000000000ull) __trap();
+      }
+    }
   }
   __syncthreads();
   asm volatile("fence.sc.sys;\n" ::: "memory");
@@ -413,7 +420,10 @@ static int dist_tucker_p2p(mumode_handle_s* h, mumode_comm_s* cm, int d, const i
     if (P > 1)
       MM_CUDA(cudaMemcpyAsync(dflags, cm->peer_flags.data(), sizeof(int64_t*) * P, cudaMemcpyHostToDevice,
                               h->stream));
-    MM_TRY(tucker_dev(h, d, m, n, T, L, nullptr, false, cplx, 1, d - 1, dsp));
+    // the local slab: m_1 x ... x m_{d-1} x c_r (the global m_d is the sum)
+    std::vector<int64_t> ext(m, m + d);
+    ext[d - 1] = pl.c_off[r + 1] - pl.c_off[r];
+    MM_TRY(tucker_dev(h, d, ext.data(), n, T, L, nullptr, false, cplx, 1, d - 1, dsp));
     if (P > 1) {
       p2p_signal_kernel<<<1, 64, 0, h->stream>>>(dflags, P, r, cm->epoch);
       MM_CUDA(cudaGetLastError());
@@ -424,6 +434,17 @@ static int dist_tucker_p2p(mumode_handle_s* h, mumode_comm_s* cm, int d, const i
     return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: phase 2 without a phase 1 for this shape");
   }
   const int par = static_cast<int>(cm->epoch & 1);
+  if (P > 1 && phase == 2) {
+    // split phases: the caller promised every rank finished phase 1; check
+    // it on the host so the wait below never has to wait on another process
+    std::vector<int64_t> fl(static_cast<size_t>(P));
+    MM_CUDA(cudaStreamSynchronize(h->stream));
+    MM_CUDA(cudaMemcpy(fl.data(), cm->flags.p, sizeof(int64_t) * P, cudaMemcpyDeviceToHost));
+    for (int q = 0; q < P; ++q)
+      if (fl[static_cast<size_t>(q)] < cm->epoch)
+        return fail(MUMODE_ERR_ARGUMENT, "dist_tucker: phase 2 before rank " + std::to_string(q) +
+                                             " completed phase 1 of epoch " + std::to_string(cm->epoch));
+  }
   if (P > 1) {
     p2p_wait_kernel<<<1, 64, 0, h->stream>>>(static_cast<const int64_t*>(cm->flags.p), P, cm->epoch);
     MM_CUDA(cudaGetLastError());
@@ -432,6 +453,35 @@ static int dist_tucker_p2p(mumode_handle_s* h, mumode_comm_s* cm, int d, const i
   if (pl.A_r == 0) return MUMODE_OK;
   const int64_t zext[2] = {pl.A_r, pl.m_d};
   return mode_product_dev(h, 2, zext, 2, pl.n_d, cm->peer_z[par][r], L[d - 1], 1, pl.n_d, cplx, false, S);
+}
+
+// No pack pass: each sub-slab's last local mode stores its rows through the
+// scatter epilogue (EPI 2) straight into the packed send layout -- row block
+// q of chunk j is the contiguous (A_q x w) matrix at send_off + a_off[q] * w
+// -- and its own row block straight into its final columns of Z. One
+// scatter table per chunk, uploaded once per call (stream-ordered).
+static int upload_scatter_tables(mumode_handle_s* h, DevBuf& buf, const DistPlan& pl, int P, int r, double* send,
+                                 double* Z, int el) {
+  const int nch = static_cast<int>(pl.ch.size());
+  std::vector<ScatterParams> tabs(static_cast<size_t>(std::max(nch, 1)));
+  for (int j = 0; j < nch; ++j) {
+    const DistChunk& c = pl.ch[j];
+    ScatterParams& sp = tabs[static_cast<size_t>(j)];
+    sp = ScatterParams{};
+    sp.P = P;
+    sp.col0 = 0;
+    for (int q = 0; q <= P; ++q) sp.a_off[q] = pl.a_off[q];
+    for (int q = 0; q < P; ++q) {
+      const bool empty = pl.a_off[q + 1] == pl.a_off[q] || c.w == 0;
+      sp.dst[q] = empty ? nullptr
+                        : (q == r ? Z + pl.A_r * (pl.c_off[r] + c.col0) * el
+                                  : send + c.send_off + pl.a_off[q] * c.w * el);
+    }
+  }
+  MM_TRY(buf.ensure(sizeof(ScatterParams) * tabs.size()));
+  MM_CUDA(cudaMemcpyAsync(buf.p, tabs.data(), sizeof(ScatterParams) * tabs.size(), cudaMemcpyHostToDevice,
+                          h->stream));
+  return MUMODE_OK;
 }
 
 static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64_t* m, const int64_t* n,
@@ -460,30 +510,8 @@ static int dist_tucker(mumode_handle_s* h, mumode_comm_s* cm, int d, const int64
   MM_TRY(comm_events(cm, size_t(nch) + 2));
   auto* send = static_cast<double*>(cm->send.p);
   auto* Z = static_cast<double*>(cm->z.p);
-  // No pack pass: each sub-slab's last local mode stores its rows through the
-  // scatter epilogue (EPI 2) straight into the packed send layout -- row
-  // block q of chunk j is the contiguous (A_q x w) matrix at
-  // send_off + a_off[q] * w -- and its own row block straight into its final
-  // columns of Z. One scatter table per chunk, uploaded once per call.
-  std::vector<ScatterParams> tabs(static_cast<size_t>(nch));
-  for (int j = 0; j < nch; ++j) {
-    const DistChunk& c = pl.ch[j];
-    ScatterParams& sp = tabs[static_cast<size_t>(j)];
-    sp = ScatterParams{};
-    sp.P = P;
-    sp.col0 = 0;
-    for (int q = 0; q <= P; ++q) sp.a_off[q] = pl.a_off[q];
-    for (int q = 0; q < P; ++q) {
-      const bool empty = pl.a_off[q + 1] == pl.a_off[q] || c.w == 0;
-      sp.dst[q] = empty ? nullptr
-                        : (q == r ? Z + A_r * (pl.c_off[r] + c.col0) * el
-                                  : send + c.send_off + pl.a_off[q] * c.w * el);
-    }
-  }
-  MM_TRY(cm->scat_tabs.ensure(sizeof(ScatterParams) * std::max<size_t>(tabs.size(), 1)));
+  MM_TRY(upload_scatter_tables(h, cm->scat_tabs, pl, P, r, send, Z, el));
   auto* dtabs = static_cast<ScatterParams*>(cm->scat_tabs.p);
-  MM_CUDA(cudaMemcpyAsync(dtabs, tabs.data(), sizeof(ScatterParams) * tabs.size(), cudaMemcpyHostToDevice,
-                          h->stream));
 
   // Z (and send) may still be read by the previous call's work on h->stream
   MM_CUDA(cudaEventRecord(cm->events[nch], h->stream));
@@ -881,5 +909,27 @@ int mumode_comm_poll(mumode_handle_t h, mumode_comm_t c, int64_t timeout_ms) {
   return comm_poll(h, c, timeout_ms);
 }
 
+int mumode_dist_local_f64(mumode_handle_t h, int nranks, int rank, int d, const int64_t* m, const int64_t* n,
+                          const double* T, const double* const* L, double* send, double* Z, int chunks) {
+  using namespace mumode_gpu;
+  if (!h || !m || !n || !T || !L || !send || !Z) return fail(MUMODE_ERR_ARGUMENT, "dist_local: null pointer");
+  MM_DEVICE(h->device);
+  DistPlan pl;
+  MM_TRY(dist_plan(nranks, rank, d, m, n, chunks, 1, pl));
+  MM_TRY(h->scat_params.ensure(sizeof(ScatterParams)));  // keep the handle's single table intact
+  static thread_local DevBuf tabs;
+  MM_TRY(upload_scatter_tables(h, tabs, pl, nranks, rank, send, Z, 1));
+  std::vector<int64_t> ext(m, m + d);
+  for (size_t j = 0; j < pl.ch.size(); ++j) {
+    const DistChunk& c = pl.ch[j];
+    if (c.w == 0) continue;
+    ext[d - 1] = c.w;
+    MM_TRY(tucker_dev(h, d, ext.data(), n, T + pl.rows_in * c.col0, L, nullptr, false, false, 1, d - 1,
+                      static_cast<const ScatterParams*>(tabs.p) + j));
+  }
+  return MUMODE_OK;
+}
+
 }  // extern "C"
+
 

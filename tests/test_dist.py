@@ -594,3 +594,64 @@ def test_dist_tucker_peer_store_exchange_single_rank():
                 assert np.array_equal(S_r.cpu().numpy(), ref), m
     finally:
         comm.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_dist_local_pack_free_send_layout_simulated_ranks(P):
+    # The NCCL path's local half on the GPU for P simulated ranks
+    # (mumode_dist_local_f64: sub-slab chains whose last local mode scatters
+    # the packed send blocks and the own block, no pack kernel), the NCCL
+    # sends / receives of the plan emulated by device copies, then mode d:
+    # bitwise equal to the single-GPU tucker().
+    import ctypes
+    from collections import defaultdict
+
+    import paper_2112_11238_b200 as mm
+    from paper_2112_11238_b200 import _lib
+    from paper_2112_11238_b200.dist import dist_plan
+    lib = _lib.lib()
+    h = mm.get_handle(0)
+    h.bind_torch_stream()
+    for m, n, chunks in [((64, 48, 40), (56, 48, 72), 3), ((24, 24, 24, 24), (24, 24, 24, 24), 2),
+                         ((40, 33, 17), (48, 31, 20), 1)]:
+        if m[-1] < P:
+            continue
+        rng = np.random.default_rng(P + len(m))
+        T = np.asfortranarray(rng.standard_normal(m))
+        Ls = [np.asfortranarray(rng.standard_normal((n[k], m[k]))) for k in range(len(m))]
+        want = mm.tucker(torch.from_numpy(T).cuda(), [torch.from_numpy(L).cuda() for L in Ls]).cpu().numpy()
+        plan = SlabPlan(m, n, P)
+        Lds = [torch.from_numpy(L).cuda() for L in Ls]
+        Lp = _lib.ptr_array([L.data_ptr() for L in Lds])
+        slabs = [torch.from_numpy(np.asfortranarray(s)).cuda() for s in scatter_slabs(plan, T)]
+        sends, zs, sched = [], [], []
+        for r in range(P):
+            ch, ops = dist_plan(P, r, m, n, chunks)
+            sched.append(ops)
+            send = torch.full((plan.A * plan.c_sizes[r],), float("nan"), dtype=torch.float64, device="cuda")
+            Z = torch.full((plan.a_sizes[r] * m[-1],), float("nan"), dtype=torch.float64, device="cuda")
+            rc = lib.mumode_dist_local_f64(h.h, P, r, len(m), _lib.i64_array(m), _lib.i64_array(n),
+                                           slabs[r].data_ptr(), Lp, send.data_ptr(), Z.data_ptr(), chunks)
+            assert rc == 0, lib.mumode_last_error().decode()
+            sends.append(send)
+            zs.append(Z)
+        torch.cuda.synchronize()
+        sq, rq = defaultdict(list), defaultdict(list)
+        for r, ops in enumerate(sched):
+            for (j, kind, peer, boff, zoff, cnt) in ops:
+                if kind == 0:
+                    sq[(r, peer)].append((boff, cnt))
+                elif kind == 1:
+                    rq[(peer, r)].append((zoff, cnt))
+        for key in sq:
+            for (boff, cnt), (zoff, cnt2) in zip(sq[key], rq[key]):
+                src, dst = key
+                zs[dst][zoff:zoff + cnt].copy_(sends[src][boff:boff + cnt])
+        rows = []
+        for r in range(P):
+            assert not torch.isnan(zs[r]).any(), "Z not fully written"
+            Zm = zs[r].cpu().numpy().reshape((plan.a_sizes[r], m[-1]), order="F")
+            rows.append(mm.mode_product(torch.from_numpy(np.asfortranarray(Zm)).cuda(), Lds[-1], 2)
+                        .cpu().numpy().reshape(-1, order="F"))
+        np.testing.assert_array_equal(gather_rows(plan, rows), want)
