@@ -50,6 +50,15 @@ PAPER_C2_GFLOPS = 115.0  # paper Fig. 1, tucker d=3 n=256, MATLAB o
 WORKLOAD = "C2: 3-D Tucker operator fp64, T 256^3 (128 MiB), three 256x256 factors (BASELINE configs[1])"
 
 
+def hbm_peak_gbs() -> float:
+    """Measured copy bandwidth of this pool's B200s (MEASURED_PEAKS.json,
+    driver-written); the profiling recipe's fallback when it is absent."""
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except Exception:
+        return 6545.6
+
+
 def tucker_flops(m, n):
     ext, f = list(m), 0.0
     for mu in range(len(m)):
@@ -368,7 +377,10 @@ def main():
                      "kernel": "modeprod_tma_kernel (TMA 64B-swizzle ring + DMMA.8x8x4)",
                      "flops_per_launch": flops_per_launch, "mean_launch_ms": round(launch_ms, 5),
                      "peak_source": "fp64 DMMA probe measured live in this run (mumode_probe_fp64_peak); "
-                                    "MEASURED_PEAKS.json has no fp64 entry"},
+                                    "MEASURED_PEAKS.json has no fp64 entry",
+                     "peak_crosscheck": {"cublas_dgemm_8192_tflops": cublas_dgemm_tflops(dev),
+                                         "nominal_tflops": 37.2,
+                                         "note": "148 SM x 128 flop/clk x 1.965 GHz"}},
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
                 "path": "mumode_host_tucker_f64_async x K + mumode_host_wait (host-buffer C-ABI), pinned "
@@ -569,6 +581,29 @@ def dist_c5(args, world, rank, dev, comm, stream, flush):
             "scaling": "strong (the full 24^6 application split over the ranks)"}
 
 
+def cublas_dgemm_tflops(dev) -> float | None:
+    """cuBLAS DGEMM (torch float64 matmul) at 8192^3 on this GPU: a library
+    yardstick printed beside the DMMA probe that is the roofline denominator."""
+    import torch
+    try:
+        a = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+        b = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+        a @ b
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = 1e30
+        for _ in range(5):
+            e0.record()
+            a @ b
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b
+        return round(2 * 8192 ** 3 / (best * 1e-3) / 1e12, 3)
+    except Exception:  # reported as unavailable, never replaces the probe
+        return None
+
+
 def ctypes_peak(lib, h) -> float:
     import ctypes
     v = ctypes.c_double()
@@ -620,7 +655,7 @@ def extras(mm, lib, h, dev, stream, peak, flush):
         return statistics.median(a.elapsed_time(b) for a, b in ts)
 
     def rec(name, flops, ms, bytes_alg):
-        t_roof = max(flops / (peak * 1e12), bytes_alg / 6545.6e9)
+        t_roof = max(flops / (peak * 1e12), bytes_alg / (hbm_peak_gbs() * 1e9))
         out[name] = {"ms": round(ms, 4), "gflops": round(flops / ms / 1e6, 2),
                      "roofline_frac": round(t_roof / (ms * 1e-3), 4)}
 

@@ -1,7 +1,11 @@
 """Parity report: the CUDA path vs the compiled reference library (oracle/_ref)
 on the BASELINE configs, identical seeded bytes. Prints one JSON object with
-relative Frobenius and relative max-norm errors per config (gate 1e-12).
-Test infrastructure: imports the oracle as the checker."""
+relative Frobenius and relative max-norm errors per config and PASS / FAIL
+against the north-star gate (relative Frobenius <= 1e-12); exit status 1 on
+any FAIL. --inject-fault perturbs one element of the C2 result (the
+reference CLI's test-only flag, tools/mumode_cli.cpp:142,168) so the failure
+path is exercised. Test infrastructure: imports the oracle as the checker."""
+import argparse
 import json
 import sys
 import time
@@ -23,12 +27,27 @@ def host(t):
     return t.cpu().numpy()
 
 
+GATE = 1e-12
+INJECT = False
+
+
 def rec(out, name, got, want, t_ref):
-    out[name] = {"rel_fro": O.rel_fro(got, want), "rel_max": O.rel_max(got, want),
-                 "ref_seconds": round(t_ref, 3)}
+    if INJECT and name == "C2_tucker_256":
+        got = got.copy()
+        got.reshape(-1, order="F")[0] += 1e-6 * float(np.max(np.abs(want)))
+    err = O.rel_fro(got, want)
+    out[name] = {"rel_fro": err, "rel_max": O.rel_max(got, want), "ref_seconds": round(t_ref, 3),
+                 "status": "PASS" if err <= GATE else "FAIL"}
 
 
 def main():
+    global INJECT
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--inject-fault", action="store_true",
+                    help="test-only: corrupt the C2 result to exercise the failure path")
+    ap.add_argument("--quick", action="store_true", help="C1 and C2 only")
+    args = ap.parse_args()
+    INJECT = args.inject_fault
     out = {"reference": f"oracle/_ref (reference library), OpenBLAS {O.ref_blas_kernel_name()}"}
     g = mm.Rng(1234 + 100)
     L1, L2 = g.normal((100, 100)), g.normal((100, 100))
@@ -44,6 +63,8 @@ def main():
     for mu in (1, 2, 3):
         t0 = time.time(); ref = O.ref_mode_product(T, Ls[mu - 1], mu); t = time.time() - t0
         rec(out, f"C2_mode{mu}", host(mm.mode_product(dev(T), dev(Ls[mu - 1]), mu)), ref, t)
+    if args.quick:
+        return finish(out)
 
     n = 200
     A = O.port_advection_diffusion(n, 0.5)
@@ -75,8 +96,16 @@ def main():
     Ls = [g.normal((24, 24)) for _ in range(6)]
     t0 = time.time(); ref = O.ref_tucker(T, Ls); t = time.time() - t0
     rec(out, "C5_6d_24", host(mm.tucker(dev(T), [dev(L) for L in Ls])), ref, t)
+    return finish(out)
+
+
+def finish(out) -> int:
+    bad = [k for k, v in out.items() if isinstance(v, dict) and v.get("status") == "FAIL"]
+    out["overall"] = "FAIL" if bad else "PASS"
+    out["failed"] = bad
     print(json.dumps(out, indent=1))
+    return 1 if bad else 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())
