@@ -73,7 +73,9 @@ int64_t mumode_launch_count(mumode_handle_t h);
  * run as one persistent launch where the tile configs allow (tma_chain.cuh),
  * 12 = auto with the fused passes' non-warp-specialised kernels
  * (fused_pair_kernel / tail_pair_kernel instead of fused_ws / tail_ws),
- * 13 = auto without the small-extent (skinny) mode-product kernel.
+ * 13 = auto without the small-extent (skinny) mode-product kernel,
+ * 14 = auto without the small-extent fused two-mode passes (spair.cuh),
+ * 15 = auto with the small-extent fused passes wherever eligible.
  * Not a fallback switch: all are CUDA kernels. */
 int mumode_set_kernel_policy(mumode_handle_t h, int policy);
 

@@ -109,7 +109,8 @@ class Handle:
         config forced, 7 auto incl. fused pairs, 8 LDG-staged DMMA, 9 / 10 tail
         pass forced / disabled, 11 whole chains as one persistent launch, 12
         fused passes without warp specialisation, 13 no skinny small-extent
-        kernel."""
+        kernel, 14 no small-extent fused pairs, 15 small-extent fused pairs
+        wherever eligible."""
         _check(_lib.lib().mumode_set_kernel_policy(self.h, int(policy)))
 
     def close(self) -> None:

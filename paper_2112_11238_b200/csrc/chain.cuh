@@ -151,6 +151,87 @@ static int fused_extent(int d, const int64_t* m, const int64_t* n, bool cplx, bo
   return static_cast<int>(MU);
 }
 
+// ------------------------------------------------------------------ small-extent pairs
+// Fused two-mode passes for extents <= 24 that the MU kernels do not cover
+// (spair.cuh): auto paths (policy 0/7/9/10/12) use them where they measured
+// faster than two skinny passes (largest extent 17..20: 20^6 1.10 -> 0.98 ms,
+// 18^6 0.68 -> 0.64 ms; tools/small_pairs_sweep.py); 15 forces them wherever
+// eligible (tests), 14 disables them.
+static bool spair_policy(int policy) {
+  return policy == 0 || policy == 7 || policy == 9 || policy == 10 || policy == 12 || policy == 15;
+}
+
+template <int P4, int NF>
+static int launch_spair_p(mumode_handle_s* h, const SpairParams& p0, bool mode1) {
+  SpairParams p = p0;
+  if (mode1) {
+    using Cfg = Spair1Cfg<P4, NF>;
+    const int64_t stages = (p.C + Cfg::CB - 1) / Cfg::CB;
+    auto k = spair1_kernel<P4, NF>;
+    MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
+    const int grid = static_cast<int>(std::min<int64_t>(stages, persistent_sms(h)));
+    MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, p));
+  } else {
+    using Cfg = SpairCfg<P4, NF>;
+    p.ablks = (p.A + 31) / 32;
+    p.tiles = p.ablks * p.C;
+    auto k = spair_kernel<P4, NF>;
+    MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
+    const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
+    MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, p));
+  }
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return MUMODE_OK;
+}
+
+// Can modes (mu, mu+1) of the current extents run as one small-extent pass?
+static int spair_size(const int64_t* ext, const int64_t* n, int d, int mu, bool forced) {
+  const int64_t K1 = ext[mu - 1], N1 = n[mu - 1], K2 = ext[mu], N2 = n[mu];
+  const int64_t e = std::max(std::max(K1, K2), std::max(N1, N2));
+  if (e > 24 || std::min(std::min(K1, K2), std::min(N1, N2)) < 2) return 0;
+  if (!forced && (e < 17 || e > 20)) return 0;
+  const int64_t A = prod(ext, 0, mu - 1);
+  if (mu == 1 ? (K1 & 1) : (A & 1)) return 0;  // 16-byte cp.async chunks
+  return static_cast<int>((e + 3) / 4 * 4);
+}
+
+static int launch_spair(mumode_handle_s* h, const int64_t* ext, const int64_t* n, int d, int mu, const double* T,
+                        const double* L1, const double* L2, double* S) {
+  SpairParams p{};
+  p.X = T;
+  p.S = S;
+  p.L1 = L1;
+  p.L2 = L2;
+  p.A = prod(ext, 0, mu - 1);
+  p.C = prod(ext, mu + 1, d);
+  p.K1 = static_cast<int>(ext[mu - 1]);
+  p.N1 = static_cast<int>(n[mu - 1]);
+  p.K2 = static_cast<int>(ext[mu]);
+  p.N2 = static_cast<int>(n[mu]);
+  const bool mode1 = (mu == 1);
+  switch (spair_size(ext, n, d, mu, true)) {
+    case 4:
+    case 8: return launch_spair_p<8, 1>(h, p, mode1);
+    case 12: return launch_spair_p<12, 2>(h, p, mode1);
+    case 16: return launch_spair_p<16, 2>(h, p, mode1);
+    case 20: return launch_spair_p<20, 3>(h, p, mode1);
+    case 24: return launch_spair_p<24, 3>(h, p, mode1);
+    default: return fail(MUMODE_ERR_ARGUMENT, "small-extent pair: unsupported extents");
+  }
+}
+
+// Chains of small extents: any real forward chain whose modes are all <= 24
+// and large enough to fill the GPU (>= 2^20 elements throughout).
+static bool spair_chain_ok(mumode_handle_s* h, int d, const int64_t* m, const int64_t* n, bool cplx, bool adjoint,
+                           int mu_lo, int mu_hi, const double* T, const double* S, const double* const* L) {
+  if (cplx || adjoint || !spair_policy(h->policy) || mu_hi - mu_lo < 1) return false;
+  if (!aligned16_ptr(T) || !aligned16_ptr(S)) return false;
+  for (int k = mu_lo - 1; k < mu_hi; ++k)
+    if (m[k] > 24 || n[k] > 24 || !L[k]) return false;
+  return std::min(prod(m, 0, d), prod(n, 0, d)) >= (int64_t(1) << 20);
+}
+
 // One mode product on device buffers: T with extents m (d modes), op(L)
 // n_mu x m_mu given by (L, sLi, sLk, conj).
 static int mode_product_dev(mumode_handle_s* h, int d, const int64_t* m, int mu, int64_t n_mu,
@@ -488,6 +569,29 @@ static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t
       eigsum_divide_kernel<<<dim3(gx, gy), 256, 0, h->stream>>>(S, div_front, div_last, A, N);
       MM_CUDA(cudaGetLastError());
       h->launches++;
+    }
+    return MUMODE_OK;
+  }
+  if (!div_front && spair_chain_ok(h, d, m, n, cplx, adjoint, mu_lo, mu_hi, T, S, L)) {
+    // pairs (mu, mu+1) as small-extent fused passes where eligible, single
+    // products (skinny kernels) otherwise
+    int pass = 0, mu = mu_lo;
+    while (mu <= mu_hi) {
+      const bool last_single = (mu == mu_hi);
+      const bool pair = !last_single && spair_size(ext.data(), n, d, mu, h->policy == 15) != 0;
+      const int step = pair ? 2 : 1;
+      double* dst = (mu + step - 1 == mu_hi) ? S : static_cast<double*>(h->ws[pass % 2].p);
+      if (pair) {
+        MM_TRY(launch_spair(h, ext.data(), n, d, mu, src, L[mu - 1], L[mu], dst));
+        ext[mu - 1] = n[mu - 1];
+        ext[mu] = n[mu];
+      } else {
+        MM_TRY(mode_product_dev(h, d, ext.data(), mu, n[mu - 1], src, L[mu - 1], 1, n[mu - 1], false, false, dst));
+        ext[mu - 1] = n[mu - 1];
+      }
+      src = dst;
+      mu += step;
+      ++pass;
     }
     return MUMODE_OK;
   }

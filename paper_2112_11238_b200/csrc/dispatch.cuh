@@ -330,7 +330,9 @@ static bool ldg_worthwhile(const ModeJob& j) {
 // 256-B rows. Policy 13 disables the path (auto otherwise).
 static bool skinny_ok(const mumode_handle_s* h, const ModeJob& j) {
   if (j.cplx || j.conj || j.accumulate || j.scat || j.div_front) return false;
-  if (!(h->policy == 0 || h->policy == 7 || h->policy == 9 || h->policy == 10 || h->policy == 12)) return false;
+  if (!(h->policy == 0 || h->policy == 7 || h->policy == 9 || h->policy == 10 || h->policy == 12 || h->policy == 14 ||
+        h->policy == 15))
+    return false;
   if (j.K > 32 || j.N > 32 || !aligned16(j.T) || !aligned16(j.S)) return false;
   if (j.A == 1) {
     // TMA box coordinates are int32: fibre offsets up to C + 32 TC

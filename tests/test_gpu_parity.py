@@ -40,9 +40,9 @@ def _require_gpu():
         pytest.fail("GPU test run without a GPU")
 
 
-@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13],
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14],
                 ids=["auto", "generic", "tma", "tma_big", "tma_tm", "tma_lm", "tma_mid", "fused", "ldg", "tail",
-                     "no_tail", "chain", "no_ws", "no_skinny"])
+                     "no_tail", "chain", "no_ws", "no_skinny", "no_spair"])
 def policy(request):
     h = mm.get_handle(0)
     h.set_kernel_policy(request.param)
@@ -751,3 +751,37 @@ def test_user_cuda_graph_capture_of_tucker_and_kronsumv():
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(S, 2.0 * ref_S)
+
+
+@pytest.mark.parametrize("m,n", [
+    ((20,) * 5, (20,) * 5), ((18,) * 5, (18,) * 5), ((12,) * 6, (12,) * 6), ((14,) * 6, (14,) * 6),
+    ((20, 18, 16, 20, 18), (18, 20, 12, 16, 20)), ((22, 10, 24, 6, 20), (24, 8, 22, 10, 12)),
+    ((24, 24, 20, 20, 24), (24, 24, 20, 20, 24)), ((19,) * 5, (19,) * 5), ((8, 12, 12, 12, 12, 10), (10, 12, 8, 12, 12, 8))])
+def test_small_extent_fused_pairs(m, n):
+    # spair_kernel / spair1_kernel (csrc/spair.cuh): two modes per HBM pass for
+    # extents <= 24 outside the MU kernels; bitwise equal to one mode per pass
+    # (policy 14: the skinny per-mode kernels) and to the oracle
+    rng = np.random.default_rng(sum(m) + len(m))
+    T = rnd(rng, m)
+    Ls = [rnd(rng, (n[k], m[k])) for k in range(len(m))]
+    Td, Lds = dev(T), [dev(L) for L in Ls]
+    h = mm.get_handle(0)
+    auto = host(mm.tucker(Td, Lds))
+    try:
+        h.set_kernel_policy(15)  # small-extent pairs wherever eligible
+        got = host(mm.tucker(Td, Lds))
+        h.set_kernel_policy(14)  # one mode per pass
+        per_mode = host(mm.tucker(Td, Lds))
+    finally:
+        h.set_kernel_policy(0)
+    np.testing.assert_array_equal(auto, got)
+    np.testing.assert_array_equal(got, per_mode)
+    want = O.ref_tucker(T, Ls) if O.ref_available() else O.port_tucker(T, Ls)
+    assert O.rel_fro(got, want) < 1e-13
+    # repeated launches on identical data are bitwise identical (pipeline races)
+    h.set_kernel_policy(15)
+    try:
+        for _ in range(3):
+            np.testing.assert_array_equal(host(mm.tucker(Td, Lds)), got)
+    finally:
+        h.set_kernel_policy(0)
