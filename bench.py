@@ -699,6 +699,25 @@ def extras(mm, lib, h, dev, stream, peak, flush):
     L5 = [mm.to_colmajor(torch.randn(24, 24, dtype=torch.float64, device=dev)) for _ in range(6)]
     ms = timeit(lambda: mm.tucker(T5, L5), reps=3)
     rec("C5_6d_24", tucker_flops((24,) * 6, (24,) * 6), ms, 2 * 8 * 24 ** 6)
+    # kronsumv (terms accumulated in the epilogues), itucker (per-mode
+    # LU solves, 2 n^2 flop per fibre and mode) and the IMEX direct solve (two
+    # Tuckers + divide) -- flops as the equivalent mode products, bytes compulsory
+    ms = timeit(lambda: mm.kronsumv(T5, L5), reps=3)
+    rec("kronsumv_6d_24", 6 * 2.0 * 24 * 24 ** 6, ms, 2 * 8 * 24 ** 6)
+    del T5
+    V3 = normal((200,) * 3)
+    A3 = [mm.to_colmajor(torch.randn(200, 200, dtype=torch.float64, device=dev)) for _ in range(3)]
+    ms = timeit(lambda: mm.kronsumv(V3, A3))
+    rec("kronsumv_200cube", 3 * 2.0 * 200 * 200 ** 3, ms, 2 * 8 * 200 ** 3)
+    F = mm.FactorizedStack([np.random.default_rng(k).standard_normal((200, 200)) + 30 * np.eye(200)
+                            for k in range(3)])
+    ms = timeit(lambda: mm.itucker(V3, F))
+    rec("itucker_200cube", 3 * 2.0 * 200 * 200 ** 3, ms, 2 * 8 * 200 ** 3)
+    An = A.numpy()
+    M = (-1e-3) * (0.5 * (An + An.T)) + np.eye(200) / 3  # symmetric tridiagonal (the Laplacian part)
+    solver = mm.KronSumSolver(Ms=[M, M, M])
+    ms = timeit(lambda: solver.solve(V3))
+    rec("imex_direct_solve_200cube", 2 * tucker_flops((200,) * 3, (200,) * 3), ms, 2 * 8 * 200 ** 3)
     return out
 
 
