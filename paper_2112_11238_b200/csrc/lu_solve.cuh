@@ -24,12 +24,10 @@
 // (n % 4 != 0) take OpenBLAS's M-tail kernels, whose grouping differs at the
 // 1e-16 level.
 //
-// Layout: one thread per fibre, 32 fibres per CTA staged in shared memory as
-// x[k * 33 + t] (every solve-phase access is a warp-wide contiguous row; the
-// fibre loads/stores are coalesced for mu > 1 and tile-linear for mu = 1).
-// The factor is read through the read-only path (all lanes read the same
-// element: broadcast). Extents too large for the shared tile solve in place in
-// global memory (same arithmetic).
+// Layout: 32 fibres per CTA staged in shared memory as x[k * 33 + fibre]
+// (loads / stores coalesced along a for mu > 1 and tile-linear for mu = 1),
+// each fibre solved by a group of UM lanes (below). Extents too large for the
+// shared tile are solved in global memory (same arithmetic).
 #pragma once
 
 namespace mumode_gpu {
@@ -37,73 +35,16 @@ namespace mumode_gpu {
 constexpr int kLuFibres = 32;
 constexpr int kLuStride = kLuFibres + 1;
 
-// --------------------------------------------------------------- real fibre
-template <class X>
-__device__ __forceinline__ void lu_fibre_f64(X x, const double* __restrict__ Q, const int64_t* __restrict__ piv,
-                                             const double* __restrict__ invd, int n) {
-  constexpr int UM = 16;
-  for (int k = 0; k < n; ++k) {  // row interchanges in order (lu.hpp:58-64)
-    const int p = static_cast<int>(__ldg(piv + k));
-    if (p != k) {
-      const double t = x(k);
-      x(k) = x(p);
-      x(p) = t;
-    }
-  }
-  const int full_end = n & ~(UM - 1);
-  // forward sweep, unit lower triangle
-  for (int r0 = 0; r0 < n;) {
-    const int bs = r0 < full_end ? UM : 1 << (31 - __clz(n - r0));
-    if (r0 > 0) {
-      double acc[UM];
-#pragma unroll
-      for (int r = 0; r < UM; ++r) acc[r] = 0.0;
-      for (int k = 0; k < r0; ++k) {
-        const double xk = x(k);
-        const double* q = Q + int64_t(k) * n + r0;
-#pragma unroll
-        for (int r = 0; r < UM; ++r)
-          if (r < bs) acc[r] = fma(__ldg(q + r), xk, acc[r]);
-      }
-#pragma unroll
-      for (int r = 0; r < UM; ++r)
-        if (r < bs) x(r0 + r) = __dsub_rn(x(r0 + r), acc[r]);
-    }
-    for (int i = r0; i < r0 + bs; ++i) {
-      const double xi = x(i);
-      for (int k = i + 1; k < r0 + bs; ++k) x(k) = fma(-xi, __ldg(Q + k + int64_t(i) * n), x(k));
-    }
-    r0 += bs;
-  }
-  // backward sweep, upper triangle with the reciprocal diagonal
-  for (int top = n; top > 0;) {
-    const int bs = top > full_end ? (top & -top) : UM;
-    const int r0 = top - bs;
-    if (top < n) {
-      double acc[UM];
-#pragma unroll
-      for (int r = 0; r < UM; ++r) acc[r] = 0.0;
-      for (int k = top; k < n; ++k) {
-        const double xk = x(k);
-        const double* q = Q + int64_t(k) * n + r0;
-#pragma unroll
-        for (int r = 0; r < UM; ++r)
-          if (r < bs) acc[r] = fma(__ldg(q + r), xk, acc[r]);
-      }
-#pragma unroll
-      for (int r = 0; r < UM; ++r)
-        if (r < bs) x(r0 + r) = __dsub_rn(x(r0 + r), acc[r]);
-    }
-    for (int i = top - 1; i >= r0; --i) {
-      const double xi = __dmul_rn(x(i), invd[i]);
-      x(i) = xi;
-      for (int k = r0; k < i; ++k) x(k) = fma(-xi, __ldg(Q + k + int64_t(i) * n), x(k));
-    }
-    top = r0;
-  }
-}
+// Cooperative layout: a fibre is solved by UM lanes (16 real, 4 complex), lane
+// l owning row r0 + l of the current block. The GEMM part of a block is then
+// UM independent k-ordered chains (one per lane, x[k] broadcast from shared
+// memory, the factor's block rows read coalesced), and the in-block solve
+// passes each finished x_i to the lanes below it by a shuffle -- the same
+// operations in the same order per element as the serial restatement
+// (host_util.cpp, tools/openblas_trsm_probe.c), on UM lanes at once.
+// Row interchanges are applied while staging: x(k) = in(perm[k]), perm being
+// the sequential swaps of piv applied to an index array (lu_perm_kernel).
 
-// ------------------------------------------------------------ complex fibre
 // c -= p * a with the grouping of OpenBLAS's ztrsm in-block update.
 __device__ __forceinline__ double2 ztrsm_update(double2 c, double2 p, double2 a) {
   const double t0 = fma(p.x, a.x, -__dmul_rn(p.y, a.y));
@@ -126,138 +67,252 @@ __device__ __forceinline__ double2 ztrsm_recip(double2 a) {
   return make_double2(__dmul_rn(ratio, den), -den);
 }
 
-template <class X>
-__device__ __forceinline__ void lu_fibre_c128(X x, const double2* __restrict__ Q, const int64_t* __restrict__ piv,
-                                              const double2* __restrict__ invd, int n) {
-  constexpr int UM = 4;
-  for (int k = 0; k < n; ++k) {
-    const int p = static_cast<int>(__ldg(piv + k));
-    if (p != k) {
-      const double2 t = x(k);
-      x(k) = x(p);
-      x(p) = t;
-    }
+template <class V>
+__device__ __forceinline__ V shfl_v(V v, int src, int width) {
+  if constexpr (sizeof(V) == 16) {
+    return make_double2(__shfl_sync(0xffffffffu, v.x, src, width), __shfl_sync(0xffffffffu, v.y, src, width));
+  } else {
+    return __shfl_sync(0xffffffffu, v, src, width);
   }
-  const int full_end = n & ~(UM - 1);
-  auto gemm_part = [&](int r0, int bs, int k0, int k1) {
-    double rr[UM], ii[UM], ri[UM], ir[UM];
-#pragma unroll
-    for (int r = 0; r < UM; ++r) rr[r] = ii[r] = ri[r] = ir[r] = 0.0;
+}
+
+// The lane's row of the factor through Qrow(k) = Q(r, k): from the block's
+// shared-memory panel (staged path: every group of the CTA solves the same
+// block at the same time, so the CTA stages the UM x k panel once per block)
+// or from global memory.
+template <class V, class QR>
+__device__ __forceinline__ V lu_gemm_row(QR Qrow, const V* x, int xs, int k0, int k1) {
+  if constexpr (sizeof(V) == 8) {
+    double acc = 0.0;
+#pragma unroll 4
+    for (int k = k0; k < k1; ++k) acc = fma(Qrow(k), x[k * xs], acc);
+    return acc;
+  } else {
+    double rr = 0.0, ii = 0.0, ri = 0.0, ir = 0.0;
+#pragma unroll 4
     for (int k = k0; k < k1; ++k) {
-      const double2 xk = x(k);
-      const double2* q = Q + int64_t(k) * n + r0;
-#pragma unroll
-      for (int r = 0; r < UM; ++r)
-        if (r < bs) {
-          const double2 a = __ldg(q + r);
-          rr[r] = fma(a.x, xk.x, rr[r]);
-          ii[r] = fma(a.y, xk.y, ii[r]);
-          ri[r] = fma(a.x, xk.y, ri[r]);
-          ir[r] = fma(a.y, xk.x, ir[r]);
-        }
+      const double2 a = Qrow(k), xk = x[k * xs];
+      rr = fma(a.x, xk.x, rr);
+      ii = fma(a.y, xk.y, ii);
+      ri = fma(a.x, xk.y, ri);
+      ir = fma(a.y, xk.x, ir);
     }
-#pragma unroll
-    for (int r = 0; r < UM; ++r)
-      if (r < bs) {
-        const double2 c = x(r0 + r);
-        x(r0 + r) = make_double2(__dsub_rn(c.x, __dsub_rn(rr[r], ii[r])), __dsub_rn(c.y, __dadd_rn(ri[r], ir[r])));
-      }
-  };
-  const double2 one = make_double2(1.0, 0.0);
+    return make_double2(__dsub_rn(rr, ii), __dadd_rn(ri, ir));
+  }
+}
+
+// Stage panel[(k - k0) * UM + l] = Q(r0 + l, k), k in [k0, k1), l < bs (zero
+// above bs): the CTA's threads cooperatively, between two barriers.
+template <class V, int UM>
+__device__ __forceinline__ void lu_stage_panel(V* panel, const V* __restrict__ Q, int n, int r0, int bs, int k0,
+                                               int k1) {
+  __syncthreads();  // the previous block's panel has been read
+  const int tot = (k1 - k0) * UM;
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int kk = e / UM, ll = e - kk * UM;
+    panel[e] = ll < bs ? __ldg(Q + (r0 + ll) + int64_t(k0 + kk) * n) : V{};
+  }
+  __syncthreads();
+}
+
+// Solve one fibre x (stride xs) cooperatively on the UM lanes of this group
+// (l = lane within the group). All threads of the CTA run this together
+// (PANEL: with CTA barriers; the groups work on different fibres of the same
+// shape, inactive groups only take part in the shuffles and barriers).
+template <bool CPLX, bool PANEL>
+__device__ __forceinline__ void lu_fibre_coop(typename std::conditional<CPLX, double2, double>::type* x, int xs,
+                                              const typename std::conditional<CPLX, double2, double>::type* __restrict__ Q,
+                                              const typename std::conditional<CPLX, double2, double>::type* invd,
+                                              typename std::conditional<CPLX, double2, double>::type* panel,
+                                              int n, int l, bool active) {
+  using V = typename std::conditional<CPLX, double2, double>::type;
+  constexpr int UM = CPLX ? 4 : 16;
+  const int full_end = n & ~(UM - 1);
+  // forward sweep, unit lower triangle
   for (int r0 = 0; r0 < n;) {
     const int bs = r0 < full_end ? UM : 1 << (31 - __clz(n - r0));
-    if (r0 > 0) gemm_part(r0, bs, 0, r0);
-    for (int i = r0; i < r0 + bs; ++i) {
-      const double2 xi = ztrsm_scale(x(i), one);
-      x(i) = xi;
-      for (int k = i + 1; k < r0 + bs; ++k) x(k) = ztrsm_update(x(k), xi, __ldg(Q + k + int64_t(i) * n));
+    const int r = r0 + l;
+    const bool own = active && l < bs;
+    if constexpr (PANEL) lu_stage_panel<V, UM>(panel, Q, n, r0, bs, 0, r0 + bs);
+    auto Qrow = [&](int k) -> V {
+      if constexpr (PANEL) return panel[k * UM + l];
+      else return __ldg(Q + r + int64_t(k) * n);
+    };
+    V xr = own ? x[r * xs] : V{};
+    if (r0 > 0 && own) {
+      const V acc = lu_gemm_row<V>(Qrow, x, xs, 0, r0);
+      if constexpr (CPLX)
+        xr = make_double2(__dsub_rn(xr.x, acc.x), __dsub_rn(xr.y, acc.y));
+      else
+        xr = __dsub_rn(xr, acc);
     }
+    for (int i = 0; i < bs; ++i) {
+      V xi = shfl_v(xr, i, UM);
+      if constexpr (CPLX) {
+        if (l == i && own) xr = ztrsm_scale(xr, make_double2(1.0, 0.0));
+        xi = ztrsm_scale(xi, make_double2(1.0, 0.0));
+        if (l > i && own) xr = ztrsm_update(xr, xi, Qrow(r0 + i));
+      } else {
+        if (l > i && own) xr = fma(-xi, Qrow(r0 + i), xr);
+      }
+    }
+    if (own) x[r * xs] = xr;
+    __syncwarp();
     r0 += bs;
   }
+  // backward sweep, upper triangle with the reciprocal diagonal
   for (int top = n; top > 0;) {
     const int bs = top > full_end ? (top & -top) : UM;
     const int r0 = top - bs;
-    if (top < n) gemm_part(r0, bs, top, n);
-    for (int i = top - 1; i >= r0; --i) {
-      const double2 xi = ztrsm_scale(x(i), invd[i]);
-      x(i) = xi;
-      for (int k = r0; k < i; ++k) x(k) = ztrsm_update(x(k), xi, __ldg(Q + k + int64_t(i) * n));
+    const int r = r0 + l;
+    const bool own = active && l < bs;
+    if constexpr (PANEL) lu_stage_panel<V, UM>(panel, Q, n, r0, bs, r0, n);
+    auto Qrow = [&](int k) -> V {
+      if constexpr (PANEL) return panel[(k - r0) * UM + l];
+      else return __ldg(Q + r + int64_t(k) * n);
+    };
+    V xr = own ? x[r * xs] : V{};
+    if (top < n && own) {
+      const V acc = lu_gemm_row<V>(Qrow, x, xs, top, n);
+      if constexpr (CPLX)
+        xr = make_double2(__dsub_rn(xr.x, acc.x), __dsub_rn(xr.y, acc.y));
+      else
+        xr = __dsub_rn(xr, acc);
     }
+    for (int i = bs - 1; i >= 0; --i) {
+      if (l == i && own) {
+        if constexpr (CPLX)
+          xr = ztrsm_scale(xr, invd[r]);
+        else
+          xr = __dmul_rn(xr, invd[r]);
+      }
+      const V xi = shfl_v(xr, i, UM);
+      if (l < i && own) {
+        if constexpr (CPLX)
+          xr = ztrsm_update(xr, xi, Qrow(r0 + i));
+        else
+          xr = fma(-xi, Qrow(r0 + i), xr);
+      }
+    }
+    if (own) x[r * xs] = xr;
+    __syncwarp();
     top = r0;
   }
 }
 
-template <class V>
-struct StridedRef {
-  V* base;
-  int64_t stride;
-  __device__ __forceinline__ V& operator()(int k) const { return base[int64_t(k) * stride]; }
+// perm[k]: the row of the input that ends in row k after lu_solve's swaps
+// (lu.hpp:58-64) -- the swaps applied in order to an index array. iperm is
+// its inverse. One thread (n is a mode extent).
+__global__ void lu_perm_kernel(const int64_t* __restrict__ piv, int* __restrict__ perm, int* __restrict__ iperm,
+                               int n) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int k = 0; k < n; ++k) perm[k] = k;
+  for (int k = 0; k < n; ++k) {
+    const int p = static_cast<int>(piv[k]);
+    if (p != k) {
+      const int t = perm[k];
+      perm[k] = perm[p];
+      perm[p] = t;
+    }
+  }
+  for (int k = 0; k < n; ++k) iperm[perm[k]] = k;
+}
+
+template <bool CPLX>
+struct LuCfg {
+  static constexpr int UM = CPLX ? 4 : 16;
+  static constexpr int THREADS = kLuFibres * UM;  // one lane group per fibre of the tile
 };
 
 // One mode of itucker: out(a, :, c) = P^-1 in(a, :, c) for all A*C fibres of
 // length n (in may equal out: every CTA reads and writes only its own fibres).
+// staged: the tile's fibres live in shared memory x[k * 33 + fibre]; else
+// (n too large) they are solved in place in `out` with the same arithmetic.
 template <bool CPLX>
-__global__ void __launch_bounds__(kLuFibres) lu_solve_mode_kernel(const double* in, double* out, int64_t A, int n,
-                                                                  int64_t C, const double* __restrict__ lu,
-                                                                  const int64_t* __restrict__ piv, int staged) {
+__global__ void __launch_bounds__(LuCfg<CPLX>::THREADS) lu_solve_mode_kernel(
+    const double* in, double* out, int64_t A, int n, int64_t C, const double* __restrict__ lu,
+    const int* __restrict__ perm, const int* __restrict__ iperm, int staged) {
   using V = typename std::conditional<CPLX, double2, double>::type;
+  constexpr int UM = LuCfg<CPLX>::UM;
   extern __shared__ __align__(16) unsigned char lu_smem[];
   V* invd = reinterpret_cast<V*>(lu_smem);
   V* xs = invd + n;
+  V* panel = xs + n * kLuStride;  // staged path: one block's factor rows
   const V* Q = reinterpret_cast<const V*>(lu);
   const V* src = reinterpret_cast<const V*>(in);
   V* dst = reinterpret_cast<V*>(out);
-  const int t = threadIdx.x;
-  for (int i = t; i < n; i += blockDim.x) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int grp = tid / UM, l = tid - grp * UM;  // fibre of the tile, row lane
+  for (int i = tid; i < n; i += nt) {
     if constexpr (CPLX)
       invd[i] = ztrsm_recip(Q[i + int64_t(i) * n]);
     else
       invd[i] = 1.0 / Q[i + int64_t(i) * n];
   }
   __syncthreads();
+  __shared__ int64_t foff[kLuFibres];  // element 0 of each fibre of the tile
   const int64_t F = A * C, An = A * n;
   for (int64_t f0 = int64_t(blockIdx.x) * kLuFibres; f0 < F; f0 += int64_t(gridDim.x) * kLuFibres) {
     const int nf = static_cast<int>(F - f0 < kLuFibres ? F - f0 : kLuFibres);
-    const int64_t f = f0 + t;
-    const int64_t a = f % A, c = f / A;
-    const int64_t off = a + c * An;  // element k of fibre f at off + k * A
+    if (tid < kLuFibres) {
+      const int64_t ff = f0 + (tid < nf ? tid : 0);
+      foff[tid] = (ff % A) + (ff / A) * An;
+    }
+    __syncthreads();
+    const int64_t off = foff[grp];  // element k of this group's fibre at off + k * A
     if (staged) {
       if (A == 1) {  // mu = 1: the tile's fibres are nf*n contiguous elements
         const V* s = src + f0 * n;
-        for (int64_t e = t; e < int64_t(nf) * n; e += kLuFibres) {
-          const int fl = static_cast<int>(e / n), k = static_cast<int>(e - int64_t(fl) * n);
-          xs[k * kLuStride + fl] = s[e];
+        const int64_t tot = int64_t(nf) * n;
+        const int dfl = nt / n, dkk = nt - dfl * n;
+        int fl = tid / n, kk = tid - (tid / n) * n;
+        for (int64_t e = tid; e < tot; e += nt) {
+          xs[iperm[kk] * kLuStride + fl] = s[e];
+          fl += dfl;
+          kk += dkk;
+          if (kk >= n) {
+            kk -= n;
+            ++fl;
+          }
         }
-      } else if (t < nf) {
-        for (int k = 0; k < n; ++k) xs[k * kLuStride + t] = src[off + int64_t(k) * A];
+      } else {  // lanes along the fibres (consecutive a): coalesced
+        const int fl = tid & (kLuFibres - 1);
+        if (fl < nf) {
+          const int64_t o = foff[fl];
+          for (int k = tid / kLuFibres; k < n; k += nt / kLuFibres) xs[k * kLuStride + fl] = src[o + int64_t(perm[k]) * A];
+        }
       }
-      __syncwarp();
-      if (t < nf) {
-        StridedRef<V> x{xs + t, kLuStride};
-        if constexpr (CPLX)
-          lu_fibre_c128(x, Q, piv, invd, n);
-        else
-          lu_fibre_f64(x, Q, piv, invd, n);
-      }
-      __syncwarp();
+      __syncthreads();
+      lu_fibre_coop<CPLX, true>(xs + grp, kLuStride, Q, invd, panel, n, l, grp < nf);
+      __syncthreads();
       if (A == 1) {
         V* d = dst + f0 * n;
-        for (int64_t e = t; e < int64_t(nf) * n; e += kLuFibres) {
-          const int fl = static_cast<int>(e / n), k = static_cast<int>(e - int64_t(fl) * n);
+        const int64_t tot = int64_t(nf) * n;
+        const int dfl = nt / n, dkk = nt - dfl * n;
+        int fl = tid / n, k = tid - (tid / n) * n;
+        for (int64_t e = tid; e < tot; e += nt) {
           d[e] = xs[k * kLuStride + fl];
+          fl += dfl;
+          k += dkk;
+          if (k >= n) {
+            k -= n;
+            ++fl;
+          }
         }
-      } else if (t < nf) {
-        for (int k = 0; k < n; ++k) dst[off + int64_t(k) * A] = xs[k * kLuStride + t];
+      } else {
+        const int fl = tid & (kLuFibres - 1);
+        if (fl < nf) {
+          const int64_t o = foff[fl];
+          for (int k = tid / kLuFibres; k < n; k += nt / kLuFibres) dst[o + int64_t(k) * A] = xs[k * kLuStride + fl];
+        }
       }
+      __syncthreads();
+    } else {  // in global memory (in != out: the host stages a copy): permuted gather, solve in place
+      if (grp < nf)
+        for (int k = l; k < n; k += UM) dst[off + int64_t(k) * A] = src[off + int64_t(perm[k]) * A];
       __syncwarp();
-    } else if (t < nf) {  // in place in global memory
-      if (src != dst)
-        for (int k = 0; k < n; ++k) dst[off + int64_t(k) * A] = src[off + int64_t(k) * A];
-      StridedRef<V> x{dst + off, A};
-      if constexpr (CPLX)
-        lu_fibre_c128(x, Q, piv, invd, n);
-      else
-        lu_fibre_f64(x, Q, piv, invd, n);
+      lu_fibre_coop<CPLX, false>(dst + (grp < nf ? off : 0), static_cast<int>(A), Q, invd, nullptr, n, l, grp < nf);
+      __syncthreads();
     }
   }
 }

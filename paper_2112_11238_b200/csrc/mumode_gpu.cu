@@ -157,6 +157,7 @@ struct mumode_handle_s {
   mumode_gpu::DevBuf lstage;    // a factor with an odd leading dimension, re-laid with an even one
   mumode_gpu::DevBuf scat_params, scat_tmp, scat_mid;  // scatter table; fallback output; chain intermediate
   mumode_gpu::DevBuf lbuf;      // materialised op(L) for adjoint / promotion
+  mumode_gpu::DevBuf lperm;     // itucker: per-mode row permutations of the pivots
   mumode_gpu::DevBuf host_in, host_out, host_mats, host_mid;  // host drop-in staging
   mumode_gpu::DevBuf slot_in[2], slot_out[2], slot_mats[2];   // pipelined host calls, double-buffered
   int64_t host_calls = 0;
@@ -719,24 +720,41 @@ static int itucker_dev(mumode_handle_t h, int d, const int64_t* m, const double*
                        const int64_t* const* piv, double* S, bool cplx) {
   const size_t vb = cplx ? 16 : 8;
   constexpr size_t kMaxSmem = 227 * 1024;
+  int64_t nsum = 0;
+  for (int k = 0; k < d; ++k) nsum += m[k];
+  MM_TRY(h->lperm.ensure(size_t(2 * nsum) * sizeof(int)));
+  int* perm = static_cast<int*>(h->lperm.p);
   for (int mu = 1; mu <= d; ++mu) {
     const int64_t n = m[mu - 1], A = prod(m, 0, mu - 1), C = prod(m, mu, d);
-    size_t smem = vb * size_t(n) * (1 + kLuStride);
+    if (n > (int64_t(1) << 30)) return fail(MUMODE_ERR_ARGUMENT, "itucker: extent too large");
+    lu_perm_kernel<<<1, 32, 0, h->stream>>>(piv[mu - 1], perm, perm + n, static_cast<int>(n));
+    MM_CUDA(cudaGetLastError());
+    h->launches++;
+    const size_t um = cplx ? LuCfg<true>::UM : LuCfg<false>::UM;
+    size_t smem = vb * size_t(n) * (1 + kLuStride + um);  // invd, fibre tile, factor panel
     int staged = 1;
+    const double* src = mu == 1 ? T : S;
     if (smem > kMaxSmem) {
       staged = 0;
       smem = vb * size_t(n);
       if (smem > kMaxSmem)
         return fail(MUMODE_ERR_ARGUMENT, "itucker: extent of mode " + std::to_string(mu) + " is too large");
+      if (src == S) {  // the global-memory path gathers from a separate copy
+        const size_t bytes = size_t(prod(m, 0, d)) * vb;
+        MM_TRY(h->ws[2].ensure(bytes));
+        MM_CUDA(cudaMemcpyAsync(h->ws[2].p, S, bytes, cudaMemcpyDeviceToDevice, h->stream));
+        src = static_cast<const double*>(h->ws[2].p);
+      }
     }
     auto kern = cplx ? lu_solve_mode_kernel<true> : lu_solve_mode_kernel<false>;
+    const int threads = cplx ? LuCfg<true>::THREADS : LuCfg<false>::THREADS;
     MM_TRY(smem_opt_in(kern, static_cast<int>(smem)));
     const int64_t tiles = (A * C + kLuFibres - 1) / kLuFibres;
     const int grid = static_cast<int>(std::min<int64_t>(tiles, int64_t(h->num_sms) * 32));
-    kern<<<grid, kLuFibres, smem, h->stream>>>(mu == 1 ? T : S, S, A, static_cast<int>(n), C, LU[mu - 1],
-                                               piv[mu - 1], staged);
+    kern<<<grid, threads, smem, h->stream>>>(src, S, A, static_cast<int>(n), C, LU[mu - 1], perm, perm + n, staged);
     MM_CUDA(cudaGetLastError());
     h->launches++;
+    perm += 2 * n;
   }
   return MUMODE_OK;
 }
