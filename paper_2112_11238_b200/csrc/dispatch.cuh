@@ -329,7 +329,7 @@ static bool ldg_worthwhile(const ModeJob& j) {
 // Small-extent real products (skinny.cuh): HBM-bound, 32-wide tiles with
 // 256-B rows. Policy 13 disables the path (auto otherwise).
 static bool skinny_ok(const mumode_handle_s* h, const ModeJob& j) {
-  if (j.cplx || j.conj || j.accumulate || j.scat || j.div_front) return false;
+  if (j.cplx || j.conj || j.scat || j.div_front || (j.accumulate && j.A == 1)) return false;
   if (!(h->policy == 0 || h->policy == 7 || h->policy == 9 || h->policy == 10 || h->policy == 12 || h->policy == 14 ||
         h->policy == 15))
     return false;
@@ -398,7 +398,9 @@ static int launch_skinny_p(mumode_handle_s* h, const ModeJob& j) {
     }
   }
   const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
-  auto k = TA == 16 ? skinny_kernel<P, false, 16> : (mode1 ? skinny_kernel<P, true> : skinny_kernel<P, false>);
+  auto k = TA == 16 ? (j.accumulate ? skinny_kernel<P, false, 16, true> : skinny_kernel<P, false, 16>)
+                    : (mode1 ? skinny_kernel<P, true>
+                             : (j.accumulate ? skinny_kernel<P, false, 32, true> : skinny_kernel<P, false>));
   MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
   MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mx, *ms, p));
   MM_CUDA(cudaGetLastError());
@@ -420,7 +422,7 @@ static int launch_skinny_slab_p(mumode_handle_s* h, const ModeJob& j) {
   MM_TRY(get_map(h, j.S, 3, ds, ss, b, &ms, 2));
   p.tiles = (j.C + p.TC - 1) / p.TC;
   const int grid = static_cast<int>(std::min<int64_t>(p.tiles, persistent_sms(h)));
-  auto k = skinny_slab_kernel<P>;
+  auto k = j.accumulate ? skinny_slab_kernel<P, true> : skinny_slab_kernel<P>;
   MM_TRY(smem_opt_in(k, Cfg::SMEM_BYTES));
   MM_TRY(launch_pdl(k, grid, Cfg::THREADS, Cfg::SMEM_BYTES, h->stream, *mx, *ms, p));
   MM_CUDA(cudaGetLastError());

@@ -71,7 +71,10 @@ struct SkinnyParams {
 // distinct 16-B bank groups of the 128B-swizzled k rows.
 __device__ __forceinline__ int skinny_col16(int f, int n) { return 4 * f + (n & 1) + 8 * ((n >> 1) & 1) + 2 * (n >> 2); }
 
-template <int P, bool MODE1, int TA = 32>
+// ACC: S += result (the kronsumv term accumulation, tucker.hpp:222-231): each
+// warp TMA-loads its output tile of S into the staging buffer while it
+// computes, and adds before the TMA store (old + term, the reference's order).
+template <int P, bool MODE1, int TA = 32, bool ACC = false>
 __global__ void __launch_bounds__(SkinnyCfg<P, TA>::THREADS, 1)
     skinny_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapS,
                   const SkinnyParams p) {
@@ -85,13 +88,16 @@ __global__ void __launch_bounds__(SkinnyCfg<P, TA>::THREADS, 1)
   uint8_t* Stg = smem + W * R * Cfg::TILE_BYTES;        // [warp]
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(Stg + W * Cfg::TILE_BYTES);
   uint64_t* empty_bar = full_bar + W * R;
+  uint64_t* acc_bar = empty_bar + W * R;  // ACC: per warp, the S tile load
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  static_assert(!(ACC && MODE1), "accumulating mode-1 products take the tile kernels");
 
   if (threadIdx.x == 0) {
     for (int b = 0; b < W * R; ++b) {
       mbar_init(&full_bar[b], 1);
       mbar_init(&empty_bar[b], 1);
     }
+    for (int w = 0; w < W; ++w) mbar_init(&acc_bar[w], 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -160,6 +166,17 @@ __global__ void __launch_bounds__(SkinnyCfg<P, TA>::THREADS, 1)
     const int b = warp * R + static_cast<int>(q % R);
     mbar_wait(&full_bar[b], static_cast<uint32_t>((q / R) & 1));
     if (lane == 0) bulk_wait_read_all();  // the staging buffer's previous store has read it
+    if constexpr (ACC) {
+      if (lane == 0) {  // the current S tile into the staging buffer (same box as the store)
+        int32_t ca, cc0;
+        coords(tile, ca, cc0);
+        mbar_arrive_expect_tx(&acc_bar[warp], Cfg::TILE_BYTES);
+        if constexpr (TA == 32)
+          tma_load_5d(slot_out, &mapS, &acc_bar[warp], 0, 0, 0, ca, cc0);
+        else
+          tma_load_3d(slot_out, &mapS, &acc_bar[warp], 16 * ca, 0, cc0);
+      }
+    }
     __syncwarp();
 #pragma unroll 1
     for (int cc = 0; cc < TC; ++cc) {
@@ -214,7 +231,13 @@ __global__ void __launch_bounds__(SkinnyCfg<P, TA>::THREADS, 1)
             off = sw128_off(static_cast<uint32_t>(2 * (8 * nf + g) + (t & 1)),
                             static_cast<uint32_t>(4 * f + 2 * (t >> 1)));
           }
-          *reinterpret_cast<double2*>(D + off) = make_double2(acc[nf][f][0], acc[nf][f][1]);
+          if constexpr (ACC) {
+            if (cc == 0 && nf == 0 && f == 0) mbar_wait(&acc_bar[warp], static_cast<uint32_t>(q & 1));
+            const double2 o = *reinterpret_cast<const double2*>(D + off);
+            *reinterpret_cast<double2*>(D + off) = make_double2(o.x + acc[nf][f][0], o.y + acc[nf][f][1]);
+          } else {
+            *reinterpret_cast<double2*>(D + off) = make_double2(acc[nf][f][0], acc[nf][f][1]);
+          }
         }
     }
     __syncwarp();
@@ -243,7 +266,7 @@ __global__ void __launch_bounds__(SkinnyCfg<P, TA>::THREADS, 1)
 // leaves as ONE contiguous box {A, P n, TC c} (n >= N and c >= C clipped).
 // Same warp-per-tile pipeline as skinny_kernel; per slab c the warp computes
 // D_c(n, a) = L(n, k) X_c(k, a) with a-fragments of 8 consecutive a's.
-template <int P>
+template <int P, bool ACC = false>
 __global__ void __launch_bounds__(SkinnyCfg<P>::THREADS, 1)
     skinny_slab_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapS,
                        const SkinnyParams p) {
@@ -255,6 +278,7 @@ __global__ void __launch_bounds__(SkinnyCfg<P>::THREADS, 1)
   uint8_t* Stg = smem + W * R * Cfg::TILE_BYTES;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(Stg + W * Cfg::TILE_BYTES);
   uint64_t* empty_bar = full_bar + W * R;
+  uint64_t* acc_bar = empty_bar + W * R;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t tile_bytes = static_cast<uint32_t>(p.TC * P * p.A * 8);
 
@@ -263,6 +287,7 @@ __global__ void __launch_bounds__(SkinnyCfg<P>::THREADS, 1)
       mbar_init(&full_bar[b], 1);
       mbar_init(&empty_bar[b], 1);
     }
+    for (int w = 0; w < W; ++w) mbar_init(&acc_bar[w], 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -302,6 +327,13 @@ __global__ void __launch_bounds__(SkinnyCfg<P>::THREADS, 1)
     mbar_wait(&full_bar[b], static_cast<uint32_t>((q / R) & 1));
     const double* X = reinterpret_cast<const double*>(Xs + b * Cfg::TILE_BYTES);
     if (lane == 0) bulk_wait_read_all();  // the staging buffer's previous store has read it
+    if constexpr (ACC) {
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&acc_bar[warp], tile_bytes);
+        tma_load_3d(slot_out, &mapS, &acc_bar[warp], 0, 0, static_cast<int32_t>(tile * p.TC));
+      }
+      mbar_wait(&acc_bar[warp], static_cast<uint32_t>(q & 1));
+    }
     __syncwarp();
     double* D = reinterpret_cast<double*>(slot_out);
     for (int cc = 0; cc < p.TC; ++cc) {
@@ -322,8 +354,15 @@ __global__ void __launch_bounds__(SkinnyCfg<P>::THREADS, 1)
           const int a = 8 * af + 2 * t;
           if (a < A) {
 #pragma unroll
-            for (int nf = 0; nf < NF; ++nf)
-              *reinterpret_cast<double2*>(D + (cc * P + 8 * nf + g) * A + a) = make_double2(acc[nf][0], acc[nf][1]);
+            for (int nf = 0; nf < NF; ++nf) {
+              double2* o = reinterpret_cast<double2*>(D + (cc * P + 8 * nf + g) * A + a);
+              if constexpr (ACC) {
+                const double2 v = *o;
+                *o = make_double2(v.x + acc[nf][0], v.y + acc[nf][1]);
+              } else {
+                *o = make_double2(acc[nf][0], acc[nf][1]);
+              }
+            }
           }
         }
       }
