@@ -33,7 +33,7 @@
 namespace mumode_gpu {
 
 constexpr int kLuFibres = 32;
-constexpr int kLuStride = kLuFibres + 1;
+constexpr int kLuStride = kLuFibres + 4;  // 36 doubles: = 8 mod 32 words, conflict-free DMMA B fragments
 
 // Cooperative layout: a fibre is solved by UM lanes (16 real, 4 complex), lane
 // l owning row r0 + l of the current block. The GEMM part of a block is then
@@ -222,7 +222,98 @@ template <bool CPLX>
 struct LuCfg {
   static constexpr int UM = CPLX ? 4 : 16;
   static constexpr int THREADS = kLuFibres * UM;  // one lane group per fibre of the tile
+  static constexpr int PS = CPLX ? 4 : 20;        // factor panel row stride (real: = 8 mod 32 words)
 };
+
+// Real staged sweeps with the blocks' GEMM parts on the tensor cores: for a
+// 16-row block at r0 the CTA's 32 fibres need D(16 x 32) = Q(r0.., 0..r0) .
+// X(0..r0, fibres) -- 2 x 4 DMMA fragments, each the k-ordered FMA chain of
+// the serial restatement (zero k-steps pad r0 to a multiple of 4), subtracted
+// from the block rows; then every 16-lane group solves its fibre's diagonal
+// block with shuffles. The block's factor rows are staged once per block
+// (panel[k * 20 + l] = Q(r0 + l, k)).
+__device__ __forceinline__ void lu_sweep_dmma(double* xs, const double* __restrict__ Q,
+                                              const double* __restrict__ invd, double* panel, int n, int nf) {
+  constexpr int UM = 16, PS = LuCfg<false>::PS, XS = kLuStride;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int grp = threadIdx.x / UM, l = threadIdx.x - grp * UM;
+  const bool active = grp < nf;
+  const int mf = warp >> 2, fr = warp & 3;  // GEMM warps 0..7: rows 8 mf.., fibres 8 fr..
+  const int full_end = n & ~(UM - 1);
+  auto stage = [&](int r0, int bs, int k0, int k1) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < (k1 - k0) * UM; e += blockDim.x) {
+      const int kk = e >> 4, ll = e & 15;
+      panel[kk * PS + ll] = ll < bs ? __ldg(Q + (r0 + ll) + int64_t(k0 + kk) * n) : 0.0;
+    }
+    __syncthreads();
+  };
+  // forward sweep, unit lower triangle
+  for (int r0 = 0; r0 < n;) {
+    const int bs = r0 < full_end ? UM : 1 << (31 - __clz(n - r0));
+    stage(r0, bs, 0, r0 + bs);
+    if (r0 > 0 && warp < 8) {
+      double d0 = 0.0, d1 = 0.0;
+      const int ks = (r0 + 3) >> 2;
+      for (int s = 0; s < ks; ++s) {
+        const int k = 4 * s + t;
+        const double a = k < r0 ? panel[k * PS + 8 * mf + g] : 0.0;
+        const double b = k < r0 ? xs[k * XS + 8 * fr + g] : 0.0;
+        dmma_8x8x4(d0, d1, a, b);
+      }
+      const int row = 8 * mf + g;
+      if (row < bs) {
+        double* xr = xs + (r0 + row) * XS + 8 * fr + 2 * t;
+        xr[0] = __dsub_rn(xr[0], d0);
+        xr[1] = __dsub_rn(xr[1], d1);
+      }
+    }
+    __syncthreads();
+    const int r = r0 + l;
+    const bool own = active && l < bs;
+    double xr = own ? xs[r * XS + grp] : 0.0;
+    for (int i = 0; i < bs; ++i) {
+      const double xi = __shfl_sync(0xffffffffu, xr, i, UM);
+      if (l > i && own) xr = fma(-xi, panel[(r0 + i) * PS + l], xr);
+    }
+    if (own) xs[r * XS + grp] = xr;
+    r0 += bs;
+  }
+  // backward sweep, upper triangle with the reciprocal diagonal
+  for (int top = n; top > 0;) {
+    const int bs = top > full_end ? (top & -top) : UM;
+    const int r0 = top - bs;
+    stage(r0, bs, r0, n);
+    if (top < n && warp < 8) {
+      double d0 = 0.0, d1 = 0.0;
+      const int ks = (n - top + 3) >> 2;
+      for (int s = 0; s < ks; ++s) {
+        const int k = top + 4 * s + t;
+        const double a = k < n ? panel[(k - r0) * PS + 8 * mf + g] : 0.0;
+        const double b = k < n ? xs[k * XS + 8 * fr + g] : 0.0;
+        dmma_8x8x4(d0, d1, a, b);
+      }
+      const int row = 8 * mf + g;
+      if (row < bs) {
+        double* xr = xs + (r0 + row) * XS + 8 * fr + 2 * t;
+        xr[0] = __dsub_rn(xr[0], d0);
+        xr[1] = __dsub_rn(xr[1], d1);
+      }
+    }
+    __syncthreads();
+    const int r = r0 + l;
+    const bool own = active && l < bs;
+    double xr = own ? xs[r * XS + grp] : 0.0;
+    for (int i = bs - 1; i >= 0; --i) {
+      if (l == i && own) xr = __dmul_rn(xr, invd[r]);
+      const double xi = __shfl_sync(0xffffffffu, xr, i, UM);
+      if (l < i && own) xr = fma(-xi, panel[i * PS + l], xr);
+    }
+    if (own) xs[r * XS + grp] = xr;
+    top = r0;
+  }
+  __syncthreads();
+}
 
 // One mode of itucker: out(a, :, c) = P^-1 in(a, :, c) for all A*C fibres of
 // length n (in may equal out: every CTA reads and writes only its own fibres).
@@ -283,7 +374,10 @@ __global__ void __launch_bounds__(LuCfg<CPLX>::THREADS) lu_solve_mode_kernel(
         }
       }
       __syncthreads();
-      lu_fibre_coop<CPLX, true>(xs + grp, kLuStride, Q, invd, panel, n, l, grp < nf);
+      if constexpr (CPLX)
+        lu_fibre_coop<CPLX, true>(xs + grp, kLuStride, Q, invd, panel, n, l, grp < nf);
+      else
+        lu_sweep_dmma(xs, Q, invd, panel, n, nf);
       __syncthreads();
       if (A == 1) {
         V* d = dst + f0 * n;

@@ -730,8 +730,8 @@ static int itucker_dev(mumode_handle_t h, int d, const int64_t* m, const double*
     lu_perm_kernel<<<1, 32, 0, h->stream>>>(piv[mu - 1], perm, perm + n, static_cast<int>(n));
     MM_CUDA(cudaGetLastError());
     h->launches++;
-    const size_t um = cplx ? LuCfg<true>::UM : LuCfg<false>::UM;
-    size_t smem = vb * size_t(n) * (1 + kLuStride + um);  // invd, fibre tile, factor panel
+    const size_t ps = cplx ? LuCfg<true>::PS : LuCfg<false>::PS;
+    size_t smem = vb * size_t(n) * (1 + kLuStride + ps);  // invd, fibre tile, factor panel
     int staged = 1;
     const double* src = mu == 1 ? T : S;
     if (smem > kMaxSmem) {
