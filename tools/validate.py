@@ -33,7 +33,7 @@ def case(g: mm.Rng, cplx: bool, inject: bool) -> float:
     Ls = [g.normal((outs[k], ins[k]), complex_=cplx) for k in range(d)]
     fast = mm.tucker(torch.from_numpy(T).cuda(), [torch.from_numpy(L).cuda() for L in Ls]).cpu().numpy()
     if inject:
-        fast.reshape(-1, order="F")[0] += 1e-6
+        fast[(0,) * fast.ndim] += 1e-6
     slow = O.ref_tucker(T, Ls, "kron")
     return float(np.max(np.abs(fast - slow)) / max(float(np.max(np.abs(slow))), 1e-300))
 
