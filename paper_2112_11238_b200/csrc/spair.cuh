@@ -66,7 +66,6 @@ struct SpairCfg {
   static constexpr int UPW = KB / 2;    // mode mu units per group-A warp per stage
   static constexpr int WB = 8, WA = 8;  // 2 + 2 warps per sub-partition; A also issues the loads
   static constexpr int THREADS = (WB + WA) * 32;
-  static constexpr int PAIR = (WB + WA) * 32;
   static constexpr int RSX = 36, RSY = 40;
   static constexpr int X_DBL = KB * P4 * RSX;
   static constexpr int YB_DBL = NP * RSY + 4;  // k2l block stride: 8 mod 32 words
@@ -92,11 +91,14 @@ template <int P4, int NF>
 __global__ void __launch_bounds__(SpairCfg<P4, NF>::THREADS, 1) spair_kernel(const SpairParams p) {
   using Cfg = SpairCfg<P4, NF>;
   constexpr int KS = Cfg::KS, NBUF = Cfg::NBUF, NYS = Cfg::NYS, RSX = Cfg::RSX, RSY = Cfg::RSY;
-  constexpr int WA = Cfg::WA, WB = Cfg::WB, PAIR = Cfg::PAIR;
+  constexpr int WA = Cfg::WA, WB = Cfg::WB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   double* Xs = reinterpret_cast<double*>(smem_raw);
   double* Ys = Xs + NBUF * Cfg::X_DBL;
   double* Slots = Ys + NYS * Cfg::YS_DBL;  // (KB = 4 only)
+  // stage hand-offs between the groups: mbarriers (one arrival per warp)
+  uint64_t* yfull = reinterpret_cast<uint64_t*>(Slots + (Cfg::EPI_IN_YS ? 0 : WB * Cfg::SLOT_DBL));
+  uint64_t* yfree = yfull + NYS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K1 = p.K1, N1 = p.N1, K2 = p.K2, N2 = p.N2;
   const int64_t A = p.A;
@@ -109,6 +111,13 @@ __global__ void __launch_bounds__(SpairCfg<P4, NF>::THREADS, 1) spair_kernel(con
       const int k2l = r / (P4 - K1), k1 = K1 + (r - k2l * (P4 - K1));
       Xs[b * Cfg::X_DBL + (k2l * P4 + k1) * RSX + col] = 0.0;
     }
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NYS; ++b) {
+      mbar_init(&yfull[b], WA);
+      mbar_init(&yfree[b], WB);
+    }
+    fence_barrier_init();
+  }
   __syncthreads();
   pdl_launch_dependents();
   pdl_wait();  // before any global access (factors included)
@@ -181,7 +190,7 @@ __global__ void __launch_bounds__(SpairCfg<P4, NF>::THREADS, 1) spair_kernel(con
       named_barrier_sync(1, WA * 32);
       if (z + NBUF - 1 < nz) issue();
       cp_async_commit();
-      if (z >= NYS) named_barrier_sync(2 + NYS + yb, PAIR);  // Ys[yb] consumed by group B
+      if (z >= NYS) mbar_wait(&yfree[yb], static_cast<uint32_t>((z / NYS - 1) & 1));  // Ys[yb] consumed by group B
       const double* X = Xs + buf * Cfg::X_DBL;
       double* Y = Ys + yb * Cfg::YS_DBL;
 #pragma unroll
@@ -209,7 +218,8 @@ __global__ void __launch_bounds__(SpairCfg<P4, NF>::THREADS, 1) spair_kernel(con
                 make_double2(acc[u][nf][0], acc[u][nf][1]);
         }
       }
-      named_barrier_arrive(2 + yb, PAIR);  // Ys[yb] complete
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&yfull[yb]);  // Ys[yb] complete (release after the warp's stores)
       if (++yb == NYS) yb = 0;
       if (++buf == NBUF) buf = 0;
     }
@@ -244,7 +254,7 @@ __global__ void __launch_bounds__(SpairCfg<P4, NF>::THREADS, 1) spair_kernel(con
           const int i = 8 * nf + g, k = Cfg::KB * st + 4 * q + t;
           l2f[q][nf] = (i < N2 && k < K2) ? __ldg(p.L2 + i + static_cast<int64_t>(N2) * k) : 0.0;
         }
-      named_barrier_sync(2 + yb, PAIR);  // Ys[yb] complete
+      mbar_wait(&yfull[yb], static_cast<uint32_t>((z / NYS) & 1));  // Ys[yb] complete
       const double* Y = Ys + yb * Cfg::YS_DBL;
 #pragma unroll
       for (int q = 0; q < KQ; ++q)
@@ -265,7 +275,9 @@ __global__ void __launch_bounds__(SpairCfg<P4, NF>::THREADS, 1) spair_kernel(con
         yb_last = yb;  // freed after the epilogue has staged through it
         free_last = release;
       } else if (release) {
-        named_barrier_arrive_after_reads(2 + NYS + yb, PAIR);
+        asm volatile("fence.acq_rel.cta;\n" ::: "memory");  // this thread's Ys loads are complete
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&yfree[yb]);
       }
       if (++yb == NYS) yb = 0;
     }
@@ -297,7 +309,11 @@ __global__ void __launch_bounds__(SpairCfg<P4, NF>::THREADS, 1) spair_kernel(con
       }
       __syncwarp();
     }
-    if (Cfg::EPI_IN_YS && free_last) named_barrier_arrive_after_reads(2 + NYS + yb_last, PAIR);
+    if (Cfg::EPI_IN_YS && free_last) {
+      asm volatile("fence.acq_rel.cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&yfree[yb_last]);
+    }
     ab += gridDim.x;
     while (ab >= p.ablks) {
       ab -= p.ablks;
@@ -320,7 +336,6 @@ struct Spair1Cfg {
   static constexpr int CB = 8;
   static constexpr int WB = 8, WA = 8;  // A also issues the loads
   static constexpr int THREADS = (WB + WA) * 32;
-  static constexpr int PAIR = (WB + WA) * 32;
   static constexpr int RX = (P4 + 3) / 8 * 8 + 4;  // = 4 mod 8 (row stride 8 or 24 mod 32 words), >= P4
   static constexpr int RO = (NP <= 24) ? 24 : 40;  // = 8 mod 16, >= NP
   static constexpr int X_DBL = CB * P4 * RX;       // rows (c, k2) for k2 < P4
@@ -339,11 +354,13 @@ template <int P4, int NF>
 __global__ void __launch_bounds__(Spair1Cfg<P4, NF>::THREADS, 1) spair1_kernel(const SpairParams p) {
   using Cfg = Spair1Cfg<P4, NF>;
   constexpr int KS = Cfg::KS, NBUF = Cfg::NBUF, NYS = Cfg::NYS, RX = Cfg::RX, RO = Cfg::RO, NP = Cfg::NP;
-  constexpr int WA = Cfg::WA, WB = Cfg::WB, PAIR = Cfg::PAIR, CB = Cfg::CB;
+  constexpr int WA = Cfg::WA, WB = Cfg::WB, CB = Cfg::CB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   double* Xs = reinterpret_cast<double*>(smem_raw);
   double* Ys = Xs + NBUF * Cfg::X_DBL;
   double* Slots = Ys + NYS * Cfg::Y_DBL;
+  uint64_t* yfull = reinterpret_cast<uint64_t*>(Slots + WB * Cfg::SLOT_DBL);  // hand-offs, one arrival per warp
+  uint64_t* yfree = yfull + NYS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K1 = p.K1, N1 = p.N1, K2 = p.K2, N2 = p.N2;
   const int64_t C = p.C;
@@ -357,6 +374,13 @@ __global__ void __launch_bounds__(Spair1Cfg<P4, NF>::THREADS, 1) spair1_kernel(c
   for (int b = 0; b < NYS; ++b)
     for (int e = threadIdx.x; e < CB * NP * RX; e += blockDim.x)
       if (e % RX >= K2) Ys[b * Cfg::Y_DBL + e] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NYS; ++b) {
+      mbar_init(&yfull[b], WA);
+      mbar_init(&yfree[b], WB);
+    }
+    fence_barrier_init();
+  }
   __syncthreads();
   pdl_launch_dependents();
   pdl_wait();
@@ -418,7 +442,7 @@ __global__ void __launch_bounds__(Spair1Cfg<P4, NF>::THREADS, 1) spair1_kernel(c
       named_barrier_sync(1, WA * 32);
       if (z + NBUF - 1 < nz) issue(z + NBUF - 1);
       cp_async_commit();
-      if (z >= NYS) named_barrier_sync(2 + NYS + yb, PAIR);
+      if (z >= NYS) mbar_wait(&yfree[yb], static_cast<uint32_t>((z / NYS - 1) & 1));
       const double* X = Xs + buf * Cfg::X_DBL;
       double* Y = Ys + yb * Cfg::Y_DBL;
       for (int f0 = wa; f0 < nfr; f0 += 2 * WA) {  // two column fragments: independent chains
@@ -457,7 +481,8 @@ __global__ void __launch_bounds__(Spair1Cfg<P4, NF>::THREADS, 1) spair1_kernel(c
           }
         }
       }
-      named_barrier_arrive(2 + yb, PAIR);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&yfull[yb]);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     return;
@@ -477,7 +502,7 @@ __global__ void __launch_bounds__(Spair1Cfg<P4, NF>::THREADS, 1) spair1_kernel(c
   int64_t z = 0;
   for (int64_t st = blockIdx.x; st < nstage; st += gridDim.x, ++z) {
     const int yb = static_cast<int>(z % NYS);
-    named_barrier_sync(2 + yb, PAIR);
+    mbar_wait(&yfull[yb], static_cast<uint32_t>((z / NYS) & 1));
     const double* Y = Ys + yb * Cfg::Y_DBL + warp * NP * RX;  // this warp's slab
     double acc[NF][NF][2];  // [i1 fragment][i2 fragment]
 #pragma unroll
@@ -492,7 +517,11 @@ __global__ void __launch_bounds__(Spair1Cfg<P4, NF>::THREADS, 1) spair1_kernel(c
 #pragma unroll
         for (int nf = 0; nf < NF; ++nf) dmma_8x8x4(acc[f][nf][0], acc[f][nf][1], l2[nf][s], yf);
       }
-    if (z + NYS < nz) named_barrier_arrive_after_reads(2 + NYS + yb, PAIR);
+    if (z + NYS < nz) {
+      asm volatile("fence.acq_rel.cta;\n" ::: "memory");  // this thread's Y loads are complete
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&yfree[yb]);
+    }
     // D(i2 = 8nf + g, i1 = 8f + 2t, +1) -> slot[i2][i1], then the contiguous slab
 #pragma unroll
     for (int f = 0; f < NF; ++f)
