@@ -75,7 +75,9 @@ int64_t mumode_launch_count(mumode_handle_t h);
  * (fused_pair_kernel / tail_pair_kernel instead of fused_ws / tail_ws),
  * 13 = auto without the small-extent (skinny) mode-product kernel,
  * 14 = auto without the small-extent fused two-mode passes (spair.cuh),
- * 15 = auto with the small-extent fused passes wherever eligible.
+ * 15 = auto with the small-extent fused passes wherever eligible,
+ * 16 = auto with the in-place block passes (block.cuh) wherever eligible,
+ * 17 = auto without the in-place block passes.
  * Not a fallback switch: all are CUDA kernels. */
 int mumode_set_kernel_policy(mumode_handle_t h, int policy);
 

@@ -131,7 +131,7 @@ static int launch_fused_mu(mumode_handle_s* h, bool first, const double* T, doub
 static int fused_extent(int d, const int64_t* m, const int64_t* n, bool cplx, bool adjoint,
                         int policy, int mu_lo, int mu_hi, const double* T, const double* S,
                         const double* const* L) {
-  if (cplx || adjoint || !(policy == 0 || policy == 7 || policy == 9 || policy == 10 || policy == 12 || policy == 13) || mu_hi - mu_lo < 1)
+  if (cplx || adjoint || !(policy == 0 || policy == 7 || policy == 9 || policy == 10 || policy == 12 || policy == 13 || policy == 17) || mu_hi - mu_lo < 1)
     return 0;
   const int64_t MU = m[0];
   if (MU != 8 && MU != 16 && MU != 24 && MU != 32) return 0;
@@ -158,7 +158,8 @@ static int fused_extent(int d, const int64_t* m, const int64_t* n, bool cplx, bo
 // 18^6 0.68 -> 0.64 ms; tools/small_pairs_sweep.py); 15 forces them wherever
 // eligible (tests), 14 disables them.
 static bool spair_policy(int policy) {
-  return policy == 0 || policy == 7 || policy == 9 || policy == 10 || policy == 12 || policy == 15;
+  return policy == 0 || policy == 7 || policy == 9 || policy == 10 || policy == 12 || policy == 15 || policy == 16 ||
+         policy == 17;
 }
 
 template <int P4, int NF>
@@ -230,6 +231,166 @@ static bool spair_chain_ok(mumode_handle_s* h, int d, const int64_t* m, const in
   for (int k = mu_lo - 1; k < mu_hi; ++k)
     if (m[k] > 24 || n[k] > 24 || !L[k]) return false;
   return std::min(prod(m, 0, d), prod(n, 0, d)) >= (int64_t(1) << 20);
+}
+
+// ------------------------------------------------------------------ block passes
+// In-place block passes (block.cuh): modes (mu .. mu+KM-1), all square with
+// extents <= 24, of a view (A, e_1..e_KM, C). R = 1 for mu = 1 (cubes of
+// CB consecutive c's), else R = 32 a's per block. The plan (layout search,
+// row tables, copy segments) is built once per shape and cached on the handle.
+static int block_plan(mumode_handle_s* h, int64_t A, const int* e, int KM, int64_t C, BlockPlan** out) {
+  *out = nullptr;
+  if (A > 1 && (A & 1)) return MUMODE_OK;
+  int emax = 0;
+  int64_t E = 1;
+  for (int j = 0; j < KM; ++j) {
+    if (e[j] < 2 || e[j] > 24) return MUMODE_OK;
+    emax = std::max(emax, e[j]);
+    E *= e[j];
+  }
+  if (A == 1 && (e[0] & 1)) return MUMODE_OK;
+  const std::vector<int64_t> key{A, C, KM, e[0], KM > 1 ? e[1] : 0, KM > 2 ? e[2] : 0};
+  auto it = h->blocks.find(key);
+  if (it != h->blocks.end()) {
+    *out = it->second.get();  // null: not eligible (cached)
+    return MUMODE_OK;
+  }
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  MM_CUDA(cudaStreamIsCapturing(h->stream, &cap));
+  if (cap != cudaStreamCaptureStatusNone) return MUMODE_OK;  // plans are built outside graph capture
+  const int P4 = (emax + 3) / 4 * 4, NF = (emax + 7) / 8;
+  auto plan = std::make_unique<BlockPlan>();
+  plan->P4 = P4 <= 8 ? 8 : (P4 <= 12 ? 12 : (P4 <= 16 ? 16 : (P4 <= 20 ? 20 : 24)));
+  plan->NF = NF;
+  const int ls_bytes = KM * (8 * NF) * plan->P4 * 8;
+  // R > 1: the widest row (32 a's = 256 B, the DRAM-friendly width) whose
+  // padded slot still gives a conflict-free layout; R = 1: CB whole cubes
+  BlockLayout lay;
+  bool ok = false;
+  int CB = 1;
+  if (A == 1) CB = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(C, 49152 / (E * 8))));
+  const int rcand[3] = {32, 28, 24};
+  for (int ri = 0; ri < (A == 1 ? 1 : 3) && !ok; ++ri) {
+    const int R = (A == 1) ? 1 : rcand[ri];
+    int64_t rows = 0;  // table bound: rows of every mode, padded to m-tiles
+    for (int j = 0; j < KM; ++j) rows += (R * CB * E / e[j] + 15) / 8 * 8;
+    const int fixed = ls_bytes + static_cast<int>(rows) * 2 + 3 * BLK_MAX_NB * 8 + 256;
+    const int budget = 227 * 1024 - fixed;
+    for (int nbmin = 3; nbmin >= 2 && !ok; --nbmin) {
+      ok = blk_plan_layout(A, e, KM, R, CB, budget / nbmin / 8, lay);
+      if (ok && R > 1 && ri < 2) {  // accept a narrower row only to avoid bank conflicts
+        int64_t ideal = 0;
+        for (int j = 0; j < KM; ++j) ideal += int64_t(lay.mt[j]) * 2 * ((e[j] + 3) / 4 + 2 * ((e[j] + 7) / 8));
+        if (lay.cost > ideal * 3 / 2) ok = false;
+      }
+    }
+  }
+  const int budget = 227 * 1024 - (ls_bytes + static_cast<int>(lay.tab.size()) * 2 + 3 * BLK_MAX_NB * 8 + 256);
+  const int R = lay.R;
+  if (ok) {
+    const int slot_bytes = lay.slot_dbl * 8;
+    plan->NB = std::min(BLK_MAX_NB, budget / slot_bytes);
+    // groups per CTA (tools/block_sweep.py, _cube_runs): 18^3 cubes 226 -> 212 us
+    // with 4 groups of 4 warps (NB 4), 20^3 352 us with 2 groups (NB 3; 4: 367)
+    plan->G = plan->NB >= 4 ? 4 : (plan->NB >= 2 ? 2 : 1);
+    if (const char* g = getenv("MUMODE_BLOCK_G")) plan->G = std::max(1, std::min(4, atoi(g)));
+    if (const char* nb = getenv("MUMODE_BLOCK_NB")) plan->NB = std::max(2, std::min(plan->NB, atoi(nb)));
+    if (plan->G == 3) plan->G = 2;  // 16 warps split in 1, 2 or 4 groups
+    plan->ls_off = plan->NB * slot_bytes;
+    plan->tab_soff = plan->ls_off + ls_bytes;
+    plan->bar_off = (plan->tab_soff + static_cast<int>(lay.tab.size()) * 2 + 15) / 16 * 16;
+    plan->smem = plan->bar_off + 3 * BLK_MAX_NB * 8;  // full, done, tags
+    plan->nblocks = (R > 1) ? ((A + R - 1) / R) * C : (C + CB - 1) / CB;
+    MM_TRY(plan->tab.ensure(lay.tab.size() * sizeof(uint16_t)));
+    MM_TRY(plan->seg.ensure(lay.seg.size() * sizeof(BlkSeg)));
+    MM_CUDA(cudaMemcpy(plan->tab.p, lay.tab.data(), lay.tab.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    MM_CUDA(cudaMemcpy(plan->seg.p, lay.seg.data(), lay.seg.size() * sizeof(BlkSeg), cudaMemcpyHostToDevice));
+    if (getenv("MUMODE_BLOCK_DEBUG")) {
+      int64_t ideal = 0;
+      for (int j = 0; j < KM; ++j) ideal += int64_t(lay.mt[j]) * 2 * ((e[j] + 3) / 4 + 2 * ((e[j] + 7) / 8));
+      fprintf(stderr, "mumode block plan: A=%lld e=(%d,%d,%d) C=%lld R=%d CB=%d slot=%d dbl NB=%d G=%d s=(%d,%d,%d) "
+              "mt=(%d,%d,%d) segs=%zu cost=%lld ideal=%lld smem=%d\n",
+              (long long)A, e[0], KM > 1 ? e[1] : 0, KM > 2 ? e[2] : 0, (long long)C, R, CB, lay.slot_dbl, plan->NB,
+              plan->G, lay.s[0], lay.s[1], lay.s[2], lay.mt[0], lay.mt[1], lay.mt[2], lay.seg.size(),
+              (long long)lay.cost, (long long)ideal, plan->smem);
+    }
+    plan->lay = std::move(lay);
+    *out = plan.get();
+    h->blocks[key] = std::move(plan);
+  } else {
+    h->blocks[key] = nullptr;
+  }
+  return MUMODE_OK;
+}
+
+template <int P4, int NF>
+static int launch_block_p(mumode_handle_s* h, const BlockParams& p, int smem) {
+  auto k = block_kernel<P4, NF>;
+  MM_TRY(smem_opt_in(k, smem));
+  const int grid = static_cast<int>(std::min<int64_t>(p.nblocks, persistent_sms(h)));
+  MM_TRY(launch_pdl(k, grid, BLK_THREADS, smem, h->stream, p));
+  MM_CUDA(cudaGetLastError());
+  h->launches++;
+  return MUMODE_OK;
+}
+
+static int launch_block(mumode_handle_s* h, BlockPlan* bp, const double* T, double* S, const double* const* Lm,
+                        int64_t A, int64_t C) {
+  const BlockLayout& lay = bp->lay;
+  BlockParams p{};
+  p.X = T;
+  p.S = S;
+  p.tab = static_cast<const uint16_t*>(bp->tab.p);
+  p.seg = static_cast<const BlkSeg*>(bp->seg.p);
+  p.A = A;
+  p.C = C;
+  p.E = 1;
+  for (int j = 0; j < lay.KM; ++j) {
+    p.L[j] = Lm[j];
+    p.e[j] = lay.e[j];
+    p.s[j] = lay.s[j];
+    p.mt[j] = lay.mt[j];
+    p.tab_off[j] = lay.tab_off[j];
+    p.E *= lay.e[j];
+  }
+  p.nblocks = bp->nblocks;
+  p.R = lay.R;
+  p.CB = lay.CB;
+  p.KM = lay.KM;
+  p.NB = bp->NB;
+  p.G = bp->G;
+  p.ntab = static_cast<int>(lay.tab.size());
+  p.nseg = static_cast<int>(lay.seg.size());
+  p.slot_dbl = lay.slot_dbl;
+  p.ls_off = bp->ls_off;
+  p.tab_soff = bp->tab_soff;
+  p.bar_off = bp->bar_off;
+  switch (bp->P4 * 4 + bp->NF) {
+    case 8 * 4 + 1: return launch_block_p<8, 1>(h, p, bp->smem);
+    case 12 * 4 + 2: return launch_block_p<12, 2>(h, p, bp->smem);
+    case 16 * 4 + 2: return launch_block_p<16, 2>(h, p, bp->smem);
+    case 20 * 4 + 3: return launch_block_p<20, 3>(h, p, bp->smem);
+    case 24 * 4 + 3: return launch_block_p<24, 3>(h, p, bp->smem);
+    default: return fail(MUMODE_ERR_ARGUMENT, "block pass: unsupported extent class");
+  }
+}
+
+// Block passes for a chain: every mode square, <= 24, real, forward. Auto
+// (policy 0) uses them where measured faster; 16 forces, 17 disables.
+static bool block_policy(int policy) { return policy == 0 || policy == 16; }
+
+static bool block_chain_ok(mumode_handle_s* h, int d, const int64_t* m, const int64_t* n, bool cplx, bool adjoint,
+                           int mu_lo, int mu_hi, const double* T, const double* S, const double* const* L) {
+  if (cplx || adjoint || !block_policy(h->policy) || mu_hi - mu_lo < 1) return false;
+  if (!aligned16_ptr(T) || !aligned16_ptr(S)) return false;
+  for (int k = mu_lo - 1; k < mu_hi; ++k)
+    if (m[k] != n[k] || m[k] > 24 || !L[k]) return false;
+  if (h->policy == 16) return true;
+  // auto: cube passes (modes 1-3 in place) beat two skinny / pair passes for
+  // the paper's d = 6 sizes (18^6 0.650 -> 0.546 ms, 20^6 1.000 -> 0.863,
+  // 14^6 128 -> 112 us, 12^6 64 -> 57 us); extents that are multiples of 8
+  // take the MU kernels before this point
+  return d - mu_lo + 1 >= 4 && mu_lo == 1 && std::min(prod(m, 0, d), prod(n, 0, d)) >= (int64_t(1) << 20);
 }
 
 // One mode product on device buffers: T with extents m (d modes), op(L)
@@ -569,6 +730,42 @@ static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t
       eigsum_divide_kernel<<<dim3(gx, gy), 256, 0, h->stream>>>(S, div_front, div_last, A, N);
       MM_CUDA(cudaGetLastError());
       h->launches++;
+    }
+    return MUMODE_OK;
+  }
+  if (!div_front && block_chain_ok(h, d, m, n, cplx, adjoint, mu_lo, mu_hi, T, S, L)) {
+    // groups of up to three modes as in-place block passes where a plan
+    // exists (largest group first), single products (skinny kernels) otherwise
+    int pass = 0, mu = mu_lo;
+    while (mu <= mu_hi) {
+      const int64_t A = prod(ext.data(), 0, mu - 1);
+      BlockPlan* bp = nullptr;
+      int km = std::min(3, mu_hi - mu + 1);
+      // R > 1 blocks (a pair with 256-B rows is 86 KB at 18^2) leave room for
+      // only two slots: too little data in flight (measured 553-687 us per
+      // 18^6 pair pass vs 216 us for spair); only cubes (mu = 1) by default
+      const bool wide_ok = getenv("MUMODE_BLOCK_WIDE") != nullptr;
+      for (; km >= 2 && (A == 1 || wide_ok); --km) {
+        int e3[3] = {0, 0, 0};
+        for (int j = 0; j < km; ++j) e3[j] = static_cast<int>(ext[mu - 1 + j]);
+        MM_TRY(block_plan(h, A, e3, km, prod(ext.data(), mu - 1 + km, d), &bp));
+        // auto: only plans with >= 3 slots (22^3 cubes fit 2: 22^5 0.099 -> 0.104 ms)
+        if (bp && h->policy == 0 && bp->NB < 3) bp = nullptr;
+        if (bp) break;
+      }
+      const bool pair = !bp && mu < mu_hi && spair_size(ext.data(), n, d, mu, false) != 0;
+      const int step = bp ? km : (pair ? 2 : 1);
+      double* dst = (mu + step - 1 == mu_hi) ? S : static_cast<double*>(h->ws[pass % 2].p);
+      if (bp) {
+        MM_TRY(launch_block(h, bp, src, dst, L + (mu - 1), A, prod(ext.data(), mu - 1 + km, d)));
+      } else if (pair) {
+        MM_TRY(launch_spair(h, ext.data(), n, d, mu, src, L[mu - 1], L[mu], dst));
+      } else {
+        MM_TRY(mode_product_dev(h, d, ext.data(), mu, n[mu - 1], src, L[mu - 1], 1, n[mu - 1], false, false, dst));
+      }
+      src = dst;
+      mu += step;
+      ++pass;
     }
     return MUMODE_OK;
   }

@@ -331,7 +331,7 @@ static bool ldg_worthwhile(const ModeJob& j) {
 static bool skinny_ok(const mumode_handle_s* h, const ModeJob& j) {
   if (j.cplx || j.conj || j.scat || j.div_front || (j.accumulate && j.A == 1)) return false;
   if (!(h->policy == 0 || h->policy == 7 || h->policy == 9 || h->policy == 10 || h->policy == 12 || h->policy == 14 ||
-        h->policy == 15))
+        h->policy == 15 || h->policy == 16 || h->policy == 17))
     return false;
   if (j.K > 32 || j.N > 32 || !aligned16(j.T) || !aligned16(j.S)) return false;
   if (j.A == 1) {

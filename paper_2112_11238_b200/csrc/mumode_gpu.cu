@@ -33,6 +33,7 @@
 #include "ldg_dmma.cuh"
 #include "lu_solve.cuh"
 #include "spair.cuh"
+#include "block.cuh"
 
 namespace mumode_gpu {
 
@@ -106,6 +107,16 @@ struct ChainPlan {
   std::vector<int64_t> target_off, sigoff_off, sigidx_off, ctr_off;  // per mode, in ints
 };
 
+// In-place block pass (block.cuh) for one shape: the host layout and its
+// device copies (row tables, copy segments), never reallocated.
+struct BlockPlan {
+  BlockLayout lay;
+  DevBuf tab, seg;
+  int NB = 0, G = 1, smem = 0, P4 = 0, NF = 0;
+  int ls_off = 0, tab_soff = 0, bar_off = 0;
+  int64_t nblocks = 0;
+};
+
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
   int64_t nodes = 0;
@@ -166,6 +177,7 @@ struct mumode_handle_s {
   std::unordered_map<mumode_gpu::MapKey, CUtensorMap, mumode_gpu::MapKeyHash> maps;
   std::map<std::vector<uint64_t>, mumode_gpu::GraphEntry> graphs;
   std::map<std::vector<int64_t>, std::unique_ptr<mumode_gpu::ChainPlan>> chains;  // per shape + configs
+  std::map<std::vector<int64_t>, std::unique_ptr<mumode_gpu::BlockPlan>> blocks;  // per block-pass shape
 };
 
 namespace mumode_gpu {
@@ -487,7 +499,7 @@ void* mumode_get_stream(mumode_handle_t h) { return h ? static_cast<void*>(h->st
 int64_t mumode_launch_count(mumode_handle_t h) { return h ? h->launches : -1; }
 
 int mumode_set_kernel_policy(mumode_handle_t h, int policy) {
-  if (!h || policy < 0 || policy > 15) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
+  if (!h || policy < 0 || policy > 17) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
   // 3..6 force real tile configuration 0..3 / complex configuration 0..3
   h->policy = policy;
   return MUMODE_OK;

@@ -389,6 +389,55 @@ def test_skinny_mode_products(shape):
     assert O.rel_fro(host(mm.tucker(Td, [dev(L) for L in Ls])), O.port_tucker(T, Ls)) < 1e-13
 
 
+@pytest.mark.parametrize("shape", [(18,) * 6, (20,) * 5, (12,) * 6, (14,) * 6, (18, 14, 16, 10, 12, 22), (16,) * 5,
+                                   (22, 20, 18, 6), (12, 12, 12, 7, 5), (24, 12, 20, 12), (8,) * 7])
+def test_block_passes_equal_per_mode_kernels(shape):
+    # in-place block passes (block.cuh, policy 16: cubes of modes 1-3, and
+    # 256-B-row blocks of later modes when MUMODE_BLOCK_WIDE is set) keep every
+    # output's k-ordered DMMA chain: bitwise equal to one skinny pass per mode
+    # (policy 14), and to the oracle; partial last blocks (C not a multiple of
+    # the cubes per slot, A not a multiple of 32) included
+    rng = np.random.default_rng(sum(shape) * 7 + len(shape))
+    T = rnd(rng, shape)
+    Ls = [rnd(rng, (e, e)) for e in shape]
+    Td, Ld = dev(T), [dev(L) for L in Ls]
+    h = mm.get_handle(0)
+    try:
+        h.set_kernel_policy(14)
+        per_mode = mm.tucker(Td, Ld)
+        h.set_kernel_policy(16)
+        launches = h.launches
+        blk = mm.tucker(Td, Ld)
+        assert h.launches - launches < len(shape)  # at least one multi-mode pass
+        for _ in range(3):
+            assert torch.equal(mm.tucker(Td, Ld), blk)
+    finally:
+        h.set_kernel_policy(0)
+    assert torch.equal(blk, per_mode)
+    assert O.rel_fro(host(blk), O.port_tucker(T, Ls)) < 1e-14
+    I = [dev(np.eye(e)) for e in shape]
+    h.set_kernel_policy(16)
+    try:
+        np.testing.assert_array_equal(host(mm.tucker(Td, I)), T)
+    finally:
+        h.set_kernel_policy(0)
+
+
+@pytest.mark.parametrize("shape", [(18,) * 6, (20,) * 6])
+def test_block_passes_paper_sizes_vs_reference(shape):
+    # the paper's d = 6 sizes through the auto path (cube pass + pairs /
+    # skinny) against the reference library on the same bytes
+    if not O.ref_available():
+        pytest.skip("reference library not built")
+    torch.manual_seed(shape[0])
+    T = mm.colmajor_empty(shape, torch.float64, "cuda").normal_()
+    Ls = [mm.to_colmajor(torch.randn(e, e, dtype=torch.float64, device="cuda")) for e in shape]
+    S = host(mm.tucker(T, Ls))
+    want = O.ref_tucker(host(T), [host(L) for L in Ls])
+    assert O.rel_fro(S, want) < 1e-13
+    np.testing.assert_array_equal(S, want)
+
+
 @pytest.mark.parametrize("policy_id", [0, 3, 4, 5, 6])
 def test_repeated_products_are_bitwise_identical(policy_id):
     # regression guard for stage-release races (a consumer warp releasing a

@@ -6,6 +6,7 @@ a few warm-up applications, then one more; nothing is timed here.
   c4        complex 128^3 -> 192^3 (configs[3])
   c5        6-D 24^6 (configs[4])
   d6 N      6-D N^6 (the paper's d = 6 sizes, e.g. 18, 20)
+  --policy P  run under kernel policy P (e.g. 16: in-place block passes)
   kronsumv  Kronecker-sum action at 24^6 and 200^3
   itucker   inverse Tucker 200^3
 """
@@ -36,6 +37,10 @@ def run(fn, reps=3):
 
 
 def main():
+    if "--policy" in sys.argv:  # kernel policy for the run (mumode_set_kernel_policy)
+        i = sys.argv.index("--policy")
+        mm.get_handle(0).set_kernel_policy(int(sys.argv[i + 1]))
+        del sys.argv[i:i + 2]
     what = sys.argv[1]
     if what == "c2":
         T, Ls = normal((256,) * 3), mats((256,) * 3, (256,) * 3)
