@@ -135,39 +135,49 @@ __global__ void __launch_bounds__(BLK_THREADS, 1) block_kernel(const BlockParams
     // cp.async.mbarrier.arrive.noinc), 16-byte LDS + STG out. Row-by-row
     // bulk copies measured 4x slower here (one TMA request per 256-B row).
     const int ct = threadIdx.x - BLK_WARPS * 32;  // 0..127
-    const int cpr = p.R >> 1;                      // chunks per row
+    const int cpr = p.R >> 1;                      // chunks per row (divides 128: R in {2, 4, .., 32})
+    const int q = ct % cpr, rstep = (BLK_CWARPS * 32) / cpr;
     const int64_t nab = (p.A + p.R - 1) / p.R;
-    const int64_t total = p.E * cpr;
+    const int E = static_cast<int>(p.E);
     const int e0 = p.e[0], e1 = p.KM > 1 ? p.e[1] : 1;
     const int s0 = p.s[0], s1 = p.s[1], s2 = p.s[2];
-    auto slot_off = [&](int64_t rho) {
-      const int i0 = static_cast<int>(rho % e0);
-      const int64_t r1 = rho / e0;
-      const int i1 = static_cast<int>(r1 % e1);
-      const int i2 = static_cast<int>(r1 / e1);
-      return i0 * s0 + i1 * s1 + i2 * s2;
-    };
     auto locate = [&](int64_t i, int64_t& origin, int& w) {
       const int64_t blk = blockIdx.x + i * gridDim.x;
       const int64_t c = blk / nab, a0 = (blk - c * nab) * p.R;
       origin = a0 + p.A * p.E * c;
       w = static_cast<int>(p.R < p.A - a0 ? int64_t(p.R) : p.A - a0);
     };
+    // rows rho = ct / cpr + k * rstep, walked incrementally (no divisions in
+    // the loop: 64-bit index math per chunk made these warps the bottleneck)
+    auto for_rows = [&](auto&& body) {
+      int rho = ct / cpr;
+      int i0 = rho % e0, r1 = rho / e0;
+      int i1 = r1 % e1, i2 = r1 / e1;
+      for (; rho < E; rho += rstep) {
+        body(rho, i0 * s0 + i1 * s1 + i2 * s2);
+        i0 += rstep;
+        while (i0 >= e0) {
+          i0 -= e0;
+          if (++i1 == e1) {
+            i1 = 0;
+            ++i2;
+          }
+        }
+      }
+    };
     auto load = [&](int64_t i) {
       const int slot = slot_of(i);
       int64_t origin;
       int w;
       locate(i, origin, w);
-      double* base = slots + static_cast<int64_t>(slot) * p.slot_dbl;
+      double* base = slots + static_cast<int64_t>(slot) * p.slot_dbl + 2 * q;
+      const double* src = p.X + origin + 2 * q;
       if (ct == 0) tag[slot] = i;
-      for (int64_t c = ct; c < total; c += BLK_CWARPS * 32) {
-        const int64_t rho = c / cpr;
-        const int q = static_cast<int>(c - rho * cpr);
-        if (2 * q < w)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(base + slot_off(rho) + 2 * q)),
-                       "l"(p.X + origin + p.A * rho + 2 * q)
+      if (2 * q < w)
+        for_rows([&](int rho, int soff) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(base + soff)), "l"(src + p.A * rho)
                        : "memory");
-      }
+        });
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[slot])) : "memory");
     };
     auto store = [&](int64_t i) {
@@ -175,26 +185,47 @@ __global__ void __launch_bounds__(BLK_THREADS, 1) block_kernel(const BlockParams
       int64_t origin;
       int w;
       locate(i, origin, w);
-      const double* base = slots + static_cast<int64_t>(slot) * p.slot_dbl;
-      for (int64_t c = ct; c < total; c += BLK_CWARPS * 32) {
-        const int64_t rho = c / cpr;
-        const int q = static_cast<int>(c - rho * cpr);
-        if (2 * q < w) {
-          const double2 v = *reinterpret_cast<const double2*>(base + slot_off(rho) + 2 * q);
-          stg_f64x2(p.S + origin + p.A * rho + 2 * q, v.x, v.y);
-        }
-      }
+      const double* base = slots + static_cast<int64_t>(slot) * p.slot_dbl + 2 * q;
+      double* dst = p.S + origin + 2 * q;
+      if (2 * q < w)
+        for_rows([&](int rho, int soff) {
+          const double2 v = *reinterpret_cast<const double2*>(base + soff);
+          stg_f64x2(dst + p.A * rho, v.x, v.y);
+        });
     };
     const int64_t pre = int64_t(NB) < n ? int64_t(NB) : n;
     for (int64_t i = 0; i < pre; ++i) load(i);
+    // store block i and load block i + NB into the same slot in one walk:
+    // every thread loads exactly the 16-byte chunks it stored, right after
+    // storing each (its LDS has returned before the STG issues), so no
+    // barrier separates the two streams
+    auto store_load = [&](int64_t i, int64_t i2) {
+      const int slot = slot_of(i);
+      int64_t o1, o2;
+      int w1, w2;
+      locate(i, o1, w1);
+      locate(i2, o2, w2);
+      double* base = slots + static_cast<int64_t>(slot) * p.slot_dbl + 2 * q;
+      double* dst = p.S + o1 + 2 * q;
+      const double* src = p.X + o2 + 2 * q;
+      const bool st = 2 * q < w1, ld = 2 * q < w2;
+      if (ct == 0) tag[slot] = i2;
+      for_rows([&](int rho, int soff) {
+        if (st) {
+          const double2 v = *reinterpret_cast<const double2*>(base + soff);
+          stg_f64x2(dst + p.A * rho, v.x, v.y);
+        }
+        if (ld)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(base + soff)), "l"(src + p.A * rho)
+                       : "memory");
+      });
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[slot])) : "memory");
+    };
     for (int64_t i = 0; i < n; ++i) {
       const int slot = slot_of(i);
       mbar_wait(&done[slot], static_cast<uint32_t>((i / NB) & 1));
-      store(i);
-      if (i + NB < n) {
-        named_barrier_sync(5, BLK_CWARPS * 32);  // every copy thread has read the slot
-        load(i + NB);
-      }
+      if (i + NB < n) store_load(i, i + NB);
+      else store(i);
     }
     return;
   }

@@ -269,7 +269,8 @@ static int block_plan(mumode_handle_s* h, int64_t A, const int* e, int KM, int64
   bool ok = false;
   int CB = 1;
   if (A == 1) CB = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(C, 49152 / (E * 8))));
-  const int rcand[3] = {32, 28, 24};
+  int rcand[3] = {32, 16, 8};  // chunks per row must divide the 128 copy threads
+  if (const char* r = getenv("MUMODE_BLOCK_R")) rcand[0] = rcand[1] = rcand[2] = std::max(2, atoi(r) / 2 * 2);
   for (int ri = 0; ri < (A == 1 ? 1 : 3) && !ok; ++ri) {
     const int R = (A == 1) ? 1 : rcand[ri];
     int64_t rows = 0;  // table bound: rows of every mode, padded to m-tiles
@@ -741,16 +742,20 @@ static int tucker_dev(mumode_handle_s* h, int d, const int64_t* m, const int64_t
       const int64_t A = prod(ext.data(), 0, mu - 1);
       BlockPlan* bp = nullptr;
       int km = std::min(3, mu_hi - mu + 1);
-      // R > 1 blocks (a pair with 256-B rows is 86 KB at 18^2) leave room for
-      // only two slots: too little data in flight (measured 553-687 us per
-      // 18^6 pair pass vs 216 us for spair); only cubes (mu = 1) by default
-      const bool wide_ok = getenv("MUMODE_BLOCK_WIDE") != nullptr;
-      for (; km >= 2 && (A == 1 || wide_ok); --km) {
+      // mu = 1: cubes of modes 1-3; mu > 1: blocks of 32 a's (256-B rows) x
+      // the modes (an 18^2 pair is 86 KB: two slots, fed by the copy warps'
+      // fused store/load walk). Auto takes cubes with >= 3 slots (22^3 fits
+      // two: 22^5 0.099 -> 0.104 ms) and 32-a pairs where the spair kernel
+      // would run (largest extent 17..20: 18^6 modes 4-5 185 vs 213 us, 20^6
+      // 319 vs 332 us; at 12^6 / 14^6 two skinny passes are faster)
+      const bool force = h->policy == 16;
+      const bool spair_here = mu < mu_hi && spair_size(ext.data(), n, d, mu, false) != 0;
+      for (; km >= 2; --km) {
+        if (!force && (A == 1 ? km != 3 : (km != 2 || !spair_here))) continue;
         int e3[3] = {0, 0, 0};
         for (int j = 0; j < km; ++j) e3[j] = static_cast<int>(ext[mu - 1 + j]);
         MM_TRY(block_plan(h, A, e3, km, prod(ext.data(), mu - 1 + km, d), &bp));
-        // auto: only plans with >= 3 slots (22^3 cubes fit 2: 22^5 0.099 -> 0.104 ms)
-        if (bp && h->policy == 0 && bp->NB < 3) bp = nullptr;
+        if (bp && !force && A == 1 && bp->NB < 3) bp = nullptr;
         if (bp) break;
       }
       const bool pair = !bp && mu < mu_hi && spair_size(ext.data(), n, d, mu, false) != 0;

@@ -392,8 +392,8 @@ def test_skinny_mode_products(shape):
 @pytest.mark.parametrize("shape", [(18,) * 6, (20,) * 5, (12,) * 6, (14,) * 6, (18, 14, 16, 10, 12, 22), (16,) * 5,
                                    (22, 20, 18, 6), (12, 12, 12, 7, 5), (24, 12, 20, 12), (8,) * 7])
 def test_block_passes_equal_per_mode_kernels(shape):
-    # in-place block passes (block.cuh, policy 16: cubes of modes 1-3, and
-    # 256-B-row blocks of later modes when MUMODE_BLOCK_WIDE is set) keep every
+    # in-place block passes (block.cuh, policy 16: cubes of modes 1-3 and
+    # 32-a (256-B row) blocks of later modes, copy warps) keep every
     # output's k-ordered DMMA chain: bitwise equal to one skinny pass per mode
     # (policy 14), and to the oracle; partial last blocks (C not a multiple of
     # the cubes per slot, A not a multiple of 32) included

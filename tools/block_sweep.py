@@ -21,7 +21,7 @@ for m in shapes:
     T = mm.colmajor_empty(m, torch.float64, 'cuda').normal_()
     Ls = [mm.to_colmajor(torch.randn(e, e, dtype=torch.float64, device='cuda')) for e in m]
     res, outs = {}, {}
-    for pol in (14, 16, 0):
+    for pol in (14, 16, 17, 0):
         h.set_kernel_policy(pol)
         outs[pol] = mm.tucker(T, Ls).clone()
         for _ in range(3):
@@ -40,7 +40,7 @@ for m in shapes:
     h.set_kernel_policy(0)
     roof = max(flops(m) / 37.0e12, 16 * np.prod(m) / 6553.6e9) * 1e3
     print(json.dumps({"shape": "x".join(map(str, m)), "block_ms": round(res[16], 4), "per_mode_ms": round(res[14], 4),
-                      "auto_ms": round(res[0], 4), "roof_ms": round(roof, 4), "frac_block": round(roof / res[16], 3),
+                      "auto_ms": round(res[0], 4), "no_block_ms": round(res[17], 4), "roof_ms": round(roof, 4), "frac_block": round(roof / res[16], 3),
                       "frac_auto": round(roof / res[0], 3), "bitwise_block_vs_per_mode": bool(torch.equal(outs[16], outs[14])),
                       "max_abs_diff": float((outs[16] - outs[14]).abs().max())}), flush=True)
     del T
