@@ -699,6 +699,15 @@ def extras(mm, lib, h, dev, stream, peak, flush):
     L5 = [mm.to_colmajor(torch.randn(24, 24, dtype=torch.float64, device=dev)) for _ in range(6)]
     ms = timeit(lambda: mm.tucker(T5, L5), reps=3)
     rec("C5_6d_24", tucker_flops((24,) * 6, (24,) * 6), ms, 2 * 8 * 24 ** 6)
+    # the paper's own d = 6 sizes (n = 12..18) and 20^6:
+    # cube passes of modes 1-3 + 32-a pair / skinny passes (block.cuh,
+    # skinny.cuh); 16^6 takes the MU kernels (fused_ws / tail_ws)
+    for n6 in (12, 14, 16, 18, 20):
+        T6 = normal((n6,) * 6)
+        L6 = [mm.to_colmajor(torch.randn(n6, n6, dtype=torch.float64, device=dev)) for _ in range(6)]
+        ms = timeit(lambda: mm.tucker(T6, L6), reps=5)
+        rec(f"d6_{n6}", tucker_flops((n6,) * 6, (n6,) * 6), ms, 2 * 8 * n6 ** 6)
+        del T6
     # kronsumv (terms accumulated in the epilogues), itucker (per-mode
     # LU solves, 2 n^2 flop per fibre and mode) and the IMEX direct solve (two
     # Tuckers + divide) -- flops as the equivalent mode products, bytes compulsory
