@@ -8,6 +8,7 @@ from collections import defaultdict
 
 path, command = sys.argv[1], sys.argv[2]
 rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+rows = rows[next(i for i, r in enumerate(rows) if r[0] == "ID"):]  # skip the program's own output
 hdr = rows[0]
 ix = {h: i for i, h in enumerate(hdr)}
 tot = defaultdict(float)
