@@ -669,6 +669,15 @@ def extras(mm, lib, h, dev, stream, peak, flush):
     for mu in (1, 2, 3):
         ms = timeit(lambda: mm.mode_product(T, L, mu))
         rec(f"C2_mode{mu}", 2.0 * 256 * 256 ** 3, ms, 2 * 8 * 256 ** 3)
+    # the reference CLI's bench-tucker (tools/mumode_cli.cpp:219-255): the fused
+    # chain against tucker_sequential (standalone mode products, fresh
+    # intermediates), with the CLI's <= 1e-12 agreement check
+    L3 = [mm.to_colmajor(torch.randn(256, 256, dtype=torch.float64, device=dev)) for _ in range(3)]
+    ms = timeit(lambda: mm.tucker_sequential(T, L3))
+    rec("C2_tucker_sequential", tucker_flops((256,) * 3, (256,) * 3), ms, 2 * 8 * 256 ** 3)
+    fused, seq = mm.tucker(T, L3), mm.tucker_sequential(T, L3)
+    out["C2_tucker_sequential"]["fused_vs_sequential_rel_max"] = float(
+        ((fused - seq).abs().max() / fused.abs().max()).item())
     # C1 2-D
     T1 = normal((100, 100))
     L1 = [mm.to_colmajor(torch.randn(100, 100, dtype=torch.float64, device=dev)) for _ in range(2)]
