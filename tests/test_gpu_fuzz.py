@@ -61,3 +61,31 @@ def test_fuzz_tucker_and_mode_products(policy):
                 assert O.rel_max(Sm, O.port_mode_product(T, Ls[mu - 1], mu)) < 1e-13, (it, m, mu)
     finally:
         h.set_kernel_policy(0)
+
+
+def test_fuzz_block_passes_bitwise():
+    # in-place block passes (block.cuh) on random square small-extent chains:
+    # policy 16 forces cubes / 32-a blocks wherever a plan exists (mixed even
+    # and odd extents, partial last blocks, orders 4..6), bitwise against one
+    # skinny / tile pass per mode (policy 14) and against the oracle
+    rng = np.random.default_rng(9191)
+    h = mm.get_handle(0)
+    pool = [2, 3, 4, 6, 7, 8, 10, 12, 13, 14, 16, 18, 20, 22, 24]
+    try:
+        for it in range(24):
+            d = int(rng.integers(4, 7))
+            cap = {4: 24, 5: 16, 6: 10}[d]
+            m = [int(rng.choice([e for e in pool if e <= cap])) for _ in range(d)]
+            m[0] = m[0] + (m[0] & 1)  # cubes need an even leading extent
+            T = _rnd(rng, m, False)
+            Ls = [_rnd(rng, (e, e), False) for e in m]
+            dT = torch.from_numpy(T).cuda()
+            dL = [torch.from_numpy(L).cuda() for L in Ls]
+            h.set_kernel_policy(14)
+            per_mode = mm.tucker(dT, dL)
+            h.set_kernel_policy(16)
+            blk = mm.tucker(dT, dL)
+            assert torch.equal(blk, per_mode), (it, m)
+            assert O.rel_max(blk.cpu().numpy(), O.port_tucker(T, Ls)) < 1e-13, (it, m)
+    finally:
+        h.set_kernel_policy(0)
