@@ -291,7 +291,7 @@ static int block_plan(mumode_handle_s* h, int64_t A, const int* e, int KM, int64
   if (ok) {
     const int slot_bytes = lay.slot_dbl * 8;
     plan->NB = std::min(BLK_MAX_NB, budget / slot_bytes);
-    // groups per CTA (tools/block_sweep.py, _cube_runs): 18^3 cubes 226 -> 212 us
+    // groups per CTA (tools/block_sweep.py, tools/block_cfg_runs.sh): 18^3 cubes 226 -> 212 us
     // with 4 groups of 4 warps (NB 4), 20^3 352 us with 2 groups (NB 3; 4: 367)
     plan->G = plan->NB >= 4 ? 4 : (plan->NB >= 2 ? 2 : 1);
     if (const char* g = getenv("MUMODE_BLOCK_G")) plan->G = std::max(1, std::min(4, atoi(g)));
