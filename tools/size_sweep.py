@@ -8,7 +8,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_2112_11238_b200 as mm  # noqa: E402
-from odd_modes import timeit  # noqa: E402
+from timing import timeit  # noqa: E402
 
 h = mm.get_handle(0)
 sizes = [int(a) for a in sys.argv[1:]] or [96, 128, 160, 192, 200, 224, 240, 256, 272, 288, 320, 352, 384, 448, 512]
