@@ -9,9 +9,11 @@
 //   * R > 1 (mu > 1): a block is R consecutive a's (256-B rows for R = 32)
 //     times the e_1 x .. x e_KM modes, for one c.
 //
-// The block is copied into a shared-memory slot by 1-D bulk copies
+// A cube is copied into a shared-memory slot by 1-D bulk copies
 // (cp.async.bulk, one per contiguous global row; rows that are contiguous in
-// both places are merged, so an unpadded cube is ONE copy) into a PADDED
+// both places are merged, so an unpadded cube is ONE copy); a 32-a block by
+// four copy warps in 16-byte cp.async chunks (row-by-row bulk copies were 4x
+// slower there: one TMA request per 256-B row) -- both into a PADDED
 // layout chosen on the host for conflict-free fragment access. Mode j of the
 // block is a GEMM with M = the block's rows for that mode (every index
 // combination except i_j), N = n_j and K = m_j = n_j (square), so in place is
@@ -24,13 +26,16 @@
 // the true k's plus exact zero terms: bitwise the per-mode kernels' results.
 //
 //   warps 0..15 : G groups of 16/G warps; block i goes to group i % G, which
-//                 runs its modes separated by a group named barrier (two
+//                 runs its modes separated by a group named barrier (several
 //                 groups keep the DMMA pipe busy through each other's
 //                 barrier tails)
-//   warp 16     : producer: bulk loads into an NB-deep ring of slots
+//   warp 16     : cubes: producer -- bulk loads into an NB-deep ring of slots
 //                 (full[] mbarriers, complete_tx), bulk stores of finished
 //                 blocks (done[] mbarriers, one arrival per compute warp),
 //                 slot reuse after the store has read it
+//   warps 16..19: 32-a blocks: copy warps -- cp.async chunks in (arrivals
+//                 on full[] via cp.async.mbarrier.arrive.noinc), LDS + STG
+//                 out, storing block i and loading block i + NB in one walk
 #pragma once
 #include <algorithm>
 #include <cstdint>
