@@ -165,6 +165,9 @@ def run_reference(args, rank: int) -> None:
 
 
 # ----------------------------------------------------------------- our arm
+_JSON_OUT = None  # the real stdout when library output is diverted (distributed runs)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -202,6 +205,13 @@ def main():
 
     torch.cuda.set_device(local)
     if world > 1 or args.force_dist:
+        # rank 0's stdout carries exactly one JSON line: anything the
+        # libraries print during the run (NCCL's "NCCL version ..." banner)
+        # goes to stderr, the JSON line to the saved stdout
+        global _JSON_OUT
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29561")
@@ -540,7 +550,7 @@ def run_distributed(args, world, rank, local):
     }
     if extras:
         line["extras"] = extras
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=_JSON_OUT or sys.stdout, flush=True)
 
 
 def dist_c5(args, world, rank, dev, comm, stream, flush):
