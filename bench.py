@@ -320,14 +320,20 @@ def main():
         if rc:
             raise RuntimeError(lib.mumode_last_error().decode())
 
-    for _ in range(2):
+    for _ in range(args.steps):  # one untimed batch (see the async warm-up below)
         e2e_step()
     if world > 1:
         dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        e2e_step()
-    e2e_sync_s = time.perf_counter() - t0
+    # each e2e figure: the median of three batches of K applications (every
+    # batch moves all of its inputs and results; one batch of ~0.1 s was at
+    # the mercy of single host hiccups: 7.8-8.7 TFLOP/s across runs)
+    sync_batches = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        sync_batches.append(time.perf_counter() - t0)
+    e2e_sync_s = statistics.median(sync_batches)
     # the same K applications queued back to back through the async entry
     # point: step k's download overlaps step k+1's upload (every step still
     # moves its input H2D and its result D2H inside the timed region)
@@ -338,17 +344,23 @@ def main():
         if rc:
             raise RuntimeError(lib.mumode_last_error().decode())
 
-    for k in range(2):
-        e2e_async(k)
-    lib.mumode_host_wait(h.h)
+    # warm-up: two untimed batches (the first ~3 batches after an idle GPU run
+    # 3.1-3.3 ms per application, then 2.95 steadily: tools/e2e_chunks.py)
+    for _ in range(2):
+        for k in range(args.steps):
+            e2e_async(k)
+        lib.mumode_host_wait(h.h)
     if world > 1:
         dist.barrier()
-    t0 = time.perf_counter()
-    for k in range(args.steps):
-        e2e_async(k)
-    if lib.mumode_host_wait(h.h):
-        raise RuntimeError(lib.mumode_last_error().decode())
-    e2e_s = time.perf_counter() - t0
+    async_batches = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            e2e_async(k)
+        if lib.mumode_host_wait(h.h):
+            raise RuntimeError(lib.mumode_last_error().decode())
+        async_batches.append(time.perf_counter() - t0)
+    e2e_s = statistics.median(async_batches)
     if world > 1:
         t = torch.tensor([e2e_s, e2e_sync_s], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -393,7 +405,7 @@ def main():
                                          "note": "148 SM x 128 flop/clk x 1.965 GHz"}},
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
-                "path": "mumode_host_tucker_f64_async x K + mumode_host_wait (host-buffer C-ABI), pinned "
+                "path": "median of 3 batches of mumode_host_tucker_f64_async x K + mumode_host_wait (host-buffer C-ABI), pinned "
                         "buffers: consecutive steps overlap download and upload",
                 "sync_value": round(e2e_sync_value, 3),
                 "sync_path": "mumode_host_tucker_f64 per step (returns with the result in host memory)"},

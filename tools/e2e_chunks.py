@@ -23,7 +23,7 @@ Lp = _lib.ptr_array([L.data_ptr() for L in Lpin])
 K = 30
 for _ in range(2):
     res = []
-    for rep in range(3):
+    for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 3):
         for k in range(2):
             assert lib.mumode_host_tucker_f64_async(h.h, 3, m, m, Tpin.data_ptr(), Lp, Spins[k % 2].data_ptr()) == 0
         lib.mumode_host_wait(h.h)
@@ -32,4 +32,5 @@ for _ in range(2):
             assert lib.mumode_host_tucker_f64_async(h.h, 3, m, m, Tpin.data_ptr(), Lp, Spins[k % 2].data_ptr()) == 0
         assert lib.mumode_host_wait(h.h) == 0
         res.append((time.perf_counter() - t0) / K * 1e3)
-    print(f"{min(res):.3f} ms per application ({2.5769e10 / (min(res) * 1e-3) / 1e12:.2f} TF/s)", flush=True)
+    print(f"{min(res):.3f} ms per application ({2.5769e10 / (min(res) * 1e-3) / 1e12:.2f} TF/s); all batches (ms): "
+          + " ".join(f"{r:.3f}" for r in res), flush=True)
