@@ -77,7 +77,9 @@ int64_t mumode_launch_count(mumode_handle_t h);
  * 14 = auto without the small-extent fused two-mode passes (spair.cuh),
  * 15 = auto with the small-extent fused passes wherever eligible,
  * 16 = auto with the in-place block passes (block.cuh) wherever eligible,
- * 17 = auto without the in-place block passes.
+ * 17 = auto without the in-place block passes,
+ * 18 / 19 = the 48-wide TMA tile configurations forced for real products
+ *      (T-side 128 x 48 / L-side 48 x 128).
  * Not a fallback switch: all are CUDA kernels. */
 int mumode_set_kernel_policy(mumode_handle_t h, int policy);
 
