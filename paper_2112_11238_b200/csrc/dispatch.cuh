@@ -31,6 +31,8 @@ using CfgMid = TmaCfg<64, 128, 32, 4, 2, 4>;   // 32x32 warp tiles
 using CfgSmall = TmaCfg<32, 32, 32, 2, 2, 4>;  // 16x8 warp tiles: spreads small products over SMs
 using CfgTM48 = TmaCfg<128, 48, 48, 3, 16, 1>;  // n = 48k (the paper's 144 / 288 / 336) and 324 (7 x 48)
 using CfgLM48 = TmaCfg<48, 128, 48, 3, 1, 16>;
+using CfgTM56 = TmaCfg<128, 56, 32, 4, 16, 1>;  // n = 56k (112, 168, 224, 280, 336) and 208 / 216 (4 x 56)
+using CfgLM56 = TmaCfg<56, 128, 32, 4, 1, 16>;
 // complex128 (E = 2): 4 real DMMAs per complex MAC, 16-B elements
 // (four accumulator chains per complex output: warp tiles hold 32 outputs)
 using CfgCa = TmaCfg<64, 64, 16, 6, 2, 4, 2>;  // 8 MMA warps, 32x16 complex warp tiles
@@ -111,6 +113,8 @@ static int choose_cfg(const ModeJob& j, int sms) {
   const double c8 = tile_cost<CfgSmall>(mfrags, N, j.K, sms, 0.5);
   const double c9 = tile_cost<CfgTM48>(mfrags, N, j.K, sms, 0.96);
   const double c10 = tile_cost<CfgLM48>(mfrags, N, j.K, sms, 0.96);
+  const double c11 = tile_cost<CfgTM56>(mfrags, N, j.K, sms, 0.96);
+  const double c12 = tile_cost<CfgLM56>(mfrags, N, j.K, sms, 0.96);
   int best = 0;
   double bc = c0;
   if (c1 < bc) best = 1, bc = c1;
@@ -119,6 +123,8 @@ static int choose_cfg(const ModeJob& j, int sms) {
   if (c8 < bc) best = 8, bc = c8;
   if (c9 < bc * 0.995) best = 9, bc = c9;  // the 48-wide tiles only where they save work
   if (c10 < bc * 0.995) best = 10, bc = c10;
+  if (c11 < bc * 0.995) best = 11, bc = c11;
+  if (c12 < bc * 0.995) best = 12, bc = c12;
   return best;
 }
 
@@ -252,8 +258,10 @@ static int launch_tma_auto(mumode_handle_s* h, const ModeJob& j) {
   const int forced = (h->policy >= 3 && h->policy <= 6) ? h->policy - 3 : -1;
   int cfg = choose_cfg(j, h->num_sms);
   if (forced >= 0) cfg = j.cplx ? 4 + forced : forced;
-  if (!j.cplx && (h->policy == 18 || h->policy == 19)) cfg = h->policy - 9;  // 48-wide tiles forced (tests)
+  if (!j.cplx && h->policy >= 18 && h->policy <= 21) cfg = h->policy - 9;  // 48- / 56-wide tiles forced (tests)
   switch (cfg) {
+    case 11: return launch_tma<CfgTM56>(h, j);
+    case 12: return launch_tma<CfgLM56>(h, j);
     case 9: return launch_tma<CfgTM48>(h, j);
     case 10: return launch_tma<CfgLM48>(h, j);
     case 1: return launch_tma<CfgTM>(h, j);

@@ -499,7 +499,7 @@ void* mumode_get_stream(mumode_handle_t h) { return h ? static_cast<void*>(h->st
 int64_t mumode_launch_count(mumode_handle_t h) { return h ? h->launches : -1; }
 
 int mumode_set_kernel_policy(mumode_handle_t h, int policy) {
-  if (!h || policy < 0 || policy > 19) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
+  if (!h || policy < 0 || policy > 21) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
   // 3..6 force real tile configuration 0..3 / complex configuration 0..3
   h->policy = policy;
   return MUMODE_OK;

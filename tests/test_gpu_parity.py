@@ -40,9 +40,10 @@ def _require_gpu():
         pytest.fail("GPU test run without a GPU")
 
 
-@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 18, 19],
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 18, 19, 20, 21],
                 ids=["auto", "generic", "tma", "tma_big", "tma_tm", "tma_lm", "tma_mid", "fused", "ldg", "tail",
-                     "no_tail", "chain", "no_ws", "no_skinny", "no_spair", "tma_tm48", "tma_lm48"])
+                     "no_tail", "chain", "no_ws", "no_skinny", "no_spair", "tma_tm48", "tma_lm48", "tma_tm56",
+                     "tma_lm56"])
 def policy(request):
     h = mm.get_handle(0)
     h.set_kernel_policy(request.param)
