@@ -739,7 +739,8 @@ static int itucker_dev(mumode_handle_t h, int d, const int64_t* m, const double*
   for (int mu = 1; mu <= d; ++mu) {
     const int64_t n = m[mu - 1], A = prod(m, 0, mu - 1), C = prod(m, mu, d);
     if (n > (int64_t(1) << 30)) return fail(MUMODE_ERR_ARGUMENT, "itucker: extent too large");
-    lu_perm_kernel<<<1, 32, 0, h->stream>>>(piv[mu - 1], perm, perm + n, static_cast<int>(n));
+    lu_perm_kernel<<<1, 256, n <= kLuPermSmem ? 2 * static_cast<size_t>(n) * sizeof(int) : 0, h->stream>>>(
+        piv[mu - 1], perm, perm + n, static_cast<int>(n));
     MM_CUDA(cudaGetLastError());
     h->launches++;
     const size_t ps = cplx ? LuCfg<true>::PS : LuCfg<false>::PS;
