@@ -37,7 +37,7 @@ def _rnd(rng, shape, cplx):
     return np.asfortranarray(x)
 
 
-@pytest.mark.parametrize("policy", [0, 1, 2, 7, 8, 9, 11, 12])
+@pytest.mark.parametrize("policy", [0, 1, 2, 7, 8, 9, 11, 12, 18, 19, 20, 21])
 def test_fuzz_tucker_and_mode_products(policy):
     rng = np.random.default_rng(4242 + policy)
     h = mm.get_handle(0)
