@@ -100,9 +100,14 @@ static int choose_cfg(const ModeJob& j, int sms) {
       if (c[i] < c[best]) best = i;
     return 4 + best;
   }
+  // relative per-tile efficiency of the narrow-N (40/48/56) and narrow-M
+  // families against the 128x128 tiles: 0.96 -> 0.99 measured better at
+  // 384^3 (34.9 -> 35.7 TF/s), 456^3 (31.1 -> 32.5), 464^3 (32.1 -> 33.7), no
+  // size slower (tools/auto_sweep.py 176..512, 200^3 and 256^3 unchanged)
+  constexpr double tm_eff = 0.99;
   const double c0 = tile_cost<CfgBig>(mfrags, N, j.K, sms, 1.00);
-  const double c1 = tile_cost<CfgTM>(mfrags, N, j.K, sms, 0.96);
-  const double c2 = tile_cost<CfgLM>(mfrags, N, j.K, sms, 0.96);
+  const double c1 = tile_cost<CfgTM>(mfrags, N, j.K, sms, tm_eff);
+  const double c2 = tile_cost<CfgLM>(mfrags, N, j.K, sms, tm_eff);
   const double c3 = tile_cost<CfgMid>(mfrags, N, j.K, sms, 0.97);
   // small tiles reuse operands poorly; they win only when they save waves
   // (products of a few tiles: C1's 100 x 100 modes take 16 CTAs, not 3).
@@ -111,10 +116,10 @@ static int choose_cfg(const ModeJob& j, int sms) {
   // 64^3 19.4 -> 11.1, >= 80^3 unchanged (efficiency 0.4-0.6 choose alike,
   // 0.25 gives up 512^2 and 64^3)
   const double c8 = tile_cost<CfgSmall>(mfrags, N, j.K, sms, 0.5);
-  const double c9 = tile_cost<CfgTM48>(mfrags, N, j.K, sms, 0.96);
-  const double c10 = tile_cost<CfgLM48>(mfrags, N, j.K, sms, 0.96);
-  const double c11 = tile_cost<CfgTM56>(mfrags, N, j.K, sms, 0.96);
-  const double c12 = tile_cost<CfgLM56>(mfrags, N, j.K, sms, 0.96);
+  const double c9 = tile_cost<CfgTM48>(mfrags, N, j.K, sms, tm_eff);
+  const double c10 = tile_cost<CfgLM48>(mfrags, N, j.K, sms, tm_eff);
+  const double c11 = tile_cost<CfgTM56>(mfrags, N, j.K, sms, tm_eff);
+  const double c12 = tile_cost<CfgLM56>(mfrags, N, j.K, sms, tm_eff);
   int best = 0;
   double bc = c0;
   if (c1 < bc) best = 1, bc = c1;
