@@ -333,6 +333,61 @@ __device__ __forceinline__ void lu_sweep_dmma(double* xs, const double* __restri
   __syncthreads();
 }
 
+// Tile staging: the tile's nf fibres into / out of shared memory as
+// xs[k * (NF + 4) + fibre], rows permuted on the way in (x(k) = in(perm[k])).
+template <class V, int NF = kLuFibres>
+__device__ __forceinline__ void lu_tile_load(V* xs, const V* src, const int64_t* foff, const int* __restrict__ perm,
+                                             const int* __restrict__ iperm, int64_t A, int n, int64_t f0, int nf) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (A == 1) {  // mu = 1: the tile's fibres are nf*n contiguous elements
+    const V* s = src + f0 * n;
+    const int64_t tot = int64_t(nf) * n;
+    const int dfl = nt / n, dkk = nt - dfl * n;
+    int fl = tid / n, kk = tid - (tid / n) * n;
+    for (int64_t e = tid; e < tot; e += nt) {
+      xs[iperm[kk] * (NF + 4) + fl] = s[e];
+      fl += dfl;
+      kk += dkk;
+      if (kk >= n) {
+        kk -= n;
+        ++fl;
+      }
+    }
+  } else {  // lanes along the fibres (consecutive a): coalesced
+    const int fl = tid & (NF - 1);
+    if (fl < nf) {
+      const int64_t o = foff[fl];
+      for (int k = tid / NF; k < n; k += nt / NF) xs[k * (NF + 4) + fl] = src[o + int64_t(perm[k]) * A];
+    }
+  }
+}
+template <class V, int NF = kLuFibres>
+__device__ __forceinline__ void lu_tile_store(const V* xs, V* dst, const int64_t* foff, int64_t A, int n, int64_t f0,
+                                              int nf) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (A == 1) {
+    V* d = dst + f0 * n;
+    const int64_t tot = int64_t(nf) * n;
+    const int dfl = nt / n, dkk = nt - dfl * n;
+    int fl = tid / n, k = tid - (tid / n) * n;
+    for (int64_t e = tid; e < tot; e += nt) {
+      d[e] = xs[k * (NF + 4) + fl];
+      fl += dfl;
+      k += dkk;
+      if (k >= n) {
+        k -= n;
+        ++fl;
+      }
+    }
+  } else {
+    const int fl = tid & (NF - 1);
+    if (fl < nf) {
+      const int64_t o = foff[fl];
+      for (int k = tid / NF; k < n; k += nt / NF) dst[o + int64_t(k) * A] = xs[k * (NF + 4) + fl];
+    }
+  }
+}
+
 // One mode of itucker: out(a, :, c) = P^-1 in(a, :, c) for all A*C fibres of
 // length n (in may equal out: every CTA reads and writes only its own fibres).
 // staged: the tile's fibres live in shared memory x[k * 33 + fibre]; else
@@ -370,54 +425,14 @@ __global__ void __launch_bounds__(LuCfg<CPLX>::THREADS) lu_solve_mode_kernel(
     __syncthreads();
     const int64_t off = foff[grp];  // element k of this group's fibre at off + k * A
     if (staged) {
-      if (A == 1) {  // mu = 1: the tile's fibres are nf*n contiguous elements
-        const V* s = src + f0 * n;
-        const int64_t tot = int64_t(nf) * n;
-        const int dfl = nt / n, dkk = nt - dfl * n;
-        int fl = tid / n, kk = tid - (tid / n) * n;
-        for (int64_t e = tid; e < tot; e += nt) {
-          xs[iperm[kk] * kLuStride + fl] = s[e];
-          fl += dfl;
-          kk += dkk;
-          if (kk >= n) {
-            kk -= n;
-            ++fl;
-          }
-        }
-      } else {  // lanes along the fibres (consecutive a): coalesced
-        const int fl = tid & (kLuFibres - 1);
-        if (fl < nf) {
-          const int64_t o = foff[fl];
-          for (int k = tid / kLuFibres; k < n; k += nt / kLuFibres) xs[k * kLuStride + fl] = src[o + int64_t(perm[k]) * A];
-        }
-      }
+      lu_tile_load<V>(xs, src, foff, perm, iperm, A, n, f0, nf);
       __syncthreads();
       if constexpr (CPLX)
         lu_fibre_coop<CPLX, true>(xs + grp, kLuStride, Q, invd, panel, n, l, grp < nf);
       else
         lu_sweep_dmma(xs, Q, invd, panel, n, nf);
       __syncthreads();
-      if (A == 1) {
-        V* d = dst + f0 * n;
-        const int64_t tot = int64_t(nf) * n;
-        const int dfl = nt / n, dkk = nt - dfl * n;
-        int fl = tid / n, k = tid - (tid / n) * n;
-        for (int64_t e = tid; e < tot; e += nt) {
-          d[e] = xs[k * kLuStride + fl];
-          fl += dfl;
-          k += dkk;
-          if (k >= n) {
-            k -= n;
-            ++fl;
-          }
-        }
-      } else {
-        const int fl = tid & (kLuFibres - 1);
-        if (fl < nf) {
-          const int64_t o = foff[fl];
-          for (int k = tid / kLuFibres; k < n; k += nt / kLuFibres) dst[o + int64_t(k) * A] = xs[k * kLuStride + fl];
-        }
-      }
+      lu_tile_store<V>(xs, dst, foff, A, n, f0, nf);
       __syncthreads();
     } else {  // in global memory (in != out: the host stages a copy): permuted gather, solve in place
       if (grp < nf)
@@ -428,5 +443,339 @@ __global__ void __launch_bounds__(LuCfg<CPLX>::THREADS) lu_solve_mode_kernel(
     }
   }
 }
+
+// ---------------------------------------------------------------------------
+// Real staged sweeps, second form (n <= kLuRlMaxN): the same arithmetic with
+// the dependent work taken off the critical path.
+//
+//  * Forward sweep RIGHT-LOOKING: row r's GEMM chain is acc = sum over
+//    k = 0..r0-1 ascending, and the blocks are solved in ascending order, so
+//    the chain can be fed block by block as the x_k become known: after block
+//    j is solved, every row below it takes the 16 k's of block j (4 DMMAs per
+//    8 x 8 fragment) into an accumulator that stays in registers (the warp's
+//    row fragments mq + 4 i, i < MAXI, of its 8 fibres). Each element sees
+//    exactly the FMA sequence of the left-looking form (zero k-steps are exact
+//    no-ops), so the result is bit for bit the same -- but the per-block
+//    critical path is the in-block solve plus 4 DMMAs instead of a chain over
+//    all solved rows, and the update is many independent chains on 16 warps.
+//  * Backward sweep left-looking as before (a row's chain starts with the x's
+//    of the block solved just before it, so it cannot start earlier).
+//  * Both sweeps: the next block's factor panel (forward: the 16 columns of
+//    block j below its diagonal; backward: the block's 16 rows right of the
+//    diagonal) arrives by 8-byte cp.async into the other of two buffers while
+//    the current block is worked on; no global-load latency and one barrier
+//    less per block.
+// Panel buffers: 16 x PST doubles, PST = roundup16(n) + 4 (= 8 mod 32 words:
+// conflict-free A fragments); forward pan[kk * PST + (row - r0)], backward
+// pan[l * PST + (k - r0)].
+constexpr int kLuRlMaxN = 408;
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+__host__ __device__ inline int lu_rl_pst(int n) { return ((n + 3) & ~7) + 4; }  // >= n, = 4 mod 8 doubles
+
+// Diagonal-block solves, one lane per fibre (x = the fibre's BS block rows,
+// stride XS = NF + 4): the same per-element update order as trsm's in-block
+// solve (row l takes the finished x_i in ascending / descending i), but 120
+// FMAs with 8-fold ILP on one warp instead of 16 shuffle steps on sixteen.
+template <int BS, int XS>
+__device__ __forceinline__ void lu_fwd_diag(double* x, const double* pj, int PST) {
+  double v[BS];
+#pragma unroll
+  for (int l = 0; l < BS; ++l) v[l] = x[l * XS];
+#pragma unroll
+  for (int i = 0; i + 1 < BS; ++i)
+#pragma unroll
+    for (int l = i + 1; l < BS; ++l) v[l] = fma(-v[i], pj[i * PST + l], v[l]);
+#pragma unroll
+  for (int l = 1; l < BS; ++l) x[l * XS] = v[l];
+}
+template <int BS, int XS>
+__device__ __forceinline__ void lu_bwd_diag(double* x, const double* pj, int PST, const double* invd) {
+  double v[BS];
+#pragma unroll
+  for (int l = 0; l < BS; ++l) v[l] = x[l * XS];
+#pragma unroll
+  for (int i = BS - 1; i >= 0; --i) {
+    v[i] = __dmul_rn(v[i], invd[i]);
+#pragma unroll
+    for (int l = 0; l < i; ++l) v[l] = fma(-v[i], pj[l * PST + i], v[l]);
+  }
+#pragma unroll
+  for (int l = 0; l < BS; ++l) x[l * XS] = v[l];
+}
+
+// Full 16-row diagonal blocks: four lanes per fibre (warps 0..3, eight fibres
+// each), lane q owning rows q, q + 4, q + 8, q + 12. Step i broadcasts the
+// finished x_i inside the quad and every lane updates its rows beyond i -- the
+// same per-row update order again; the factor loads do not depend on the
+// chain, so a step costs one shuffle plus one FMA of latency (the one-lane
+// form pays a shared-memory load per FMA, the 16-lane form 16 warps of
+// instructions per step).
+template <int XS>
+__device__ __forceinline__ void lu_fwd_diag_quad(double* xs, const double* pj, int PST, int r0, int warp, int lane) {
+  const int q = lane & 3, f = 8 * warp + (lane >> 2);
+  double* x = xs + (r0 + q) * XS + f;
+  const double* pq = pj + q;
+  double v[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) v[m] = x[4 * m * XS];
+#pragma unroll
+  for (int i = 0; i < 15; ++i) {
+    const int qi = i & 3, mi = i >> 2;
+    const double xi = __shfl_sync(0xffffffffu, v[mi], qi, 4);
+#pragma unroll
+    for (int m = mi; m < 4; ++m) {
+      const double u = fma(-xi, pq[i * PST + 4 * m], v[m]);
+      v[m] = (m > mi || q > qi) ? u : v[m];
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < 4; ++m) x[4 * m * XS] = v[m];
+}
+template <int XS>
+__device__ __forceinline__ void lu_bwd_diag_quad(double* xs, const double* pj, int PST, const double* invd, int r0,
+                                                 int warp, int lane) {
+  const int q = lane & 3, f = 8 * warp + (lane >> 2);
+  double* x = xs + (r0 + q) * XS + f;
+  const double* pq = pj + q * PST;
+  double v[4], dinv[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    v[m] = x[4 * m * XS];
+    dinv[m] = invd[r0 + q + 4 * m];
+  }
+#pragma unroll
+  for (int i = 15; i >= 0; --i) {
+    const int qi = i & 3, mi = i >> 2;
+    v[mi] = q == qi ? __dmul_rn(v[mi], dinv[mi]) : v[mi];
+    const double xi = __shfl_sync(0xffffffffu, v[mi], qi, 4);
+#pragma unroll
+    for (int m = 0; m <= mi; ++m) {
+      const double u = fma(-xi, pq[4 * m * PST + i], v[m]);
+      v[m] = (m < mi || q < qi) ? u : v[m];
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < 4; ++m) x[4 * m * XS] = v[m];
+}
+
+template <int NF, int MAXI>
+__device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict__ Q, const double* __restrict__ invd,
+                                            double* pan, int n) {
+  constexpr int UM = 16, XS = NF + 4, FRW = NF / 8, RG = 16 / FRW;  // fibre fragments, row groups of the 16 warps
+  const int PST = lu_rl_pst(n), PSZ = 16 * PST;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int mq = warp / FRW, fr = warp % FRW;
+  const int full_end = n & ~(UM - 1);
+  auto fwd_bs = [&](int r0) { return r0 < full_end ? UM : 1 << (31 - __clz(n - r0)); };
+  auto bwd_bs = [&](int top) { return top > full_end ? (top & -top) : UM; };
+  // forward panel of the block at r0: Q(r0.., r0 + kk), kk < bs -- warp kk copies column kk
+  constexpr int CW = 8;  // copy warps: the last CW warps (the diagonal solves run on the first FRW <= 8)
+  const int cw = warp - (16 - CW);
+  auto issue_fwd = [&](double* pb, int r0, int bs) {
+    for (int kk = cw; kk < bs; kk += CW) {
+      const double* q = Q + r0 + int64_t(r0 + kk) * n;
+      double* d = pb + kk * PST;
+      for (int rr = lane; rr < n - r0; rr += 32) cp_async8(d + rr, q + rr);
+    }
+  };
+  // backward panel of the block at r0: Q(r0 + ll, r0..n-1), ll < bs
+  auto issue_bwd = [&](double* pb, int r0, int bs) {
+    const int ll = lane & 15;
+    if (ll < bs) {
+      const double* q = Q + (r0 + ll) + int64_t(r0) * n;
+      double* d = pb + ll * PST;
+      for (int kk = 2 * cw + (lane >> 4); kk < n - r0; kk += 2 * CW) cp_async8(d + kk, q + int64_t(kk) * n);
+    }
+  };
+
+  const int ihi = (n - 8 * mq + 8 * RG - 1) / (8 * RG);  // this warp's row fragments: mq + RG i, i < ihi
+  double acc[MAXI][2];  // acc[ip]: fragment i = ihi - 1 - ip (indexed from the bottom, see the update)
+#pragma unroll
+  for (int i = 0; i < MAXI; ++i) acc[i][0] = acc[i][1] = 0.0;
+  int buf = 0;
+  if (warp >= 16 - CW) issue_fwd(pan, 0, fwd_bs(0));
+  // forward sweep, unit lower triangle
+  for (int r0 = 0; r0 < n;) {
+    const int bs = fwd_bs(r0), rn = r0 + bs;
+    double* pj = pan + buf * PSZ;
+    if (r0 > 0) {
+#pragma unroll
+      for (int ip = 0; ip < MAXI; ++ip) {
+        const int row = 8 * (mq + RG * (ihi - 1 - ip)) + g;
+        if (ip < ihi && row >= r0 && row < rn) {
+          double* xr = xs + row * XS + 8 * fr + 2 * t;
+          xr[0] = __dsub_rn(xr[0], acc[ip][0]);
+          xr[1] = __dsub_rn(xr[1], acc[ip][1]);
+        }
+      }
+    }
+    cp_async_commit_wait_all();
+    __syncthreads();  // panel j and the flushed rows are visible; the other buffer is free
+    if (warp >= 16 - CW) {  // the solve's idle warps fetch the next panel
+      if (rn < n) issue_fwd(pan + (buf ^ 1) * PSZ, rn, fwd_bs(rn));
+      else issue_bwd(pan + (buf ^ 1) * PSZ, n - bwd_bs(n), bwd_bs(n));
+    }
+    if (bs == UM) {
+      if (warp < FRW) lu_fwd_diag_quad<XS>(xs, pj, PST, r0, warp, lane);
+    } else if (warp < NF / 32) {
+      double* x = xs + r0 * XS + 32 * warp + lane;
+      switch (bs) {
+        case 8: lu_fwd_diag<8, XS>(x, pj, PST); break;
+        case 4: lu_fwd_diag<4, XS>(x, pj, PST); break;
+        case 2: lu_fwd_diag<2, XS>(x, pj, PST); break;
+        default: break;
+      }
+    }
+    __syncthreads();
+    if (rn < n) {
+      if (bs == UM) {  // full block: fragments are entirely above or below it, no k padding
+        double b[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) b[s] = xs[(r0 + 4 * s + t) * XS + 8 * fr + g];
+        // k-step outer, fragments inner: a DMMA's result is ~90 cycles away, so the warp's
+        // fragments advance together as independent chains (rows >= n of the last fragment are
+        // never flushed; a fragment above the block only accumulates into dead registers)
+        // The accumulators are indexed from the bottom (acc[ip]: the warp's ip-th fragment from
+        // the last one), so the live ones are ip < cnt and the unrolled loops leave by a uniform
+        // branch -- a predicated-off DMMA still takes its slot in the fp64 pipe.
+        const int cnt = ihi - (rn - 8 * mq + 8 * RG - 1) / (8 * RG);
+        const double* pa = pj + (8 * (mq + RG * (ihi - 1)) + g - r0) + t * PST;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          double a[MAXI];
+#pragma unroll
+          for (int ip = 0; ip < MAXI; ++ip) {
+            if (ip >= cnt) break;
+            a[ip] = pa[-8 * RG * ip + 4 * s * PST];
+          }
+#pragma unroll
+          for (int ip = 0; ip < MAXI; ++ip) {
+            if (ip >= cnt) break;
+            dmma_8x8x4(acc[ip][0], acc[ip][1], a[ip], b[s]);
+          }
+        }
+      } else {
+        const int ks = (bs + 3) >> 2;
+        double b[2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const int k = 4 * s + t;
+          b[s] = (s < ks && k < bs) ? xs[(r0 + k) * XS + 8 * fr + g] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < MAXI; ++i) {
+          const int rb = 8 * (mq + RG * (ihi - 1 - i));
+          if (i < ihi && rb + 8 > rn) {  // the fragment has rows below block j
+            const int row = rb + g;
+            const bool rv = row >= rn && row < n;
+            const double* pa = pj + (row - r0);
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              if (s < ks) {
+                const int k = 4 * s + t;
+                const double a = (rv && k < bs) ? pa[k * PST] : 0.0;
+                dmma_8x8x4(acc[i][0], acc[i][1], a, b[s]);
+              }
+            }
+          }
+        }
+      }
+    }
+    r0 = rn;
+    buf ^= 1;
+  }
+  // backward sweep, upper triangle with the reciprocal diagonal
+  for (int top = n; top > 0;) {
+    const int bs = bwd_bs(top), r0 = top - bs;
+    double* pj = pan + buf * PSZ;
+    cp_async_commit_wait_all();
+    __syncthreads();  // panel j and the previous block's x are visible; the other buffer is free
+    if (top < n && mq < 2) {
+      double d0 = 0.0, d1 = 0.0;
+      const int ks = (n - top + 3) >> 2;
+      const double* pa = pj + (8 * mq + g) * PST + (top - r0) + t;
+      const double* pb = xs + (top + t) * XS + 8 * fr + g;
+      int s = 0;
+      for (; s + 4 <= ks - 1; s += 4) {  // full k-steps, four loads ahead of the chain
+        double a4[4], b4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a4[u] = pa[4 * (s + u)];
+          b4[u] = pb[4 * (s + u) * XS];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma_8x8x4(d0, d1, a4[u], b4[u]);
+      }
+      for (; s < ks; ++s) {
+        const bool kv = top + 4 * s + t < n;
+        const double a = kv ? pa[4 * s] : 0.0;
+        const double b = kv ? pb[4 * s * XS] : 0.0;
+        dmma_8x8x4(d0, d1, a, b);
+      }
+      const int row = 8 * mq + g;
+      if (row < bs) {
+        double* xr = xs + (r0 + row) * XS + 8 * fr + 2 * t;
+        xr[0] = __dsub_rn(xr[0], d0);
+        xr[1] = __dsub_rn(xr[1], d1);
+      }
+    }
+    __syncthreads();
+    if (r0 > 0 && warp >= 16 - CW) issue_bwd(pan + (buf ^ 1) * PSZ, r0 - bwd_bs(r0), bwd_bs(r0));
+    if (bs == UM) {
+      if (warp < FRW) lu_bwd_diag_quad<XS>(xs, pj, PST, invd, r0, warp, lane);
+    } else if (warp < NF / 32) {
+      double* x = xs + r0 * XS + 32 * warp + lane;
+      switch (bs) {
+        case 8: lu_bwd_diag<8, XS>(x, pj, PST, invd + r0); break;
+        case 4: lu_bwd_diag<4, XS>(x, pj, PST, invd + r0); break;
+        case 2: lu_bwd_diag<2, XS>(x, pj, PST, invd + r0); break;
+        default: lu_bwd_diag<1, XS>(x, pj, PST, invd + r0); break;
+      }
+    }
+    top = r0;
+    buf ^= 1;
+  }
+  __syncthreads();
+}
+
+// One real mode of itucker through lu_sweep_rl (staged tiles, n <= kLuRlMaxN).
+// Shared memory: invd[n], xs[n * (NF + 4)], two panel buffers of 16 * PST. NF = 64 fibres per CTA (one CTA per SM,
+// every warp busy in the backward chains) while the tile fits, else 32.
+template <int NF, int MAXI, int MINB>
+__global__ void __launch_bounds__(LuCfg<false>::THREADS, MINB) lu_solve_rl_kernel(
+    const double* in, double* out, int64_t A, int n, int64_t C, const double* __restrict__ lu,
+    const int* __restrict__ perm, const int* __restrict__ iperm) {
+  extern __shared__ __align__(16) unsigned char lu_smem[];
+  double* invd = reinterpret_cast<double*>(lu_smem);
+  double* xs = invd + n;
+  double* pan = xs + n * (NF + 4);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < n; i += nt) invd[i] = 1.0 / lu[i + int64_t(i) * n];
+  __shared__ int64_t foff[NF];
+  const int64_t F = A * C, An = A * n;
+  for (int64_t f0 = int64_t(blockIdx.x) * NF; f0 < F; f0 += int64_t(gridDim.x) * NF) {
+    const int nf = static_cast<int>(F - f0 < NF ? F - f0 : NF);
+    if (tid < NF) {
+      const int64_t ff = f0 + (tid < nf ? tid : 0);
+      foff[tid] = (ff % A) + (ff / A) * An;
+    }
+    __syncthreads();
+    lu_tile_load<double, NF>(xs, in, foff, perm, iperm, A, n, f0, nf);
+    __syncthreads();
+    lu_sweep_rl<NF, MAXI>(xs, lu, invd, pan, n);
+    lu_tile_store<double, NF>(xs, out, foff, A, n, f0, nf);
+    __syncthreads();
+  }
+}
+
+inline size_t lu_rl_smem(int n, int nf) { return sizeof(double) * (size_t(n) * (1 + nf + 4) + 2 * 16 * size_t(lu_rl_pst(n))); }
 
 }  // namespace mumode_gpu

@@ -499,7 +499,7 @@ void* mumode_get_stream(mumode_handle_t h) { return h ? static_cast<void*>(h->st
 int64_t mumode_launch_count(mumode_handle_t h) { return h ? h->launches : -1; }
 
 int mumode_set_kernel_policy(mumode_handle_t h, int policy) {
-  if (!h || policy < 0 || policy > 21) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
+  if (!h || policy < 0 || policy > 23) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
   // 3..6 force real tile configuration 0..3 / complex configuration 0..3
   h->policy = policy;
   return MUMODE_OK;
@@ -759,12 +759,31 @@ static int itucker_dev(mumode_handle_t h, int d, const int64_t* m, const double*
         src = static_cast<const double*>(h->ws[2].p);
       }
     }
-    auto kern = cplx ? lu_solve_mode_kernel<true> : lu_solve_mode_kernel<false>;
-    const int threads = cplx ? LuCfg<true>::THREADS : LuCfg<false>::THREADS;
-    MM_TRY(smem_opt_in(kern, static_cast<int>(smem)));
     const int64_t tiles = (A * C + kLuFibres - 1) / kLuFibres;
     const int grid = static_cast<int>(std::min<int64_t>(tiles, int64_t(h->num_sms) * 32));
-    kern<<<grid, threads, smem, h->stream>>>(src, S, A, static_cast<int>(n), C, LU[mu - 1], perm, perm + n, staged);
+    if (!cplx && n <= kLuRlMaxN && h->policy != 23) {
+      // real extents up to 408: right-looking forward sweep, prefetched panels (lu_sweep_rl)
+      const int ni = static_cast<int>(n);
+      auto launch = [&](auto kern, int nf) -> int {
+        const size_t rsmem = lu_rl_smem(ni, nf);
+        MM_TRY(smem_opt_in(kern, static_cast<int>(rsmem)));
+        const int64_t tiles = (A * C + nf - 1) / nf;
+        const int grid = static_cast<int>(std::min<int64_t>(tiles, int64_t(h->num_sms) * 32));
+        kern<<<grid, LuCfg<false>::THREADS, rsmem, h->stream>>>(src, S, A, ni, C, LU[mu - 1], perm, perm + n);
+        return MUMODE_OK;
+      };
+      // 64 fibres per CTA while the tile fits in shared memory (n <= 280), else 32
+      if (n <= 64) MM_TRY(launch(lu_solve_rl_kernel<64, 4, 2>, 64));
+      else if (n <= 128) MM_TRY(launch(lu_solve_rl_kernel<64, 8, 1>, 64));
+      else if (n <= 208) MM_TRY(launch(lu_solve_rl_kernel<64, 13, 1>, 64));
+      else if (n <= 280) MM_TRY(launch(lu_solve_rl_kernel<64, 18, 1>, 64));
+      else MM_TRY(launch(lu_solve_rl_kernel<32, 13, 1>, 32));
+    } else {
+      auto kern = cplx ? lu_solve_mode_kernel<true> : lu_solve_mode_kernel<false>;
+      const int threads = cplx ? LuCfg<true>::THREADS : LuCfg<false>::THREADS;
+      MM_TRY(smem_opt_in(kern, static_cast<int>(smem)));
+      kern<<<grid, threads, smem, h->stream>>>(src, S, A, static_cast<int>(n), C, LU[mu - 1], perm, perm + n, staged);
+    }
     MM_CUDA(cudaGetLastError());
     h->launches++;
     perm += 2 * n;

@@ -574,6 +574,31 @@ def test_itucker_ill_conditioned_bitwise_against_reference(shape):
             assert O.rel_fro(got, want) < 1e-12, shape
 
 
+@pytest.mark.skipif(not O.ref_available(), reason="reference library not built")
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 13, 16, 17, 23, 31, 32, 33, 47, 48, 63, 64, 65, 100, 127, 128, 129, 200,
+                               204, 206, 207, 255, 256, 257, 300, 391, 407, 408, 409])
+def test_itucker_extent_sweep_bitwise_against_reference(n):
+    # the right-looking sweep kernel (lu_solve_rl_kernel, n <= 408: every remainder-block pattern 8/4/2/1, each
+    # accumulator count MAXI) and the left-looking one beyond, with the extent as first, middle and last mode,
+    # a full and a partial 32-fibre tile: bit for bit the reference's ops::itucker and the left-looking kernel
+    rng = np.random.default_rng(1000 + n)
+    h = mm.get_handle(0)
+    for shape in ((n, 7, 5), (3, n, 13), (5, 7, n)):
+        T = rnd(rng, shape)
+        Ps = [rnd(rng, (e, e)) + (2.0 + 0.05 * e) * np.eye(e) for e in shape]
+        F = mm.FactorizedStack(Ps)
+        got = host(mm.itucker(dev(T), F))
+        if n <= 384:
+            np.testing.assert_array_equal(got, O.ref_itucker(T, Ps), err_msg=str(shape))
+        else:  # OpenBLAS splits the trsm update at GEMM_Q = 384 columns: two chains per row
+            assert O.rel_fro(got, O.ref_itucker(T, Ps)) < 1e-13, shape
+        h.set_kernel_policy(23)
+        try:
+            np.testing.assert_array_equal(host(mm.itucker(dev(T), F)), got, err_msg=str(shape))
+        finally:
+            h.set_kernel_policy(0)
+
+
 def test_itucker_in_place_and_large_extent():
     # S may alias T through the C-ABI (every CTA solves only its own fibres);
     # an extent beyond the shared-memory tile (real n > 835) solves in place in
