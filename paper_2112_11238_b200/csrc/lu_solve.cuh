@@ -354,7 +354,7 @@ __device__ __forceinline__ void lu_tile_load(V* xs, const V* src, const int64_t*
       }
     }
   } else {  // lanes along the fibres (consecutive a): coalesced
-    const int fl = tid & (NF - 1);
+    const int fl = tid % NF;
     if (fl < nf) {
       const int64_t o = foff[fl];
       for (int k = tid / NF; k < n; k += nt / NF) xs[k * (NF + 4) + fl] = src[o + int64_t(perm[k]) * A];
@@ -380,7 +380,7 @@ __device__ __forceinline__ void lu_tile_store(const V* xs, V* dst, const int64_t
       }
     }
   } else {
-    const int fl = tid & (NF - 1);
+    const int fl = tid % NF;
     if (fl < nf) {
       const int64_t o = foff[fl];
       for (int k = tid / NF; k < n; k += nt / NF) dst[o + int64_t(k) * A] = xs[k * (NF + 4) + fl];
@@ -477,6 +477,7 @@ __device__ __forceinline__ void cp_async_commit_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+__host__ __device__ constexpr int lu_rl_warps(int nf) { return nf == 32 ? 16 : nf / 4; }  // 32 fibres: 4 row groups, else 2
 __host__ __device__ inline int lu_rl_pst(int n) { return ((n + 3) & ~7) + 4; }  // >= n, = 4 mod 8 doubles
 
 // Diagonal-block solves, one lane per fibre (x = the fibre's BS block rows,
@@ -568,7 +569,7 @@ __device__ __forceinline__ void lu_bwd_diag_quad(double* xs, const double* pj, i
 template <int NF, int MAXI>
 __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict__ Q, const double* __restrict__ invd,
                                             double* pan, int n) {
-  constexpr int UM = 16, XS = NF + 4, FRW = NF / 8, RG = 16 / FRW;  // fibre fragments, row groups of the 16 warps
+  constexpr int UM = 16, XS = NF + 4, FRW = NF / 8, NW = lu_rl_warps(NF), RG = NW / FRW;  // fibre fragments, row groups of the warps
   const int PST = lu_rl_pst(n), PSZ = 16 * PST;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -577,8 +578,8 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
   auto fwd_bs = [&](int r0) { return r0 < full_end ? UM : 1 << (31 - __clz(n - r0)); };
   auto bwd_bs = [&](int top) { return top > full_end ? (top & -top) : UM; };
   // forward panel of the block at r0: Q(r0.., r0 + kk), kk < bs -- warp kk copies column kk
-  constexpr int CW = 8;  // copy warps: the last CW warps (the diagonal solves run on the first FRW <= 8)
-  const int cw = warp - (16 - CW);
+  constexpr int CW = NW;  // every warp copies its share of the next panel at the start of the DMMA phases
+  const int cw = warp;
   auto issue_fwd = [&](double* pb, int r0, int bs) {
     for (int kk = cw; kk < bs; kk += CW) {
       const double* q = Q + r0 + int64_t(r0 + kk) * n;
@@ -601,28 +602,30 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
 #pragma unroll
   for (int i = 0; i < MAXI; ++i) acc[i][0] = acc[i][1] = 0.0;
   int buf = 0;
-  if (warp >= 16 - CW) issue_fwd(pan, 0, fwd_bs(0));
+  issue_fwd(pan, 0, fwd_bs(0));
   // forward sweep, unit lower triangle
   for (int r0 = 0; r0 < n;) {
     const int bs = fwd_bs(r0), rn = r0 + bs;
     double* pj = pan + buf * PSZ;
     if (r0 > 0) {
+      // a block spans at most two row fragments, owned by different row groups: the warp's only
+      // candidate is its topmost fragment with rows >= r0
+      const int il = (r0 - 8 - 8 * mq + 8 * RG) / (8 * RG), ipf = ihi - 1 - il;
+      const int row = 8 * (mq + RG * il) + g;
+      if (ipf >= 0 && row >= r0 && row < rn) {
+        double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-      for (int ip = 0; ip < MAXI; ++ip) {
-        const int row = 8 * (mq + RG * (ihi - 1 - ip)) + g;
-        if (ip < ihi && row >= r0 && row < rn) {
-          double* xr = xs + row * XS + 8 * fr + 2 * t;
-          xr[0] = __dsub_rn(xr[0], acc[ip][0]);
-          xr[1] = __dsub_rn(xr[1], acc[ip][1]);
+        for (int ip = 0; ip < MAXI; ++ip) {
+          a0 = ip == ipf ? acc[ip][0] : a0;
+          a1 = ip == ipf ? acc[ip][1] : a1;
         }
+        double* xr = xs + row * XS + 8 * fr + 2 * t;
+        xr[0] = __dsub_rn(xr[0], a0);
+        xr[1] = __dsub_rn(xr[1], a1);
       }
     }
     cp_async_commit_wait_all();
     __syncthreads();  // panel j and the flushed rows are visible; the other buffer is free
-    if (warp >= 16 - CW) {  // the solve's idle warps fetch the next panel
-      if (rn < n) issue_fwd(pan + (buf ^ 1) * PSZ, rn, fwd_bs(rn));
-      else issue_bwd(pan + (buf ^ 1) * PSZ, n - bwd_bs(n), bwd_bs(n));
-    }
     if (bs == UM) {
       if (warp < FRW) lu_fwd_diag_quad<XS>(xs, pj, PST, r0, warp, lane);
     } else if (warp < NF / 32) {
@@ -635,6 +638,9 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
       }
     }
     __syncthreads();
+    // the next panel (its buffer was last read before the barrier above), under the DMMA phase
+    if (rn < n) issue_fwd(pan + (buf ^ 1) * PSZ, rn, fwd_bs(rn));
+    else issue_bwd(pan + (buf ^ 1) * PSZ, n - bwd_bs(n), bwd_bs(n));
     if (rn < n) {
       if (bs == UM) {  // full block: fragments are entirely above or below it, no k padding
         double b[4];
@@ -650,16 +656,19 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
         const double* pa = pj + (8 * (mq + RG * (ihi - 1)) + g - r0) + t * PST;
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
-          double a[MAXI];
+          constexpr int CH = 4;  // A fragments loaded CH at a time (registers)
 #pragma unroll
-          for (int ip = 0; ip < MAXI; ++ip) {
-            if (ip >= cnt) break;
-            a[ip] = pa[-8 * RG * ip + 4 * s * PST];
-          }
+          for (int c = 0; c < MAXI; c += CH) {
+            if (c >= cnt) break;
+            double a[CH];
 #pragma unroll
-          for (int ip = 0; ip < MAXI; ++ip) {
-            if (ip >= cnt) break;
-            dmma_8x8x4(acc[ip][0], acc[ip][1], a[ip], b[s]);
+            for (int u = 0; u < CH; ++u)
+              if (c + u < MAXI && c + u < cnt) a[u] = pa[-8 * RG * (c + u) + 4 * s * PST];
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+              if (c + u >= MAXI || c + u >= cnt) break;
+              dmma_8x8x4(acc[c + u][0], acc[c + u][1], a[u], b[s]);
+            }
           }
         }
       } else {
@@ -698,6 +707,7 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
     double* pj = pan + buf * PSZ;
     cp_async_commit_wait_all();
     __syncthreads();  // panel j and the previous block's x are visible; the other buffer is free
+    if (r0 > 0) issue_bwd(pan + (buf ^ 1) * PSZ, r0 - bwd_bs(r0), bwd_bs(r0));
     if (top < n && mq < 2) {
       double d0 = 0.0, d1 = 0.0;
       const int ks = (n - top + 3) >> 2;
@@ -728,7 +738,6 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
       }
     }
     __syncthreads();
-    if (r0 > 0 && warp >= 16 - CW) issue_bwd(pan + (buf ^ 1) * PSZ, r0 - bwd_bs(r0), bwd_bs(r0));
     if (bs == UM) {
       if (warp < FRW) lu_bwd_diag_quad<XS>(xs, pj, PST, invd, r0, warp, lane);
     } else if (warp < NF / 32) {
@@ -750,7 +759,7 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
 // Shared memory: invd[n], xs[n * (NF + 4)], two panel buffers of 16 * PST. NF = 64 fibres per CTA (one CTA per SM,
 // every warp busy in the backward chains) while the tile fits, else 32.
 template <int NF, int MAXI, int MINB>
-__global__ void __launch_bounds__(LuCfg<false>::THREADS, MINB) lu_solve_rl_kernel(
+__global__ void __launch_bounds__(32 * lu_rl_warps(NF), MINB) lu_solve_rl_kernel(
     const double* in, double* out, int64_t A, int n, int64_t C, const double* __restrict__ lu,
     const int* __restrict__ perm, const int* __restrict__ iperm) {
   extern __shared__ __align__(16) unsigned char lu_smem[];

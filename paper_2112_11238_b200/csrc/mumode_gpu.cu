@@ -499,7 +499,7 @@ void* mumode_get_stream(mumode_handle_t h) { return h ? static_cast<void*>(h->st
 int64_t mumode_launch_count(mumode_handle_t h) { return h ? h->launches : -1; }
 
 int mumode_set_kernel_policy(mumode_handle_t h, int policy) {
-  if (!h || policy < 0 || policy > 23) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
+  if (!h || policy < 0 || policy > 24) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
   // 3..6 force real tile configuration 0..3 / complex configuration 0..3
   h->policy = policy;
   return MUMODE_OK;
@@ -769,12 +769,13 @@ static int itucker_dev(mumode_handle_t h, int d, const int64_t* m, const double*
         MM_TRY(smem_opt_in(kern, static_cast<int>(rsmem)));
         const int64_t tiles = (A * C + nf - 1) / nf;
         const int grid = static_cast<int>(std::min<int64_t>(tiles, int64_t(h->num_sms) * 32));
-        kern<<<grid, LuCfg<false>::THREADS, rsmem, h->stream>>>(src, S, A, ni, C, LU[mu - 1], perm, perm + n);
+        kern<<<grid, 32 * lu_rl_warps(nf), rsmem, h->stream>>>(src, S, A, ni, C, LU[mu - 1], perm, perm + n);
         return MUMODE_OK;
       };
       // 64 fibres per CTA while the tile fits in shared memory (n <= 280), else 32
       if (n <= 64) MM_TRY(launch(lu_solve_rl_kernel<64, 4, 2>, 64));
       else if (n <= 128) MM_TRY(launch(lu_solve_rl_kernel<64, 8, 1>, 64));
+      else if (n <= 208 && h->policy != 24) MM_TRY(launch(lu_solve_rl_kernel<96, 13, 1>, 96));
       else if (n <= 208) MM_TRY(launch(lu_solve_rl_kernel<64, 13, 1>, 64));
       else if (n <= 280) MM_TRY(launch(lu_solve_rl_kernel<64, 18, 1>, 64));
       else MM_TRY(launch(lu_solve_rl_kernel<32, 13, 1>, 32));

@@ -1,4 +1,4 @@
-"""GPU time of itucker on n^3 (real), per policy: 0 = right-looking sweep kernel, 23 = left-looking.
+"""GPU time of itucker on n^3 (real), per policy: 0 = auto (right-looking sweep kernel), 24 = without its 96-fibre tiles, 23 = left-looking.
 python tools/itucker_time.py [n ...]"""
 import sys
 sys.path.insert(0, '/root/repo')
@@ -14,7 +14,7 @@ for n in ns:
     T = mm.to_colmajor(T)
     F = mm.FactorizedStack([rng.standard_normal((n, n)) + 3.0 * np.eye(n) for _ in range(3)])
     res = {}
-    for pol in (23, 0):
+    for pol in (23, 24, 0):
         h.set_kernel_policy(pol)
         for _ in range(2):
             out = mm.itucker(T, F)
@@ -28,6 +28,6 @@ for n in ns:
         res[pol] = (float(np.median(ts)), out.clone())
     h.set_kernel_policy(0)
     roof = 3 * 2.0 * n ** 4 / 37.0e12 * 1e3
-    same = bool(torch.equal(res[0][1], res[23][1]))
-    print(f"n={n}: left-looking {res[23][0]:.4f} ms, right-looking {res[0][0]:.4f} ms "
+    same = bool(torch.equal(res[0][1], res[23][1])) and bool(torch.equal(res[24][1], res[23][1]))
+    print(f"n={n}: left-looking {res[23][0]:.4f} ms, right-looking with 64-fibre tiles {res[24][0]:.4f} ms, auto {res[0][0]:.4f} ms "
           f"({100 * roof / res[0][0]:.1f} % of the mode-product roofline), bitwise equal: {same}", flush=True)
