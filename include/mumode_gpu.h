@@ -81,7 +81,9 @@ int64_t mumode_launch_count(mumode_handle_t h);
  * 18 / 19 = the 48-wide TMA tile configurations forced for real products
  *      (T-side 128 x 48 / L-side 48 x 128), 20 / 21 = the 56-wide ones,
  * 23 = itucker's real modes through the left-looking sweep kernel (22 is
- *      unused; auto takes the right-looking lu_solve_rl_kernel for n <= 408).
+ *      unused; auto takes the right-looking lu_solve_rl_kernel for n <= 408),
+ * 24 = auto without that kernel's 96-fibre tiles, 25 = auto with its factor
+ *      panels copied by cp.async also where bulk copies would be used.
  * Not a fallback switch: all are CUDA kernels. */
 int mumode_set_kernel_policy(mumode_handle_t h, int policy);
 

@@ -473,6 +473,23 @@ constexpr int kLuRlMaxN = 408;
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void lu_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// Qt(k, r) = Q(r, k): the backward panels' rows become contiguous (bulk copies)
+__global__ void lu_transpose_kernel(const double* __restrict__ Q, double* __restrict__ Qt, int n) {
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y)
+    if (bx + threadIdx.x < n && by + j < n) tile[j][threadIdx.x] = Q[(bx + threadIdx.x) + int64_t(by + j) * n];
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y)
+    if (by + threadIdx.x < n && bx + j < n) Qt[(by + threadIdx.x) + int64_t(bx + j) * n] = tile[threadIdx.x][j];
+}
 __device__ __forceinline__ void cp_async_commit_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
@@ -566,9 +583,10 @@ __device__ __forceinline__ void lu_bwd_diag_quad(double* xs, const double* pj, i
   for (int m = 0; m < 4; ++m) x[4 * m * XS] = v[m];
 }
 
-template <int NF, int MAXI>
-__device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict__ Q, const double* __restrict__ invd,
-                                            double* pan, int n) {
+template <int NF, int MAXI, bool BULK>
+__device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict__ Q, const double* __restrict__ Qt,
+                                            const double* __restrict__ invd, double* pan, int n, uint64_t* pbar,
+                                            uint32_t& st) {
   constexpr int UM = 16, XS = NF + 4, FRW = NF / 8, NW = lu_rl_warps(NF), RG = NW / FRW;  // fibre fragments, row groups of the warps
   const int PST = lu_rl_pst(n), PSZ = 16 * PST;
   const int tid = threadIdx.x;
@@ -580,6 +598,22 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
   // forward panel of the block at r0: Q(r0.., r0 + kk), kk < bs -- warp kk copies column kk
   constexpr int CW = NW;  // every warp copies its share of the next panel at the start of the DMMA phases
   const int cw = warp;
+  // BULK (even n, Qt given): panels by bulk copies, one per column (forward) / row (backward, from the
+  // transposed factor), issued by the last warp and completing on the buffer's mbarrier; the
+  // step counter st picks the buffer (st & 1) and its phase parity ((st >> 1) & 1). Otherwise:
+  // 8-byte cp.async by every warp at the start of the DMMA phases.
+  constexpr bool bulk = BULK;
+  auto issue_bulk = [&](int b, const double* src, int bs, int len) {  // bs pieces of len doubles, source pitch n
+    if (warp == NW - 1) {
+      if (lane == 0) mbar_arrive_expect_tx(pbar + b, uint32_t(bs) * uint32_t(len) * 8u);
+      __syncwarp();
+      if (lane < bs) lu_bulk_load(pan + b * PSZ + lane * PST, src + int64_t(lane) * n, uint32_t(len) * 8u, pbar + b);
+    }
+  };
+  auto panel_wait = [&]() {
+    if (bulk) mbar_wait(pbar + (st & 1), (st >> 1) & 1);
+    else cp_async_commit_wait_all();
+  };
   auto issue_fwd = [&](double* pb, int r0, int bs) {
     for (int kk = cw; kk < bs; kk += CW) {
       const double* q = Q + r0 + int64_t(r0 + kk) * n;
@@ -601,8 +635,9 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
   double acc[MAXI][2];  // acc[ip]: fragment i = ihi - 1 - ip (indexed from the bottom, see the update)
 #pragma unroll
   for (int i = 0; i < MAXI; ++i) acc[i][0] = acc[i][1] = 0.0;
-  int buf = 0;
-  issue_fwd(pan, 0, fwd_bs(0));
+  int buf = st & 1;
+  if (bulk) issue_bulk(buf, Q, fwd_bs(0), n);
+  else issue_fwd(pan + buf * PSZ, 0, fwd_bs(0));
   // forward sweep, unit lower triangle
   for (int r0 = 0; r0 < n;) {
     const int bs = fwd_bs(r0), rn = r0 + bs;
@@ -624,8 +659,12 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
         xr[1] = __dsub_rn(xr[1], a1);
       }
     }
-    cp_async_commit_wait_all();
+    panel_wait();
     __syncthreads();  // panel j and the flushed rows are visible; the other buffer is free
+    if (bulk) {
+      if (rn < n) issue_bulk(buf ^ 1, Q + rn + int64_t(rn) * n, fwd_bs(rn), n - rn);
+      else issue_bulk(buf ^ 1, Qt + (n - bwd_bs(n)) + int64_t(n - bwd_bs(n)) * n, bwd_bs(n), bwd_bs(n));
+    }
     if (bs == UM) {
       if (warp < FRW) lu_fwd_diag_quad<XS>(xs, pj, PST, r0, warp, lane);
     } else if (warp < NF / 32) {
@@ -638,9 +677,11 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
       }
     }
     __syncthreads();
-    // the next panel (its buffer was last read before the barrier above), under the DMMA phase
-    if (rn < n) issue_fwd(pan + (buf ^ 1) * PSZ, rn, fwd_bs(rn));
-    else issue_bwd(pan + (buf ^ 1) * PSZ, n - bwd_bs(n), bwd_bs(n));
+    // cp.async panels: the next one (its buffer was last read before the barrier above), under the DMMA phase
+    if (!bulk) {
+      if (rn < n) issue_fwd(pan + (buf ^ 1) * PSZ, rn, fwd_bs(rn));
+      else issue_bwd(pan + (buf ^ 1) * PSZ, n - bwd_bs(n), bwd_bs(n));
+    }
     if (rn < n) {
       if (bs == UM) {  // full block: fragments are entirely above or below it, no k padding
         double b[4];
@@ -700,14 +741,19 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
     }
     r0 = rn;
     buf ^= 1;
+    ++st;
   }
   // backward sweep, upper triangle with the reciprocal diagonal
   for (int top = n; top > 0;) {
     const int bs = bwd_bs(top), r0 = top - bs;
     double* pj = pan + buf * PSZ;
-    cp_async_commit_wait_all();
+    panel_wait();
     __syncthreads();  // panel j and the previous block's x are visible; the other buffer is free
-    if (r0 > 0) issue_bwd(pan + (buf ^ 1) * PSZ, r0 - bwd_bs(r0), bwd_bs(r0));
+    if (r0 > 0) {
+      const int nb = bwd_bs(r0), nr = r0 - nb;
+      if (bulk) issue_bulk(buf ^ 1, Qt + nr + int64_t(nr) * n, nb, n - nr);
+      else issue_bwd(pan + (buf ^ 1) * PSZ, nr, nb);
+    }
     if (top < n && mq < 2) {
       double d0 = 0.0, d1 = 0.0;
       const int ks = (n - top + 3) >> 2;
@@ -751,6 +797,7 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
     }
     top = r0;
     buf ^= 1;
+    ++st;
   }
   __syncthreads();
 }
@@ -758,14 +805,21 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
 // One real mode of itucker through lu_sweep_rl (staged tiles, n <= kLuRlMaxN).
 // Shared memory: invd[n], xs[n * (NF + 4)], two panel buffers of 16 * PST. NF = 64 fibres per CTA (one CTA per SM,
 // every warp busy in the backward chains) while the tile fits, else 32.
-template <int NF, int MAXI, int MINB>
+template <int NF, int MAXI, int MINB, bool BULK>
 __global__ void __launch_bounds__(32 * lu_rl_warps(NF), MINB) lu_solve_rl_kernel(
     const double* in, double* out, int64_t A, int n, int64_t C, const double* __restrict__ lu,
-    const int* __restrict__ perm, const int* __restrict__ iperm) {
+    const double* __restrict__ lut, const int* __restrict__ perm, const int* __restrict__ iperm) {
   extern __shared__ __align__(16) unsigned char lu_smem[];
   double* invd = reinterpret_cast<double*>(lu_smem);
   double* xs = invd + n;
-  double* pan = xs + n * (NF + 4);
+  double* pan = xs + (n + (n & 1)) * (NF + 4);  // 16-byte aligned for the bulk copies
+  __shared__ __align__(8) uint64_t pbar[2];
+  if (threadIdx.x == 0) {
+    mbar_init(pbar, 1);
+    mbar_init(pbar + 1, 1);
+    fence_barrier_init();
+  }
+  uint32_t st = 0;
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int i = tid; i < n; i += nt) invd[i] = 1.0 / lu[i + int64_t(i) * n];
   __shared__ int64_t foff[NF];
@@ -779,12 +833,14 @@ __global__ void __launch_bounds__(32 * lu_rl_warps(NF), MINB) lu_solve_rl_kernel
     __syncthreads();
     lu_tile_load<double, NF>(xs, in, foff, perm, iperm, A, n, f0, nf);
     __syncthreads();
-    lu_sweep_rl<NF, MAXI>(xs, lu, invd, pan, n);
+    lu_sweep_rl<NF, MAXI, BULK>(xs, lu, lut, invd, pan, n, pbar, st);
     lu_tile_store<double, NF>(xs, out, foff, A, n, f0, nf);
     __syncthreads();
   }
 }
 
-inline size_t lu_rl_smem(int n, int nf) { return sizeof(double) * (size_t(n) * (1 + nf + 4) + 2 * 16 * size_t(lu_rl_pst(n))); }
+inline size_t lu_rl_smem(int n, int nf) {
+  return sizeof(double) * (size_t(n) + size_t(n + (n & 1)) * (nf + 4) + 2 * 16 * size_t(lu_rl_pst(n)));
+}
 
 }  // namespace mumode_gpu

@@ -499,7 +499,7 @@ void* mumode_get_stream(mumode_handle_t h) { return h ? static_cast<void*>(h->st
 int64_t mumode_launch_count(mumode_handle_t h) { return h ? h->launches : -1; }
 
 int mumode_set_kernel_policy(mumode_handle_t h, int policy) {
-  if (!h || policy < 0 || policy > 24) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
+  if (!h || policy < 0 || policy > 25) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
   // 3..6 force real tile configuration 0..3 / complex configuration 0..3
   h->policy = policy;
   return MUMODE_OK;
@@ -734,8 +734,15 @@ static int itucker_dev(mumode_handle_t h, int d, const int64_t* m, const double*
   constexpr size_t kMaxSmem = 227 * 1024;
   int64_t nsum = 0;
   for (int k = 0; k < d; ++k) nsum += m[k];
-  MM_TRY(h->lperm.ensure(size_t(2 * nsum) * sizeof(int)));
+  // per-mode row permutations, then one transposed factor (real extents up to kLuRlMaxN: the
+  // backward panels of lu_sweep_rl are rows of the factor)
+  int64_t nt_max = 0;
+  for (int k = 0; k < d; ++k)
+    if (!cplx && m[k] <= kLuRlMaxN) nt_max = std::max(nt_max, m[k]);
+  const size_t perm_bytes = (size_t(2 * nsum) * sizeof(int) + 255) & ~size_t(255);
+  MM_TRY(h->lperm.ensure(perm_bytes + size_t(nt_max * nt_max) * sizeof(double)));
   int* perm = static_cast<int*>(h->lperm.p);
+  double* lut_buf = reinterpret_cast<double*>(static_cast<char*>(h->lperm.p) + perm_bytes);
   for (int mu = 1; mu <= d; ++mu) {
     const int64_t n = m[mu - 1], A = prod(m, 0, mu - 1), C = prod(m, mu, d);
     if (n > (int64_t(1) << 30)) return fail(MUMODE_ERR_ARGUMENT, "itucker: extent too large");
@@ -764,21 +771,41 @@ static int itucker_dev(mumode_handle_t h, int d, const int64_t* m, const double*
     if (!cplx && n <= kLuRlMaxN && h->policy != 23) {
       // real extents up to 408: right-looking forward sweep, prefetched panels (lu_sweep_rl)
       const int ni = static_cast<int>(n);
+      // large even extents with a 16-byte aligned factor: panels by bulk copies (backward ones from the
+      // transpose). Measured: 256^3 2.16 -> 2.06 ms, 300^3 5.41 -> 4.93 ms; up to ~208 the transpose
+      // launch costs more than the copies save (policy 25 forbids the bulk path).
+      const double* lut = nullptr;
+      if (n > 208 && n % 2 == 0 && reinterpret_cast<uintptr_t>(LU[mu - 1]) % 16 == 0 && h->policy != 25) {
+        const unsigned tb = static_cast<unsigned>((n + 31) / 32);
+        lu_transpose_kernel<<<dim3(tb, tb), dim3(32, 8), 0, h->stream>>>(LU[mu - 1], lut_buf, ni);
+        MM_CUDA(cudaGetLastError());
+        h->launches++;
+        lut = lut_buf;
+      }
       auto launch = [&](auto kern, int nf) -> int {
         const size_t rsmem = lu_rl_smem(ni, nf);
         MM_TRY(smem_opt_in(kern, static_cast<int>(rsmem)));
         const int64_t tiles = (A * C + nf - 1) / nf;
         const int grid = static_cast<int>(std::min<int64_t>(tiles, int64_t(h->num_sms) * 32));
-        kern<<<grid, 32 * lu_rl_warps(nf), rsmem, h->stream>>>(src, S, A, ni, C, LU[mu - 1], perm, perm + n);
+        kern<<<grid, 32 * lu_rl_warps(nf), rsmem, h->stream>>>(src, S, A, ni, C, LU[mu - 1], lut, perm, perm + n);
         return MUMODE_OK;
       };
       // 64 fibres per CTA while the tile fits in shared memory (n <= 280), else 32
-      if (n <= 64) MM_TRY(launch(lu_solve_rl_kernel<64, 4, 2>, 64));
-      else if (n <= 128) MM_TRY(launch(lu_solve_rl_kernel<64, 8, 1>, 64));
-      else if (n <= 208 && h->policy != 24) MM_TRY(launch(lu_solve_rl_kernel<96, 13, 1>, 96));
-      else if (n <= 208) MM_TRY(launch(lu_solve_rl_kernel<64, 13, 1>, 64));
-      else if (n <= 280) MM_TRY(launch(lu_solve_rl_kernel<64, 18, 1>, 64));
-      else MM_TRY(launch(lu_solve_rl_kernel<32, 13, 1>, 32));
+      if (n <= 64) MM_TRY(launch(lu_solve_rl_kernel<64, 4, 2, false>, 64));
+      else if (n <= 128) MM_TRY(launch(lu_solve_rl_kernel<64, 8, 2, false>, 64));
+      else if (n <= 208) {
+        // 96-fibre tiles (24 warps) take ~1.4x a 64-fibre tile's time: fewer, longer waves
+        const int64_t sms = h->num_sms, F = A * C;
+        const int64_t w64 = ((F + 63) / 64 + sms - 1) / sms, w96 = ((F + 95) / 96 + sms - 1) / sms;
+        if (h->policy != 24 && 14 * w96 < 10 * w64) MM_TRY(launch(lu_solve_rl_kernel<96, 13, 1, false>, 96));
+        else MM_TRY(launch(lu_solve_rl_kernel<64, 13, 1, false>, 64));
+      } else if (n <= 280) {
+        if (lut) MM_TRY(launch(lu_solve_rl_kernel<64, 18, 1, true>, 64));
+        else MM_TRY(launch(lu_solve_rl_kernel<64, 18, 1, false>, 64));
+      } else {
+        if (lut) MM_TRY(launch(lu_solve_rl_kernel<32, 13, 1, true>, 32));
+        else MM_TRY(launch(lu_solve_rl_kernel<32, 13, 1, false>, 32));
+      }
     } else {
       auto kern = cplx ? lu_solve_mode_kernel<true> : lu_solve_mode_kernel<false>;
       const int threads = cplx ? LuCfg<true>::THREADS : LuCfg<false>::THREADS;

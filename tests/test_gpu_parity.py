@@ -576,7 +576,7 @@ def test_itucker_ill_conditioned_bitwise_against_reference(shape):
 
 @pytest.mark.skipif(not O.ref_available(), reason="reference library not built")
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 13, 16, 17, 23, 31, 32, 33, 47, 48, 63, 64, 65, 100, 127, 128, 129, 200,
-                               204, 206, 207, 255, 256, 257, 300, 391, 407, 408, 409])
+                               204, 206, 207, 210, 255, 256, 257, 280, 282, 300, 391, 406, 407, 408, 409])
 def test_itucker_extent_sweep_bitwise_against_reference(n):
     # the right-looking sweep kernel (lu_solve_rl_kernel, n <= 408: every remainder-block pattern 8/4/2/1, each
     # accumulator count MAXI) and the left-looking one beyond, with the extent as first, middle and last mode,
@@ -592,11 +592,12 @@ def test_itucker_extent_sweep_bitwise_against_reference(n):
             np.testing.assert_array_equal(got, O.ref_itucker(T, Ps), err_msg=str(shape))
         else:  # OpenBLAS splits the trsm update at GEMM_Q = 384 columns: two chains per row
             assert O.rel_fro(got, O.ref_itucker(T, Ps)) < 1e-13, shape
-        h.set_kernel_policy(23)
-        try:
-            np.testing.assert_array_equal(host(mm.itucker(dev(T), F)), got, err_msg=str(shape))
-        finally:
-            h.set_kernel_policy(0)
+        for pol in (23, 24, 25):  # left-looking kernel; 64-fibre tiles only; cp.async panels only
+            h.set_kernel_policy(pol)
+            try:
+                np.testing.assert_array_equal(host(mm.itucker(dev(T), F)), got, err_msg=f"{shape} policy {pol}")
+            finally:
+                h.set_kernel_policy(0)
 
 
 def test_itucker_in_place_and_large_extent():
