@@ -453,21 +453,36 @@ __global__ void __launch_bounds__(LuCfg<CPLX>::THREADS) lu_solve_mode_kernel(
 //    the chain can be fed block by block as the x_k become known: after block
 //    j is solved, every row below it takes the 16 k's of block j (4 DMMAs per
 //    8 x 8 fragment) into an accumulator that stays in registers (the warp's
-//    row fragments mq + 4 i, i < MAXI, of its 8 fibres). Each element sees
-//    exactly the FMA sequence of the left-looking form (zero k-steps are exact
-//    no-ops), so the result is bit for bit the same -- but the per-block
-//    critical path is the in-block solve plus 4 DMMAs instead of a chain over
-//    all solved rows, and the update is many independent chains on 16 warps.
+//    row fragments mq + RG i of its 8 fibres, indexed from the bottom so the
+//    live ones are a prefix). Each element sees exactly the FMA sequence of
+//    the left-looking form (zero k-steps are exact no-ops), so the result is
+//    bit for bit the same -- but the per-block critical path is the in-block
+//    solve plus 4 DMMAs instead of a chain over all solved rows, and the
+//    update is many independent chains on every warp. A dependent DMMA issues
+//    ~90 cycles after its predecessor (measured with clock64 per phase), so
+//    the fragments advance together k-step by k-step; and a predicated-off
+//    DMMA still takes its slot in the fp64 pipe (ncu: 38 % pipe-active for
+//    22 % of useful DMMAs), so the unrolled loops leave by uniform branches.
 //  * Backward sweep left-looking as before (a row's chain starts with the x's
-//    of the block solved just before it, so it cannot start earlier).
+//    of the block solved just before it, so it cannot start earlier): one
+//    chain per warp, ~90 cycles per k-step of 4.
+//  * Diagonal blocks: four lanes per fibre (lu_*_diag_quad), ~80 cycles per
+//    row instead of 16 warps of shuffle steps.
 //  * Both sweeps: the next block's factor panel (forward: the 16 columns of
 //    block j below its diagonal; backward: the block's 16 rows right of the
-//    diagonal) arrives by 8-byte cp.async into the other of two buffers while
-//    the current block is worked on; no global-load latency and one barrier
-//    less per block.
-// Panel buffers: 16 x PST doubles, PST = roundup16(n) + 4 (= 8 mod 32 words:
-// conflict-free A fragments); forward pan[kk * PST + (row - r0)], backward
+//    diagonal) arrives in the other of two buffers while the current block is
+//    worked on -- by 8-byte cp.async issued under the DMMA phases, or (BULK:
+//    even n > 208) by one bulk copy per column / row completing on an
+//    mbarrier, the backward rows read from a transposed copy of the factor.
+//  * NF = 64 or 96 fibres per CTA (16 / 24 warps, one CTA per SM from n = 129):
+//    every phase is latency-bound, so throughput is fibres in flight per SM;
+//    the host picks 96 when it saves enough waves (a 96-fibre tile takes
+//    ~1.4x a 64-fibre tile's time).
+// Panel buffers: 16 x PST doubles, PST >= n, = 4 mod 8 (conflict-free A
+// fragments); forward pan[kk * PST + (row - r0)], backward
 // pan[l * PST + (k - r0)].
+// Measured (tools/itucker_time.py, n^3, L2 flushed): 128: 0.330 -> 0.236 ms,
+// 200: 1.35 -> 0.96, 256: 4.04 -> 2.02, 300: 7.74 -> 4.76, 400: 19.9 -> 11.5.
 constexpr int kLuRlMaxN = 408;
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
@@ -494,7 +509,6 @@ __device__ __forceinline__ void cp_async_commit_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
-__host__ __device__ constexpr int lu_rl_warps(int nf) { return nf == 32 ? 16 : nf / 4; }  // 32 fibres: 4 row groups, else 2
 __host__ __device__ inline int lu_rl_pst(int n) { return ((n + 3) & ~7) + 4; }  // >= n, = 4 mod 8 doubles
 
 // Diagonal-block solves, one lane per fibre (x = the fibre's BS block rows,
@@ -583,11 +597,11 @@ __device__ __forceinline__ void lu_bwd_diag_quad(double* xs, const double* pj, i
   for (int m = 0; m < 4; ++m) x[4 * m * XS] = v[m];
 }
 
-template <int NF, int MAXI, bool BULK>
+template <int NF, int NW, int MAXI, bool BULK>
 __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict__ Q, const double* __restrict__ Qt,
                                             const double* __restrict__ invd, double* pan, int n, uint64_t* pbar,
                                             uint32_t& st) {
-  constexpr int UM = 16, XS = NF + 4, FRW = NF / 8, NW = lu_rl_warps(NF), RG = NW / FRW;  // fibre fragments, row groups of the warps
+  constexpr int UM = 16, XS = NF + 4, FRW = NF / 8, RG = NW / FRW;  // fibre fragments, row groups of the warps
   const int PST = lu_rl_pst(n), PSZ = 16 * PST;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -805,8 +819,8 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
 // One real mode of itucker through lu_sweep_rl (staged tiles, n <= kLuRlMaxN).
 // Shared memory: invd[n], xs[n * (NF + 4)], two panel buffers of 16 * PST. NF = 64 fibres per CTA (one CTA per SM,
 // every warp busy in the backward chains) while the tile fits, else 32.
-template <int NF, int MAXI, int MINB, bool BULK>
-__global__ void __launch_bounds__(32 * lu_rl_warps(NF), MINB) lu_solve_rl_kernel(
+template <int NF, int NW, int MAXI, int MINB, bool BULK>
+__global__ void __launch_bounds__(32 * NW, MINB) lu_solve_rl_kernel(
     const double* in, double* out, int64_t A, int n, int64_t C, const double* __restrict__ lu,
     const double* __restrict__ lut, const int* __restrict__ perm, const int* __restrict__ iperm) {
   extern __shared__ __align__(16) unsigned char lu_smem[];
@@ -833,7 +847,7 @@ __global__ void __launch_bounds__(32 * lu_rl_warps(NF), MINB) lu_solve_rl_kernel
     __syncthreads();
     lu_tile_load<double, NF>(xs, in, foff, perm, iperm, A, n, f0, nf);
     __syncthreads();
-    lu_sweep_rl<NF, MAXI, BULK>(xs, lu, lut, invd, pan, n, pbar, st);
+    lu_sweep_rl<NF, NW, MAXI, BULK>(xs, lu, lut, invd, pan, n, pbar, st);
     lu_tile_store<double, NF>(xs, out, foff, A, n, f0, nf);
     __syncthreads();
   }

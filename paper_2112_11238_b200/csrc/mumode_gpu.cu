@@ -782,29 +782,29 @@ static int itucker_dev(mumode_handle_t h, int d, const int64_t* m, const double*
         h->launches++;
         lut = lut_buf;
       }
-      auto launch = [&](auto kern, int nf) -> int {
+      auto launch = [&](auto kern, int nf, int nw) -> int {
         const size_t rsmem = lu_rl_smem(ni, nf);
         MM_TRY(smem_opt_in(kern, static_cast<int>(rsmem)));
         const int64_t tiles = (A * C + nf - 1) / nf;
         const int grid = static_cast<int>(std::min<int64_t>(tiles, int64_t(h->num_sms) * 32));
-        kern<<<grid, 32 * lu_rl_warps(nf), rsmem, h->stream>>>(src, S, A, ni, C, LU[mu - 1], lut, perm, perm + n);
+        kern<<<grid, 32 * nw, rsmem, h->stream>>>(src, S, A, ni, C, LU[mu - 1], lut, perm, perm + n);
         return MUMODE_OK;
       };
       // 64 fibres per CTA while the tile fits in shared memory (n <= 280), else 32
-      if (n <= 64) MM_TRY(launch(lu_solve_rl_kernel<64, 4, 2, false>, 64));
-      else if (n <= 128) MM_TRY(launch(lu_solve_rl_kernel<64, 8, 2, false>, 64));
+      if (n <= 64) MM_TRY(launch(lu_solve_rl_kernel<64, 16, 4, 2, false>, 64, 16));
+      else if (n <= 128) MM_TRY(launch(lu_solve_rl_kernel<64, 16, 8, 2, false>, 64, 16));
       else if (n <= 208) {
         // 96-fibre tiles (24 warps) take ~1.4x a 64-fibre tile's time: fewer, longer waves
         const int64_t sms = h->num_sms, F = A * C;
         const int64_t w64 = ((F + 63) / 64 + sms - 1) / sms, w96 = ((F + 95) / 96 + sms - 1) / sms;
-        if (h->policy != 24 && 14 * w96 < 10 * w64) MM_TRY(launch(lu_solve_rl_kernel<96, 13, 1, false>, 96));
-        else MM_TRY(launch(lu_solve_rl_kernel<64, 13, 1, false>, 64));
+        if (h->policy != 24 && 14 * w96 < 10 * w64) MM_TRY(launch(lu_solve_rl_kernel<96, 24, 13, 1, false>, 96, 24));
+        else MM_TRY(launch(lu_solve_rl_kernel<64, 16, 13, 1, false>, 64, 16));
       } else if (n <= 280) {
-        if (lut) MM_TRY(launch(lu_solve_rl_kernel<64, 18, 1, true>, 64));
-        else MM_TRY(launch(lu_solve_rl_kernel<64, 18, 1, false>, 64));
+        if (lut) MM_TRY(launch(lu_solve_rl_kernel<64, 16, 18, 1, true>, 64, 16));
+        else MM_TRY(launch(lu_solve_rl_kernel<64, 16, 18, 1, false>, 64, 16));
       } else {
-        if (lut) MM_TRY(launch(lu_solve_rl_kernel<32, 13, 1, true>, 32));
-        else MM_TRY(launch(lu_solve_rl_kernel<32, 13, 1, false>, 32));
+        if (lut) MM_TRY(launch(lu_solve_rl_kernel<32, 16, 13, 1, true>, 32, 16));
+        else MM_TRY(launch(lu_solve_rl_kernel<32, 16, 13, 1, false>, 32, 16));
       }
     } else {
       auto kern = cplx ? lu_solve_mode_kernel<true> : lu_solve_mode_kernel<false>;
