@@ -600,6 +600,26 @@ def test_itucker_extent_sweep_bitwise_against_reference(n):
                 h.set_kernel_policy(0)
 
 
+def test_itucker_many_tiles_per_cta():
+    # more fibre tiles than the grid cap (148 * 32 CTAs): every CTA of the right-looking kernel walks several
+    # tiles (accumulators, panel buffers and barrier phases carried across tiles); cp.async panels (n = 16,
+    # 307200 fibres) and bulk-copied panels (n = 210, 318000 fibres): bitwise equal to the left-looking kernel
+    rng = np.random.default_rng(5)
+    h = mm.get_handle(0)
+    for shape in ((16, 640, 480), (210, 600, 530)):
+        T = mm.to_colmajor(torch.from_numpy(rng.standard_normal(shape)).cuda())
+        Ps = [rnd(rng, (e, e)) + (2.0 + 0.05 * e) * np.eye(e) if i == 0 else np.eye(e) for i, e in enumerate(shape)]
+        F = mm.FactorizedStack(Ps)
+        got = mm.itucker(T, F)
+        h.set_kernel_policy(23)
+        try:
+            want = mm.itucker(T, F)
+        finally:
+            h.set_kernel_policy(0)
+        assert torch.equal(got, want), shape
+        del T, got, want
+
+
 def test_itucker_in_place_and_large_extent():
     # S may alias T through the C-ABI (every CTA solves only its own fibres);
     # an extent beyond the shared-memory tile (real n > 835) solves in place in
