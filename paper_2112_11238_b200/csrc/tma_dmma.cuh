@@ -435,7 +435,7 @@ __device__ __forceinline__ void tma_consume_tile(const TmaParams& p, int mtile, 
         double* dst = base + static_cast<int64_t>(n) * p.ldD;
         if constexpr (EPI == 3) {
           // the last mode: rows m, m+1 index the modes before it (batch 0)
-          const double2 fr = *reinterpret_cast<const double2*>(p.div_front + m);
+          const double2 fr = __ldg(reinterpret_cast<const double2*>(p.div_front + m));  // read-only: not reloaded after the stores
           const double ln = __ldg(p.div_last + n);
           stg_f64x2(dst, acc[fm][fn][0] / (fr.x + ln), acc[fm][fn][1] / (fr.y + ln));
           continue;
