@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(LuCfg<CPLX>::THREADS) lu_solve_mode_kernel(
 //    block j below its diagonal; backward: the block's 16 rows right of the
 //    diagonal) arrives in the other of two buffers while the current block is
 //    worked on -- by 8-byte cp.async issued under the DMMA phases, or (BULK:
-//    even n > 208) by one bulk copy per column / row completing on an
+//    even n > 128, 64- / 32-fibre tiles) by one bulk copy per column / row completing on an
 //    mbarrier, the backward rows read from a transposed copy of the factor.
 //  * NF = 64 or 96 fibres per CTA (16 / 24 warps, one CTA per SM from n = 129):
 //    every phase is latency-bound, so throughput is fibres in flight per SM;

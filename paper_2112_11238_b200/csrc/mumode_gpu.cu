@@ -771,11 +771,17 @@ static int itucker_dev(mumode_handle_t h, int d, const int64_t* m, const double*
     if (!cplx && n <= kLuRlMaxN && h->policy != 23) {
       // real extents up to 408: right-looking forward sweep, prefetched panels (lu_sweep_rl)
       const int ni = static_cast<int>(n);
-      // large even extents with a 16-byte aligned factor: panels by bulk copies (backward ones from the
-      // transpose). Measured: 256^3 2.16 -> 2.06 ms, 300^3 5.41 -> 4.93 ms; up to ~208 the transpose
-      // launch costs more than the copies save (policy 25 forbids the bulk path).
+      // 64-fibre tiles (16 warps, one CTA per SM from n = 129) or, up to 208, 96-fibre tiles (24 warps),
+      // which take ~1.4x a 64-fibre tile's time: chosen by wave count
+      const int64_t sms = h->num_sms, F = A * C;
+      const int64_t w64 = ((F + 63) / 64 + sms - 1) / sms, w96 = ((F + 95) / 96 + sms - 1) / sms;
+      const bool nf96 = n > 128 && n <= 208 && h->policy != 24 && 14 * w96 < 10 * w64;
+      // even extents above 128 with a 16-byte aligned factor: panels by bulk copies (backward ones from
+      // a transposed copy of the factor). Measured: 208^3 1.15 -> 1.09 ms, 256^3 2.16 -> 2.06, 300^3
+      // 5.41 -> 4.93; no gain with the 96-fibre tiles (their cp.async issue hides under the DMMA phases) or
+      // up to 128, where the transpose launch costs more than it saves. Policy 25 forbids the bulk path.
       const double* lut = nullptr;
-      if (n > 208 && n % 2 == 0 && reinterpret_cast<uintptr_t>(LU[mu - 1]) % 16 == 0 && h->policy != 25) {
+      if (n > 128 && !nf96 && n % 2 == 0 && reinterpret_cast<uintptr_t>(LU[mu - 1]) % 16 == 0 && h->policy != 25) {
         const unsigned tb = static_cast<unsigned>((n + 31) / 32);
         lu_transpose_kernel<<<dim3(tb, tb), dim3(32, 8), 0, h->stream>>>(LU[mu - 1], lut_buf, ni);
         MM_CUDA(cudaGetLastError());
@@ -793,11 +799,9 @@ static int itucker_dev(mumode_handle_t h, int d, const int64_t* m, const double*
       // 64 fibres per CTA while the tile fits in shared memory (n <= 280), else 32
       if (n <= 64) MM_TRY(launch(lu_solve_rl_kernel<64, 16, 4, 2, false>, 64, 16));
       else if (n <= 128) MM_TRY(launch(lu_solve_rl_kernel<64, 16, 8, 2, false>, 64, 16));
+      else if (nf96) MM_TRY(launch(lu_solve_rl_kernel<96, 24, 13, 1, false>, 96, 24));
       else if (n <= 208) {
-        // 96-fibre tiles (24 warps) take ~1.4x a 64-fibre tile's time: fewer, longer waves
-        const int64_t sms = h->num_sms, F = A * C;
-        const int64_t w64 = ((F + 63) / 64 + sms - 1) / sms, w96 = ((F + 95) / 96 + sms - 1) / sms;
-        if (h->policy != 24 && 14 * w96 < 10 * w64) MM_TRY(launch(lu_solve_rl_kernel<96, 24, 13, 1, false>, 96, 24));
+        if (lut) MM_TRY(launch(lu_solve_rl_kernel<64, 16, 13, 1, true>, 64, 16));
         else MM_TRY(launch(lu_solve_rl_kernel<64, 16, 13, 1, false>, 64, 16));
       } else if (n <= 280) {
         if (lut) MM_TRY(launch(lu_solve_rl_kernel<64, 16, 18, 1, true>, 64, 16));
