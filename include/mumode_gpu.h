@@ -328,7 +328,12 @@ int mumode_lu_factor_c128(int64_t n, const double* P, double* lu, int64_t* piv);
 /* Replaces ops::itucker (tucker.hpp:187-204): S = T x_1 P_1^-1 ... x_d P_d^-1
  * by per-mode triangular solves with DEVICE factors LU[k] (m_k x m_k, as
  * mumode_lu_factor_*) and DEVICE pivots piv[k] (m_k int64); lu_solve's
- * arithmetic (lu.hpp:52-69 on OpenBLAS's trsm kernels). S may alias T. */
+ * arithmetic (lu.hpp:52-69 on OpenBLAS's trsm kernels). S may alias T.
+ * Bitwise equal to the reference linked against OpenBLAS 0.3.15 (SkylakeX)
+ * for real extents up to 384; beyond, that build splits each trsm update at
+ * GEMM_Q = 384 columns (two chains per row) and the two agree to ~1e-16
+ * relative (tests: 391..409 within 1e-13). Complex: bitwise for extents
+ * that are multiples of 4. */
 int mumode_itucker_f64(mumode_handle_t h, int d, const int64_t* m, const double* T, const double* const* LU,
                        const int64_t* const* piv, double* S);
 int mumode_itucker_c128(mumode_handle_t h, int d, const int64_t* m, const double* T, const double* const* LU,

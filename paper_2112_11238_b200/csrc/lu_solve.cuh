@@ -19,7 +19,8 @@
 //     solves inside the block with fused multiply-add updates;
 //   * the backward sweep multiplies by the reciprocal diagonal (real 1/u;
 //     complex the packing routine's Smith reciprocal with a fused 1 + r*r).
-// Bitwise equal to the reference for every real extent (n <= 400 probed) and
+// Bitwise equal to the reference for every real extent up to 384 (beyond, the
+// library splits each trsm update at GEMM_Q = 384 columns: ~1e-16 apart) and
 // for complex extents that are multiples of 4; complex remainder blocks
 // (n % 4 != 0) take OpenBLAS's M-tail kernels, whose grouping differs at the
 // 1e-16 level.
