@@ -203,15 +203,23 @@ __device__ __forceinline__ void lu_fibre_coop(typename std::conditional<CPLX, do
 
 // perm[k]: the row of the input that ends in row k after lu_solve's swaps
 // (lu.hpp:58-64) -- the swaps applied in order to an index array. iperm is
-// its inverse. One thread (n is a mode extent).
-// The swaps are sequential; they run on one thread over shared-memory copies
+// its inverse. One block per mode (all modes of an itucker in one launch);
+// the swaps are sequential: one thread walks them over shared-memory copies
 // of the index array and the pivots when they fit (n <= kLuPermSmem: 24 ->
 // 8 us at n = 200, each swap a shared round trip instead of a global one), in
 // global memory otherwise; the block fills and inverts the array in parallel.
-constexpr int kLuPermSmem = 12288;
-__global__ void lu_perm_kernel(const int64_t* __restrict__ piv, int* __restrict__ perm, int* __restrict__ iperm,
-                               int n) {
+constexpr int kLuPermSmem = 6144;  // 2 n ints <= 48 KB of dynamic shared memory
+struct LuPermBatch {
+  const int64_t* piv[32];
+  int n[32];
+  int off[32];  // perm of mode b at base + off[b], iperm at base + off[b] + n[b]
+};
+__global__ void lu_perm_kernel(const LuPermBatch pb, int* __restrict__ base) {
   extern __shared__ int sperm[];  // [n] index array, [n] pivots (shared path)
+  const int n = pb.n[blockIdx.x];
+  const int64_t* __restrict__ piv = pb.piv[blockIdx.x];
+  int* perm = base + pb.off[blockIdx.x];
+  int* iperm = perm + n;
   const bool in_smem = n <= kLuPermSmem;
   int* w = in_smem ? sperm : perm;
   int* spiv = sperm + n;

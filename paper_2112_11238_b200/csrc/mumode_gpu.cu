@@ -743,13 +743,25 @@ static int itucker_dev(mumode_handle_t h, int d, const int64_t* m, const double*
   MM_TRY(h->lperm.ensure(perm_bytes + size_t(nt_max * nt_max) * sizeof(double)));
   int* perm = static_cast<int*>(h->lperm.p);
   double* lut_buf = reinterpret_cast<double*>(static_cast<char*>(h->lperm.p) + perm_bytes);
+  {  // every mode's permutation in one launch (one block per mode)
+    LuPermBatch pb{};
+    int64_t off = 0, nsm = 0;
+    for (int k = 0; k < d; ++k) {
+      if (m[k] > (int64_t(1) << 30)) return fail(MUMODE_ERR_ARGUMENT, "itucker: extent too large");
+      pb.piv[k] = piv[k];
+      pb.n[k] = static_cast<int>(m[k]);
+      pb.off[k] = static_cast<int>(off);
+      off += 2 * m[k];
+      if (m[k] <= kLuPermSmem) nsm = std::max(nsm, m[k]);
+    }
+    if (off > (int64_t(1) << 31) - 1) return fail(MUMODE_ERR_ARGUMENT, "itucker: extents too large");
+    lu_perm_kernel<<<d, 256, 2 * static_cast<size_t>(nsm) * sizeof(int), h->stream>>>(pb, perm);
+    MM_CUDA(cudaGetLastError());
+    h->launches++;
+  }
   for (int mu = 1; mu <= d; ++mu) {
     const int64_t n = m[mu - 1], A = prod(m, 0, mu - 1), C = prod(m, mu, d);
     if (n > (int64_t(1) << 30)) return fail(MUMODE_ERR_ARGUMENT, "itucker: extent too large");
-    lu_perm_kernel<<<1, 256, n <= kLuPermSmem ? 2 * static_cast<size_t>(n) * sizeof(int) : 0, h->stream>>>(
-        piv[mu - 1], perm, perm + n, static_cast<int>(n));
-    MM_CUDA(cudaGetLastError());
-    h->launches++;
     const size_t ps = cplx ? LuCfg<true>::PS : LuCfg<false>::PS;
     size_t smem = vb * size_t(n) * (1 + kLuStride + ps);  // invd, fibre tile, factor panel
     int staged = 1;
