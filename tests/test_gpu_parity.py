@@ -620,6 +620,24 @@ def test_itucker_many_tiles_per_cta():
         del T, got, want
 
 
+@pytest.mark.parametrize("shape", [(200, 200, 200), (208, 96, 208), (300, 40, 300), (201, 50, 201)])
+def test_itucker_repeats_are_bitwise_stable(shape):
+    # the right-looking kernel's double-buffered panels, barrier phases and warp roles under load (96-fibre
+    # tiles, bulk-copied panels, 32-fibre tiles, odd extent): 20 repeats at full occupancy, each bit for bit
+    # the left-looking kernel's result (a race shows up as an intermittent mismatch)
+    rng = np.random.default_rng(shape[0])
+    h = mm.get_handle(0)
+    T = mm.to_colmajor(torch.from_numpy(np.asfortranarray(rng.standard_normal(shape))).cuda())
+    F = mm.FactorizedStack([rng.standard_normal((e, e)) + 3.0 * np.eye(e) for e in shape])
+    h.set_kernel_policy(23)
+    try:
+        want = mm.itucker(T, F).clone()
+    finally:
+        h.set_kernel_policy(0)
+    for rep in range(20):
+        assert torch.equal(mm.itucker(T, F), want), (shape, rep)
+
+
 def test_itucker_in_place_and_large_extent():
     # S may alias T through the C-ABI (every CTA solves only its own fibres);
     # an extent beyond the shared-memory tile (real n > 835) solves in place in
