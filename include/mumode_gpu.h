@@ -83,7 +83,8 @@ int64_t mumode_launch_count(mumode_handle_t h);
  * 23 = itucker's real modes through the left-looking sweep kernel (22 is
  *      unused; auto takes the right-looking lu_solve_rl_kernel for n <= 408),
  * 24 = auto without that kernel's 96-fibre tiles, 25 = auto with its factor
- *      panels copied by cp.async also where bulk copies would be used.
+ *      panels copied by cp.async also where bulk copies would be used,
+ * 26 = kronsumv without the fused pass over its first two terms (kron12.cuh).
  * Not a fallback switch: all are CUDA kernels. */
 int mumode_set_kernel_policy(mumode_handle_t h, int policy);
 

@@ -34,6 +34,7 @@
 #include "lu_solve.cuh"
 #include "spair.cuh"
 #include "block.cuh"
+#include "kron12.cuh"
 
 namespace mumode_gpu {
 
@@ -499,7 +500,7 @@ void* mumode_get_stream(mumode_handle_t h) { return h ? static_cast<void*>(h->st
 int64_t mumode_launch_count(mumode_handle_t h) { return h ? h->launches : -1; }
 
 int mumode_set_kernel_policy(mumode_handle_t h, int policy) {
-  if (!h || policy < 0 || policy > 25) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
+  if (!h || policy < 0 || policy > 26) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
   // 3..6 force real tile configuration 0..3 / complex configuration 0..3
   h->policy = policy;
   return MUMODE_OK;
@@ -709,8 +710,28 @@ static int kronsumv_entry(mumode_handle_t h, int d, const int64_t* m, const doub
   // W = V x_1 A_1, then W += V x_mu A_mu for mu = 2..d in the products'
   // epilogues (the reference's acc += term order, tucker.hpp:222-231): no
   // term buffer and no separate accumulation pass over W.
-  MM_TRY(mode_product_dev(h, d, m, 1, m[0], V, A[0], 1, m[0], cplx, false, W));
-  for (int mu = 2; mu <= d; ++mu)
+  int first = 2;
+  // small square modes 1 and 2 (16 or 24): both terms in one pass over V (kron12.cuh)
+  if (!cplx && d >= 3 && m[0] == m[1] && (m[0] == 16 || m[0] == 24) && prod(m, 2, d) >= 2048 &&
+      aligned16_ptr(V) && aligned16_ptr(W) && h->policy != 26) {
+    const int n = static_cast<int>(m[0]);
+    const int64_t nsl = prod(m, 2, d);
+    const size_t smem = kron12_smem(n);
+    const int grid = static_cast<int>(std::min<int64_t>((nsl + kKron12Warps - 1) / kKron12Warps, h->num_sms));
+    if (n == 16) {
+      MM_TRY(smem_opt_in(kron12_kernel<2>, static_cast<int>(smem)));
+      kron12_kernel<2><<<grid, 32 * kKron12Warps, smem, h->stream>>>(V, A[0], A[1], W, nsl);
+    } else {
+      MM_TRY(smem_opt_in(kron12_kernel<3>, static_cast<int>(smem)));
+      kron12_kernel<3><<<grid, 32 * kKron12Warps, smem, h->stream>>>(V, A[0], A[1], W, nsl);
+    }
+    MM_CUDA(cudaGetLastError());
+    h->launches++;
+    first = 3;
+  } else {
+    MM_TRY(mode_product_dev(h, d, m, 1, m[0], V, A[0], 1, m[0], cplx, false, W));
+  }
+  for (int mu = first; mu <= d; ++mu)
     MM_TRY(mode_product_dev(h, d, m, mu, m[mu - 1], V, A[mu - 1], 1, m[mu - 1], cplx, false, W, true));
   return MUMODE_OK;
 }

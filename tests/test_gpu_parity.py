@@ -515,6 +515,30 @@ def test_kronsumv_complex_against_reference(shape):
     assert O.rel_fro(host(mm.kronsumv(dev(Vr), [dev(A) for A in As])), O.ref_tucker(Vr.astype(complex), As, "kronsumv")) < 1e-13
 
 
+@pytest.mark.parametrize("shape", [(24, 24, 24, 24, 7), (16, 16, 16, 16, 16), (24, 24, 2100), (16, 16, 50, 60),
+                                   (24, 24, 24, 24, 24, 24)])
+def test_kronsumv_fused_first_pair_equals_per_mode_passes(shape):
+    # kron12_kernel (terms 1 and 2 in one pass, small square modes 1-2) against one pass per term (policy 26):
+    # bit for bit; the small shapes also against the reference's kronsumv
+    rng = np.random.default_rng(len(shape) * 100 + shape[0])
+    h = mm.get_handle(0)
+    V = mm.colmajor_empty(shape, torch.float64, "cuda").normal_()
+    As = [mm.to_colmajor(torch.randn(e, e, dtype=torch.float64, device="cuda")) for e in shape]
+    got = mm.kronsumv(V, As)
+    h.set_kernel_policy(26)
+    try:
+        want = mm.kronsumv(V, As)
+    finally:
+        h.set_kernel_policy(0)
+    assert torch.equal(got, want), shape
+    if O.ref_available() and V.numel() <= 4_000_000:
+        ref = O.ref_tucker(host(V), [host(A) for A in As], "kronsumv")
+        if max(shape) <= 384:
+            np.testing.assert_array_equal(host(got), ref)
+        else:  # OpenBLAS splits contractions longer than GEMM_Q = 384 into several chains
+            assert O.rel_fro(host(got), ref) < 1e-13
+
+
 def test_itucker_restated_reference_cases(policy):
     # test_tucker_ops.cpp:236-288
     rng = np.random.default_rng(113)
