@@ -18,12 +18,12 @@
 // One slice per warp per iteration: the slice (n x n doubles, contiguous) is
 // copied by 16-byte cp.async into a padded buffer (column pitch n + 4: both
 // fragment patterns conflict-free), three buffers per warp (two slices in
-// flight); the factor fragments stay in registers.
+// flight); A2's fragments stay in registers, A1 sits in shared memory.
 #pragma once
 
 namespace mumode_gpu {
 
-constexpr int kKron12Warps = 8;
+constexpr int kKron12Warps = 12;
 constexpr int kKron12Bufs = 3;
 
 __device__ __forceinline__ void kron_cp_async16(double* dst, const double* src) {
@@ -38,15 +38,17 @@ __global__ void __launch_bounds__(32 * kKron12Warps, 1) kron12_kernel(const doub
   constexpr int N = 8 * NB, KS = N / 4, PS = N + 4, SL = N * PS, HALF = N / 2;
   extern __shared__ __align__(16) double kron_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  double* buf = kron_smem + warp * kKron12Bufs * SL;
-  double a1f[NB][KS], a2f[NB][KS];
+  double* buf = kron_smem + SL + warp * kKron12Bufs * SL;
+  // A2's fragments (A operand of t2') in registers, A1 (B operand of t1') in shared memory with the
+  // slices' column pitch: twelve warps fit the register file that way
+  double* sA1 = kron_smem;
+  for (int e = threadIdx.x; e < N * N; e += blockDim.x) sA1[(e / N) * PS + (e % N)] = A1[e];
+  double a2f[NB][KS];
 #pragma unroll
   for (int f = 0; f < NB; ++f)
 #pragma unroll
-    for (int s = 0; s < KS; ++s) {
-      a1f[f][s] = A1[(8 * f + g) + N * (4 * s + t)];
-      a2f[f][s] = A2[(8 * f + g) + N * (4 * s + t)];
-    }
+    for (int s = 0; s < KS; ++s) a2f[f][s] = A2[(8 * f + g) + N * (4 * s + t)];
+  __syncthreads();
   const int64_t stride = int64_t(gridDim.x) * kKron12Warps;
   auto issue = [&](int64_t c, double* dst) {
     const double* src = V + c * (N * N);
@@ -78,17 +80,18 @@ __global__ void __launch_bounds__(32 * kKron12Warps, 1) kron12_kernel(const doub
       for (int fi = 0; fi < NB; ++fi) d1[fj][fi][0] = d1[fj][fi][1] = d2[fj][fi][0] = d2[fj][fi][1] = 0.0;
 #pragma unroll
     for (int s = 0; s < KS; ++s) {
-      double va[NB], vb[NB];
+      double va[NB], vb[NB], a1[NB];
 #pragma unroll
       for (int f = 0; f < NB; ++f) {
         va[f] = v[(8 * f + g) * PS + 4 * s + t];  // V(k, j): column j at j * PS
         vb[f] = v[(4 * s + t) * PS + 8 * f + g];  // V(i, k)
+        a1[f] = sA1[(4 * s + t) * PS + 8 * f + g];  // A1(i, k)
       }
 #pragma unroll
       for (int fj = 0; fj < NB; ++fj)
 #pragma unroll
         for (int fi = 0; fi < NB; ++fi) {
-          dmma_8x8x4(d1[fj][fi][0], d1[fj][fi][1], va[fj], a1f[fi][s]);
+          dmma_8x8x4(d1[fj][fi][0], d1[fj][fi][1], va[fj], a1[fi]);
           dmma_8x8x4(d2[fj][fi][0], d2[fj][fi][1], a2f[fj][s], vb[fi]);
         }
     }
@@ -104,6 +107,6 @@ __global__ void __launch_bounds__(32 * kKron12Warps, 1) kron12_kernel(const doub
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
-inline size_t kron12_smem(int n) { return sizeof(double) * size_t(kKron12Warps) * kKron12Bufs * size_t(n) * (n + 4); }
+inline size_t kron12_smem(int n) { return sizeof(double) * (size_t(kKron12Warps) * kKron12Bufs + 1) * size_t(n) * (n + 4); }
 
 }  // namespace mumode_gpu
