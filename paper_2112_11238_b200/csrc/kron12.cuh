@@ -1,6 +1,6 @@
 // kronsumv's first two terms in ONE pass (ops::kronsumv, tucker.hpp:209-232):
 //   W(:, :, c) = A1 V_c + V_c A2^T   for every slice c of the modes beyond 2,
-// for small square modes 1 and 2 (n = 16 or 24). One pass per term reads V
+// for small square modes 1 and 2 (even n from 10 to 24). One pass per term reads V
 // twice and reads W once more than needed (24^6: 7.7 GB for the two terms
 // against 3.1 GB here); the per-mode passes are at the HBM rate, so the bytes
 // are the time.
@@ -30,29 +30,36 @@ __device__ __forceinline__ void kron_cp_async16(double* dst, const double* src) 
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
-template <int NB>
+template <int NB, bool FULL>  // FULL: n = 8 NB exactly (compile-time bounds)
 __global__ void __launch_bounds__(32 * kKron12Warps, 1) kron12_kernel(const double* __restrict__ V,
                                                                        const double* __restrict__ A1,
                                                                        const double* __restrict__ A2,
-                                                                       double* __restrict__ W, int64_t nslices) {
-  constexpr int N = 8 * NB, KS = N / 4, PS = N + 4, SL = N * PS, HALF = N / 2;
+                                                                       double* __restrict__ W, int64_t nslices,
+                                                                       int n_arg) {
+  // n <= N = 8 NB, n even: the buffers' rows and columns n..N-1 and the factor fragments beyond n are
+  // zero, so every chain is the k-ordered chain over the true k's plus exact zero steps
+  constexpr int N = 8 * NB, KS = N / 4, PS = N + 4, SL = N * PS;
+  const int n = FULL ? N : n_arg, HALF = n / 2;
   extern __shared__ __align__(16) double kron_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   double* buf = kron_smem + SL + warp * kKron12Bufs * SL;
   // A2's fragments (A operand of t2') in registers, A1 (B operand of t1') in shared memory with the
   // slices' column pitch: twelve warps fit the register file that way
   double* sA1 = kron_smem;
-  for (int e = threadIdx.x; e < N * N; e += blockDim.x) sA1[(e / N) * PS + (e % N)] = A1[e];
+  for (int e = threadIdx.x; e < (1 + kKron12Warps * kKron12Bufs) * SL; e += blockDim.x) kron_smem[e] = 0.0;
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) sA1[(e / n) * PS + (e % n)] = A1[e];
   double a2f[NB][KS];
 #pragma unroll
   for (int f = 0; f < NB; ++f)
 #pragma unroll
-    for (int s = 0; s < KS; ++s) a2f[f][s] = A2[(8 * f + g) + N * (4 * s + t)];
+    for (int s = 0; s < KS; ++s)
+      a2f[f][s] = (8 * f + g < n && 4 * s + t < n) ? A2[(8 * f + g) + n * (4 * s + t)] : 0.0;
   __syncthreads();
   const int64_t stride = int64_t(gridDim.x) * kKron12Warps;
   auto issue = [&](int64_t c, double* dst) {
-    const double* src = V + c * (N * N);
-    for (int q = lane; q < N * HALF; q += 32) {
+    const double* src = V + c * (int64_t(n) * n);
+    for (int q = lane; q < n * HALF; q += 32) {
       const int r = q / HALF, cp = q - r * HALF;
       kron_cp_async16(dst + r * PS + 2 * cp, src + 2 * q);
     }
@@ -96,17 +103,21 @@ __global__ void __launch_bounds__(32 * kKron12Warps, 1) kron12_kernel(const doub
         }
     }
     __syncwarp();  // every lane has read the slice: its buffer may be refilled
-    double* w = W + c * (N * N);
+    double* w = W + c * (int64_t(n) * n);
 #pragma unroll
     for (int fj = 0; fj < NB; ++fj)
 #pragma unroll
       for (int fi = 0; fi < NB; ++fi)
-        stg_f64x2(w + (8 * fj + g) * N + 8 * fi + 2 * t, d1[fj][fi][0] + d2[fj][fi][0], d1[fj][fi][1] + d2[fj][fi][1]);
+        if (8 * fj + g < n && 8 * fi + 2 * t < n)
+          stg_f64x2(w + (8 * fj + g) * n + 8 * fi + 2 * t, d1[fj][fi][0] + d2[fj][fi][0],
+                    d1[fj][fi][1] + d2[fj][fi][1]);
     if (++b == kKron12Bufs) b = 0;
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
-inline size_t kron12_smem(int n) { return sizeof(double) * (size_t(kKron12Warps) * kKron12Bufs + 1) * size_t(n) * (n + 4); }
+inline size_t kron12_smem(int nb) {  // nb = ceil(n / 8)
+  return sizeof(double) * (size_t(kKron12Warps) * kKron12Bufs + 1) * size_t(8 * nb) * (8 * nb + 4);
+}
 
 }  // namespace mumode_gpu

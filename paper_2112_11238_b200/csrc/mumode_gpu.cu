@@ -162,6 +162,7 @@ struct mumode_handle_s {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   int policy = 0;
+  int aux_policy = 0;  // 23..26: itucker / kronsumv kernel choices; every other decision stays auto
   int sm_reserve = 0;           // SMs left free by the persistent kernels (dist exchange overlap)
   int64_t launches = 0;
   mumode_gpu::DevBuf ws[3];     // Tucker ping-pong intermediates + expint buffer
@@ -502,7 +503,8 @@ int64_t mumode_launch_count(mumode_handle_t h) { return h ? h->launches : -1; }
 int mumode_set_kernel_policy(mumode_handle_t h, int policy) {
   if (!h || policy < 0 || policy > 26) return fail(MUMODE_ERR_ARGUMENT, "bad kernel policy");
   // 3..6 force real tile configuration 0..3 / complex configuration 0..3
-  h->policy = policy;
+  h->policy = policy >= 23 ? 0 : policy;
+  h->aux_policy = policy >= 23 ? policy : 0;
   return MUMODE_OK;
 }
 
@@ -711,20 +713,22 @@ static int kronsumv_entry(mumode_handle_t h, int d, const int64_t* m, const doub
   // epilogues (the reference's acc += term order, tucker.hpp:222-231): no
   // term buffer and no separate accumulation pass over W.
   int first = 2;
-  // small square modes 1 and 2 (16 or 24): both terms in one pass over V (kron12.cuh)
-  if (!cplx && d >= 3 && m[0] == m[1] && (m[0] == 16 || m[0] == 24) && prod(m, 2, d) >= 2048 &&
-      aligned16_ptr(V) && aligned16_ptr(W) && h->policy != 26) {
-    const int n = static_cast<int>(m[0]);
+  // small square modes 1 and 2 (even extents 10..24): both terms in one pass over V (kron12.cuh)
+  if (!cplx && d >= 3 && m[0] == m[1] && m[0] >= 10 && m[0] <= 24 && m[0] % 2 == 0 && prod(m, 2, d) >= 2048 &&
+      aligned16_ptr(V) && aligned16_ptr(W) && h->aux_policy != 26) {
+    const int n = static_cast<int>(m[0]), nb = (n + 7) / 8;
     const int64_t nsl = prod(m, 2, d);
-    const size_t smem = kron12_smem(n);
+    const size_t smem = kron12_smem(nb);
     const int grid = static_cast<int>(std::min<int64_t>((nsl + kKron12Warps - 1) / kKron12Warps, h->num_sms));
-    if (n == 16) {
-      MM_TRY(smem_opt_in(kron12_kernel<2>, static_cast<int>(smem)));
-      kron12_kernel<2><<<grid, 32 * kKron12Warps, smem, h->stream>>>(V, A[0], A[1], W, nsl);
-    } else {
-      MM_TRY(smem_opt_in(kron12_kernel<3>, static_cast<int>(smem)));
-      kron12_kernel<3><<<grid, 32 * kKron12Warps, smem, h->stream>>>(V, A[0], A[1], W, nsl);
-    }
+    auto launch = [&](auto kern) -> int {
+      MM_TRY(smem_opt_in(kern, static_cast<int>(smem)));
+      kern<<<grid, 32 * kKron12Warps, smem, h->stream>>>(V, A[0], A[1], W, nsl, n);
+      return MUMODE_OK;
+    };
+    if (n == 16) MM_TRY(launch(kron12_kernel<2, true>));
+    else if (n == 24) MM_TRY(launch(kron12_kernel<3, true>));
+    else if (nb == 2) MM_TRY(launch(kron12_kernel<2, false>));
+    else MM_TRY(launch(kron12_kernel<3, false>));
     MM_CUDA(cudaGetLastError());
     h->launches++;
     first = 3;
@@ -801,20 +805,20 @@ static int itucker_dev(mumode_handle_t h, int d, const int64_t* m, const double*
     }
     const int64_t tiles = (A * C + kLuFibres - 1) / kLuFibres;
     const int grid = static_cast<int>(std::min<int64_t>(tiles, int64_t(h->num_sms) * 32));
-    if (!cplx && n <= kLuRlMaxN && h->policy != 23) {
+    if (!cplx && n <= kLuRlMaxN && h->aux_policy != 23) {
       // real extents up to 408: right-looking forward sweep, prefetched panels (lu_sweep_rl)
       const int ni = static_cast<int>(n);
       // 64-fibre tiles (16 warps, one CTA per SM from n = 129) or, up to 208, 96-fibre tiles (24 warps),
       // which take ~1.4x a 64-fibre tile's time: chosen by wave count
       const int64_t sms = h->num_sms, F = A * C;
       const int64_t w64 = ((F + 63) / 64 + sms - 1) / sms, w96 = ((F + 95) / 96 + sms - 1) / sms;
-      const bool nf96 = n > 128 && n <= 208 && h->policy != 24 && 14 * w96 < 10 * w64;
+      const bool nf96 = n > 128 && n <= 208 && h->aux_policy != 24 && 14 * w96 < 10 * w64;
       // even extents above 128 with a 16-byte aligned factor: panels by bulk copies (backward ones from
       // a transposed copy of the factor). Measured: 208^3 1.15 -> 1.09 ms, 256^3 2.16 -> 2.06, 300^3
       // 5.41 -> 4.93; no gain with the 96-fibre tiles (their cp.async issue hides under the DMMA phases) or
       // up to 128, where the transpose launch costs more than it saves. Policy 25 forbids the bulk path.
       const double* lut = nullptr;
-      if (n > 128 && !nf96 && n % 2 == 0 && reinterpret_cast<uintptr_t>(LU[mu - 1]) % 16 == 0 && h->policy != 25) {
+      if (n > 128 && !nf96 && n % 2 == 0 && reinterpret_cast<uintptr_t>(LU[mu - 1]) % 16 == 0 && h->aux_policy != 25) {
         const unsigned tb = static_cast<unsigned>((n + 31) / 32);
         lu_transpose_kernel<<<dim3(tb, tb), dim3(32, 8), 0, h->stream>>>(LU[mu - 1], lut_buf, ni);
         MM_CUDA(cudaGetLastError());

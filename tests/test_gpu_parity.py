@@ -516,9 +516,11 @@ def test_kronsumv_complex_against_reference(shape):
 
 
 @pytest.mark.parametrize("shape", [(24, 24, 24, 24, 7), (16, 16, 16, 16, 16), (24, 24, 2100), (16, 16, 50, 60),
-                                   (24, 24, 24, 24, 24, 24)])
+                                   (24, 24, 24, 24, 24, 24), (18, 18, 18, 18, 18), (20, 20, 20, 20, 20),
+                                   (12, 12, 12, 12, 12, 12), (14, 14, 14, 14, 14), (10, 10, 30, 70), (22, 22, 3000)])
 def test_kronsumv_fused_first_pair_equals_per_mode_passes(shape):
-    # kron12_kernel (terms 1 and 2 in one pass, small square modes 1-2) against one pass per term (policy 26):
+    # kron12_kernel (terms 1 and 2 in one pass, small square modes 1-2, even extents 10..24 zero-padded to 16 / 24)
+    # against one pass per term (policy 26):
     # bit for bit; the small shapes also against the reference's kronsumv
     rng = np.random.default_rng(len(shape) * 100 + shape[0])
     h = mm.get_handle(0)
