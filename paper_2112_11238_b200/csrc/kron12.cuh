@@ -46,8 +46,10 @@ __global__ void __launch_bounds__(32 * kKron12Warps, 1) kron12_kernel(const doub
   // A2's fragments (A operand of t2') in registers, A1 (B operand of t1') in shared memory with the
   // slices' column pitch: twelve warps fit the register file that way
   double* sA1 = kron_smem;
-  for (int e = threadIdx.x; e < (1 + kKron12Warps * kKron12Bufs) * SL; e += blockDim.x) kron_smem[e] = 0.0;
-  __syncthreads();
+  if constexpr (!FULL) {  // the padding rows / columns are read as zeros (FULL: every element read is loaded)
+    for (int e = threadIdx.x; e < (1 + kKron12Warps * kKron12Bufs) * SL; e += blockDim.x) kron_smem[e] = 0.0;
+    __syncthreads();
+  }
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) sA1[(e / n) * PS + (e % n)] = A1[e];
   double a2f[NB][KS];
 #pragma unroll
