@@ -690,7 +690,7 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
     }
     if (bs == UM) {
       if (warp < FRW) lu_fwd_diag_quad<XS>(xs, pj, PST, r0, warp, lane);
-    } else if (warp < NF / 32) {
+    } else if (32 * warp + lane < NF) {  // remainder blocks: one lane per fibre
       double* x = xs + r0 * XS + 32 * warp + lane;
       switch (bs) {
         case 8: lu_fwd_diag<8, XS>(x, pj, PST); break;
@@ -809,7 +809,7 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
     __syncthreads();
     if (bs == UM) {
       if (warp < FRW) lu_bwd_diag_quad<XS>(xs, pj, PST, invd, r0, warp, lane);
-    } else if (warp < NF / 32) {
+    } else if (32 * warp + lane < NF) {  // remainder blocks: one lane per fibre
       double* x = xs + r0 * XS + 32 * warp + lane;
       switch (bs) {
         case 8: lu_bwd_diag<8, XS>(x, pj, PST, invd + r0); break;

@@ -843,6 +843,9 @@ static int itucker_dev(mumode_handle_t h, int d, const int64_t* m, const double*
       } else if (n <= 280) {
         if (lut) MM_TRY(launch(lu_solve_rl_kernel<64, 16, 18, 1, true>, 64, 16));
         else MM_TRY(launch(lu_solve_rl_kernel<64, 16, 18, 1, false>, 64, 16));
+      } else if (n <= 328 && h->aux_policy != 24) {  // 48 fibres (12 warps) still fit beside the panels
+        if (lut) MM_TRY(launch(lu_solve_rl_kernel<48, 12, 21, 1, true>, 48, 12));
+        else MM_TRY(launch(lu_solve_rl_kernel<48, 12, 21, 1, false>, 48, 12));
       } else {
         if (lut) MM_TRY(launch(lu_solve_rl_kernel<32, 16, 13, 1, true>, 32, 16));
         else MM_TRY(launch(lu_solve_rl_kernel<32, 16, 13, 1, false>, 32, 16));

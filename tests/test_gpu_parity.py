@@ -602,7 +602,7 @@ def test_itucker_ill_conditioned_bitwise_against_reference(shape):
 
 @pytest.mark.skipif(not O.ref_available(), reason="reference library not built")
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 13, 16, 17, 23, 31, 32, 33, 47, 48, 63, 64, 65, 100, 127, 128, 129, 200,
-                               204, 206, 207, 210, 255, 256, 257, 280, 282, 300, 391, 406, 407, 408, 409])
+                               204, 206, 207, 210, 255, 256, 257, 280, 282, 300, 315, 328, 330, 391, 406, 407, 408, 409])
 def test_itucker_extent_sweep_bitwise_against_reference(n):
     # the right-looking sweep kernel (lu_solve_rl_kernel, n <= 408: every remainder-block pattern 8/4/2/1, each
     # accumulator count MAXI) and the left-looking one beyond, with the extent as first, middle and last mode,
@@ -646,7 +646,7 @@ def test_itucker_many_tiles_per_cta():
         del T, got, want
 
 
-@pytest.mark.parametrize("shape", [(200, 200, 200), (208, 96, 208), (300, 40, 300), (201, 50, 201)])
+@pytest.mark.parametrize("shape", [(200, 200, 200), (208, 96, 208), (300, 40, 300), (201, 50, 201), (350, 30, 350)])
 def test_itucker_repeats_are_bitwise_stable(shape):
     # the right-looking kernel's double-buffered panels, barrier phases and warp roles under load (96-fibre
     # tiles, bulk-copied panels, 32-fibre tiles, odd extent): 20 repeats at full occupancy, each bit for bit
