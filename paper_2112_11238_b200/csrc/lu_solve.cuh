@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(LuCfg<CPLX>::THREADS) lu_solve_mode_kernel(
 //    every phase is latency-bound, so throughput is fibres in flight per SM;
 //    the host picks 96 when it saves enough waves (a 96-fibre tile takes
 //    ~1.4x a 64-fibre tile's time).
-// Panel buffers: 16 x PST doubles, PST >= n, = 4 mod 8 (conflict-free A
+// Panel buffers: 16 x PST doubles, PST >= roundup8(n), = 4 mod 8 (conflict-free A
 // fragments); forward pan[kk * PST + (row - r0)], backward
 // pan[l * PST + (k - r0)].
 // Measured (tools/itucker_time.py, n^3, L2 flushed): 128: 0.330 -> 0.236 ms,
@@ -518,7 +518,8 @@ __device__ __forceinline__ void cp_async_commit_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
-__host__ __device__ inline int lu_rl_pst(int n) { return ((n + 3) & ~7) + 4; }  // >= n, = 4 mod 8 doubles
+// >= the rows of the last 8-row fragment (its rows beyond n are read, never used), = 4 mod 8 doubles
+__host__ __device__ inline int lu_rl_pst(int n) { return ((n + 7) & ~7) + 4; }
 
 // Diagonal-block solves, one lane per fibre (x = the fibre's BS block rows,
 // stride XS = NF + 4): the same per-element update order as trsm's in-block
