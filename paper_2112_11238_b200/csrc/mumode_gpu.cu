@@ -833,8 +833,13 @@ static int itucker_dev(mumode_handle_t h, int d, const int64_t* m, const double*
         kern<<<grid, 32 * nw, rsmem, h->stream>>>(src, S, A, ni, C, LU[mu - 1], lut, perm, perm + n);
         return MUMODE_OK;
       };
-      // 64 fibres per CTA while the tile fits in shared memory (n <= 280), else 32
-      if (n <= 64) MM_TRY(launch(lu_solve_rl_kernel<64, 16, 4, 2, false>, 64, 16));
+      // 64 fibres per CTA while the tile fits in shared memory (n <= 280), else 48 / 32; 32 also when
+      // the 32-fibre tiles fit in one wave (few fibres: every tile is one serial chain of steps, so more,
+      // smaller tiles finish sooner: 200 x 200 x 10 0.206 -> 0.168 ms)
+      if (n > 128 && (F + 31) / 32 <= sms && F > 32 && h->aux_policy != 24) {
+        if (lut) MM_TRY(launch(lu_solve_rl_kernel<32, 16, 13, 1, true>, 32, 16));
+        else MM_TRY(launch(lu_solve_rl_kernel<32, 16, 13, 1, false>, 32, 16));
+      } else if (n <= 64) MM_TRY(launch(lu_solve_rl_kernel<64, 16, 4, 2, false>, 64, 16));
       else if (n <= 128) MM_TRY(launch(lu_solve_rl_kernel<64, 16, 8, 2, false>, 64, 16));
       else if (nf96) MM_TRY(launch(lu_solve_rl_kernel<96, 24, 13, 1, false>, 96, 24));
       else if (n <= 208) {
