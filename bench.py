@@ -324,7 +324,7 @@ def main():
         e2e_step()
     if world > 1:
         dist.barrier()
-    # each e2e figure: the median of three batches of K applications (every
+    # each e2e figure: the median of three (sync) / seven (async) batches of K applications (every
     # batch moves all of its inputs and results; one batch of ~0.1 s was at
     # the mercy of single host hiccups: 7.8-8.7 TFLOP/s across runs)
     sync_batches = []
@@ -353,7 +353,7 @@ def main():
     if world > 1:
         dist.barrier()
     async_batches = []
-    for _ in range(3):
+    for _ in range(7):  # median of seven: one run measured 7.2 TFLOP/s with two of three batches disturbed
         t0 = time.perf_counter()
         for k in range(args.steps):
             e2e_async(k)
@@ -405,8 +405,9 @@ def main():
                                          "note": "148 SM x 128 flop/clk x 1.965 GHz"}},
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
-                "path": "median of 3 batches of mumode_host_tucker_f64_async x K + mumode_host_wait (host-buffer C-ABI), pinned "
+                "path": "median of 7 batches of mumode_host_tucker_f64_async x K + mumode_host_wait (host-buffer C-ABI), pinned "
                         "buffers: consecutive steps overlap download and upload",
+                "batch_ms_per_step": [round(b / args.steps * 1e3, 4) for b in async_batches],
                 "sync_value": round(e2e_sync_value, 3),
                 "sync_path": "mumode_host_tucker_f64 per step (returns with the result in host memory)"},
         "gpu_launches": int(launches),
