@@ -521,10 +521,10 @@ __device__ __forceinline__ void cp_async_commit_wait_all() {
 // >= the rows of the last 8-row fragment (its rows beyond n are read, never used), = 4 mod 8 doubles
 __host__ __device__ inline int lu_rl_pst(int n) { return ((n + 7) & ~7) + 4; }
 
-// Diagonal-block solves, one lane per fibre (x = the fibre's BS block rows,
-// stride XS = NF + 4): the same per-element update order as trsm's in-block
-// solve (row l takes the finished x_i in ascending / descending i), but 120
-// FMAs with 8-fold ILP on one warp instead of 16 shuffle steps on sixteen.
+// Diagonal-block solves of the remainder blocks (8 / 4 / 2 / 1 rows), one lane
+// per fibre (x = the fibre's BS block rows, stride XS = NF + 4): the same
+// per-element update order as trsm's in-block solve (row l takes the finished
+// x_i in ascending / descending i). Full 16-row blocks take the quad form below.
 template <int BS, int XS>
 __device__ __forceinline__ void lu_fwd_diag(double* x, const double* pj, int PST) {
   double v[BS];
@@ -827,8 +827,9 @@ __device__ __forceinline__ void lu_sweep_rl(double* xs, const double* __restrict
 }
 
 // One real mode of itucker through lu_sweep_rl (staged tiles, n <= kLuRlMaxN).
-// Shared memory: invd[n], xs[n * (NF + 4)], two panel buffers of 16 * PST. NF = 64 fibres per CTA (one CTA per SM,
-// every warp busy in the backward chains) while the tile fits, else 32.
+// Shared memory: invd[n], xs[n * (NF + 4)], two panel buffers of 16 * PST. NF fibres per CTA on NW warps (NW / (NF / 8)
+// row groups): 64 on 16 (or 96 on 24 up to n = 208) while the tile fits, 48 on 12 up to 328, else 32 on 16 -- the host
+// chooses (itucker_dev); BULK: panels by bulk copies, lut = the transposed factor.
 template <int NF, int NW, int MAXI, int MINB, bool BULK>
 __global__ void __launch_bounds__(32 * NW, MINB) lu_solve_rl_kernel(
     const double* in, double* out, int64_t A, int n, int64_t C, const double* __restrict__ lu,
